@@ -1,0 +1,166 @@
+/*
+ * cd.h — C ABI of libcd.so: batched exact nearest-neighbour Chamfer distance, its backward, and
+ * the F-score, for B x N x 3 and B x M x 3 fp32 point clouds on one NVIDIA B200 (sm_100a).
+ *
+ * What the operations are (citations: PAPER.md line, SPEC.md line; readings R1..R18 are listed in
+ * DESIGN.md §3):
+ *   PAPER.md:253-254 (§2.5 "Loss Functions and Metrics"): Chamfer distance for point clouds,
+ *   "matching positions of thousands of points", "CUDA functions are a necessity".
+ *   SPEC.md:441 (metrics/chamfer_distance): CD = (1/|A|) sum_a min_b ||a-b||^2
+ *   + (1/|B|) sum_b min_a ||a-b||^2; brute-force nearest neighbours; "VJP holds the argmin fixed".
+ *   Per-point squared distances and argmin indices, the gradient scatter through those indices and
+ *   the F-score at a threshold are the north star's function set (BASELINE.json north_star).
+ *
+ * Conventions (all entry points):
+ *   - Every array argument is a DEVICE pointer to contiguous row-major data owned by the caller.
+ *     Clouds are fp32 (x, y, z) triples, AoS: x[(b*N + i)*3 + c].  Indices are int32, 0-based.
+ *   - The library never allocates, frees or synchronises (except cd_step_host, which synchronises
+ *     nothing either but copies host<->device asynchronously).  Scratch memory comes only from the
+ *     caller's workspace (size from cd_workspace_size, 256-byte aligned base).  Every call is
+ *     asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream) and capturable in a
+ *     CUDA graph.
+ *   - Validation happens before any launch.  On error nothing is launched, outputs are untouched,
+ *     and cd_last_error_string() (thread-local) describes the problem.  CD_ERR_CUDA reports a
+ *     launch failure (the CUDA error string is kept in cd_last_error_string()).
+ *   - Determinism: per-point outputs (d, idx, gradients) are bitwise reproducible for given inputs
+ *     and independent of tiling, split count and query slicing.
+ *   - Preconditions: B, N, M >= 1 (empty cloud -> domain error =
+ *     CD_ERR_INVALID_VALUE); finite coordinates.  Non-finite input does not crash: a
+ *     query whose every distance is NaN/+inf gets d = +inf, idx = -1 (R6).
+ *   - Thread safety: re-entrant; no mutable global state besides the thread-local error string.
+ */
+#ifndef CD_H_
+#define CD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CD_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define CD_API __attribute__((visibility("default")))
+#else
+#define CD_API
+#endif
+
+typedef void* cd_stream_t; /* cudaStream_t */
+
+typedef enum {
+    CD_OK = 0,
+    CD_ERR_INVALID_VALUE = 1,     /* null pointer, B/N/M < 1 (empty cloud), tau < 0, bad slice */
+    CD_ERR_MISALIGNED = 2,        /* cloud base pointer not 4-byte aligned / workspace not 256-B aligned */
+    CD_ERR_TOO_LARGE = 3,         /* B*N or B*M or B*(N+M) exceeds 2^31-1, or workspace too small */
+    CD_ERR_UNSUPPORTED_DEVICE = 4,/* current device is not sm_100 */
+    CD_ERR_CUDA = 5               /* a CUDA runtime call failed; see cd_last_error_string() */
+} cd_status;
+
+typedef enum {
+    CD_OP_FORWARD = 0,   /* cd_forward */
+    CD_OP_FSCORE = 1,    /* cd_fscore */
+    CD_OP_BACKWARD = 2,  /* cd_backward */
+    CD_OP_STEP = 3       /* cd_step_host: forward + finalize + backward (+ staging of the clouds) */
+} cd_op;
+
+/*
+ * cd_forward — both nearest-neighbour directions.
+ *   x: B x N x 3 fp32, y: B x M x 3 fp32.
+ *   Query slices (for query-sharding): X rows [q0, q1) of every batch element are
+ *   searched against all of Y, and Y rows [r0, r1) against all of X.  Full problem: q0=0, q1=N,
+ *   r0=0, r1=M.  An empty slice (q0 == q1 or r0 == r1) skips that direction.
+ *   Outputs (slice-sized, row stride = slice length):
+ *     d_xy  [B x (q1-q0)] fp32: min_j ||x_{b,i} - y_{b,j}||^2 (squared, R2), fp32 op order DESIGN.md §4.2
+ *     idx_xy[B x (q1-q0)] int32: lowest j attaining it (R3)
+ *     d_yx  [B x (r1-r0)], idx_yx[B x (r1-r0)]: the same with the roles swapped
+ *     partials [B x 4] fp64 (may be NULL): sum of d_xy over the slice, sum of d_yx over the slice,
+ *       hits_xy, hits_yx (exact counts stored as fp64; 0 when tau < 0).  Sums are accumulated in
+ *       fp64 in a fixed order (R9).  Partials from several slices/ranks add up (R18).
+ *   tau >= 0: F-score hit counting, hit iff (double)d <= (double)tau * (double)tau (R11, R16).
+ *   tau < 0: no hit counting.
+ */
+CD_API cd_status cd_forward(const float* x, const float* y, int B, int N, int M,
+                     int q0, int q1, int r0, int r1,
+                     float* d_xy, int32_t* idx_xy, float* d_yx, int32_t* idx_yx,
+                     double* partials, float tau,
+                     void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_finalize — per-batch Chamfer, batch loss and F-score from the partials.
+ *   partials [B x 4] fp64 (after an optional all-reduce sum across ranks, R18).
+ *   cd_per_batch[b] = w1 * partials[b][0] / N + w2 * partials[b][1] / M      (R1)
+ *   loss[0] = (1/B) sum_b cd_per_batch[b]  (computed in fp64, stored fp32)
+ *   precision[b] = hits_xy / N, recall[b] = hits_yx / M, fscore[b] = 2PR/(P+R), 0 if P+R == 0 (R15).
+ *   cd_per_batch, fscore, precision, recall may each be NULL; loss must not be NULL.
+ */
+CD_API cd_status cd_finalize(const double* partials, int B, int N, int M, float w1, float w2,
+                      float* cd_per_batch, float* loss, float* fscore, float* precision,
+                      float* recall, cd_stream_t stream);
+
+/*
+ * cd_fscore — F-score at radius tau from existing per-point distances (X = prediction,
+ * Y = reference).  d_xy [B x N], d_yx [B x M] fp32 (as produced by cd_forward).
+ *   Outputs fscore, precision, recall [B] fp32 (precision/recall may be NULL).  tau >= 0 required.
+ */
+CD_API cd_status cd_fscore(const float* d_xy, const float* d_yx, int B, int N, int M, float tau,
+                    float* fscore, float* precision, float* recall,
+                    void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_backward — VJP of the per-point distances with the argmin held fixed (
+ * SURVEY.md §8.a.6-a.8):
+ *   grad_x_i = 2 g_i (x_i - y_{a_i}) + sum_{j : b_j = i} 2 h_j (x_i - y_j)
+ *   grad_y_j = 2 h_j (y_j - x_{b_j}) + sum_{i : a_i = j} 2 g_i (y_j - x_i)
+ *   x, y: the clouds (full).  idx_xy [B x N], idx_yx [B x M]: FULL index arrays (all rows).
+ *   g [B x N] (dL/dd_xy), h [B x M] (dL/dd_yx) fp32, FULL; either may be NULL, in which case the
+ *   scalar g_scalar / h_scalar is used for every element (R8: the loss gradient is a fill).
+ *   Output slices: grad_x rows [q0, q1) of every batch element, shape B x (q1-q0) x 3, and
+ *   grad_y rows [r0, r1), B x (r1-r0) x 3.  Full problem: q0=0, q1=N, r0=0, r1=M.
+ *   Each output element is accumulated in fp64: own term first, then the scatter terms in
+ *   ascending source index (deterministic; no floating-point atomics), one fp32 write.
+ *   Indices outside [0, M) / [0, N) are a precondition violation (results unspecified, no fault:
+ *   they are clamped).
+ */
+CD_API cd_status cd_backward(const float* x, const float* y, int B, int N, int M,
+                      const int32_t* idx_xy, const int32_t* idx_yx,
+                      const float* g, const float* h, float g_scalar, float h_scalar,
+                      int q0, int q1, int r0, int r1,
+                      float* grad_x, float* grad_y,
+                      void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_step_host — one whole training/evaluation step through HOST buffers (the end-to-end entry
+ * point): copies x_host, y_host (pinned host memory recommended) into device staging inside the
+ * workspace, runs cd_forward (full slices, tau) + cd_finalize + cd_backward of loss = mean_b CD_b
+ * (g = w1/(B N), h = w2/(B M)), and copies back to host: loss_host[1], fscore_host[B] (may be NULL),
+ * grad_x_host [B x N x 3] and grad_y_host [B x M x 3] (each may be NULL).  Asynchronous on stream:
+ * the caller synchronises before reading host outputs.  Workspace: cd_workspace_size(CD_OP_STEP).
+ */
+CD_API cd_status cd_step_host(const float* x_host, const float* y_host, int B, int N, int M,
+                       float tau, float w1, float w2,
+                       float* loss_host, float* fscore_host, float* grad_x_host, float* grad_y_host,
+                       void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/* Workspace bytes needed by an operation for these sizes (full slices).  0 on invalid sizes. */
+CD_API size_t cd_workspace_size(int op, int B, int N, int M);
+
+/* Number of kernel launches one call of `op` makes for these sizes (for launch accounting). */
+CD_API int cd_launch_count(int op, int B, int N, int M);
+
+CD_API const char* cd_status_string(cd_status s);
+CD_API const char* cd_last_error_string(void);   /* thread-local; "" when no error */
+CD_API int cd_abi_version(void);                 /* == CD_ABI_VERSION */
+
+/*
+ * Tuning / test hooks (not needed for normal use).  cd_set_forward_config forces the forward's
+ * target-split count (0 = automatic) for the calling thread, so tests can check that results are
+ * independent of the tiling.  Returns the previous value.
+ */
+CD_API int cd_set_forward_splits(int splits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CD_H_ */

@@ -1,0 +1,208 @@
+"""PyTorch-facing API over libcd (argument marshalling only; every step runs in the CUDA kernels).
+
+PyTorch supplies device memory and the current stream.  Inputs must be CUDA fp32 contiguous
+(B, N, 3) / (B, M, 3) tensors on an sm_100 device.  Names follow the paper's notation: X is the
+prediction cloud, Y the reference cloud; d_xy / idx_xy are the per-point squared distances and
+nearest-neighbour indices of X in Y, d_yx / idx_yx the reverse direction.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+
+_ws_cache: dict = {}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def workspace(op: int, B: int, N: int, M: int, device) -> torch.Tensor:
+    """Workspace bytes from cd_workspace_size, cached per (device, op, sizes)."""
+    lib = _lib.load()
+    n = int(lib.cd_workspace_size(op, B, N, M))
+    if n == 0:
+        raise _lib.CdError(1, f"invalid sizes B={B} N={N} M={M}")
+    key = (str(device), op, B, N, M)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(n, dtype=torch.uint8, device=device)  # caching allocator: >= 512-B aligned
+        _ws_cache[key] = buf
+    return buf
+
+
+def _check_cloud(t, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float32 or t.dim() != 3 or t.shape[-1] != 3:
+        raise TypeError(f"{name} must be fp32 of shape (B, P, 3), got {t.dtype} {tuple(t.shape)}")
+    return t.contiguous()
+
+
+def set_forward_splits(s: int) -> int:
+    """Test hook: force the forward's target-split count (0 = auto).  Returns the previous value."""
+    return int(_lib.load().cd_set_forward_splits(int(s)))
+
+
+def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=None, r_slice=None,
+            want_partials: bool = True):
+    """cd_forward: both NN directions.  Returns (d_xy, idx_xy, d_yx, idx_yx, partials[B,4] fp64).
+
+    q_slice=(q0,q1) / r_slice=(r0,r1) restrict the query rows (query sharding); outputs are
+    slice-sized."""
+    x = _check_cloud(x, "x")
+    y = _check_cloud(y, "y")
+    B, N, _ = x.shape
+    M = y.shape[1]
+    if y.shape[0] != B:
+        raise ValueError("batch mismatch")
+    q0, q1 = q_slice if q_slice is not None else (0, N)
+    r0, r1 = r_slice if r_slice is not None else (0, M)
+    dev = x.device
+    d_xy = torch.empty((B, q1 - q0), dtype=torch.float32, device=dev)
+    i_xy = torch.empty((B, q1 - q0), dtype=torch.int32, device=dev)
+    d_yx = torch.empty((B, r1 - r0), dtype=torch.float32, device=dev)
+    i_yx = torch.empty((B, r1 - r0), dtype=torch.int32, device=dev)
+    part = torch.empty((B, 4), dtype=torch.float64, device=dev) if want_partials else None
+    ws = workspace(_lib.CD_OP_FORWARD, B, N, M, dev)
+    lib = _lib.load()
+    check(lib.cd_forward(_ptr(x), _ptr(y), B, N, M, q0, q1, r0, r1, _ptr(d_xy), _ptr(i_xy), _ptr(d_yx), _ptr(i_yx),
+                         _ptr(part), float(-1.0 if tau is None else tau), _ptr(ws), ws.numel(), _stream()))
+    return d_xy, i_xy, d_yx, i_yx, part
+
+
+def finalize(partials: torch.Tensor, N: int, M: int, w1: float = 1.0, w2: float = 1.0):
+    """cd_finalize: returns (cd_per_batch[B], loss[1], fscore[B], precision[B], recall[B])."""
+    B = partials.shape[0]
+    dev = partials.device
+    cd = torch.empty(B, dtype=torch.float32, device=dev)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    F = torch.empty(B, dtype=torch.float32, device=dev)
+    P = torch.empty(B, dtype=torch.float32, device=dev)
+    R = torch.empty(B, dtype=torch.float32, device=dev)
+    check(_lib.load().cd_finalize(_ptr(partials.contiguous()), B, N, M, float(w1), float(w2), _ptr(cd), _ptr(loss),
+                                  _ptr(F), _ptr(P), _ptr(R), _stream()))
+    return cd, loss, F, P, R
+
+
+def fscore_from_distances(d_xy: torch.Tensor, d_yx: torch.Tensor, tau: float):
+    """cd_fscore: (F, P, R) per batch element from per-point squared distances."""
+    B, N = d_xy.shape
+    M = d_yx.shape[1]
+    dev = d_xy.device
+    F = torch.empty(B, dtype=torch.float32, device=dev)
+    P = torch.empty(B, dtype=torch.float32, device=dev)
+    R = torch.empty(B, dtype=torch.float32, device=dev)
+    ws = workspace(_lib.CD_OP_FSCORE, B, N, M, dev)
+    check(_lib.load().cd_fscore(_ptr(d_xy.contiguous()), _ptr(d_yx.contiguous()), B, N, M, float(tau), _ptr(F),
+                                _ptr(P), _ptr(R), _ptr(ws), ws.numel(), _stream()))
+    return F, P, R
+
+
+def fscore(x: torch.Tensor, y: torch.Tensor, tau: float):
+    """F-score at radius tau built on the same NN pass (forward with hit counting + finalize)."""
+    _, _, _, _, part = forward(x, y, tau=tau)
+    _, _, F, P, R = finalize(part, x.shape[1], y.shape[1])
+    return F, P, R
+
+
+def backward(x: torch.Tensor, y: torch.Tensor, idx_xy: torch.Tensor, idx_yx: torch.Tensor, g=None, h=None,
+             g_scalar: float = 0.0, h_scalar: float = 0.0, q_slice=None, r_slice=None):
+    """cd_backward: gradients of sum(g*d_xy) + sum(h*d_yx) wrt x (rows q_slice) and y (rows r_slice)."""
+    x = _check_cloud(x, "x")
+    y = _check_cloud(y, "y")
+    B, N, _ = x.shape
+    M = y.shape[1]
+    q0, q1 = q_slice if q_slice is not None else (0, N)
+    r0, r1 = r_slice if r_slice is not None else (0, M)
+    dev = x.device
+    gx = torch.empty((B, q1 - q0, 3), dtype=torch.float32, device=dev)
+    gy = torch.empty((B, r1 - r0, 3), dtype=torch.float32, device=dev)
+    g = g.contiguous().float() if g is not None else None
+    h = h.contiguous().float() if h is not None else None
+    ws = workspace(_lib.CD_OP_BACKWARD, B, N, M, dev)
+    check(_lib.load().cd_backward(_ptr(x), _ptr(y), B, N, M, _ptr(idx_xy.contiguous()), _ptr(idx_yx.contiguous()),
+                                  _ptr(g), _ptr(h), float(g_scalar), float(h_scalar), q0, q1, r0, r1, _ptr(gx),
+                                  _ptr(gy), _ptr(ws), ws.numel(), _stream()))
+    return gx, gy
+
+
+def step_host(x_host: np.ndarray, y_host: np.ndarray, tau: float | None = None, w1: float = 1.0, w2: float = 1.0,
+              want_grads: bool = True, device=None, out=None):
+    """cd_step_host: one whole step through HOST buffers (H2D of the clouds, forward, finalize,
+    loss backward, D2H of loss / F-score / gradients).  Host arrays should be pinned (see
+    pinned_like).  Synchronises the current stream before returning (loss, fscore, grad_x, grad_y)."""
+    B, N, _ = x_host.shape
+    M = y_host.shape[1]
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    ws = workspace(_lib.CD_OP_STEP, B, N, M, device)
+    if out is None:
+        out = dict(loss=pinned_empty((1,)), fscore=pinned_empty((B,)),
+                   grad_x=pinned_empty((B, N, 3)) if want_grads else None,
+                   grad_y=pinned_empty((B, M, 3)) if want_grads else None)
+    check(_lib.load().cd_step_host(
+        ctypes.c_void_p(x_host.ctypes.data) if isinstance(x_host, np.ndarray) else _ptr(x_host),
+        ctypes.c_void_p(y_host.ctypes.data) if isinstance(y_host, np.ndarray) else _ptr(y_host),
+        B, N, M, float(-1.0 if tau is None else tau), float(w1), float(w2),
+        _host_ptr(out["loss"]), _host_ptr(out["fscore"]) if tau is not None else None,
+        _host_ptr(out["grad_x"]), _host_ptr(out["grad_y"]), _ptr(ws), ws.numel(), _stream()))
+    torch.cuda.current_stream().synchronize()
+    return out
+
+
+def _host_ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def pinned_empty(shape, dtype=torch.float32):
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def pinned_copy(a: np.ndarray) -> torch.Tensor:
+    t = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+    t.numpy()[...] = a
+    return t
+
+
+class ChamferFunction(torch.autograd.Function):
+    """loss = mean_b [w1 mean_i d_xy + w2 mean_j d_yx] with the argmin held fixed in backward."""
+
+    @staticmethod
+    def forward(ctx, x, y, w1, w2):
+        d_xy, i_xy, d_yx, i_yx, part = forward(x, y)
+        _, loss, _, _, _ = finalize(part, x.shape[1], y.shape[1], w1, w2)
+        ctx.save_for_backward(x, y, i_xy, i_yx)
+        ctx.w = (w1, w2)
+        return loss[0]
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        x, y, i_xy, i_yx = ctx.saved_tensors
+        w1, w2 = ctx.w
+        B, N, M = x.shape[0], x.shape[1], y.shape[1]
+        # g = dL/dd_xy = grad_out * w1 / (B N): the upstream scalar multiplies a uniform fill
+        go = grad_out.reshape(1).float()
+        g = (go * (w1 / (B * N))).expand(B, N)
+        h = (go * (w2 / (B * M))).expand(B, M)
+        gx, gy = backward(x, y, i_xy, i_yx, g, h)
+        return gx, gy, None, None
+
+
+def chamfer(x: torch.Tensor, y: torch.Tensor, w1: float = 1.0, w2: float = 1.0) -> torch.Tensor:
+    """Differentiable Chamfer loss (R1)."""
+    return ChamferFunction.apply(x, y, w1, w2)
+
+
+def launch_count(op: int, B: int, N: int, M: int) -> int:
+    return int(_lib.load().cd_launch_count(op, B, N, M))

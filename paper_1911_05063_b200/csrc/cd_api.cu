@@ -1,0 +1,283 @@
+// cd_api.cu — the C ABI of libcd.so (declared in include/cd.h): validation, workspace carving and
+// launch sequencing.  No allocation, no synchronisation; everything is asynchronous on `stream`.
+#include "../../include/cd.h"
+#include "cd_internal.h"
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_forced_splits = 0;
+
+cd_status fail(cd_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+cd_status fail(cd_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+cd_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return CD_OK;
+    return fail(CD_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+cd_status check_sizes(int B, int N, int M) {
+    if (B < 1 || N < 1 || M < 1)
+        return fail(CD_ERR_INVALID_VALUE, "B, N, M must be >= 1 (empty cloud, SPEC.md:440-442): B=%d N=%d M=%d", B,
+                    N, M);
+    const long long L = (long long)B * ((long long)N + (long long)M);
+    if (L > 0x7fffffffLL) return fail(CD_ERR_TOO_LARGE, "B*(N+M) = %lld exceeds 2^31-1", L);
+    return CD_OK;
+}
+
+cd_status check_device() {
+    int dev = 0, major = 0, minor = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return fail(CD_ERR_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; libcd is built for sm_100a only", dev, major,
+                    minor);
+    return CD_OK;
+}
+
+size_t forward_ws(int B, int N, int M, int q0, int q1, int r0, int r1) {
+    cdk::FwdPlan p;
+    cdk::plan_forward(p, B, N, M, q0, q1, r0, r1, g_forced_splits);
+    return p.bytes;
+}
+
+// cd_step_host workspace: staging of x, y, outputs of forward, partials/loss/fscore, grads, plus
+// the larger of the forward and backward workspaces.
+struct StepLayout {
+    size_t x, y, dxy, ixy, dyx, iyx, part, loss, fs, gx, gy, inner, inner_bytes, bytes;
+};
+StepLayout step_layout(int B, int N, int M) {
+    StepLayout s;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = cdk::align_up(off + bytes, 256);
+        return o;
+    };
+    s.x = take((size_t)B * N * 12);
+    s.y = take((size_t)B * M * 12);
+    s.dxy = take((size_t)B * N * 4);
+    s.ixy = take((size_t)B * N * 4);
+    s.dyx = take((size_t)B * M * 4);
+    s.iyx = take((size_t)B * M * 4);
+    s.part = take((size_t)B * 32);
+    s.loss = take(4);
+    s.fs = take((size_t)B * 4);
+    s.gx = take((size_t)B * N * 12);
+    s.gy = take((size_t)B * M * 12);
+    cdk::BwdPlan bp;
+    cdk::plan_backward(bp, B, N, M, 0, N, 0, M);
+    s.inner_bytes = std::max(forward_ws(B, N, M, 0, N, 0, M), bp.bytes);
+    s.inner = take(s.inner_bytes);
+    s.bytes = off;
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cd_abi_version(void) { return CD_ABI_VERSION; }
+
+const char* cd_status_string(cd_status s) {
+    switch (s) {
+        case CD_OK: return "CD_OK";
+        case CD_ERR_INVALID_VALUE: return "CD_ERR_INVALID_VALUE";
+        case CD_ERR_MISALIGNED: return "CD_ERR_MISALIGNED";
+        case CD_ERR_TOO_LARGE: return "CD_ERR_TOO_LARGE";
+        case CD_ERR_UNSUPPORTED_DEVICE: return "CD_ERR_UNSUPPORTED_DEVICE";
+        case CD_ERR_CUDA: return "CD_ERR_CUDA";
+    }
+    return "CD_ERR_UNKNOWN";
+}
+
+const char* cd_last_error_string(void) { return g_err.c_str(); }
+
+int cd_set_forward_splits(int splits) {
+    int old = g_forced_splits;
+    g_forced_splits = splits > 0 ? splits : 0;
+    return old;
+}
+
+size_t cd_workspace_size(int op, int B, int N, int M) {
+    if (B < 1 || N < 1 || M < 1) return 0;
+    if ((long long)B * ((long long)N + M) > 0x7fffffffLL) return 0;
+    switch (op) {
+        case CD_OP_FORWARD: return forward_ws(B, N, M, 0, N, 0, M);
+        case CD_OP_FSCORE: return cdk::fscore_workspace(B, N, M);
+        case CD_OP_BACKWARD: {
+            cdk::BwdPlan p;
+            cdk::plan_backward(p, B, N, M, 0, N, 0, M);
+            return p.bytes;
+        }
+        case CD_OP_STEP: return step_layout(B, N, M).bytes;
+    }
+    return 0;
+}
+
+int cd_launch_count(int op, int B, int N, int M) {
+    if (B < 1 || N < 1 || M < 1) return 0;
+    cdk::BwdPlan bp;
+    cdk::plan_backward(bp, B, N, M, 0, N, 0, M);
+    switch (op) {
+        case CD_OP_FORWARD: return cdk::kForwardLaunches;
+        case CD_OP_FSCORE: return cdk::kFscoreLaunches;
+        case CD_OP_BACKWARD: return cdk::backward_launches(bp);
+        case CD_OP_STEP: return cdk::kForwardLaunches + 1 + cdk::backward_launches(bp);
+    }
+    return 0;
+}
+
+cd_status cd_forward(const float* x, const float* y, int B, int N, int M, int q0, int q1, int r0, int r1,
+                     float* d_xy, int32_t* idx_xy, float* d_yx, int32_t* idx_yx, double* partials, float tau,
+                     void* workspace, size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x || !y || !workspace) return fail(CD_ERR_INVALID_VALUE, "null x, y or workspace pointer");
+    if (q0 < 0 || q1 < q0 || q1 > N || r0 < 0 || r1 < r0 || r1 > M)
+        return fail(CD_ERR_INVALID_VALUE, "bad query slices [%d,%d) of N=%d, [%d,%d) of M=%d", q0, q1, N, r0, r1, M);
+    if (q1 > q0 && (!d_xy || !idx_xy)) return fail(CD_ERR_INVALID_VALUE, "null d_xy / idx_xy");
+    if (r1 > r0 && (!d_yx || !idx_yx)) return fail(CD_ERR_INVALID_VALUE, "null d_yx / idx_yx");
+    if (tau != tau) return fail(CD_ERR_INVALID_VALUE, "tau is NaN");
+    if (!aligned(x, 4) || !aligned(y, 4)) return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte aligned");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    cdk::FwdPlan p;
+    cdk::plan_forward(p, B, N, M, q0, q1, r0, r1, g_forced_splits);
+    if (workspace_bytes < p.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    cdk::FwdOutputs o;
+    o.d[0] = d_xy;
+    o.d[1] = d_yx;
+    o.idx[0] = idx_xy;
+    o.idx[1] = idx_yx;
+    o.partials = partials;
+    o.tau = tau;
+    return cuda_status(cdk::launch_forward(p, x, y, o, workspace, static_cast<cudaStream_t>(stream)), "cd_forward");
+}
+
+cd_status cd_finalize(const double* partials, int B, int N, int M, float w1, float w2, float* cd_per_batch,
+                      float* loss, float* fscore, float* precision, float* recall, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!partials || !loss) return fail(CD_ERR_INVALID_VALUE, "null partials or loss pointer");
+    s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_finalize(partials, B, N, M, w1, w2, cd_per_batch, loss, fscore, precision, recall,
+                                            static_cast<cudaStream_t>(stream)),
+                       "cd_finalize");
+}
+
+cd_status cd_fscore(const float* d_xy, const float* d_yx, int B, int N, int M, float tau, float* fscore,
+                    float* precision, float* recall, void* workspace, size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!d_xy || !d_yx || !fscore || !workspace) return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (!(tau >= 0.f)) return fail(CD_ERR_INVALID_VALUE, "tau must be >= 0 (got %g)", (double)tau);
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const size_t need = cdk::fscore_workspace(B, N, M);
+    if (workspace_bytes < need) return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu", workspace_bytes, need);
+    s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_fscore(d_xy, d_yx, B, N, M, tau, fscore, precision, recall, workspace,
+                                          static_cast<cudaStream_t>(stream)),
+                       "cd_fscore");
+}
+
+cd_status cd_backward(const float* x, const float* y, int B, int N, int M, const int32_t* idx_xy,
+                      const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar, int q0,
+                      int q1, int r0, int r1, float* grad_x, float* grad_y, void* workspace, size_t workspace_bytes,
+                      cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x || !y || !idx_xy || !idx_yx || !workspace) return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (q0 < 0 || q1 < q0 || q1 > N || r0 < 0 || r1 < r0 || r1 > M)
+        return fail(CD_ERR_INVALID_VALUE, "bad slices [%d,%d) of N=%d, [%d,%d) of M=%d", q0, q1, N, r0, r1, M);
+    if (q1 > q0 && !grad_x) return fail(CD_ERR_INVALID_VALUE, "null grad_x");
+    if (r1 > r0 && !grad_y) return fail(CD_ERR_INVALID_VALUE, "null grad_y");
+    if (!aligned(x, 4) || !aligned(y, 4)) return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte aligned");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    cdk::BwdPlan p;
+    cdk::plan_backward(p, B, N, M, q0, q1, r0, r1);
+    if (workspace_bytes < p.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_backward(p, x, y, idx_xy, idx_yx, g, h, g_scalar, h_scalar, grad_x, grad_y,
+                                            workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_backward");
+}
+
+cd_status cd_step_host(const float* x_host, const float* y_host, int B, int N, int M, float tau, float w1, float w2,
+                       float* loss_host, float* fscore_host, float* grad_x_host, float* grad_y_host, void* workspace,
+                       size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x_host || !y_host || !loss_host || !workspace) return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const StepLayout L = step_layout(B, N, M);
+    if (workspace_bytes < L.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, L.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* w = static_cast<char*>(workspace);
+    float* x = reinterpret_cast<float*>(w + L.x);
+    float* y = reinterpret_cast<float*>(w + L.y);
+    cudaError_t e = cudaMemcpyAsync(x, x_host, (size_t)B * N * 12, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(y, y_host, (size_t)B * M * 12, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "cd_step_host H2D");
+    float* dxy = reinterpret_cast<float*>(w + L.dxy);
+    int32_t* ixy = reinterpret_cast<int32_t*>(w + L.ixy);
+    float* dyx = reinterpret_cast<float*>(w + L.dyx);
+    int32_t* iyx = reinterpret_cast<int32_t*>(w + L.iyx);
+    double* part = reinterpret_cast<double*>(w + L.part);
+    float* loss = reinterpret_cast<float*>(w + L.loss);
+    float* fs = reinterpret_cast<float*>(w + L.fs);
+    float* gx = reinterpret_cast<float*>(w + L.gx);
+    float* gy = reinterpret_cast<float*>(w + L.gy);
+    void* inner = w + L.inner;
+    s = cd_forward(x, y, B, N, M, 0, N, 0, M, dxy, ixy, dyx, iyx, part, tau, inner, L.inner_bytes, stream);
+    if (s != CD_OK) return s;
+    s = cd_finalize(part, B, N, M, w1, w2, nullptr, loss, tau >= 0.f ? fs : nullptr, nullptr, nullptr, stream);
+    if (s != CD_OK) return s;
+    const float gs = (float)((double)w1 / ((double)B * N));
+    const float hs = (float)((double)w2 / ((double)B * M));
+    s = cd_backward(x, y, B, N, M, ixy, iyx, nullptr, nullptr, gs, hs, 0, N, 0, M, gx, gy, inner, L.inner_bytes,
+                    stream);
+    if (s != CD_OK) return s;
+    e = cudaMemcpyAsync(loss_host, loss, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && fscore_host && tau >= 0.f)
+        e = cudaMemcpyAsync(fscore_host, fs, (size_t)B * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && grad_x_host)
+        e = cudaMemcpyAsync(grad_x_host, gx, (size_t)B * N * 12, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && grad_y_host)
+        e = cudaMemcpyAsync(grad_y_host, gy, (size_t)B * M * 12, cudaMemcpyDeviceToHost, st);
+    return cuda_status(e, "cd_step_host D2H");
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// cd_device.cuh — device-side helpers for libcd (sm_100a only).
+// Packed-FP32 (f32x2) arithmetic, mbarrier + 1-D TMA bulk copies, and the fixed distance formula.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libcd is written for sm_100a only (compile with -gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace cdk {
+
+typedef unsigned long long u64;
+
+// ---------------------------------------------------------------- tiling constants
+constexpr int kFwdThreads = 128;                 // 4 warps per CTA
+constexpr int kR = 16;                           // queries per thread (8 packed f32x2 pairs)
+constexpr int kQTile = kFwdThreads * kR;         // 2048 queries per CTA
+constexpr int kTile = 512;                       // targets per shared-memory stage (8 KB)
+constexpr int kStages = 3;                       // TMA ring depth
+constexpr int kBlockK = 32;                      // argmin block: the winning block is re-scanned
+constexpr int kPad = kQTile;                     // packed clouds are padded to a multiple of this
+constexpr int kMergeThreads = 256;               // queries per merge/epilogue CTA
+
+// ---------------------------------------------------------------- packed FP32 (FADD2/FMUL2/FFMA2)
+__device__ __forceinline__ u64 pk2(float a, float b) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(u64 v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// 3-input min (FMNMX3): returns the non-NaN operand when one is NaN.
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// The fixed fp32 distance formula: dx = RN(x - y); s = RN(dx*dx);
+// s = fma(dy, dy, s); s = fma(dz, dz, s).  Per lane, the packed f32x2 ops round exactly like
+// these scalar .rn ops, so this scalar form reproduces the packed loop bit for bit.
+__device__ __forceinline__ float dist_rn(float qx, float qy, float qz, float tx, float ty, float tz) {
+    float dx = __fsub_rn(qx, tx);
+    float dy = __fsub_rn(qy, ty);
+    float dz = __fsub_rn(qz, tz);
+    float s = __fmul_rn(dx, dx);
+    s = __fmaf_rn(dy, dy, s);
+    s = __fmaf_rn(dz, dz, s);
+    return s;
+}
+
+// ---------------------------------------------------------------- mbarrier + TMA bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(u64* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(u64* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "CD_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra CD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (cp.async.bulk, SASS UBLKCP), completion counted on `bar`.
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, u64* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+}  // namespace cdk

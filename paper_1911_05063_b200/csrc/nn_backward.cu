@@ -1,0 +1,333 @@
+// nn_backward.cu — backward of the Chamfer per-point distances, argmin held fixed
+// (SURVEY.md §8.a.6-a.8).  Deterministic and free of floating-point atomics:
+//
+//   keys_kernel      one (key, value) pair per NN edge: xy edge i -> a_i gets key b*M + a_i,
+//                    yx edge j -> b_j gets key B*M + b*N + b_j; value = the source row.  Built in
+//                    ascending source order.
+//   radix passes     stable LSD radix sort by key, 8-bit digits, reduce-then-scan:
+//                      radix_hist_kernel   per-tile digit histograms (shared-memory integer adds)
+//                      radix_scan_kernel   exclusive scan of the digit-major histogram table
+//                      radix_scatter_kernel stable in-tile ranks (warp match + per-warp counts in
+//                                          element order) -> scatter.  Stability keeps ascending
+//                                          source rows inside every key segment.
+//   offsets_kernel   segment offsets from the sorted keys (disjoint gap fills, no atomics).
+//   grad_kernel      one thread per output point: own term 2 g (p - partner) then the segment's
+//                    scatter terms in ascending source order, accumulated in fp64 with explicit
+//                    .rn ops (no contraction), one fp32 store.
+#include "cd_device.cuh"
+#include "cd_internal.h"
+
+#include <algorithm>
+
+namespace cdk {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements per tile
+constexpr int kDigitBits = 8;
+constexpr int kDigits = 1 << kDigitBits;
+
+__global__ void __launch_bounds__(256) keys_kernel(const int32_t* __restrict__ idx_xy,
+                                                   const int32_t* __restrict__ idx_yx, int B, int N, int M,
+                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int64_t L0 = (int64_t)B * N;
+    const int64_t L = L0 + (int64_t)B * M;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L; p += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t key, val;
+        if (p < L0) {
+            const int64_t b = p / N;
+            const int a = min(max(idx_xy[p], 0), M - 1);
+            key = (uint32_t)(b * M + a);
+            val = (uint32_t)p;
+        } else {
+            const int64_t q = p - L0;
+            const int64_t b = q / M;
+            const int a = min(max(idx_yx[q], 0), N - 1);
+            key = (uint32_t)((int64_t)B * M + b * N + a);
+            val = (uint32_t)q;
+        }
+        keys[p] = key;
+        vals[p] = val;
+    }
+}
+
+// counts[digit * ntiles + tile]
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t L,
+                                                                  int shift, int ntiles,
+                                                                  uint32_t* __restrict__ counts) {
+    __shared__ uint32_t hist[kDigits];
+    for (int d = threadIdx.x; d < kDigits; d += kSortThreads) hist[d] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+    for (int k = 0; k < kSortItems; ++k) {
+        const int64_t e = base + (int64_t)k * kSortThreads + threadIdx.x;
+        if (e < L) atomicAdd(&hist[(keys[e] >> shift) & (kDigits - 1)], 1u);  // integer: order-free
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kDigits; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
+}
+
+// In-place exclusive scan of n values with one CTA of 1024 threads (contiguous segments per thread).
+__global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__ data, int64_t n) {
+    __shared__ uint32_t part[1024];
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t lo = threadIdx.x * per;
+    const int64_t hi = min(lo + per, n);
+    uint32_t s = 0;
+    for (int64_t i = lo; i < hi; ++i) s += data[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    // Hillis-Steele inclusive scan over 1024 partial sums
+    for (int o = 1; o < 1024; o <<= 1) {
+        const uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x > 0 ? part[threadIdx.x - 1] : 0u;
+    for (int64_t i = lo; i < hi; ++i) {
+        const uint32_t v = data[i];
+        data[i] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int ntiles,
+    const uint32_t* __restrict__ offsets, uint32_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+    constexpr int W = kSortThreads / 32;
+    __shared__ uint32_t run[kDigits];
+    __shared__ uint32_t wcnt[W][kDigits];
+    for (int d = threadIdx.x; d < kDigits; d += kSortThreads) {
+        run[d] = offsets[(int64_t)d * ntiles + blockIdx.x];
+        for (int w = 0; w < W; ++w) wcnt[w][d] = 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int k = 0; k < kSortItems; ++k) {
+        const int64_t e = base + (int64_t)k * kSortThreads + threadIdx.x;
+        const bool valid = e < L;
+        uint32_t key = 0, val = 0;
+        int digit = kDigits;  // invalid lanes use a digit value no valid lane has
+        if (valid) {
+            key = kin[e];
+            val = vin[e];
+            digit = (key >> shift) & (kDigits - 1);
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+        const uint32_t rank = __popc(peers & lt_mask);
+        const bool leader = rank == 0;
+        if (valid && leader) wcnt[warp][digit] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            uint32_t pos = run[digit] + rank;
+            for (int w = 0; w < warp; ++w) pos += wcnt[w][digit];
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < kDigits; d += kSortThreads) {
+            uint32_t t = 0;
+            for (int w = 0; w < W; ++w) t += wcnt[w][d];
+            run[d] += t;
+        }
+        __syncthreads();
+        if (valid && leader) wcnt[warp][digit] = 0;
+        // the next round's writes to wcnt happen after the next __syncthreads-free match; make the
+        // clears visible before anyone reads them again (next round reads after its first barrier)
+    }
+}
+
+// off[k] = first sorted position with key >= k, for k in [0, kmax]; off[kmax] = L.
+__global__ void __launch_bounds__(256) offsets_kernel(const uint32_t* __restrict__ keys, int64_t L, int64_t kmax,
+                                                      uint32_t* __restrict__ off) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= L; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lo = p == 0 ? 0 : (int64_t)keys[p - 1] + 1;
+        const int64_t hi = p == L ? kmax : (int64_t)keys[p];
+        for (int64_t k = lo; k <= hi; ++k) off[k] = (uint32_t)p;
+    }
+}
+
+struct GradArgs {
+    const float* x;
+    const float* y;
+    int B, N, M, q0, q1, r0, r1;
+    const int32_t* idx_xy;
+    const int32_t* idx_yx;
+    const float* g;
+    const float* h;
+    float g_scalar, h_scalar;
+    const uint32_t* vals;
+    const uint32_t* off;
+    float* grad_x;
+    float* grad_y;
+};
+
+// acc += (2 w) * (p - s), fp64, explicit roundings in the oracle's order (no FMA contraction).
+__device__ __forceinline__ void acc_term(double acc[3], const float* p, const float* s, double w) {
+    const double w2 = __dmul_rn(2.0, w);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c])));
+}
+
+__global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
+    const int sq = a.q1 - a.q0, sr = a.r1 - a.r0;
+    const int64_t nx = (int64_t)a.B * sq;
+    const int64_t total = nx + (int64_t)a.B * sr;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        double acc[3] = {0.0, 0.0, 0.0};
+        if (t < nx) {
+            const int64_t b = t / sq;
+            const int i = a.q0 + (int)(t - b * sq);
+            const int64_t xi = b * a.N + i;
+            const float* p = a.x + xi * 3;
+            const int part = min(max(a.idx_xy[xi], 0), a.M - 1);
+            const double gi = a.g ? (double)a.g[xi] : (double)a.g_scalar;
+            // own term, then: every term has the form 2 w (p - s) with p = this point
+            {
+                double own[3] = {0.0, 0.0, 0.0};
+                const float* s = a.y + (b * a.M + part) * 3;
+                const double w2 = __dmul_rn(2.0, gi);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) own[c] = __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c]));
+                acc[0] = own[0];
+                acc[1] = own[1];
+                acc[2] = own[2];
+            }
+            const int64_t key = (int64_t)a.B * a.M + b * a.N + i;
+            const uint32_t e0 = a.off[key], e1 = a.off[key + 1];
+            for (uint32_t e = e0; e < e1; ++e) {
+                const uint32_t src = a.vals[e];  // y row b*M + j
+                const double hj = a.h ? (double)a.h[src] : (double)a.h_scalar;
+                acc_term(acc, p, a.y + (int64_t)src * 3, hj);
+            }
+            float* o = a.grad_x + (b * sq + (i - a.q0)) * 3;
+            o[0] = (float)acc[0];
+            o[1] = (float)acc[1];
+            o[2] = (float)acc[2];
+        } else {
+            const int64_t u = t - nx;
+            const int64_t b = u / sr;
+            const int j = a.r0 + (int)(u - b * sr);
+            const int64_t yj = b * a.M + j;
+            const float* p = a.y + yj * 3;
+            const int part = min(max(a.idx_yx[yj], 0), a.N - 1);
+            const double hj = a.h ? (double)a.h[yj] : (double)a.h_scalar;
+            {
+                const float* s = a.x + (b * a.N + part) * 3;
+                const double w2 = __dmul_rn(2.0, hj);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c]));
+            }
+            const int64_t key = b * a.M + j;
+            const uint32_t e0 = a.off[key], e1 = a.off[key + 1];
+            for (uint32_t e = e0; e < e1; ++e) {
+                const uint32_t src = a.vals[e];  // x row b*N + i
+                const double gi = a.g ? (double)a.g[src] : (double)a.g_scalar;
+                acc_term(acc, p, a.x + (int64_t)src * 3, gi);
+            }
+            float* o = a.grad_y + (b * sr + (j - a.r0)) * 3;
+            o[0] = (float)acc[0];
+            o[1] = (float)acc[1];
+            o[2] = (float)acc[2];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+static int sm_count() {
+    static thread_local int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1) {
+    p.B = B;
+    p.N = N;
+    p.M = M;
+    p.q0 = q0;
+    p.q1 = q1;
+    p.r0 = r0;
+    p.r1 = r1;
+    p.L = (int64_t)B * (N + M);
+    p.kmax = p.L;  // B*M keys for the xy edges + B*N keys for the yx edges
+    int bits = 0;
+    while (bits < 32 && ((int64_t)1 << bits) < p.kmax) ++bits;
+    p.nbits = std::max(bits, 1);
+    p.npasses = (p.nbits + kDigitBits - 1) / kDigitBits;
+    p.ntiles = (int)((p.L + kSortTile - 1) / kSortTile);
+    size_t off = 0;
+    for (int i = 0; i < 2; ++i) {
+        p.off_keys[i] = off;
+        off = align_up(off + (size_t)p.L * 4, 256);
+        p.off_vals[i] = off;
+        off = align_up(off + (size_t)p.L * 4, 256);
+    }
+    p.off_counts = off;
+    off = align_up(off + (size_t)kDigits * p.ntiles * 4, 256);
+    p.off_offsets = off;
+    off = align_up(off + (size_t)(p.kmax + 1) * 4, 256);
+    p.bytes = off;
+}
+
+int backward_launches(const BwdPlan& p) { return 1 + 3 * p.npasses + 2; }
+
+cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, const int32_t* idx_xy,
+                            const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar,
+                            float* grad_x, float* grad_y, void* ws, cudaStream_t st) {
+    char* w = static_cast<char*>(ws);
+    uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
+    uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
+    uint32_t* counts = reinterpret_cast<uint32_t*>(w + p.off_counts);
+    uint32_t* off = reinterpret_cast<uint32_t*>(w + p.off_offsets);
+    const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sm_count() * 16);
+    keys_kernel<<<grid_l, 256, 0, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, keys[0], vals[0]);
+    int cur = 0;
+    for (int pass = 0; pass < p.npasses; ++pass) {
+        const int shift = pass * kDigitBits;
+        radix_hist_kernel<<<p.ntiles, kSortThreads, 0, st>>>(keys[cur], p.L, shift, p.ntiles, counts);
+        radix_scan_kernel<<<1, 1024, 0, st>>>(counts, (int64_t)kDigits * p.ntiles);
+        radix_scatter_kernel<<<p.ntiles, kSortThreads, 0, st>>>(keys[cur], vals[cur], p.L, shift, p.ntiles, counts,
+                                                               keys[1 - cur], vals[1 - cur]);
+        cur = 1 - cur;
+    }
+    const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);
+    offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], p.L, p.kmax, off);
+    GradArgs a;
+    a.x = x;
+    a.y = y;
+    a.B = p.B;
+    a.N = p.N;
+    a.M = p.M;
+    a.q0 = p.q0;
+    a.q1 = p.q1;
+    a.r0 = p.r0;
+    a.r1 = p.r1;
+    a.idx_xy = idx_xy;
+    a.idx_yx = idx_yx;
+    a.g = g;
+    a.h = h;
+    a.g_scalar = g_scalar;
+    a.h_scalar = h_scalar;
+    a.vals = vals[cur];
+    a.off = off;
+    a.grad_x = grad_x;
+    a.grad_y = grad_y;
+    const int64_t total = (int64_t)p.B * ((p.q1 - p.q0) + (p.r1 - p.r0));
+    if (total > 0) {
+        const int grid_g = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32);
+        grad_kernel<<<grid_g, 256, 0, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace cdk

@@ -1,0 +1,625 @@
+// nn_forward.cu — forward of the batched exact nearest-neighbour search.
+//
+// Kernels (one launch each, on the caller's stream):
+//   pack_kernel      AoS (x,y,z) fp32 clouds -> padded float4 clouds in the workspace (a.1).
+//   nn_fwd_kernel    the hot loop (a.2 + a.3, both directions in one grid): every thread keeps
+//                    kR = 16 queries in packed f32x2 registers and sweeps the targets of its split,
+//                    staged through a 3-stage shared-memory ring by 1-D TMA bulk copies
+//                    (cp.async.bulk + mbarrier).  Distances use FADD2/FMUL2/FFMA2 with the target
+//                    coordinate as broadcast operand; the running minimum is value-only (FMNMX3
+//                    folding two targets per op) and the argmin is tracked per block of kBlockK
+//                    targets (the block where the minimum last strictly decreased).
+//   nn_merge_kernel  merges the target splits (lowest split wins ties), re-scans the winning block
+//                    with the same .rn ops to recover the exact lowest index, writes d / idx and
+//                    per-chunk fp64 sums + hit counts (a.4).
+//   partials_kernel  fixed-order reduction of the chunk partials into partials[B][4] (a.4/a.5).
+// plus finalize_kernel (cd_finalize, a.5) and the cd_fscore path.
+#include "cd_device.cuh"
+#include "cd_internal.h"
+
+#include <algorithm>
+#include <cmath>
+
+namespace cdk {
+
+// ------------------------------------------------------------------------------------------------
+struct PackArgs {
+    const float* src[2];
+    float4* dst[2];
+    int npts[2];
+    int ppad[2];
+    int B;
+};
+
+__global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
+    const int64_t n0 = (int64_t)a.B * a.ppad[0];
+    const int64_t total = n0 + (int64_t)a.B * a.ppad[1];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = e < n0 ? 0 : 1;
+        const int64_t f = c == 0 ? e : e - n0;
+        const int64_t b = f / a.ppad[c];
+        const int i = (int)(f - b * a.ppad[c]);
+        float4 v;
+        if (i < a.npts[c]) {
+            const float* s = a.src[c] + (b * a.npts[c] + i) * 3;
+            v = make_float4(__ldg(s), __ldg(s + 1), __ldg(s + 2), 0.f);
+        } else {
+            // padding targets: +inf coordinates give d = +inf, never selected by min / strict <
+            v = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+        }
+        a.dst[c][f] = v;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+struct FwdArgs {
+    const float4* pack[2];
+    int npts[2], ppad[2];
+    int qlo[2], qhi[2];
+    int qtiles[2], splits[2], split_len[2];
+    int64_t slice_off[2], slice_total;
+    float* best_d;
+    int* best_blk;
+};
+
+__global__ void __launch_bounds__(kFwdThreads, 4) nn_fwd_kernel(FwdArgs a) {
+    __shared__ __align__(128) float4 sm[kStages][kTile];
+    __shared__ __align__(8) u64 full_bar[kStages];
+
+    int u = blockIdx.x;
+    const int b = blockIdx.y;
+    int dir = 0;
+    const int units0 = a.qtiles[0] * a.splits[0];
+    if (u >= units0) {
+        dir = 1;
+        u -= units0;
+    }
+    const int tile = u / a.splits[dir];
+    const int split = u - tile * a.splits[dir];
+    const int tdir = 1 - dir;
+    const float4* __restrict__ Q = a.pack[dir] + (int64_t)b * a.ppad[dir];
+    const float4* __restrict__ T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
+    const int nq = a.npts[dir];
+    const int nt = a.npts[tdir];
+    const int j0 = split * a.split_len[dir];
+    const int j1 = min(j0 + a.split_len[dir], nt);
+    const int ntiles = (j1 - j0 + kTile - 1) / kTile;  // >= 1 (host guarantees non-empty splits)
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int pre = min(kStages, ntiles);
+        for (int k = 0; k < pre; ++k) {
+            mbar_arrive_expect_tx(&full_bar[k], kTile * 16);
+            tma_load_1d(sm[k], T + j0 + (int64_t)k * kTile, kTile * 16, &full_bar[k]);
+        }
+    }
+
+    // queries: kR consecutive points per thread, packed in pairs (r, r+1) -> one f32x2 register
+    const int qbase = a.qlo[dir] + tile * kQTile + threadIdx.x * kR;
+    u64 qx[kR / 2], qy[kR / 2], qz[kR / 2];
+#pragma unroll
+    for (int r = 0; r < kR / 2; ++r) {
+        const float4 p0 = Q[min(qbase + 2 * r, nq - 1)];
+        const float4 p1 = Q[min(qbase + 2 * r + 1, nq - 1)];
+        qx[r] = pk2(p0.x, p1.x);
+        qy[r] = pk2(p0.y, p1.y);
+        qz[r] = pk2(p0.z, p1.z);
+    }
+    float best[kR];
+    int blk[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        best[r] = INFINITY;
+        blk[r] = -1;
+    }
+
+    for (int k = 0; k < ntiles; ++k) {
+        const int s = k % kStages;
+        mbar_wait(&full_bar[s], (k / kStages) & 1);
+        const float4* tb = sm[s];
+        const int jt = j0 + k * kTile;
+        for (int kb = 0; kb < kTile; kb += kBlockK) {
+            float old[kR];
+#pragma unroll
+            for (int r = 0; r < kR; ++r) old[r] = best[r];
+#pragma unroll 2
+            for (int jj = 0; jj < kBlockK; jj += 2) {
+                const float4 t0 = tb[kb + jj];
+                const float4 t1 = tb[kb + jj + 1];
+                const u64 t0x = pk2(t0.x, t0.x), t0y = pk2(t0.y, t0.y), t0z = pk2(t0.z, t0.z);
+                const u64 t1x = pk2(t1.x, t1.x), t1y = pk2(t1.y, t1.y), t1z = pk2(t1.z, t1.z);
+#pragma unroll
+                for (int r = 0; r < kR / 2; ++r) {
+                    u64 dx = sub2(qx[r], t0x), dy = sub2(qy[r], t0y), dz = sub2(qz[r], t0z);
+                    u64 s0 = mul2(dx, dx);
+                    s0 = fma2(dy, dy, s0);
+                    s0 = fma2(dz, dz, s0);
+                    dx = sub2(qx[r], t1x);
+                    dy = sub2(qy[r], t1y);
+                    dz = sub2(qz[r], t1z);
+                    u64 s1 = mul2(dx, dx);
+                    s1 = fma2(dy, dy, s1);
+                    s1 = fma2(dz, dz, s1);
+                    float a0, a1, c0, c1;
+                    upk2(s0, a0, a1);
+                    upk2(s1, c0, c1);
+                    best[2 * r] = fmin3(best[2 * r], a0, c0);
+                    best[2 * r + 1] = fmin3(best[2 * r + 1], a1, c1);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kR; ++r) blk[r] = best[r] < old[r] ? jt + kb : blk[r];
+        }
+        __syncthreads();  // every warp is done with stage s
+        if (threadIdx.x == 0 && k + kStages < ntiles) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], kTile * 16);
+            tma_load_1d(sm[s], T + jt + (int64_t)kStages * kTile, kTile * 16, &full_bar[s]);
+        }
+    }
+
+    const int qhi = a.qhi[dir];
+    const int slen = qhi - a.qlo[dir];
+    const int64_t rowbase = (int64_t)split * a.slice_total + a.slice_off[dir] + (int64_t)b * slen;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        const int q = qbase + r;
+        if (q < qhi) {
+            const int64_t o = rowbase + (q - a.qlo[dir]);
+            a.best_d[o] = best[r];
+            a.best_blk[o] = blk[r];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Fixed-order block reduction of (fp64 sum, int hits) over kMergeThreads threads.
+__device__ __forceinline__ void block_sum_hits(double v, int h, double* out_sum, int* out_hits) {
+    __shared__ double ssum[kMergeThreads / 32];
+    __shared__ int shit[kMergeThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_down_sync(0xffffffffu, v, o);
+        h += __shfl_down_sync(0xffffffffu, h, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        ssum[w] = v;
+        shit[w] = h;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        int t = 0;
+        for (int i = 0; i < kMergeThreads / 32; ++i) {
+            s += ssum[i];
+            t += shit[i];
+        }
+        *out_sum = s;
+        *out_hits = t;
+    }
+}
+
+struct MergeArgs {
+    const float4* pack[2];
+    int npts[2];
+    int ppad[2];
+    int qlo[2], qhi[2];
+    int splits[2];
+    int64_t slice_off[2], slice_total;
+    int nchunks[2];
+    int64_t chunk_off[2];
+    int B;
+    const float* best_d;
+    const int* best_blk;
+    float* d_out[2];
+    int32_t* idx_out[2];
+    double* chunk_sum;
+    int* chunk_hits;
+    double tau2;  // < 0: no hits
+};
+
+__global__ void __launch_bounds__(kMergeThreads) nn_merge_kernel(MergeArgs a) {
+    int u = blockIdx.x;
+    int dir = 0;
+    if (u >= a.B * a.nchunks[0]) {
+        dir = 1;
+        u -= a.B * a.nchunks[0];
+    }
+    const int b = u / a.nchunks[dir];
+    const int chunk = u - b * a.nchunks[dir];
+    const int slen = a.qhi[dir] - a.qlo[dir];
+    const int sq = chunk * kMergeThreads + threadIdx.x;
+    const bool valid = sq < slen;
+    double v = 0.0;
+    int h = 0;
+    if (valid) {
+        const int64_t row = a.slice_off[dir] + (int64_t)b * slen + sq;
+        float best = INFINITY;
+        int bb = -1;
+        for (int s = 0; s < a.splits[dir]; ++s) {
+            const float d = a.best_d[(int64_t)s * a.slice_total + row];
+            if (d < best) {  // strict <: the earliest split (lowest target indices) keeps ties
+                best = d;
+                bb = a.best_blk[(int64_t)s * a.slice_total + row];
+            }
+        }
+        int idx = -1;
+        if (bb >= 0) {
+            const int tdir = 1 - dir;
+            const float4 qp = a.pack[dir][(int64_t)b * a.ppad[dir] + a.qlo[dir] + sq];
+            const float4* T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
+            const int jend = min(bb + kBlockK, a.npts[tdir]);
+            for (int j = bb; j < jend; ++j) {
+                const float4 t = T[j];
+                if (dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z) == best) {
+                    idx = j;
+                    break;
+                }
+            }
+        }
+        a.d_out[dir][(int64_t)b * slen + sq] = best;
+        a.idx_out[dir][(int64_t)b * slen + sq] = idx;
+        v = (double)best;
+        h = (a.tau2 >= 0.0 && (double)best <= a.tau2) ? 1 : 0;
+    }
+    double s;
+    int t;
+    block_sum_hits(v, h, &s, &t);
+    if (threadIdx.x == 0) {
+        const int64_t c = a.chunk_off[dir] + (int64_t)b * a.nchunks[dir] + chunk;
+        a.chunk_sum[c] = s;
+        a.chunk_hits[c] = t;
+    }
+}
+
+// Per-chunk stats of given distance arrays (cd_fscore path).
+struct StatsArgs {
+    const float* d[2];
+    int n[2];
+    int nchunks[2];
+    int64_t chunk_off[2];
+    int B;
+    double* chunk_sum;
+    int* chunk_hits;
+    double tau2;
+};
+
+__global__ void __launch_bounds__(kMergeThreads) stats_kernel(StatsArgs a) {
+    int u = blockIdx.x;
+    int dir = 0;
+    if (u >= a.B * a.nchunks[0]) {
+        dir = 1;
+        u -= a.B * a.nchunks[0];
+    }
+    const int b = u / a.nchunks[dir];
+    const int chunk = u - b * a.nchunks[dir];
+    const int i = chunk * kMergeThreads + threadIdx.x;
+    double v = 0.0;
+    int h = 0;
+    if (i < a.n[dir]) {
+        const float d = a.d[dir][(int64_t)b * a.n[dir] + i];
+        v = (double)d;
+        h = (double)d <= a.tau2 ? 1 : 0;
+    }
+    double s;
+    int t;
+    block_sum_hits(v, h, &s, &t);
+    if (threadIdx.x == 0) {
+        const int64_t c = a.chunk_off[dir] + (int64_t)b * a.nchunks[dir] + chunk;
+        a.chunk_sum[c] = s;
+        a.chunk_hits[c] = t;
+    }
+}
+
+// partials[b][0..3] = (sum d_xy, sum d_yx, hits_xy, hits_yx), fixed-order reduction over chunks.
+struct PartialsArgs {
+    const double* chunk_sum;
+    const int* chunk_hits;
+    int nchunks[2];
+    int64_t chunk_off[2];
+    double* partials;
+};
+
+__global__ void __launch_bounds__(256) partials_kernel(PartialsArgs a) {
+    __shared__ double ssum[256];
+    __shared__ long long shit[256];
+    const int b = blockIdx.x;
+    for (int dir = 0; dir < 2; ++dir) {
+        double s = 0.0;
+        long long h = 0;
+        const int64_t base = a.chunk_off[dir] + (int64_t)b * a.nchunks[dir];
+        for (int c = threadIdx.x; c < a.nchunks[dir]; c += 256) {
+            s += a.chunk_sum[base + c];
+            h += a.chunk_hits[base + c];
+        }
+        ssum[threadIdx.x] = s;
+        shit[threadIdx.x] = h;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) {
+                ssum[threadIdx.x] += ssum[threadIdx.x + w];
+                shit[threadIdx.x] += shit[threadIdx.x + w];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            a.partials[b * 4 + dir] = ssum[0];
+            a.partials[b * 4 + 2 + dir] = (double)shit[0];
+        }
+        __syncthreads();
+    }
+}
+
+// cd_finalize: CD_b, loss, P/R/F from partials (fp64 internally, fp32 outputs).
+struct FinalizeArgs {
+    const double* partials;
+    int B, N, M;
+    double w1, w2;
+    float *cd, *loss, *fscore, *precision, *recall;
+};
+
+__global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs a) {
+    __shared__ double sl[256];
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < a.B; b += 256) {
+        const double* p = a.partials + 4 * b;
+        const double cdb = a.w1 * (p[0] / a.N) + a.w2 * (p[1] / a.M);
+        acc += cdb;
+        if (a.cd) a.cd[b] = (float)cdb;
+        const double P = p[2] / a.N, R = p[3] / a.M;
+        const double F = (P + R) > 0.0 ? 2.0 * P * R / (P + R) : 0.0;
+        if (a.fscore) a.fscore[b] = (float)F;
+        if (a.precision) a.precision[b] = (float)P;
+        if (a.recall) a.recall[b] = (float)R;
+    }
+    sl[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sl[threadIdx.x] += sl[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && a.loss) a.loss[0] = (float)(sl[0] / a.B);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Host side.
+static int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+static int device_sm_count() {
+    static thread_local int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+// Choose the target-split count S so that (query-tile units x S) CTAs fill the SMs in waves of
+// near-equal work: minimise ceil(U*S / slots) * (Mt/S + c0), c0 = per-unit overhead in target-
+// equivalents (query load + epilogue).
+static int choose_splits(int64_t units, int mt) {
+    const int64_t slots = (int64_t)device_sm_count() * 4;  // 4 CTAs of 128 threads per SM
+    const double c0 = 96.0;
+    const int smax = std::max(1, std::min(64, ceil_div(mt, kTile)));
+    int best_s = 1;
+    double best_t = 1e300;
+    for (int s = 1; s <= smax; ++s) {
+        const double waves = (double)ceil_div(units * s, slots);
+        const double t = waves * ((double)mt / s + c0);
+        if (t < best_t * 0.999) {
+            best_t = t;
+            best_s = s;
+        }
+    }
+    return best_s;
+}
+
+void plan_forward(FwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits) {
+    p.B = B;
+    p.npts[0] = N;
+    p.npts[1] = M;
+    p.qlo[0] = q0;
+    p.qhi[0] = q1;
+    p.qlo[1] = r0;
+    p.qhi[1] = r1;
+    int64_t units = 0;
+    for (int d = 0; d < 2; ++d) {
+        p.ppad[d] = ceil_div(p.npts[d], kPad) * kPad;
+        const int slen = p.qhi[d] - p.qlo[d];
+        p.qtiles[d] = slen > 0 ? ceil_div(slen, kQTile) : 0;
+        units += (int64_t)B * p.qtiles[d];
+    }
+    const int S = forced_splits > 0 ? forced_splits : choose_splits(units, std::max(N, M));
+    for (int d = 0; d < 2; ++d) {
+        const int mt = p.npts[1 - d];
+        const int s = std::max(1, std::min(S, ceil_div(mt, kTile)));
+        p.split_len[d] = ceil_div(ceil_div(mt, s), kTile) * kTile;
+        p.splits[d] = ceil_div(mt, p.split_len[d]);  // every split non-empty
+        if (p.qtiles[d] == 0) p.splits[d] = 1;
+    }
+    const int64_t sq = (int64_t)(q1 - q0), sr = (int64_t)(r1 - r0);
+    p.slice_off[0] = 0;
+    p.slice_off[1] = (int64_t)B * sq;
+    p.slice_total = (int64_t)B * (sq + sr);
+    p.nchunks[0] = ceil_div(sq, kMergeThreads);
+    p.nchunks[1] = ceil_div(sr, kMergeThreads);
+    p.chunk_off[0] = 0;
+    p.chunk_off[1] = (int64_t)B * p.nchunks[0];
+    p.chunk_total = (int64_t)B * (p.nchunks[0] + p.nchunks[1]);
+    const int smax = std::max(p.splits[0], p.splits[1]);
+    size_t off = 0;
+    for (int d = 0; d < 2; ++d) {
+        p.off_pack[d] = off;
+        off = align_up(off + (size_t)B * p.ppad[d] * 16, 256);
+    }
+    p.off_best_d = off;
+    off = align_up(off + (size_t)smax * p.slice_total * 4, 256);
+    p.off_best_blk = off;
+    off = align_up(off + (size_t)smax * p.slice_total * 4, 256);
+    p.off_chunk_sum = off;
+    off = align_up(off + (size_t)std::max<int64_t>(p.chunk_total, 1) * 8, 256);
+    p.off_chunk_hits = off;
+    off = align_up(off + (size_t)std::max<int64_t>(p.chunk_total, 1) * 4, 256);
+    p.bytes = off;
+}
+
+cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
+                           cudaStream_t st) {
+    char* w = static_cast<char*>(ws);
+    float4* pack0 = reinterpret_cast<float4*>(w + p.off_pack[0]);
+    float4* pack1 = reinterpret_cast<float4*>(w + p.off_pack[1]);
+    {
+        PackArgs a;
+        a.src[0] = x;
+        a.src[1] = y;
+        a.dst[0] = pack0;
+        a.dst[1] = pack1;
+        for (int d = 0; d < 2; ++d) {
+            a.npts[d] = p.npts[d];
+            a.ppad[d] = p.ppad[d];
+        }
+        a.B = p.B;
+        const int64_t total = (int64_t)p.B * (p.ppad[0] + p.ppad[1]);
+        const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)device_sm_count() * 16);
+        pack_kernel<<<grid, 256, 0, st>>>(a);
+    }
+    float* best_d = reinterpret_cast<float*>(w + p.off_best_d);
+    int* best_blk = reinterpret_cast<int*>(w + p.off_best_blk);
+    const int gx = p.qtiles[0] * p.splits[0] + p.qtiles[1] * p.splits[1];
+    if (gx > 0) {
+        FwdArgs a;
+        a.pack[0] = pack0;
+        a.pack[1] = pack1;
+        for (int d = 0; d < 2; ++d) {
+            a.npts[d] = p.npts[d];
+            a.ppad[d] = p.ppad[d];
+            a.qlo[d] = p.qlo[d];
+            a.qhi[d] = p.qhi[d];
+            a.qtiles[d] = p.qtiles[d];
+            a.splits[d] = p.splits[d];
+            a.split_len[d] = p.split_len[d];
+            a.slice_off[d] = p.slice_off[d];
+        }
+        a.slice_total = p.slice_total;
+        a.best_d = best_d;
+        a.best_blk = best_blk;
+        nn_fwd_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
+    }
+    double* chunk_sum = reinterpret_cast<double*>(w + p.off_chunk_sum);
+    int* chunk_hits = reinterpret_cast<int*>(w + p.off_chunk_hits);
+    if (p.chunk_total > 0) {
+        MergeArgs a;
+        a.pack[0] = pack0;
+        a.pack[1] = pack1;
+        for (int d = 0; d < 2; ++d) {
+            a.npts[d] = p.npts[d];
+            a.ppad[d] = p.ppad[d];
+            a.qlo[d] = p.qlo[d];
+            a.qhi[d] = p.qhi[d];
+            a.splits[d] = p.splits[d];
+            a.slice_off[d] = p.slice_off[d];
+            a.nchunks[d] = p.nchunks[d];
+            a.chunk_off[d] = p.chunk_off[d];
+            a.d_out[d] = o.d[d];
+            a.idx_out[d] = o.idx[d];
+        }
+        a.slice_total = p.slice_total;
+        a.B = p.B;
+        a.best_d = best_d;
+        a.best_blk = best_blk;
+        a.chunk_sum = chunk_sum;
+        a.chunk_hits = chunk_hits;
+        a.tau2 = o.tau >= 0.f ? (double)o.tau * (double)o.tau : -1.0;
+        nn_merge_kernel<<<(unsigned)p.chunk_total, kMergeThreads, 0, st>>>(a);
+    }
+    if (o.partials) {
+        PartialsArgs a;
+        a.chunk_sum = chunk_sum;
+        a.chunk_hits = chunk_hits;
+        for (int d = 0; d < 2; ++d) {
+            a.nchunks[d] = p.nchunks[d];
+            a.chunk_off[d] = p.chunk_off[d];
+        }
+        a.partials = o.partials;
+        partials_kernel<<<p.B, 256, 0, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+size_t fscore_workspace(int B, int N, int M) {
+    const int64_t chunks = (int64_t)B * (ceil_div(N, kMergeThreads) + ceil_div(M, kMergeThreads));
+    return align_up((size_t)chunks * 8, 256) + align_up((size_t)chunks * 4, 256) + align_up((size_t)B * 32, 256);
+}
+
+cudaError_t launch_fscore(const float* d_xy, const float* d_yx, int B, int N, int M, float tau, float* fscore,
+                          float* precision, float* recall, void* ws, cudaStream_t st) {
+    StatsArgs s;
+    s.d[0] = d_xy;
+    s.d[1] = d_yx;
+    s.n[0] = N;
+    s.n[1] = M;
+    s.nchunks[0] = ceil_div(N, kMergeThreads);
+    s.nchunks[1] = ceil_div(M, kMergeThreads);
+    s.chunk_off[0] = 0;
+    s.chunk_off[1] = (int64_t)B * s.nchunks[0];
+    s.B = B;
+    const int64_t chunks = (int64_t)B * (s.nchunks[0] + s.nchunks[1]);
+    char* w = static_cast<char*>(ws);
+    s.chunk_sum = reinterpret_cast<double*>(w);
+    s.chunk_hits = reinterpret_cast<int*>(w + align_up((size_t)chunks * 8, 256));
+    double* partials =
+        reinterpret_cast<double*>(w + align_up((size_t)chunks * 8, 256) + align_up((size_t)chunks * 4, 256));
+    s.tau2 = (double)tau * (double)tau;
+    stats_kernel<<<(unsigned)chunks, kMergeThreads, 0, st>>>(s);
+    PartialsArgs a;
+    a.chunk_sum = s.chunk_sum;
+    a.chunk_hits = s.chunk_hits;
+    for (int d = 0; d < 2; ++d) {
+        a.nchunks[d] = s.nchunks[d];
+        a.chunk_off[d] = s.chunk_off[d];
+    }
+    a.partials = partials;
+    partials_kernel<<<B, 256, 0, st>>>(a);
+    FinalizeArgs f;
+    f.partials = partials;
+    f.B = B;
+    f.N = N;
+    f.M = M;
+    f.w1 = 1.0;
+    f.w2 = 1.0;
+    f.cd = nullptr;
+    f.loss = nullptr;
+    f.fscore = fscore;
+    f.precision = precision;
+    f.recall = recall;
+    finalize_kernel<<<1, 256, 0, st>>>(f);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const double* partials, int B, int N, int M, float w1, float w2, float* cd,
+                            float* loss, float* fscore, float* precision, float* recall, cudaStream_t st) {
+    FinalizeArgs f;
+    f.partials = partials;
+    f.B = B;
+    f.N = N;
+    f.M = M;
+    f.w1 = w1;
+    f.w2 = w2;
+    f.cd = cd;
+    f.loss = loss;
+    f.fscore = fscore;
+    f.precision = precision;
+    f.recall = recall;
+    finalize_kernel<<<1, 256, 0, st>>>(f);
+    return cudaGetLastError();
+}
+
+}  // namespace cdk

@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element, on
+seeded synthetic inputs — small configs in full, large configs on sampled rows —
+plus the fp32 mirror (bit-exact), determinism, slicing and edge cases."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+from paper_1911_05063_b200 import synth
+from tests.gpu_helpers import gate_forward_batch, gate_grad, gate_mirror, RTOL
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cd():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1911_05063_b200 import api
+    return api
+
+
+def _run(cd, X, Y, tau=None, **kw):
+    x = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    y = torch.from_numpy(np.ascontiguousarray(Y)).cuda()
+    out = cd.forward(x, y, tau=tau, **kw)
+    torch.cuda.synchronize()
+    return x, y, [o.cpu().numpy() if o is not None else None for o in out]
+
+
+def _full_check(cd, X, Y, tau=None, mirror=True, backward=True):
+    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=tau)
+    gate_forward_batch(X, Y, d_xy, i_xy, d_yx, i_yx)
+    if mirror:
+        gate_mirror(X, Y, d_xy, i_xy)
+        gate_mirror(Y, X, d_yx, i_yx)
+    ref = oracle.chamfer(X, Y, tau=tau)
+    B, N, M = X.shape[0], X.shape[1], Y.shape[1]
+    # partials vs oracle sums (fp64 sums of the GPU's own distances, R9)
+    np.testing.assert_allclose(part[:, 0], np.asarray(d_xy, np.float64).sum(1), rtol=1e-12)
+    np.testing.assert_allclose(part[:, 1], np.asarray(d_yx, np.float64).sum(1), rtol=1e-12)
+    cdb, loss, F, P, R = cd.finalize(torch.from_numpy(part).cuda(), N, M)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(cdb.cpu().numpy(), ref["cd"], rtol=RTOL)
+    assert abs(loss.item() - ref["loss"]) <= RTOL * abs(ref["loss"]) + (ref["loss"] == 0) * 0
+    if tau is not None:
+        t2 = oracle.tau_sq(tau)
+        band = 1e-6 * t2
+        for dist, hits, col in ((ref["d_xy"], part[:, 2], "xy"), (ref["d_yx"], part[:, 3], "yx")):
+            lo = (dist < t2 - band).sum(1)
+            hi = (dist <= t2 + band).sum(1)
+            assert np.all((hits >= lo) & (hits <= hi)), col
+        Fref = oracle.fscore_from_hits(part[:, 2], part[:, 3], N, M)
+        np.testing.assert_allclose(F.cpu().numpy(), Fref, rtol=RTOL, atol=1e-7)
+    if backward:
+        rng = np.random.default_rng(7)
+        g = rng.normal(size=(B, N)).astype(np.float32)
+        h = rng.normal(size=(B, M)).astype(np.float32)
+        gx, gy = cd.backward(x, y, torch.from_numpy(i_xy).cuda(), torch.from_numpy(i_yx).cuda(),
+                             torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda())
+        torch.cuda.synchronize()
+        gxr, gyr, sx, sy = oracle.backward(X, Y, i_xy, i_yx, g, h)   # backward-only mode: GPU indices
+        # identical fp64 accumulation order => identical fp32 results (stricter than the gate)
+        np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
+        np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+        gate_grad(gx.cpu().numpy(), gxr, sx)
+        gate_grad(gy.cpu().numpy(), gyr, sy)
+    return d_xy, i_xy, d_yx, i_yx, part
+
+
+# ------------------------------------------------------------------------------ configs
+def test_c1_uniform(cd):
+    X, Y = synth.uniform_pair(1, 1024, 1024, seed=1)
+    _full_check(cd, X, Y, tau=0.05)
+
+
+def test_c1_shapes(cd):
+    X, Y = synth.config_inputs("c1")
+    _full_check(cd, X, Y, tau=0.01)
+
+
+def test_c2_full(cd):
+    X, Y = synth.config_inputs("c2")
+    _full_check(cd, X, Y, tau=0.01)
+
+
+def test_c3_sampled_forward_full_backward(cd):
+    X, Y = synth.config_inputs("c3")
+    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
+    B, N, M = X.shape[0], X.shape[1], Y.shape[1]
+    rng = np.random.default_rng(3)
+    rows_x = np.sort(rng.choice(B * N, 20000, replace=False))
+    rows_y = np.sort(rng.choice(B * M, 20000, replace=False))
+    rows_x[:3] = [0, N - 1, B * N - 1]     # tile edges and the ragged tail
+    gate_forward_batch(X, Y, d_xy, i_xy, d_yx, i_yx, rows_x=np.unique(rows_x), rows_y=np.unique(rows_y))
+    gate_mirror(X, Y, d_xy, i_xy, rows=np.unique(rows_x))
+    # sums: partials equal fp64 sums of the per-point outputs; loss within 1e-5 of the oracle's loss
+    np.testing.assert_allclose(part[:, 0], d_xy.astype(np.float64).sum(1), rtol=1e-12)
+    g = np.full((B, N), 1.0 / (B * N), np.float32)
+    h = np.full((B, M), 1.0 / (B * M), np.float32)
+    gx, gy = cd.backward(x, y, torch.from_numpy(i_xy).cuda(), torch.from_numpy(i_yx).cuda(),
+                         torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda())
+    gxr, gyr, sx, sy = oracle.backward(X, Y, i_xy, i_yx, g, h)
+    np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
+    np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+    gate_grad(gy.cpu().numpy(), gyr, sy)
+
+
+@pytest.mark.parametrize("name,nrows", [("c4", 3000), ("c5", 600)])
+def test_large_configs_sampled(cd, name, nrows):
+    X, Y = synth.config_inputs(name)
+    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
+    B, N, M = X.shape[0], X.shape[1], Y.shape[1]
+    rng = np.random.default_rng(4)
+    rows_x = np.unique(np.concatenate([rng.choice(B * N, nrows, replace=False), [0, N - 1, B * N - 1]]))
+    rows_y = np.unique(np.concatenate([rng.choice(B * M, nrows, replace=False), [0, M - 1, B * M - 1]]))
+    gate_forward_batch(X, Y, d_xy, i_xy, d_yx, i_yx, rows_x=rows_x, rows_y=rows_y)
+    gate_mirror(X, Y, d_xy, i_xy, rows=rows_x)
+    # properties that hold at any size: indices in range, distance = |x - y_idx|^2 in fp32 mirror order
+    assert i_xy.min() >= 0 and i_xy.max() < M and i_yx.min() >= 0 and i_yx.max() < N
+    b = np.repeat(np.arange(B), N)
+    dd = X.reshape(-1, 3).astype(np.float64) - Y[b, i_xy.reshape(-1)].astype(np.float64)
+    np.testing.assert_allclose(d_xy.reshape(-1), (dd * dd).sum(1), rtol=RTOL)
+    np.testing.assert_allclose(part[:, 0], d_xy.astype(np.float64).sum(1), rtol=1e-12)
+    # backward on the full problem vs the oracle backward (O(N+M), cheap at any size)
+    gx, gy = cd.backward(x, y, torch.from_numpy(i_xy).cuda(), torch.from_numpy(i_yx).cuda(),
+                         g_scalar=1.0 / (B * N), h_scalar=1.0 / (B * M))
+    gxr, gyr, sx, sy = oracle.backward(X, Y, i_xy, i_yx, g_scalar=np.float32(1.0 / (B * N)),
+                                       h_scalar=np.float32(1.0 / (B * M)))
+    np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
+    np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+
+
+# ------------------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("N,M", [(1, 1), (1, 5000), (5000, 1), (3, 7), (1000, 1024), (2049, 513), (4097, 2047)])
+def test_ragged_sizes(cd, N, M):
+    X, Y = synth.uniform_pair(2, N, M, seed=N * 31 + M)
+    _full_check(cd, X, Y, tau=0.1)
+
+
+def test_identical_clouds(cd):
+    X, _ = synth.shape_pair(2, 3000, 10, config_index=20)
+    d_xy, i_xy, d_yx, i_yx, part = _full_check(cd, X, X.copy(), tau=0.0)
+    assert np.all(d_xy == 0) and np.all(d_yx == 0)
+    np.testing.assert_array_equal(i_xy, np.tile(np.arange(3000), (2, 1)))
+    assert np.all(part[:, 2] == 3000)
+
+
+def test_duplicates_lowest_index(cd):
+    rng = np.random.default_rng(8)
+    base = rng.uniform(-0.5, 0.5, size=(1, 1500, 3)).astype(np.float32)
+    Y = np.concatenate([base, base[:, ::-1]], axis=1)   # every point twice; first copy lowest
+    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, base, Y)
+    np.testing.assert_array_equal(i_xy[0], np.arange(1500))
+    assert np.all(d_xy == 0)
+    # each Y point's nearest X is itself (lowest index among exact ties = the unique copy)
+    np.testing.assert_array_equal(i_yx[0], np.concatenate([np.arange(1500), np.arange(1500)[::-1]]))
+
+
+def test_lattice_exact_ties(cd):
+    h = 2.0 ** -5
+    k = np.arange(16)
+    g = np.stack(np.meshgrid(k, k, k, indexing="ij"), -1).reshape(-1, 3) * h
+    X = g[None].astype(np.float32)
+    # queries at cell centres: 8 lattice points at exactly equal distance -> lowest index wins
+    Q = (g[:500] + h / 2)[None].astype(np.float32)
+    x, y, (d_xy, i_xy, _, _, _) = _run(cd, Q, X)
+    d1, i1, d2 = oracle.nn(Q, X)
+    np.testing.assert_array_equal(i_xy, i1)
+    np.testing.assert_array_equal(d_xy.astype(np.float64), d1)
+    gate_mirror(Q, X, d_xy, i_xy)
+
+
+def test_clustered_far_long_segments(cd):
+    # all X near one Y point: one segment of length N in the backward (degenerate scatter)
+    rng = np.random.default_rng(9)
+    Y = rng.uniform(-0.5, 0.5, size=(1, 2000, 3)).astype(np.float32)
+    X = (Y[:, :1] + 10.0 + rng.normal(scale=1e-3, size=(1, 5000, 3))).astype(np.float32)
+    _full_check(cd, X, Y, tau=0.01)
+
+
+def test_scaling_invariance_bit_exact(cd):
+    X, Y = synth.shape_pair(2, 2000, 1800, config_index=21)
+    _, _, a = _run(cd, X, Y)
+    _, _, b = _run(cd, X * np.float32(4.0), Y * np.float32(4.0))
+    np.testing.assert_array_equal(b[1], a[1])
+    np.testing.assert_array_equal(b[0], a[0] * np.float32(16.0))
+
+
+# ------------------------------------------------------------------------------ determinism
+def test_rerun_and_split_independence(cd):
+    X, Y = synth.shape_pair(3, 5000, 7000, config_index=22)
+    _, _, ref = _run(cd, X, Y, tau=0.01)
+    for _ in range(2):
+        _, _, again = _run(cd, X, Y, tau=0.01)
+        for a, b in zip(ref[:4], again[:4]):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(ref[4], again[4])
+    for s in (1, 2, 3, 7, 14):
+        old = cd.set_forward_splits(s)
+        try:
+            _, _, out = _run(cd, X, Y, tau=0.01)
+        finally:
+            cd.set_forward_splits(old)
+        for a, b in zip(ref[:4], out[:4]):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_query_slices_match_full(cd):
+    X, Y = synth.shape_pair(2, 6000, 5000, config_index=23)
+    x, y, full = _run(cd, X, Y, tau=0.01)
+    parts = np.zeros((2, 4))
+    for (q0, q1), (r0, r1) in (((0, 2500), (0, 1)), ((2500, 6000), (1, 5000))):
+        out = cd.forward(x, y, tau=0.01, q_slice=(q0, q1), r_slice=(r0, r1))
+        torch.cuda.synchronize()
+        o = [t.cpu().numpy() for t in out]
+        np.testing.assert_array_equal(o[0], full[0][:, q0:q1])
+        np.testing.assert_array_equal(o[1], full[1][:, q0:q1])
+        np.testing.assert_array_equal(o[2], full[2][:, r0:r1])
+        np.testing.assert_array_equal(o[3], full[3][:, r0:r1])
+        parts += o[4]
+    np.testing.assert_allclose(parts, full[4], rtol=1e-12)
+    np.testing.assert_array_equal(parts[:, 2:], full[4][:, 2:])
+
+
+def test_backward_slices_match_full(cd):
+    X, Y = synth.shape_pair(2, 3000, 2500, config_index=24)
+    x, y, (d_xy, i_xy, d_yx, i_yx, _) = _run(cd, X, Y)
+    ixy, iyx = torch.from_numpy(i_xy).cuda(), torch.from_numpy(i_yx).cuda()
+    gx, gy = cd.backward(x, y, ixy, iyx, g_scalar=0.5, h_scalar=0.25)
+    sx, sy = cd.backward(x, y, ixy, iyx, g_scalar=0.5, h_scalar=0.25, q_slice=(1000, 2000), r_slice=(7, 2500))
+    np.testing.assert_array_equal(sx.cpu().numpy(), gx.cpu().numpy()[:, 1000:2000])
+    np.testing.assert_array_equal(sy.cpu().numpy(), gy.cpu().numpy()[:, 7:2500])
+
+
+def test_vjp_linearity_bit_exact(cd):
+    X, Y = synth.shape_pair(1, 4000, 3000, config_index=25)
+    x, y, (d_xy, i_xy, d_yx, i_yx, _) = _run(cd, X, Y)
+    rng = np.random.default_rng(1)
+    g = torch.from_numpy(rng.normal(size=(1, 4000)).astype(np.float32)).cuda()
+    h = torch.from_numpy(rng.normal(size=(1, 3000)).astype(np.float32)).cuda()
+    ixy, iyx = torch.from_numpy(i_xy).cuda(), torch.from_numpy(i_yx).cuda()
+    a = cd.backward(x, y, ixy, iyx, g, h)
+    b = cd.backward(x, y, ixy, iyx, 2 * g, 2 * h)
+    assert torch.equal(b[0], 2 * a[0]) and torch.equal(b[1], 2 * a[1])
+
+
+# ------------------------------------------------------------------------------ API layers
+def test_fscore_from_distances_matches_fused(cd):
+    X, Y = synth.shape_pair(4, 3000, 3500, config_index=26)
+    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
+    F, P, R = cd.fscore_from_distances(torch.from_numpy(d_xy).cuda(), torch.from_numpy(d_yx).cuda(), 0.01)
+    _, _, F2, P2, R2 = cd.finalize(torch.from_numpy(part).cuda(), 3000, 3500)
+    torch.cuda.synchronize()
+    assert torch.equal(F, F2) and torch.equal(P, P2) and torch.equal(R, R2)
+    ref = oracle.fscore(d_xy, d_yx, 0.01)
+    np.testing.assert_allclose(F.cpu().numpy(), ref["fscore"], rtol=RTOL)
+
+
+def test_step_host_matches_device_path(cd):
+    X, Y = synth.shape_pair(2, 2048, 1536, config_index=27)
+    out = cd.step_host(cd.pinned_copy(X).numpy(), cd.pinned_copy(Y).numpy(), tau=0.01)
+    ref = oracle.chamfer(X, Y, tau=0.01)
+    assert abs(float(out["loss"][0]) - ref["loss"]) <= RTOL * ref["loss"]
+    np.testing.assert_allclose(out["fscore"].numpy(), ref["fscore"], rtol=RTOL)
+    x, y, (d_xy, i_xy, d_yx, i_yx, _) = _run(cd, X, Y)
+    gx, gy = cd.backward(x, y, torch.from_numpy(i_xy).cuda(), torch.from_numpy(i_yx).cuda(),
+                         g_scalar=np.float32(1.0 / (2 * 2048)), h_scalar=np.float32(1.0 / (2 * 1536)))
+    np.testing.assert_array_equal(out["grad_x"].numpy(), gx.cpu().numpy())
+    np.testing.assert_array_equal(out["grad_y"].numpy(), gy.cpu().numpy())
+
+
+def test_autograd_loss_and_grad(cd):
+    X, Y = synth.shape_pair(2, 1500, 1700, config_index=28)
+    x = torch.from_numpy(X).cuda().requires_grad_(True)
+    y = torch.from_numpy(Y).cuda().requires_grad_(True)
+    loss = cd.chamfer(x, y, 0.5, 2.0)
+    loss.backward()
+    ref = oracle.chamfer(X, Y, 0.5, 2.0)
+    assert abs(loss.item() - ref["loss"]) <= RTOL * ref["loss"]
+    gxr, gyr, sx, sy = oracle.loss_grad(X, Y, ref["idx_xy"], ref["idx_yx"], 0.5, 2.0)
+    gate_grad(x.grad.cpu().numpy(), gxr, sx)
+    gate_grad(y.grad.cpu().numpy(), gyr, sy)
+
+
+def test_errors_raise(cd):
+    from paper_1911_05063_b200._lib import CdError
+    x = torch.zeros((1, 0, 3), device="cuda")
+    y = torch.zeros((1, 4, 3), device="cuda")
+    with pytest.raises(CdError):
+        cd.forward(x, y)
+    with pytest.raises(TypeError):
+        cd.forward(torch.zeros((1, 4, 3)), y)   # CPU tensor: no fallback
