@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py — Chamfer fwd+bwd point-pairs/s on B200 (BASELINE.json metric), one JSON line.
+
+A step is one pass of the whole hot path: cd_forward (both NN
+directions + F-score hit counting at tau) -> [all-reduce of the B x 4 partials when N > 1] ->
+cd_finalize (CD_b, loss, F) -> cd_backward of the loss (argmin fixed), all through the C ABI.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Default workload: config c3 (B=32, N=M=16,384, F-score at tau=0.01) — the smallest BASELINE.json
+config that exercises every §8.a row (c2 has no F-score) and one the forward roofline is judged on
+(BASELINE.md §3).  --gpus N > 1 (under torchrun) shards batches (weak scaling: each rank runs the
+full c3 batch of 32 on its own batch elements; the loss is combined by one NCCL all-reduce); with
+--config c5 it shards query rows (strong scaling, target broadcast).  Inputs are seeded synthetic
+ShapeNet-like clouds.  Timing: W untimed warm-up steps; K timed steps, each
+bracketed by CUDA events on the launching stream with an L2 flush (256 MiB write) between steps
+outside the events; barrier + synchronize on both sides; max over ranks.
+
+--impl reference times the CPU oracle (oracle/, fp64 brute force) on the host cores on bounded
+row samples of the same workload (the tier's reference arm; there is no installable reference).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1911_05063_b200 import synth  # noqa: E402
+
+METRIC = "Chamfer fwd+bwd point-pairs/sec at 1/2/4/8 B200; % of FP32 FMA peak"
+UNIT = "directed point-pairs/s"
+FP32_OPS_PER_PAIR = 6        # 3 FADD + 1 FMUL + 2 FFMA per directed pair
+FLOPS_PER_PAIR = 8           # the same counting an FMA as 2 flops
+SM_MAX_MHZ_FALLBACK = 1965.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline oracle sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--quiet", action="store_true")
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        loaded = [s for s in sm if mx is None or s >= 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------------------------------------ dist
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------------------ oracle timing
+def oracle_sample(X, Y, budget_s: float, min_rows: int = 8):
+    """Time the fp64 oracle brute force on row samples of both directions (bounded, ~budget_s).
+    Returns (pairs/s, cores, description).  Rows are spread uniformly over all batch elements."""
+    import oracle
+    B, N, _ = X.shape
+    M = Y.shape[1]
+    threads = oracle.max_threads()
+    # calibrate on a small sample
+    rows = max(min_rows, threads * 32)
+    t0 = time.perf_counter()
+    oracle.nn(X, Y, rows=np.linspace(0, B * N - 1, rows).astype(np.int64))
+    dt = max(time.perf_counter() - t0, 1e-4)
+    rate = rows * M / dt
+    per_dir_pairs = max(budget_s * rate / 2, rows * M)
+    rx = int(min(B * N, max(min_rows, per_dir_pairs // M)))
+    ry = int(min(B * M, max(min_rows, per_dir_pairs // N)))
+    rows_x = np.linspace(0, B * N - 1, rx).astype(np.int64)
+    rows_y = np.linspace(0, B * M - 1, ry).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.nn(X, Y, rows=rows_x)
+    oracle.nn(Y, X, rows=rows_y)
+    dt = time.perf_counter() - t0
+    pairs = rx * M + ry * N
+    desc = (f"fp64 brute-force oracle (oracle/chamfer_oracle.c, OpenMP) on {rx} X rows x {M} targets + {ry} Y rows "
+            f"x {N} targets ({pairs:.3g} directed pairs, {dt:.1f} s) of the same workload; backward O(N+M) omitted")
+    return pairs / dt, threads, desc, dt
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    c = synth.CONFIGS[args.config]
+    X, Y = synth.config_inputs(args.config)
+    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    vals = []
+    for k in range(args.warmup + args.steps):
+        v, cores, desc, dt = oracle_sample(X, Y, budget)
+        if k >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    B, N, M = c["B"], c["N"], c["M"]
+    pairs = 2 * B * N * M
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": pairs / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": c["desc"], "B": B, "N": N, "M": M, "tau": c["tau"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------ ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1911_05063_b200 import api as cd
+    from paper_1911_05063_b200 import distributed as pdist
+    from paper_1911_05063_b200 import _lib
+
+    rank, world, local = dist_env()
+    if args.gpus != world and world > 1:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+    c = synth.CONFIGS[args.config]
+    B, N, M, tau = c["B"], c["N"], c["M"], c["tau"]
+    query_sharded = args.config == "c5" and world > 1
+    if query_sharded:
+        B_local, b0, B_global = B, 0, B
+        X, Y = synth.config_inputs(args.config) if rank == 0 else (np.empty((B, N, 3), np.float32),
+                                                                    np.empty((B, M, 3), np.float32))
+        scaling = "strong"
+    else:
+        B_local, b0, B_global = B, rank * B, B * world
+        X, Y = synth.config_inputs(args.config, b0=b0, B=B_local)
+        scaling = "weak"
+    x = torch.from_numpy(X).to(dev)
+    y = torch.from_numpy(Y).to(dev)
+    w1 = w2 = 1.0
+    pairs_total = 2 * B_global * N * M           # directed pairs of the whole job per step
+    # the fused kernel evaluates each distance once for both directions: B*N*M evaluations per launch
+    evals_fwd_launch = (B * N * M) // (world if query_sharded else 1)
+
+    def step():
+        if query_sharded:
+            pdist.broadcast_clouds(x, y, src=0)
+            return pdist.query_sharded_step(cd, x, y, tau=tau, w1=w1, w2=w2)
+        return pdist.batch_sharded_step(cd, x, y, B_global, b0, tau=tau, w1=w1, w2=w2)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for a, b in fev:   # materialise the cudaEvent handles (torch creates them lazily); libcd re-records them
+        a.record()
+        b.record()
+    sampler = ClockSampler(local) if not args.no_clocks else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(K):
+        flush.fill_(k & 0xFF)                     # L2 flush, outside the timed events
+        cd.set_profile_events(*fev[k])
+        ev[k][0].record()
+        out = step()
+        ev[k][1].record()
+    cd.set_profile_events(None, None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    fwd_ms = [a.elapsed_time(b) for a, b in fev]
+    tot = torch.tensor([sum(step_ms), sum(fwd_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = tot[0].item() / K
+    fwd_kernel_ms = tot[1].item() / K
+    value = pairs_total / (ms_per_step * 1e-3)
+    loss = float(out["loss"].item())
+
+    # ---------------------------------------------------------------- e2e through host buffers
+    e2e = None
+    if not args.no_e2e:
+        if query_sharded:
+            e2e = {"value": None, "unit": UNIT, "note": "query-sharded e2e not measured (clouds originate on rank 0)"}
+        else:
+            xh = cd.pinned_copy(X)
+            yh = cd.pinned_copy(Y)
+            outs = dict(loss=cd.pinned_empty((1,)), fscore=cd.pinned_empty((B_local,)), grad_x=None, grad_y=None)
+            lib = _lib.load()
+            ws = cd.workspace(_lib.CD_OP_STEP, B_local, N, M, dev)
+            import ctypes
+
+            def e2e_step():
+                _lib.check(lib.cd_step_host(ctypes.c_void_p(xh.data_ptr()), ctypes.c_void_p(yh.data_ptr()), B_local,
+                                            N, M, float(tau if tau is not None else -1.0), w1, w2,
+                                            ctypes.c_void_p(outs["loss"].data_ptr()),
+                                            ctypes.c_void_p(outs["fscore"].data_ptr()) if tau is not None else None,
+                                            None, None, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            for _ in range(max(1, args.warmup)):
+                e2e_step()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+            for k in range(K):
+                flush.fill_(k & 0xFF)
+                eev[k][0].record()
+                e2e_step()
+                eev[k][1].record()
+            torch.cuda.synchronize()
+            et = torch.tensor([sum(a.elapsed_time(b) for a, b in eev)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.barrier()
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            e2e_ms = et.item() / K
+            e2e = {"value": pairs_total / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                   "h2d_bytes_per_step": int(X.nbytes + Y.nbytes),
+                   "d2h_bytes_per_step": int(4 + (4 * B_local if tau is not None else 0)),
+                   "api": "cd_step_host (pinned host clouds -> H2D -> forward+F -> finalize -> backward -> D2H loss, F)"}
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_max = (clocks or {}).get("sm_max_mhz") or SM_MAX_MHZ_FALLBACK
+    peak_ops = sms * 128 * sm_max * 1e6 / 1e12      # FP32-pipe lane ops/s, T
+    achieved_ops = FP32_OPS_PER_PAIR * evals_fwd_launch / (fwd_kernel_ms * 1e-3) / 1e12
+    roofline = {
+        "bound": "alu", "kernel": "nn_fused_kernel", "unit": "Tops/s (FP32-pipe lane ops: FADD/FMUL/FFMA = 1)",
+        "achieved": achieved_ops, "peak": peak_ops, "frac": achieved_ops / peak_ops,
+        "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz (max SM clock); DESIGN.md §7",
+        "algorithmic": (f"{FP32_OPS_PER_PAIR} FP32-pipe ops per distance evaluation x {evals_fwd_launch} evaluations "
+                        "per launch (B*N*M: each distance serves both directions)"),
+        "kernel_ms": fwd_kernel_ms, "kernel_share_of_step": fwd_kernel_ms / ms_per_step,
+        "traffic": None,
+        "flops_view": {"achieved_tflops": FLOPS_PER_PAIR * evals_fwd_launch / (fwd_kernel_ms * 1e-3) / 1e12,
+                       "peak_tflops": 2 * peak_ops},
+    }
+    if clocks and clocks.get("sm_mhz"):
+        roofline["frac_at_sampled_clock"] = achieved_ops / (sms * 128 * clocks["sm_mhz"] * 1e6 / 1e12)
+
+    # ---------------------------------------------------------------- cpu baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, desc, dt = oracle_sample(X, Y, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+    launches = cd.launch_count(_lib.CD_OP_STEP, B_local, N, M)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded ShapeNet-like deformed-icosphere surface samples, DESIGN.md §5)",
+            "config": {"workload": args.config, "desc": c["desc"], "global_batch": B_global, "B_per_rank": B_local,
+                       "N": N, "M": M, "tau": tau,
+                       "parallelism": (f"query-sharded x{world}" if query_sharded else f"batch-sharded x{world}"),
+                       "l2": "flushed between timed steps (256 MiB write outside the step events)"},
+            # north-star "effective" view: directed pairs/s x 6 ops / FP32-pipe peak per GPU; can exceed 100
+            # because the fused kernel evaluates each distance once for both directions
+            "pct_fp32_fma_peak_effective": 100.0 * FP32_OPS_PER_PAIR * pairs_total / world / (ms_per_step * 1e-3) /
+                                           (sms * 128 * sm_max * 1e6),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * K,
+            "gpu_launches_per_step": launches,
+            "clocks": clocks,
+            "loss": loss,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

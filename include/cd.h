@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define CD_ABI_VERSION 1
+#define CD_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define CD_API __attribute__((visibility("default")))
@@ -86,6 +86,30 @@ CD_API cd_status cd_forward(const float* x, const float* y, int B, int N, int M,
                      float* d_xy, int32_t* idx_xy, float* d_yx, int32_t* idx_yx,
                      double* partials, float tau,
                      void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_forward_rows / cd_forward_cols — the forward split for query sharding: the fused
+ * kernel evaluates every distance once for both directions, so a rank that owns X rows [q0, q1)
+ * gets (a) the final d_xy / idx_xy for those rows and (b) for EVERY Y point a column key
+ *     colkeys[b*M + j] = (float bits of min_{i in [q0,q1)} ||x_i - y_j||^2) << 32 | (first row of the
+ *                        lowest 16-row group attaining it)        (int64, always >= 0)
+ * or INT64_MAX when no row contributed.  Keys from several row slices combine with an element-wise
+ * MIN (e.g. an all-reduce MIN over ranks): the minimum key encodes the minimum distance and the
+ * lowest row group.  cd_forward_cols then turns reduced keys into d_yx / idx_yx for Y rows [r0, r1)
+ * (re-evaluating the winning group's 16 rows with the same fp32 ops, lowest index).
+ *   cd_forward_rows: d_xy, idx_xy [B x (q1-q0)]; colkeys [B x M] (written); partials [B x 4] (may be
+ *     NULL): writes columns 0 and 2 only (sum d_xy over the slice, hits_xy).  Requires q0 < q1.
+ *   cd_forward_cols: colkeys [B x M] (read); d_yx, idx_yx [B x (r1-r0)]; partials: writes columns 1
+ *     and 3 only.  Requires r0 < r1.
+ * Results are bit-identical to cd_forward on the full problem.
+ */
+CD_API cd_status cd_forward_rows(const float* x, const float* y, int B, int N, int M, int q0, int q1,
+                          float* d_xy, int32_t* idx_xy, int64_t* colkeys, double* partials, float tau,
+                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
+CD_API cd_status cd_forward_cols(const float* x, const float* y, int B, int N, int M,
+                          const int64_t* colkeys, int r0, int r1, float* d_yx, int32_t* idx_yx,
+                          double* partials, float tau,
+                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
 
 /*
  * cd_finalize — per-batch Chamfer, batch loss and F-score from the partials.
@@ -159,6 +183,22 @@ CD_API int cd_abi_version(void);                 /* == CD_ABI_VERSION */
  * independent of the tiling.  Returns the previous value.
  */
 CD_API int cd_set_forward_splits(int splits);
+
+/*
+ * Measurement hook: when start/stop are non-NULL cudaEvent_t handles, every subsequent cd_forward
+ * on the calling thread records `start` immediately before and `stop` immediately after its
+ * nearest-neighbour kernel (nn_fwd_kernel), on the call's stream, so a benchmark can time the
+ * dominant kernel alone.  Pass NULL, NULL to disable.
+ */
+CD_API void cd_set_profile_events(void* start, void* stop);
+
+/*
+ * Test hook: forward kernel selection for cd_forward on the calling thread.  0 = automatic (the
+ * fused bidirectional kernel for full problems, the per-direction kernel for query slices),
+ * 1 = always the per-direction kernel, 2 = automatic (reserved).  Returns the previous value.
+ * Both kernels produce bit-identical outputs.
+ */
+CD_API int cd_set_forward_mode(int mode);
 
 #ifdef __cplusplus
 }

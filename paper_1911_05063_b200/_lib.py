@@ -39,6 +39,10 @@ _SIGS = {
     "cd_last_error_string": ([], ctypes.c_char_p),
     "cd_abi_version": ([], i32),
     "cd_set_forward_splits": ([i32], i32),
+    "cd_set_profile_events": ([vp, vp], None),
+    "cd_set_forward_mode": ([i32], i32),
+    "cd_forward_rows": ([vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, f32, vp, sz, vp], i32),
+    "cd_forward_cols": ([vp, vp, i32, i32, i32, vp, i32, i32, vp, vp, vp, f32, vp, sz, vp], i32),
 }
 
 
@@ -68,7 +72,7 @@ def load():
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res
-            if lib.cd_abi_version() != 1:
+            if lib.cd_abi_version() != 2:
                 raise RuntimeError("libcd ABI version mismatch")
             _lib = lib
     return _lib

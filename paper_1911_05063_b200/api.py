@@ -80,6 +80,58 @@ def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=
     return d_xy, i_xy, d_yx, i_yx, part
 
 
+def set_forward_mode(mode: int) -> int:
+    """Test hook: 0 = automatic (fused bidirectional kernel for full problems), 1 = per-direction
+    kernel always.  Returns the previous value."""
+    return int(_lib.load().cd_set_forward_mode(int(mode)))
+
+
+COLKEY_EMPTY = (1 << 63) - 1
+
+
+def forward_rows(x: torch.Tensor, y: torch.Tensor, q_slice, tau: float | None = None, partials=None):
+    """cd_forward_rows: X rows q_slice fully + column keys for every Y point (query sharding).
+
+    Returns (d_xy, idx_xy, colkeys[B,M] int64, partials[B,4] fp64 with columns 0 and 2 set)."""
+    x = _check_cloud(x, "x")
+    y = _check_cloud(y, "y")
+    B, N, _ = x.shape
+    M = y.shape[1]
+    q0, q1 = q_slice
+    dev = x.device
+    d_xy = torch.empty((B, q1 - q0), dtype=torch.float32, device=dev)
+    i_xy = torch.empty((B, q1 - q0), dtype=torch.int32, device=dev)
+    keys = torch.empty((B, M), dtype=torch.int64, device=dev)
+    if partials is None:
+        partials = torch.zeros((B, 4), dtype=torch.float64, device=dev)
+    ws = workspace(_lib.CD_OP_FORWARD, B, N, M, dev)
+    check(_lib.load().cd_forward_rows(_ptr(x), _ptr(y), B, N, M, q0, q1, _ptr(d_xy), _ptr(i_xy), _ptr(keys),
+                                      _ptr(partials), float(-1.0 if tau is None else tau), _ptr(ws), ws.numel(),
+                                      _stream()))
+    return d_xy, i_xy, keys, partials
+
+
+def forward_cols(x: torch.Tensor, y: torch.Tensor, colkeys: torch.Tensor, r_slice, tau: float | None = None,
+                 partials=None):
+    """cd_forward_cols: resolve Y rows r_slice from (reduced) column keys.  Returns (d_yx, idx_yx,
+    partials) with partials columns 1 and 3 set."""
+    x = _check_cloud(x, "x")
+    y = _check_cloud(y, "y")
+    B, N, _ = x.shape
+    M = y.shape[1]
+    r0, r1 = r_slice
+    dev = x.device
+    d_yx = torch.empty((B, r1 - r0), dtype=torch.float32, device=dev)
+    i_yx = torch.empty((B, r1 - r0), dtype=torch.int32, device=dev)
+    if partials is None:
+        partials = torch.zeros((B, 4), dtype=torch.float64, device=dev)
+    ws = workspace(_lib.CD_OP_FORWARD, B, N, M, dev)
+    check(_lib.load().cd_forward_cols(_ptr(x), _ptr(y), B, N, M, _ptr(colkeys.contiguous()), r0, r1, _ptr(d_yx),
+                                      _ptr(i_yx), _ptr(partials), float(-1.0 if tau is None else tau), _ptr(ws),
+                                      ws.numel(), _stream()))
+    return d_yx, i_yx, partials
+
+
 def finalize(partials: torch.Tensor, N: int, M: int, w1: float = 1.0, w2: float = 1.0):
     """cd_finalize: returns (cd_per_batch[B], loss[1], fscore[B], precision[B], recall[B])."""
     B = partials.shape[0]
@@ -206,3 +258,9 @@ def chamfer(x: torch.Tensor, y: torch.Tensor, w1: float = 1.0, w2: float = 1.0) 
 
 def launch_count(op: int, B: int, N: int, M: int) -> int:
     return int(_lib.load().cd_launch_count(op, B, N, M))
+
+
+def set_profile_events(start=None, stop=None):
+    """Record torch.cuda.Events around the nn_fwd_kernel of subsequent forwards (None disables)."""
+    _lib.load().cd_set_profile_events(ctypes.c_void_p(start.cuda_event) if start is not None else None,
+                                      ctypes.c_void_p(stop.cuda_event) if stop is not None else None)

@@ -13,6 +13,13 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_forced_splits = 0;
+thread_local int g_forward_mode = 0;  // 0 auto (fused for full problems), 1 unfused, 2 fused
+
+int auto_mode(int N, int M, int q0, int q1, int r0, int r1) {
+    const bool full = q0 == 0 && q1 == N && r0 == 0 && r1 == M;
+    if (g_forward_mode == 1 || !full) return cdk::kUnfused;
+    return cdk::kFusedFull;
+}
 
 cd_status fail(cd_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 cd_status fail(cd_status s, const char* fmt, ...) {
@@ -54,9 +61,17 @@ cd_status check_device() {
 }
 
 size_t forward_ws(int B, int N, int M, int q0, int q1, int r0, int r1) {
+    // large enough for either forward kernel (the mode is chosen per call)
+    cdk::FwdPlan p, u;
+    cdk::plan_forward(p, cdk::kFusedFull, B, N, M, q0, q1, r0, r1, g_forced_splits);
+    cdk::plan_forward(u, cdk::kUnfused, B, N, M, q0, q1, r0, r1, g_forced_splits);
+    return std::max(p.bytes, u.bytes);
+}
+
+int fwd_launches(int B, int N, int M) {
     cdk::FwdPlan p;
-    cdk::plan_forward(p, B, N, M, q0, q1, r0, r1, g_forced_splits);
-    return p.bytes;
+    cdk::plan_forward(p, auto_mode(N, M, 0, N, 0, M), B, N, M, 0, N, 0, M, g_forced_splits);
+    return cdk::forward_launches(p);
 }
 
 // cd_step_host workspace: staging of x, y, outputs of forward, partials/loss/fscore, grads, plus
@@ -111,6 +126,11 @@ const char* cd_status_string(cd_status s) {
 
 const char* cd_last_error_string(void) { return g_err.c_str(); }
 
+void cd_set_profile_events(void* start, void* stop) {
+    cdk::g_prof_start = static_cast<cudaEvent_t>(start);
+    cdk::g_prof_stop = static_cast<cudaEvent_t>(stop);
+}
+
 int cd_set_forward_splits(int splits) {
     int old = g_forced_splits;
     g_forced_splits = splits > 0 ? splits : 0;
@@ -138,10 +158,10 @@ int cd_launch_count(int op, int B, int N, int M) {
     cdk::BwdPlan bp;
     cdk::plan_backward(bp, B, N, M, 0, N, 0, M);
     switch (op) {
-        case CD_OP_FORWARD: return cdk::kForwardLaunches;
+        case CD_OP_FORWARD: return fwd_launches(B, N, M);
         case CD_OP_FSCORE: return cdk::kFscoreLaunches;
         case CD_OP_BACKWARD: return cdk::backward_launches(bp);
-        case CD_OP_STEP: return cdk::kForwardLaunches + 1 + cdk::backward_launches(bp);
+        case CD_OP_STEP: return fwd_launches(B, N, M) + 1 + cdk::backward_launches(bp);
     }
     return 0;
 }
@@ -161,7 +181,7 @@ cd_status cd_forward(const float* x, const float* y, int B, int N, int M, int q0
     if (!aligned(x, 4) || !aligned(y, 4)) return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte aligned");
     if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
     cdk::FwdPlan p;
-    cdk::plan_forward(p, B, N, M, q0, q1, r0, r1, g_forced_splits);
+    cdk::plan_forward(p, auto_mode(N, M, q0, q1, r0, r1), B, N, M, q0, q1, r0, r1, g_forced_splits);
     if (workspace_bytes < p.bytes)
         return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
     s = check_device();
@@ -173,7 +193,76 @@ cd_status cd_forward(const float* x, const float* y, int B, int N, int M, int q0
     o.idx[1] = idx_yx;
     o.partials = partials;
     o.tau = tau;
+    o.colkey = nullptr;
     return cuda_status(cdk::launch_forward(p, x, y, o, workspace, static_cast<cudaStream_t>(stream)), "cd_forward");
+}
+
+cd_status cd_forward_rows(const float* x, const float* y, int B, int N, int M, int q0, int q1, float* d_xy,
+                          int32_t* idx_xy, int64_t* colkeys, double* partials, float tau, void* workspace,
+                          size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x || !y || !workspace || !colkeys) return fail(CD_ERR_INVALID_VALUE, "null x, y, colkeys or workspace");
+    if (q0 < 0 || q1 <= q0 || q1 > N) return fail(CD_ERR_INVALID_VALUE, "bad row slice [%d,%d) of N=%d", q0, q1, N);
+    if (!d_xy || !idx_xy) return fail(CD_ERR_INVALID_VALUE, "null d_xy / idx_xy");
+    if (tau != tau) return fail(CD_ERR_INVALID_VALUE, "tau is NaN");
+    if (!aligned(x, 4) || !aligned(y, 4) || !aligned(colkeys, 8))
+        return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte and colkeys 8-byte aligned");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    cdk::FwdPlan p;
+    cdk::plan_forward(p, cdk::kFusedRows, B, N, M, q0, q1, 0, 0, g_forced_splits);
+    if (workspace_bytes < p.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    cdk::FwdOutputs o;
+    o.d[0] = d_xy;
+    o.d[1] = nullptr;
+    o.idx[0] = idx_xy;
+    o.idx[1] = nullptr;
+    o.partials = partials;
+    o.tau = tau;
+    o.colkey = reinterpret_cast<long long*>(colkeys);
+    return cuda_status(cdk::launch_forward(p, x, y, o, workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_forward_rows");
+}
+
+cd_status cd_forward_cols(const float* x, const float* y, int B, int N, int M, const int64_t* colkeys, int r0,
+                          int r1, float* d_yx, int32_t* idx_yx, double* partials, float tau, void* workspace,
+                          size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x || !y || !workspace || !colkeys) return fail(CD_ERR_INVALID_VALUE, "null x, y, colkeys or workspace");
+    if (r0 < 0 || r1 <= r0 || r1 > M) return fail(CD_ERR_INVALID_VALUE, "bad column slice [%d,%d) of M=%d", r0, r1, M);
+    if (!d_yx || !idx_yx) return fail(CD_ERR_INVALID_VALUE, "null d_yx / idx_yx");
+    if (tau != tau) return fail(CD_ERR_INVALID_VALUE, "tau is NaN");
+    if (!aligned(x, 4) || !aligned(y, 4) || !aligned(colkeys, 8))
+        return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte and colkeys 8-byte aligned");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    cdk::FwdPlan p;
+    cdk::plan_forward(p, cdk::kFusedCols, B, N, M, 0, 0, r0, r1, g_forced_splits);
+    if (workspace_bytes < p.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    cdk::FwdOutputs o;
+    o.d[0] = nullptr;
+    o.d[1] = d_yx;
+    o.idx[0] = nullptr;
+    o.idx[1] = idx_yx;
+    o.partials = partials;
+    o.tau = tau;
+    o.colkey = const_cast<long long*>(reinterpret_cast<const long long*>(colkeys));
+    return cuda_status(cdk::launch_forward(p, x, y, o, workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_forward_cols");
+}
+
+int cd_set_forward_mode(int mode) {
+    int old = g_forward_mode;
+    g_forward_mode = (mode == 1 || mode == 2) ? mode : 0;
+    return old;
 }
 
 cd_status cd_finalize(const double* partials, int B, int N, int M, float w1, float w2, float* cd_per_batch,

@@ -6,8 +6,15 @@
 
 namespace cdk {
 
+// Forward modes: the unfused kernel searches each direction separately (any query slices); the
+// fused kernel evaluates every distance once for both directions.
+enum FwdMode { kUnfused = 0, kFusedFull = 1, kFusedRows = 2, kFusedCols = 3 };
+// identity of the column-key min: larger than every key (keys are non-negative int64)
+constexpr long long kColKeyEmpty = 0x7fffffffffffffffLL;
+
 // Forward problem description (one direction = "dir": 0 = X queries vs Y targets, 1 = Y vs X).
 struct FwdPlan {
+    int mode;
     int B;
     int npts[2];        // points per batch element of cloud 0 (X: N) and cloud 1 (Y: M)
     int ppad[2];        // padded stride of the packed clouds
@@ -21,7 +28,7 @@ struct FwdPlan {
     int64_t chunk_off[2];
     int64_t chunk_total;
     // workspace carve (byte offsets)
-    size_t off_pack[2], off_best_d, off_best_blk, off_chunk_sum, off_chunk_hits, bytes;
+    size_t off_pack[2], off_best_d, off_best_blk, off_chunk_sum, off_chunk_hits, off_colkey, bytes;
 };
 
 struct FwdOutputs {
@@ -29,12 +36,21 @@ struct FwdOutputs {
     int32_t* idx[2];
     double* partials;   // B x 4 or nullptr
     float tau;          // < 0: no hits
+    long long* colkey;  // fused rows/cols modes: caller's B x M column keys (out / in)
 };
 
-void plan_forward(FwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits);
+void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits);
 cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
                            cudaStream_t st);
-constexpr int kForwardLaunches = 4;
+int forward_launches(const FwdPlan& p);
+int fused_ctas_per_sm();
+int unfused_ctas_per_sm();
+// fused kernels (nn_fused.cu)
+cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey, float* best_d,
+                              int* best_blk, cudaStream_t st);
+cudaError_t launch_col_resolve(const FwdPlan& p, const float4* xp, const float4* yp, const long long* colkey, int r0,
+                               int r1, float* d_out, int32_t* idx_out, double* chunk_sum, int* chunk_hits, float tau,
+                               cudaStream_t st);
 
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.
 size_t fscore_workspace(int B, int N, int M);
@@ -52,13 +68,17 @@ struct BwdPlan {
     int64_t L;          // B*(N+M) key/value pairs
     int64_t kmax;       // number of distinct keys B*(M+N)
     int nbits, npasses, ntiles;
-    size_t off_keys[2], off_vals[2], off_counts, off_offsets, bytes;
+    size_t off_keys[2], off_vals[2], off_counts, off_totals, off_offsets, bytes;
 };
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1);
 cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, const int32_t* idx_xy,
                             const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar,
                             float* grad_x, float* grad_y, void* ws, cudaStream_t st);
 int backward_launches(const BwdPlan& p);
+
+// thread-local measurement hook (cd_set_profile_events)
+extern thread_local cudaEvent_t g_prof_start;
+extern thread_local cudaEvent_t g_prof_stop;
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

@@ -6,7 +6,8 @@
 //                    ascending source order.
 //   radix passes     stable LSD radix sort by key, 8-bit digits, reduce-then-scan:
 //                      radix_hist_kernel   per-tile digit histograms (shared-memory integer adds)
-//                      radix_scan_kernel   exclusive scan of the digit-major histogram table
+//                      radix_rowscan_kernel exclusive scan of each digit's row of tile counts (the
+//                                          digit bases are scanned inside the scatter kernel)
 //                      radix_scatter_kernel stable in-tile ranks (warp match + per-warp counts in
 //                                          element order) -> scatter.  Stability keeps ascending
 //                                          source rows inside every key segment.
@@ -68,40 +69,61 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t
     for (int d = threadIdx.x; d < kDigits; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
 }
 
-// In-place exclusive scan of n values with one CTA of 1024 threads (contiguous segments per thread).
-__global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__ data, int64_t n) {
-    __shared__ uint32_t part[1024];
-    const int64_t per = (n + 1023) / 1024;
-    const int64_t lo = threadIdx.x * per;
-    const int64_t hi = min(lo + per, n);
-    uint32_t s = 0;
-    for (int64_t i = lo; i < hi; ++i) s += data[i];
-    part[threadIdx.x] = s;
+// Block-wide exclusive scan of one value per thread (kSortThreads threads); returns the block total.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
-    // Hillis-Steele inclusive scan over 1024 partial sums
-    for (int o = 1; o < 1024; o <<= 1) {
-        const uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
+    uint32_t before = 0, all = 0;
+    for (int w = 0; w < kSortThreads / 32; ++w) {
+        const uint32_t t = warp_tot[w];
+        before += w < warp ? t : 0u;
+        all += t;
     }
-    uint32_t run = threadIdx.x > 0 ? part[threadIdx.x - 1] : 0u;
-    for (int64_t i = lo; i < hi; ++i) {
-        const uint32_t v = data[i];
-        data[i] = run;
-        run += v;
+    __syncthreads();
+    total = all;
+    return before + incl - v;
+}
+
+// Row-wise exclusive scan of the digit-major histogram table: block d scans counts[d][0..ntiles)
+// in place and writes the row total to totals[d] (coalesced, one CTA per digit).
+__global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* __restrict__ counts, int ntiles,
+                                                                     uint32_t* __restrict__ totals) {
+    __shared__ uint32_t warp_tot[kSortThreads / 32];
+    uint32_t* row = counts + (int64_t)blockIdx.x * ntiles;
+    uint32_t carry = 0;
+    for (int base = 0; base < ntiles; base += kSortThreads) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < ntiles ? row[i] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan(v, warp_tot, tot);
+        if (i < ntiles) row[i] = carry + ex;
+        carry += tot;
     }
+    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int ntiles,
-    const uint32_t* __restrict__ offsets, uint32_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals, uint32_t* __restrict__ kout,
+    uint32_t* __restrict__ vout) {
     constexpr int W = kSortThreads / 32;
+    static_assert(kDigits == kSortThreads, "one digit per thread in the base scan");
     __shared__ uint32_t run[kDigits];
     __shared__ uint32_t wcnt[W][kDigits];
-    for (int d = threadIdx.x; d < kDigits; d += kSortThreads) {
-        run[d] = offsets[(int64_t)d * ntiles + blockIdx.x];
-        for (int w = 0; w < W; ++w) wcnt[w][d] = 0;
+    __shared__ uint32_t warp_tot[W];
+    {
+        // digit base = exclusive scan of the per-digit totals; + this tile's row-scan offset
+        uint32_t tot;
+        const uint32_t base = block_exclusive_scan(totals[threadIdx.x], warp_tot, tot);
+        run[threadIdx.x] = base + offsets[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+        for (int w = 0; w < W; ++w) wcnt[w][threadIdx.x] = 0;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -137,8 +159,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
         }
         __syncthreads();
         if (valid && leader) wcnt[warp][digit] = 0;
-        // the next round's writes to wcnt happen after the next __syncthreads-free match; make the
-        // clears visible before anyone reads them again (next round reads after its first barrier)
+        __syncwarp();  // clears by one lane are ordered before the next round's writes by another lane
     }
 }
 
@@ -274,6 +295,8 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
     }
     p.off_counts = off;
     off = align_up(off + (size_t)kDigits * p.ntiles * 4, 256);
+    p.off_totals = off;
+    off = align_up(off + (size_t)kDigits * 4, 256);
     p.off_offsets = off;
     off = align_up(off + (size_t)(p.kmax + 1) * 4, 256);
     p.bytes = off;
@@ -288,6 +311,7 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
     uint32_t* counts = reinterpret_cast<uint32_t*>(w + p.off_counts);
+    uint32_t* totals = reinterpret_cast<uint32_t*>(w + p.off_totals);
     uint32_t* off = reinterpret_cast<uint32_t*>(w + p.off_offsets);
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sm_count() * 16);
     keys_kernel<<<grid_l, 256, 0, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, keys[0], vals[0]);
@@ -295,9 +319,9 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     for (int pass = 0; pass < p.npasses; ++pass) {
         const int shift = pass * kDigitBits;
         radix_hist_kernel<<<p.ntiles, kSortThreads, 0, st>>>(keys[cur], p.L, shift, p.ntiles, counts);
-        radix_scan_kernel<<<1, 1024, 0, st>>>(counts, (int64_t)kDigits * p.ntiles);
+        radix_rowscan_kernel<<<kDigits, kSortThreads, 0, st>>>(counts, p.ntiles, totals);
         radix_scatter_kernel<<<p.ntiles, kSortThreads, 0, st>>>(keys[cur], vals[cur], p.L, shift, p.ntiles, counts,
-                                                               keys[1 - cur], vals[1 - cur]);
+                                                               totals, keys[1 - cur], vals[1 - cur]);
         cur = 1 - cur;
     }
     const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);

@@ -22,6 +22,9 @@
 
 namespace cdk {
 
+thread_local cudaEvent_t g_prof_start = nullptr;
+thread_local cudaEvent_t g_prof_stop = nullptr;
+
 // ------------------------------------------------------------------------------------------------
 struct PackArgs {
     const float* src[2];
@@ -29,6 +32,8 @@ struct PackArgs {
     int npts[2];
     int ppad[2];
     int B;
+    long long* colkey;   // optional: column keys to reset to the identity of min (fused modes)
+    int64_t ncolkey;
 };
 
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
@@ -50,6 +55,9 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
         }
         a.dst[c][f] = v;
     }
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.ncolkey;
+         e += (int64_t)gridDim.x * blockDim.x)
+        a.colkey[e] = kColKeyEmpty;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -324,6 +332,7 @@ struct PartialsArgs {
     int nchunks[2];
     int64_t chunk_off[2];
     double* partials;
+    int dirmask;   // bit d set: write partials[b][d] and partials[b][2+d]
 };
 
 __global__ void __launch_bounds__(256) partials_kernel(PartialsArgs a) {
@@ -331,6 +340,7 @@ __global__ void __launch_bounds__(256) partials_kernel(PartialsArgs a) {
     __shared__ long long shit[256];
     const int b = blockIdx.x;
     for (int dir = 0; dir < 2; ++dir) {
+        if (!((a.dirmask >> dir) & 1)) continue;
         double s = 0.0;
         long long h = 0;
         const int64_t base = a.chunk_off[dir] + (int64_t)b * a.nchunks[dir];
@@ -405,8 +415,20 @@ static int device_sm_count() {
 // Choose the target-split count S so that (query-tile units x S) CTAs fill the SMs in waves of
 // near-equal work: minimise ceil(U*S / slots) * (Mt/S + c0), c0 = per-unit overhead in target-
 // equivalents (query load + epilogue).
-static int choose_splits(int64_t units, int mt) {
-    const int64_t slots = (int64_t)device_sm_count() * 4;  // 4 CTAs of 128 threads per SM
+int unfused_ctas_per_sm() {
+    static thread_local int occ = 0;
+    if (occ == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nn_fwd_kernel, kFwdThreads, 0) != cudaSuccess ||
+            occ <= 0) {
+            cudaGetLastError();
+            occ = 4;
+        }
+    }
+    return occ;
+}
+
+static int choose_splits(int64_t units, int mt, int ctas_per_sm) {
+    const int64_t slots = (int64_t)device_sm_count() * ctas_per_sm;
     const double c0 = 96.0;
     const int smax = std::max(1, std::min(64, ceil_div(mt, kTile)));
     int best_s = 1;
@@ -422,7 +444,8 @@ static int choose_splits(int64_t units, int mt) {
     return best_s;
 }
 
-void plan_forward(FwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits) {
+void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits) {
+    p.mode = mode;
     p.B = B;
     p.npts[0] = N;
     p.npts[1] = M;
@@ -435,9 +458,11 @@ void plan_forward(FwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r
         p.ppad[d] = ceil_div(p.npts[d], kPad) * kPad;
         const int slen = p.qhi[d] - p.qlo[d];
         p.qtiles[d] = slen > 0 ? ceil_div(slen, kQTile) : 0;
+        if (mode != kUnfused && d == 1) p.qtiles[d] = 0;  // dir 1 comes from the column keys
         units += (int64_t)B * p.qtiles[d];
     }
-    const int S = forced_splits > 0 ? forced_splits : choose_splits(units, std::max(N, M));
+    const int occ = mode == kUnfused ? unfused_ctas_per_sm() : fused_ctas_per_sm();
+    const int S = forced_splits > 0 ? forced_splits : choose_splits(units, std::max(N, M), occ);
     for (int d = 0; d < 2; ++d) {
         const int mt = p.npts[1 - d];
         const int s = std::max(1, std::min(S, ceil_div(mt, kTile)));
@@ -468,6 +493,8 @@ void plan_forward(FwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r
     off = align_up(off + (size_t)std::max<int64_t>(p.chunk_total, 1) * 8, 256);
     p.off_chunk_hits = off;
     off = align_up(off + (size_t)std::max<int64_t>(p.chunk_total, 1) * 4, 256);
+    p.off_colkey = off;
+    if (mode == kFusedFull) off = align_up(off + (size_t)B * M * 8, 256);
     p.bytes = off;
 }
 
@@ -476,6 +503,7 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
     char* w = static_cast<char*>(ws);
     float4* pack0 = reinterpret_cast<float4*>(w + p.off_pack[0]);
     float4* pack1 = reinterpret_cast<float4*>(w + p.off_pack[1]);
+    long long* colkey = p.mode == kFusedFull ? reinterpret_cast<long long*>(w + p.off_colkey) : o.colkey;
     {
         PackArgs a;
         a.src[0] = x;
@@ -487,35 +515,47 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
             a.ppad[d] = p.ppad[d];
         }
         a.B = p.B;
+        const bool init = p.mode == kFusedFull || p.mode == kFusedRows;
+        a.colkey = init ? colkey : nullptr;
+        a.ncolkey = init ? (int64_t)p.B * p.npts[1] : 0;
         const int64_t total = (int64_t)p.B * (p.ppad[0] + p.ppad[1]);
         const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)device_sm_count() * 16);
         pack_kernel<<<grid, 256, 0, st>>>(a);
     }
     float* best_d = reinterpret_cast<float*>(w + p.off_best_d);
     int* best_blk = reinterpret_cast<int*>(w + p.off_best_blk);
-    const int gx = p.qtiles[0] * p.splits[0] + p.qtiles[1] * p.splits[1];
-    if (gx > 0) {
-        FwdArgs a;
-        a.pack[0] = pack0;
-        a.pack[1] = pack1;
-        for (int d = 0; d < 2; ++d) {
-            a.npts[d] = p.npts[d];
-            a.ppad[d] = p.ppad[d];
-            a.qlo[d] = p.qlo[d];
-            a.qhi[d] = p.qhi[d];
-            a.qtiles[d] = p.qtiles[d];
-            a.splits[d] = p.splits[d];
-            a.split_len[d] = p.split_len[d];
-            a.slice_off[d] = p.slice_off[d];
+    if (p.mode == kUnfused) {
+        const int gx = p.qtiles[0] * p.splits[0] + p.qtiles[1] * p.splits[1];
+        if (gx > 0) {
+            FwdArgs a;
+            a.pack[0] = pack0;
+            a.pack[1] = pack1;
+            for (int d = 0; d < 2; ++d) {
+                a.npts[d] = p.npts[d];
+                a.ppad[d] = p.ppad[d];
+                a.qlo[d] = p.qlo[d];
+                a.qhi[d] = p.qhi[d];
+                a.qtiles[d] = p.qtiles[d];
+                a.splits[d] = p.splits[d];
+                a.split_len[d] = p.split_len[d];
+                a.slice_off[d] = p.slice_off[d];
+            }
+            a.slice_total = p.slice_total;
+            a.best_d = best_d;
+            a.best_blk = best_blk;
+            if (g_prof_start) cudaEventRecord(g_prof_start, st);
+            nn_fwd_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
+            if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
         }
-        a.slice_total = p.slice_total;
-        a.best_d = best_d;
-        a.best_blk = best_blk;
-        nn_fwd_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
+    } else if (p.mode == kFusedFull || p.mode == kFusedRows) {
+        cudaError_t e = launch_fused_rows(p, pack0, pack1, colkey, best_d, best_blk, st);
+        if (e != cudaSuccess) return e;
     }
     double* chunk_sum = reinterpret_cast<double*>(w + p.off_chunk_sum);
     int* chunk_hits = reinterpret_cast<int*>(w + p.off_chunk_hits);
-    if (p.chunk_total > 0) {
+    // rows (and, unfused, both directions): merge splits + exact index re-scan + chunk partials
+    const int64_t merge_chunks = p.mode == kUnfused ? p.chunk_total : (int64_t)p.B * p.nchunks[0];
+    if (merge_chunks > 0) {
         MergeArgs a;
         a.pack[0] = pack0;
         a.pack[1] = pack1;
@@ -538,7 +578,13 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
         a.chunk_sum = chunk_sum;
         a.chunk_hits = chunk_hits;
         a.tau2 = o.tau >= 0.f ? (double)o.tau * (double)o.tau : -1.0;
-        nn_merge_kernel<<<(unsigned)p.chunk_total, kMergeThreads, 0, st>>>(a);
+        nn_merge_kernel<<<(unsigned)merge_chunks, kMergeThreads, 0, st>>>(a);
+    }
+    // columns of the fused modes: resolve the Y rows from the (reduced) column keys
+    if ((p.mode == kFusedFull || p.mode == kFusedCols) && p.nchunks[1] > 0) {
+        cudaError_t e = launch_col_resolve(p, pack0, pack1, colkey, p.qlo[1], p.qhi[1], o.d[1], o.idx[1],
+                                           chunk_sum + p.chunk_off[1], chunk_hits + p.chunk_off[1], o.tau, st);
+        if (e != cudaSuccess) return e;
     }
     if (o.partials) {
         PartialsArgs a;
@@ -549,9 +595,19 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
             a.chunk_off[d] = p.chunk_off[d];
         }
         a.partials = o.partials;
+        a.dirmask = p.mode == kFusedRows ? 1 : (p.mode == kFusedCols ? 2 : 3);
         partials_kernel<<<p.B, 256, 0, st>>>(a);
     }
     return cudaGetLastError();
+}
+
+int forward_launches(const FwdPlan& p) {
+    int n = 1;                                                      // pack (+ column-key reset)
+    if (p.mode == kUnfused) n += 2;                                 // nn_fwd + merge
+    if (p.mode == kFusedFull) n += 3;                               // fused + merge + resolve
+    if (p.mode == kFusedRows) n += 2;                               // fused + merge
+    if (p.mode == kFusedCols) n += 1;                               // resolve
+    return n + 1;                                                   // partials
 }
 
 size_t fscore_workspace(int B, int N, int M) {
@@ -587,6 +643,7 @@ cudaError_t launch_fscore(const float* d_xy, const float* d_yx, int B, int N, in
         a.chunk_off[d] = s.chunk_off[d];
     }
     a.partials = partials;
+    a.dirmask = 3;
     partials_kernel<<<B, 256, 0, st>>>(a);
     FinalizeArgs f;
     f.partials = partials;

@@ -1,0 +1,341 @@
+// nn_fused.cu — fused bidirectional forward (built into the hot path):
+// every distance d(x_i, y_j) is evaluated ONCE and feeds both nearest-neighbour directions.
+//
+//   nn_fused_kernel   CTA = 2048 X rows (kR = 16 per thread, packed f32x2) x one split of Y
+//                     (3-stage TMA bulk ring).  Row direction (x -> nearest y): value-only running
+//                     min folded two targets per FMNMX3, argmin block tracked per kBlockK targets
+//                     (as nn_fwd_kernel).  Column direction (y -> nearest x): per target, min over
+//                     the thread's 16 rows (FMNMX3 tree), the warp minimum by one REDUX.MIN on the
+//                     float bits (d >= 0: unsigned order is float order), and the lowest lane
+//                     holding it by ballot; lane t keeps target t of each 32-target block.
+//                     Per smem tile the 4 warps' results are combined in shared memory and one
+//                     packed key (float bits << 32 | first row of the winning thread) per target
+//                     goes to global memory with atomicMin (u64): the minimum key is the minimum
+//                     distance with the lowest row group, independent of CTA order (deterministic).
+//   nn_col_resolve_kernel  per Y row: unpack the key, re-evaluate the winning thread's 16 rows
+//                     with the same .rn ops, keep the lowest row index with d == min (exact).
+//
+// (y - x)^2 == (x - y)^2 bit for bit in IEEE arithmetic (negation is exact), so the column
+// distances equal a direct y -> x evaluation with the fixed op order of DESIGN.md §4.2.
+#include "cd_device.cuh"
+#include "cd_internal.h"
+
+#include <algorithm>
+
+namespace cdk {
+
+struct FusedArgs {
+    const float4* xp;   // packed X (rows)
+    const float4* yp;   // packed Y (targets / columns)
+    int N, M, xpad, ypad;
+    int q0, q1;         // X row slice
+    int qtiles, splits, split_len;
+    int64_t slice_total;  // B * (q1 - q0)
+    float* best_d;      // [splits][B*(q1-q0)]
+    int* best_blk;
+    long long* colkey;  // [B][M], non-negative keys; kColKeyEmpty = none
+};
+
+__global__ void __launch_bounds__(kFwdThreads, 3) nn_fused_kernel(FusedArgs a) {
+    __shared__ __align__(128) float4 sm[kStages][kTile];
+    __shared__ float colv[2][kFwdThreads / 32][kTile];
+    __shared__ unsigned char coll[2][kFwdThreads / 32][kTile];
+    __shared__ __align__(8) u64 full_bar[kStages];
+
+    const int b = blockIdx.y;
+    const int tile = blockIdx.x / a.splits;
+    const int split = blockIdx.x - tile * a.splits;
+    const float4* __restrict__ Q = a.xp + (int64_t)b * a.xpad;
+    const float4* __restrict__ T = a.yp + (int64_t)b * a.ypad;
+    const int j0 = split * a.split_len;
+    const int j1 = min(j0 + a.split_len, a.M);
+    const int ntiles = (j1 - j0 + kTile - 1) / kTile;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int pre = min(kStages, ntiles);
+        for (int k = 0; k < pre; ++k) {
+            mbar_arrive_expect_tx(&full_bar[k], kTile * 16);
+            tma_load_1d(sm[k], T + j0 + (int64_t)k * kTile, kTile * 16, &full_bar[k]);
+        }
+    }
+
+    const int qbase = a.q0 + tile * kQTile + threadIdx.x * kR;  // first row of this thread's group
+    u64 qx[kR / 2], qy[kR / 2], qz[kR / 2];
+#pragma unroll
+    for (int r = 0; r < kR / 2; ++r) {
+        // rows past the slice end duplicate the last row of the slice: same values, higher index,
+        // so they never win a column and their row results are never stored
+        const float4 p0 = Q[min(qbase + 2 * r, a.q1 - 1)];
+        const float4 p1 = Q[min(qbase + 2 * r + 1, a.q1 - 1)];
+        qx[r] = pk2(p0.x, p1.x);
+        qy[r] = pk2(p0.y, p1.y);
+        qz[r] = pk2(p0.z, p1.z);
+    }
+    float best[kR];
+    int blk[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        best[r] = INFINITY;
+        blk[r] = -1;
+    }
+
+    for (int k = 0; k < ntiles; ++k) {
+        const int s = k % kStages;
+        mbar_wait(&full_bar[s], (k / kStages) & 1);
+        const float4* tb = sm[s];
+        float* cv = colv[k & 1][warp];
+        unsigned char* cl = coll[k & 1][warp];
+        const int jt = j0 + k * kTile;
+        for (int kb = 0; kb < kTile; kb += kBlockK) {
+            static_assert(kBlockK == 32, "one column result per lane per block");
+            float old[kR];
+#pragma unroll
+            for (int r = 0; r < kR; ++r) old[r] = best[r];
+            unsigned keep_m = 0x7f800000u, keep_e = 0u;  // this lane's target (kb + lane) results
+#pragma unroll 2
+            for (int jj = 0; jj < kBlockK; jj += 2) {
+                const float4 t0 = tb[kb + jj];
+                const float4 t1 = tb[kb + jj + 1];
+                const u64 t0x = pk2(t0.x, t0.x), t0y = pk2(t0.y, t0.y), t0z = pk2(t0.z, t0.z);
+                const u64 t1x = pk2(t1.x, t1.x), t1y = pk2(t1.y, t1.y), t1z = pk2(t1.z, t1.z);
+                float ca[kR / 2], cb[kR / 2];
+#pragma unroll
+                for (int r = 0; r < kR / 2; ++r) {
+                    u64 dx = sub2(qx[r], t0x), dy = sub2(qy[r], t0y), dz = sub2(qz[r], t0z);
+                    u64 s0 = mul2(dx, dx);
+                    s0 = fma2(dy, dy, s0);
+                    s0 = fma2(dz, dz, s0);
+                    dx = sub2(qx[r], t1x);
+                    dy = sub2(qy[r], t1y);
+                    dz = sub2(qz[r], t1z);
+                    u64 s1 = mul2(dx, dx);
+                    s1 = fma2(dy, dy, s1);
+                    s1 = fma2(dz, dz, s1);
+                    float a0, a1, b0, b1;
+                    upk2(s0, a0, a1);
+                    upk2(s1, b0, b1);
+                    best[2 * r] = fmin3(best[2 * r], a0, b0);      // row mins
+                    best[2 * r + 1] = fmin3(best[2 * r + 1], a1, b1);
+                    ca[r] = fminf(a0, a1);                           // column partials (tree below)
+                    cb[r] = fminf(b0, b1);
+                }
+                // column min over this thread's 16 rows: FMNMX3 tree (depth 2 instead of a chain)
+                const float c0 = fmin3(fmin3(ca[0], ca[1], ca[2]), fmin3(ca[3], ca[4], ca[5]), fminf(ca[6], ca[7]));
+                const float c1 = fmin3(fmin3(cb[0], cb[1], cb[2]), fmin3(cb[3], cb[4], cb[5]), fminf(cb[6], cb[7]));
+                // warp min (REDUX on the bits: d >= 0, so unsigned order == float order, NaN > inf)
+                const unsigned u0 = __float_as_uint(c0), u1 = __float_as_uint(c1);
+                const unsigned m0 = __reduce_min_sync(0xffffffffu, u0);
+                const unsigned m1 = __reduce_min_sync(0xffffffffu, u1);
+                const unsigned e0 = __ballot_sync(0xffffffffu, u0 == m0);  // lanes holding the min
+                const unsigned e1 = __ballot_sync(0xffffffffu, u1 == m1);
+                keep_m = lane == jj ? m0 : keep_m;
+                keep_e = lane == jj ? e0 : keep_e;
+                keep_m = lane == jj + 1 ? m1 : keep_m;
+                keep_e = lane == jj + 1 ? e1 : keep_e;
+            }
+            cv[kb + lane] = __uint_as_float(keep_m);
+            cl[kb + lane] = (unsigned char)(__ffs(keep_e) - 1);  // lowest lane; 255 if none (NaN)
+#pragma unroll
+            for (int r = 0; r < kR; ++r) blk[r] = best[r] < old[r] ? jt + kb : blk[r];
+        }
+        __syncthreads();  // every warp is done with stage s and has written colv[k & 1]
+        if (threadIdx.x == 0 && k + kStages < ntiles) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], kTile * 16);
+            tma_load_1d(sm[s], T + jt + (int64_t)kStages * kTile, kTile * 16, &full_bar[s]);
+        }
+        // combine the 4 warps per target and publish one key per (CTA, target)
+        for (int t = threadIdx.x; t < kTile; t += kFwdThreads) {
+            const int j = jt + t;
+            if (j >= j1) break;
+            float m = colv[k & 1][0][t];
+            int w = 0;
+#pragma unroll
+            for (int ww = 1; ww < kFwdThreads / 32; ++ww) {
+                const float v = colv[k & 1][ww][t];
+                if (v < m || m != m) {  // strict <: the lowest warp keeps ties (NaN never wins)
+                    m = v;
+                    w = ww;
+                }
+            }
+            const unsigned l = coll[k & 1][w][t];
+            if (l < 32u) {
+                const unsigned row0 = (unsigned)(a.q0 + tile * kQTile + (w * 32 + (int)l) * kR);
+                const long long key = (long long)(((unsigned long long)__float_as_uint(m) << 32) | row0);
+                atomicMin(&a.colkey[(int64_t)b * a.M + j], key);  // keys >= 0: signed min == lexicographic
+            }
+        }
+    }
+
+    const int slen = a.q1 - a.q0;
+    const int64_t rowbase = (int64_t)split * a.slice_total + (int64_t)b * slen;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        const int q = qbase + r;
+        if (q < a.q1) {
+            const int64_t o = rowbase + (q - a.q0);
+            a.best_d[o] = best[r];
+            a.best_blk[o] = blk[r];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+struct ResolveArgs {
+    const float4* xp;
+    const float4* yp;
+    int N, M, xpad, ypad;
+    int q0, q1;            // X rows that took part in the column minima
+    int r0, r1;            // Y rows to resolve
+    int B, nchunks;
+    const long long* colkey;
+    float* d_out;          // [B][r1-r0]
+    int32_t* idx_out;
+    double* chunk_sum;     // dir-1 chunk partials
+    int* chunk_hits;
+    double tau2;
+};
+
+__device__ void block_sum_hits_fused(double v, int h, double* out_sum, int* out_hits) {
+    __shared__ double ssum[kMergeThreads / 32];
+    __shared__ int shit[kMergeThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_down_sync(0xffffffffu, v, o);
+        h += __shfl_down_sync(0xffffffffu, h, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        ssum[w] = v;
+        shit[w] = h;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        int t = 0;
+        for (int i = 0; i < kMergeThreads / 32; ++i) {
+            s += ssum[i];
+            t += shit[i];
+        }
+        *out_sum = s;
+        *out_hits = t;
+    }
+}
+
+__global__ void __launch_bounds__(kMergeThreads) nn_col_resolve_kernel(ResolveArgs a) {
+    const int b = blockIdx.x / a.nchunks;
+    const int chunk = blockIdx.x - b * a.nchunks;
+    const int slen = a.r1 - a.r0;
+    const int sj = chunk * kMergeThreads + threadIdx.x;
+    double v = 0.0;
+    int h = 0;
+    if (sj < slen) {
+        const int j = a.r0 + sj;
+        const unsigned long long key = (unsigned long long)a.colkey[(int64_t)b * a.M + j];
+        float m = INFINITY;
+        int idx = -1;
+        if ((long long)key != kColKeyEmpty) {
+            m = __uint_as_float((unsigned)(key >> 32));
+            const int i0 = (int)(unsigned)(key & 0xffffffffull);
+            const float4 t = a.yp[(int64_t)b * a.ypad + j];
+            const float4* X = a.xp + (int64_t)b * a.xpad;
+            const int iend = min(i0 + kR, a.q1);
+            float d[kR];
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                const float4 q = X[min(i0 + r, a.q1 - 1)];
+                d[r] = dist_rn(q.x, q.y, q.z, t.x, t.y, t.z);  // same operand order as the kernel
+            }
+#pragma unroll
+            for (int r = kR - 1; r >= 0; --r)
+                if (i0 + r < iend && d[r] == m) idx = i0 + r;
+            if (idx < 0) m = INFINITY;  // only when every distance was NaN
+        }
+        a.d_out[(int64_t)b * slen + sj] = m;
+        a.idx_out[(int64_t)b * slen + sj] = idx;
+        v = (double)m;
+        h = (a.tau2 >= 0.0 && (double)m <= a.tau2) ? 1 : 0;
+    }
+    double s;
+    int t;
+    block_sum_hits_fused(v, h, &s, &t);
+    if (threadIdx.x == 0) {
+        a.chunk_sum[(int64_t)b * a.nchunks + chunk] = s;
+        a.chunk_hits[(int64_t)b * a.nchunks + chunk] = t;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+int fused_ctas_per_sm() {
+    static thread_local int occ = 0;
+    if (occ == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nn_fused_kernel, kFwdThreads, 0) != cudaSuccess ||
+            occ <= 0) {
+            cudaGetLastError();
+            occ = 3;
+        }
+    }
+    return occ;
+}
+
+cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey, float* best_d,
+                              int* best_blk, cudaStream_t st) {
+    FusedArgs a;
+    a.xp = xp;
+    a.yp = yp;
+    a.N = p.npts[0];
+    a.M = p.npts[1];
+    a.xpad = p.ppad[0];
+    a.ypad = p.ppad[1];
+    a.q0 = p.qlo[0];
+    a.q1 = p.qhi[0];
+    a.qtiles = p.qtiles[0];
+    a.splits = p.splits[0];
+    a.split_len = p.split_len[0];
+    a.slice_total = p.slice_total;
+    a.best_d = best_d;
+    a.best_blk = best_blk;
+    a.colkey = colkey;
+    const int gx = p.qtiles[0] * p.splits[0];
+    if (gx > 0) {
+        if (g_prof_start) cudaEventRecord(g_prof_start, st);
+        nn_fused_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
+        if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_col_resolve(const FwdPlan& p, const float4* xp, const float4* yp, const long long* colkey, int r0,
+                               int r1, float* d_out, int32_t* idx_out, double* chunk_sum, int* chunk_hits, float tau,
+                               cudaStream_t st) {
+    ResolveArgs a;
+    a.xp = xp;
+    a.yp = yp;
+    a.N = p.npts[0];
+    a.M = p.npts[1];
+    a.xpad = p.ppad[0];
+    a.ypad = p.ppad[1];
+    a.q0 = 0;
+    a.q1 = p.npts[0];
+    a.r0 = r0;
+    a.r1 = r1;
+    a.B = p.B;
+    a.nchunks = (r1 - r0 + kMergeThreads - 1) / kMergeThreads;
+    a.colkey = colkey;
+    a.d_out = d_out;
+    a.idx_out = idx_out;
+    a.chunk_sum = chunk_sum;
+    a.chunk_hits = chunk_hits;
+    a.tau2 = tau >= 0.f ? (double)tau * (double)tau : -1.0;
+    if (a.nchunks > 0) nn_col_resolve_kernel<<<p.B * a.nchunks, kMergeThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace cdk

@@ -37,7 +37,7 @@ def test_only_cd_symbols_exported():
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.cd_abi_version() == 1
+    assert lib.cd_abi_version() == 2
     assert lib.cd_status_string(0) == b"CD_OK"
     assert lib.cd_status_string(1) == b"CD_ERR_INVALID_VALUE"
     assert lib.cd_status_string(5) == b"CD_ERR_CUDA"
@@ -53,10 +53,11 @@ def test_workspace_sizes(lib):
 
 
 def test_launch_counts(lib):
-    assert lib.cd_launch_count(0, 32, 16384, 16384) == 4
+    # fused forward: pack + fused + row merge + column resolve + partials
+    assert lib.cd_launch_count(0, 32, 16384, 16384) == 5
     # backward: keys + 3 radix passes x 3 kernels + offsets + grad for 2^20 keys
     assert lib.cd_launch_count(2, 32, 16384, 16384) == 1 + 3 * 3 + 2
-    assert lib.cd_launch_count(3, 32, 16384, 16384) == 4 + 1 + 12
+    assert lib.cd_launch_count(3, 32, 16384, 16384) == 5 + 1 + 12
 
 
 def _forward(lib, B=1, N=8, M=8, q=(0, 8), r=(0, 8), x=4, y=4, ws=256, wsb=1 << 30, tau=-1.0, dxy=64, ixy=64,

@@ -85,6 +85,15 @@ def test_c2_full(cd):
     _full_check(cd, X, Y, tau=0.01)
 
 
+def test_c2_full_per_direction_kernel(cd):
+    X, Y = synth.config_inputs("c2")
+    old = cd.set_forward_mode(1)
+    try:
+        _full_check(cd, X, Y, tau=0.01)
+    finally:
+        cd.set_forward_mode(old)
+
+
 def test_c3_sampled_forward_full_backward(cd):
     X, Y = synth.config_inputs("c3")
     x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
@@ -292,3 +301,51 @@ def test_errors_raise(cd):
         cd.forward(x, y)
     with pytest.raises(TypeError):
         cd.forward(torch.zeros((1, 4, 3)), y)   # CPU tensor: no fallback
+
+
+# ------------------------------------------------------------------------------ fused vs per-direction
+@pytest.mark.parametrize("B,N,M", [(1, 1, 1), (2, 3, 7), (2, 1000, 1024), (3, 2049, 4097), (1, 5000, 1),
+                                   (4, 8192, 3000)])
+def test_fused_equals_unfused_bitwise(cd, B, N, M):
+    X, Y = synth.shape_pair(B, N, M, config_index=40 + N % 7)
+    _, _, fused = _run(cd, X, Y, tau=0.01)
+    old = cd.set_forward_mode(1)
+    try:
+        _, _, unf = _run(cd, X, Y, tau=0.01)
+    finally:
+        cd.set_forward_mode(old)
+    for a, b in zip(fused[:4], unf[:4]):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_allclose(fused[4], unf[4], rtol=1e-12)
+    np.testing.assert_array_equal(fused[4][:, 2:], unf[4][:, 2:])
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_rows_cols_sharding_emulated(cd, world):
+    """Query sharding on one GPU: every 'rank' runs cd_forward_rows on its X slice, the column keys
+    are combined with an element-wise MIN (what the NCCL all-reduce does), each rank resolves its
+    Y slice with cd_forward_cols.  Per-point results must equal the 1-GPU forward bit for bit."""
+    from paper_1911_05063_b200.distributed import shard_range
+    X, Y = synth.shape_pair(2, 5000, 4100, config_index=50)
+    x, y, full = _run(cd, X, Y, tau=0.01)
+    B, N, M = 2, 5000, 4100
+    keys = None
+    rows = []
+    part = torch.zeros((B, 4), dtype=torch.float64, device="cuda")
+    for r in range(world):
+        d, i, k, p = cd.forward_rows(x, y, shard_range(N, r, world), tau=0.01)
+        rows.append((d, i))
+        part += p
+        keys = k if keys is None else torch.minimum(keys, k)
+    cols = []
+    for r in range(world):
+        d, i, p = cd.forward_cols(x, y, keys, shard_range(M, r, world), tau=0.01)
+        cols.append((d, i))
+        part += p
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(torch.cat([d for d, _ in rows], 1).cpu().numpy(), full[0])
+    np.testing.assert_array_equal(torch.cat([i for _, i in rows], 1).cpu().numpy(), full[1])
+    np.testing.assert_array_equal(torch.cat([d for d, _ in cols], 1).cpu().numpy(), full[2])
+    np.testing.assert_array_equal(torch.cat([i for _, i in cols], 1).cpu().numpy(), full[3])
+    np.testing.assert_allclose(part.cpu().numpy(), full[4], rtol=1e-12)
+    np.testing.assert_array_equal(part.cpu().numpy()[:, 2:], full[4][:, 2:])
