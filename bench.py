@@ -200,6 +200,18 @@ def run_reference(args):
         dist.destroy_process_group()
 
 
+def _traffic(kernel, cfg):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(f"{kernel}/{cfg}")
+        return None if e is None else {"bytes_per_launch": e["dram_bytes_per_launch"], "source": "profiles/" + e["source"]}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 # ------------------------------------------------------------------------------------------ ours
 def main():
     args = parse()
@@ -337,7 +349,7 @@ def main():
         "algorithmic": (f"{FP32_OPS_PER_PAIR} FP32-pipe ops per distance evaluation x {evals_fwd_launch} evaluations "
                         "per launch (B*N*M: each distance serves both directions)"),
         "kernel_ms": fwd_kernel_ms, "kernel_share_of_step": fwd_kernel_ms / ms_per_step,
-        "traffic": None,
+        "traffic": _traffic("nn_fused_kernel", args.config),
         "flops_view": {"achieved_tflops": FLOPS_PER_PAIR * evals_fwd_launch / (fwd_kernel_ms * 1e-3) / 1e12,
                        "peak_tflops": 2 * peak_ops},
     }
