@@ -47,7 +47,7 @@ SM_MAX_MHZ_FALLBACK = 1965.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: ~1 s of work per config)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -56,7 +56,13 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise the multi-rank "
+                    "logic when several ranks share one GPU")
     return ap.parse_args()
+
+
+DEFAULT_STEPS = {"c1": 300, "c2": 300, "c3": 300, "c4": 20, "c5": 3}
 
 
 def log(*a):
@@ -215,6 +221,8 @@ def _traffic(kernel, cfg):
 # ------------------------------------------------------------------------------------------ ours
 def main():
     args = parse()
+    if args.steps is None:
+        args.steps = DEFAULT_STEPS[args.config]
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -227,10 +235,15 @@ def main():
     rank, world, local = dist_env()
     if args.gpus != world and world > 1:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; several ranks only share a GPU in the gloo logic check (--dist-backend gloo)
+    gpu = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend, init_method="env://")
     c = synth.CONFIGS[args.config]
     B, N, M, tau = c["B"], c["N"], c["M"], c["tau"]
     query_sharded = args.config == "c5" and world > 1
@@ -267,26 +280,51 @@ def main():
     for a, b in fev:   # materialise the cudaEvent handles (torch creates them lazily); libcd re-records them
         a.record()
         b.record()
-    sampler = ClockSampler(local) if not args.no_clocks else None
+    # single rank: the whole step (all kernels of rows a.1-a.8) is captured once into a CUDA graph and
+    # replayed, so small configs are not bound by host launch overhead
+    graph = None
+    if world == 1 and not args.no_graph:
+        gev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        gev[0].record()
+        gev[1].record()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        cd.set_profile_events(*gev)
+        with torch.cuda.graph(graph):
+            out = step()
+        cd.set_profile_events(None, None)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+    sampler = ClockSampler(gpu) if not args.no_clocks else None
     if sampler:
         sampler.start()
         time.sleep(0.3)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    fwd_ms = []
     for k in range(K):
         flush.fill_(k & 0xFF)                     # L2 flush, outside the timed events
-        cd.set_profile_events(*fev[k])
-        ev[k][0].record()
-        out = step()
-        ev[k][1].record()
+        if graph is not None:
+            ev[k][0].record()
+            graph.replay()
+            ev[k][1].record()
+            ev[k][1].synchronize()                # read the in-graph kernel events of this replay
+            fwd_ms.append(gev[0].elapsed_time(gev[1]))
+        else:
+            cd.set_profile_events(*fev[k])
+            ev[k][0].record()
+            out = step()
+            ev[k][1].record()
     cd.set_profile_events(None, None)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    fwd_ms = [a.elapsed_time(b) for a, b in fev]
+    if graph is None:
+        fwd_ms = [a.elapsed_time(b) for a, b in fev]
     tot = torch.tensor([sum(step_ms), sum(fwd_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -371,6 +409,7 @@ def main():
             "config": {"workload": args.config, "desc": c["desc"], "global_batch": B_global, "B_per_rank": B_local,
                        "N": N, "M": M, "tau": tau,
                        "parallelism": (f"query-sharded x{world}" if query_sharded else f"batch-sharded x{world}"),
+                       "launch": "cuda_graph" if graph is not None else "eager",
                        "l2": "flushed between timed steps (256 MiB write outside the step events)"},
             # north-star "effective" view: directed pairs/s x 6 ops / FP32-pipe peak per GPU; can exceed 100
             # because the fused kernel evaluates each distance once for both directions

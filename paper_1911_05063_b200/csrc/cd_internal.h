@@ -67,7 +67,7 @@ struct BwdPlan {
     int q0, q1, r0, r1;
     int64_t L;          // B*(N+M) key/value pairs
     int64_t kmax;       // number of distinct keys B*(M+N)
-    int nbits, npasses, ntiles;
+    int nbits, npasses, digit_bits, ntiles;
     size_t off_keys[2], off_vals[2], off_counts, off_totals, off_offsets, bytes;
 };
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1);
@@ -79,6 +79,17 @@ int backward_launches(const BwdPlan& p);
 // thread-local measurement hook (cd_set_profile_events)
 extern thread_local cudaEvent_t g_prof_start;
 extern thread_local cudaEvent_t g_prof_stop;
+
+// Record a measurement event; inside stream capture it must be an external event-record node so a
+// graph replay re-records it (a plain record during capture only expresses a dependency).
+inline void record_profile_event(cudaEvent_t ev, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+    else
+        cudaEventRecord(ev, st);
+}
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

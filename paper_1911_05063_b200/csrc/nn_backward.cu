@@ -4,7 +4,8 @@
 //   keys_kernel      one (key, value) pair per NN edge: xy edge i -> a_i gets key b*M + a_i,
 //                    yx edge j -> b_j gets key B*M + b*N + b_j; value = the source row.  Built in
 //                    ascending source order.
-//   radix passes     stable LSD radix sort by key, 8-bit digits, reduce-then-scan:
+//   radix passes     stable LSD radix sort by key, digits of <= 11 bits (2 passes up to 2^22
+//                    keys), reduce-then-scan:
 //                      radix_hist_kernel   per-tile digit histograms (shared-memory integer adds)
 //                      radix_rowscan_kernel exclusive scan of each digit's row of tile counts (the
 //                                          digit bases are scanned inside the scatter kernel)
@@ -23,10 +24,10 @@
 namespace cdk {
 
 constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements per tile
-constexpr int kDigitBits = 8;
-constexpr int kDigits = 1 << kDigitBits;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements per tile (512 per warp)
+constexpr int kMaxDigitBits = 11;                     // digits of up to 11 bits: 2 passes cover 2^22 keys
 
 __global__ void __launch_bounds__(256) keys_kernel(const int32_t* __restrict__ idx_xy,
                                                    const int32_t* __restrict__ idx_yx, int B, int N, int M,
@@ -52,21 +53,21 @@ __global__ void __launch_bounds__(256) keys_kernel(const int32_t* __restrict__ i
     }
 }
 
-// counts[digit * ntiles + tile]
+// counts[digit * ntiles + tile]; D = 1 << digit bits (dynamic shared memory: D words)
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t L,
-                                                                  int shift, int ntiles,
+                                                                  int shift, int D, int ntiles,
                                                                   uint32_t* __restrict__ counts) {
-    __shared__ uint32_t hist[kDigits];
-    for (int d = threadIdx.x; d < kDigits; d += kSortThreads) hist[d] = 0;
+    extern __shared__ uint32_t hist[];
+    for (int d = threadIdx.x; d < D; d += kSortThreads) hist[d] = 0;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * kSortTile;
 #pragma unroll 4
     for (int k = 0; k < kSortItems; ++k) {
         const int64_t e = base + (int64_t)k * kSortThreads + threadIdx.x;
-        if (e < L) atomicAdd(&hist[(keys[e] >> shift) & (kDigits - 1)], 1u);  // integer: order-free
+        if (e < L) atomicAdd(&hist[(keys[e] >> shift) & (D - 1)], 1u);  // integer adds: order-free
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < kDigits; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
+    for (int d = threadIdx.x; d < D; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
 }
 
 // Block-wide exclusive scan of one value per thread (kSortThreads threads); returns the block total.
@@ -81,7 +82,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
     if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
     uint32_t before = 0, all = 0;
-    for (int w = 0; w < kSortThreads / 32; ++w) {
+    for (int w = 0; w < kSortWarps; ++w) {
         const uint32_t t = warp_tot[w];
         before += w < warp ? t : 0u;
         all += t;
@@ -95,7 +96,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
 // in place and writes the row total to totals[d] (coalesced, one CTA per digit).
 __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* __restrict__ counts, int ntiles,
                                                                      uint32_t* __restrict__ totals) {
-    __shared__ uint32_t warp_tot[kSortThreads / 32];
+    __shared__ uint32_t warp_tot[kSortWarps];
     uint32_t* row = counts + (int64_t)blockIdx.x * ntiles;
     uint32_t carry = 0;
     for (int base = 0; base < ntiles; base += kSortThreads) {
@@ -109,57 +110,74 @@ __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* _
     if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
+// Stable scatter of one tile.  Warp w owns elements [w*512, (w+1)*512) of the tile (16 rounds of
+// 32), so tile order = (warp, round, lane).  Phase 1: per-warp digit counters in shared memory give
+// every element its rank among equal digits of its warp (warp match; only the warp's own counter row
+// is touched, no block barrier per round).  Phase 2: per digit, exclusive prefix over the warps plus
+// the digit's global base (exclusive scan of the digit totals) plus this tile's row-scan offset.
+// Phase 3: scatter.  Dynamic shared memory: (kSortWarps + 1) * D words.
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
-    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int ntiles,
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int D, int ntiles,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout) {
-    constexpr int W = kSortThreads / 32;
-    static_assert(kDigits == kSortThreads, "one digit per thread in the base scan");
-    __shared__ uint32_t run[kDigits];
-    __shared__ uint32_t wcnt[W][kDigits];
-    __shared__ uint32_t warp_tot[W];
-    {
-        // digit base = exclusive scan of the per-digit totals; + this tile's row-scan offset
-        uint32_t tot;
-        const uint32_t base = block_exclusive_scan(totals[threadIdx.x], warp_tot, tot);
-        run[threadIdx.x] = base + offsets[(int64_t)threadIdx.x * ntiles + blockIdx.x];
-        for (int w = 0; w < W; ++w) wcnt[w][threadIdx.x] = 0;
-    }
-    __syncthreads();
+    extern __shared__ uint32_t smem[];
+    uint32_t* wcnt = smem;                      // [kSortWarps][D]
+    uint32_t* dbase = smem + kSortWarps * D;    // [D]
+    __shared__ uint32_t warp_tot[kSortWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kSortWarps * D; i += kSortThreads) wcnt[i] = 0;
+    // global digit bases: exclusive scan of totals[0..D), each thread owns D/256 consecutive digits
+    {
+        const int per = (D + kSortThreads - 1) / kSortThreads;
+        const int d0 = threadIdx.x * per;
+        uint32_t loc = 0;
+        for (int d = d0; d < min(d0 + per, D); ++d) loc += totals[d];
+        uint32_t tot;
+        uint32_t run = block_exclusive_scan(loc, warp_tot, tot);
+        for (int d = d0; d < min(d0 + per, D); ++d) {
+            dbase[d] = run + offsets[(int64_t)d * ntiles + blockIdx.x];
+            run += totals[d];
+        }
+    }
+    __syncthreads();
     const uint32_t lt_mask = (1u << lane) - 1u;
-    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    const int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * (kSortItems * 32);
+    uint32_t kk[kSortItems], vv[kSortItems], rk[kSortItems];
+    uint32_t* my = wcnt + warp * D;
+#pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
-        const int64_t e = base + (int64_t)k * kSortThreads + threadIdx.x;
+        const int64_t e = wbase + k * 32 + lane;
         const bool valid = e < L;
-        uint32_t key = 0, val = 0;
-        int digit = kDigits;  // invalid lanes use a digit value no valid lane has
-        if (valid) {
-            key = kin[e];
-            val = vin[e];
-            digit = (key >> shift) & (kDigits - 1);
-        }
+        kk[k] = valid ? kin[e] : 0u;
+        vv[k] = valid ? vin[e] : 0u;
+        const int digit = valid ? (int)((kk[k] >> shift) & (D - 1)) : D;  // D: sentinel group
         const uint32_t peers = __match_any_sync(0xffffffffu, digit);
-        const uint32_t rank = __popc(peers & lt_mask);
-        const bool leader = rank == 0;
-        if (valid && leader) wcnt[warp][digit] = __popc(peers);
-        __syncthreads();
-        if (valid) {
-            uint32_t pos = run[digit] + rank;
-            for (int w = 0; w < warp; ++w) pos += wcnt[w][digit];
-            kout[pos] = key;
-            vout[pos] = val;
+        const uint32_t before = valid ? my[digit] : 0u;
+        rk[k] = before + __popc(peers & lt_mask);
+        __syncwarp();
+        if (valid && (peers & lt_mask) == 0u) my[digit] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: prefix over warps (warp order = element order), plus the digit base
+    for (int d = threadIdx.x; d < D; d += kSortThreads) {
+        uint32_t run = dbase[d];
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t t = wcnt[w * D + d];
+            wcnt[w * D + d] = run;
+            run += t;
         }
-        __syncthreads();
-        for (int d = threadIdx.x; d < kDigits; d += kSortThreads) {
-            uint32_t t = 0;
-            for (int w = 0; w < W; ++w) t += wcnt[w][d];
-            run[d] += t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+        const int64_t e = wbase + k * 32 + lane;
+        if (e < L) {
+            const uint32_t pos = my[(kk[k] >> shift) & (D - 1)] + rk[k];
+            kout[pos] = kk[k];
+            vout[pos] = vv[k];
         }
-        __syncthreads();
-        if (valid && leader) wcnt[warp][digit] = 0;
-        __syncwarp();  // clears by one lane are ordered before the next round's writes by another lane
     }
 }
 
@@ -284,7 +302,8 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
     int bits = 0;
     while (bits < 32 && ((int64_t)1 << bits) < p.kmax) ++bits;
     p.nbits = std::max(bits, 1);
-    p.npasses = (p.nbits + kDigitBits - 1) / kDigitBits;
+    p.npasses = (p.nbits + kMaxDigitBits - 1) / kMaxDigitBits;
+    p.digit_bits = (p.nbits + p.npasses - 1) / p.npasses;
     p.ntiles = (int)((p.L + kSortTile - 1) / kSortTile);
     size_t off = 0;
     for (int i = 0; i < 2; ++i) {
@@ -293,10 +312,11 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
         p.off_vals[i] = off;
         off = align_up(off + (size_t)p.L * 4, 256);
     }
+    const int D = 1 << p.digit_bits;
     p.off_counts = off;
-    off = align_up(off + (size_t)kDigits * p.ntiles * 4, 256);
+    off = align_up(off + (size_t)D * p.ntiles * 4, 256);
     p.off_totals = off;
-    off = align_up(off + (size_t)kDigits * 4, 256);
+    off = align_up(off + (size_t)D * 4, 256);
     p.off_offsets = off;
     off = align_up(off + (size_t)(p.kmax + 1) * 4, 256);
     p.bytes = off;
@@ -316,12 +336,21 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sm_count() * 16);
     keys_kernel<<<grid_l, 256, 0, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, keys[0], vals[0]);
     int cur = 0;
+    const int D = 1 << p.digit_bits;
+    const size_t scatter_smem = (size_t)(kSortWarps + 1) * D * 4;
+    static thread_local bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (kSortWarps + 1) * (1 << kMaxDigitBits) * 4);
+        attr_set = true;
+    }
     for (int pass = 0; pass < p.npasses; ++pass) {
-        const int shift = pass * kDigitBits;
-        radix_hist_kernel<<<p.ntiles, kSortThreads, 0, st>>>(keys[cur], p.L, shift, p.ntiles, counts);
-        radix_rowscan_kernel<<<kDigits, kSortThreads, 0, st>>>(counts, p.ntiles, totals);
-        radix_scatter_kernel<<<p.ntiles, kSortThreads, 0, st>>>(keys[cur], vals[cur], p.L, shift, p.ntiles, counts,
-                                                               totals, keys[1 - cur], vals[1 - cur]);
+        const int shift = pass * p.digit_bits;
+        radix_hist_kernel<<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], p.L, shift, D, p.ntiles, counts);
+        radix_rowscan_kernel<<<D, kSortThreads, 0, st>>>(counts, p.ntiles, totals);
+        radix_scatter_kernel<<<p.ntiles, kSortThreads, scatter_smem, st>>>(keys[cur], vals[cur], p.L, shift, D,
+                                                                           p.ntiles, counts, totals, keys[1 - cur],
+                                                                           vals[1 - cur]);
         cur = 1 - cur;
     }
     const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);

@@ -263,12 +263,17 @@ __global__ void __launch_bounds__(kMergeThreads) nn_merge_kernel(MergeArgs a) {
             const float4 qp = a.pack[dir][(int64_t)b * a.ppad[dir] + a.qlo[dir] + sq];
             const float4* T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
             const int jend = min(bb + kBlockK, a.npts[tdir]);
-            for (int j = bb; j < jend; ++j) {
-                const float4 t = T[j];
-                if (dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z) == best) {
-                    idx = j;
-                    break;
+            // chunks of 8 independent loads (memory-level parallelism), first match wins
+            for (int c = bb; c < jend && idx < 0; c += 8) {
+                float d[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const float4 t = T[min(c + r, jend - 1)];
+                    d[r] = dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z);
                 }
+#pragma unroll
+                for (int r = 7; r >= 0; --r)
+                    if (c + r < jend && d[r] == best) idx = c + r;
             }
         }
         a.d_out[dir][(int64_t)b * slen + sq] = best;
@@ -543,9 +548,9 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
             a.slice_total = p.slice_total;
             a.best_d = best_d;
             a.best_blk = best_blk;
-            if (g_prof_start) cudaEventRecord(g_prof_start, st);
+            if (g_prof_start) record_profile_event(g_prof_start, st);
             nn_fwd_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
-            if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
+            if (g_prof_stop) record_profile_event(g_prof_stop, st);
         }
     } else if (p.mode == kFusedFull || p.mode == kFusedRows) {
         cudaError_t e = launch_fused_rows(p, pack0, pack1, colkey, best_d, best_blk, st);

@@ -305,9 +305,9 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
     a.colkey = colkey;
     const int gx = p.qtiles[0] * p.splits[0];
     if (gx > 0) {
-        if (g_prof_start) cudaEventRecord(g_prof_start, st);
+        if (g_prof_start) record_profile_event(g_prof_start, st);
         nn_fused_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
-        if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
+        if (g_prof_stop) record_profile_event(g_prof_stop, st);
     }
     return cudaGetLastError();
 }
