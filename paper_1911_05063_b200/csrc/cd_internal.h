@@ -21,7 +21,7 @@ struct FwdPlan {
     int qlo[2], qhi[2]; // query slice per dir (dir 0 queries X, dir 1 queries Y)
     int qtiles[2];      // query tiles per (dir, b)
     int splits[2];      // target splits per dir
-    int split_len[2];   // targets per split (multiple of kTile)
+    int ttiles[2];      // target tiles (kTile points) per dir; split s covers [s*T/S, (s+1)*T/S)
     int64_t slice_off[2];  // offset of dir's rows inside the [B*sq + B*sr] per-split arrays
     int64_t slice_total;   // B*sq + B*sr
     int nchunks[2];     // merge chunks (kMergeThreads queries) per (dir, b)

@@ -65,7 +65,7 @@ struct FwdArgs {
     const float4* pack[2];
     int npts[2], ppad[2];
     int qlo[2], qhi[2];
-    int qtiles[2], splits[2], split_len[2];
+    int qtiles[2], splits[2], ttiles[2];
     int64_t slice_off[2], slice_total;
     float* best_d;
     int* best_blk;
@@ -90,8 +90,9 @@ __global__ void __launch_bounds__(kFwdThreads, 4) nn_fwd_kernel(FwdArgs a) {
     const float4* __restrict__ T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
     const int nq = a.npts[dir];
     const int nt = a.npts[tdir];
-    const int j0 = split * a.split_len[dir];
-    const int j1 = min(j0 + a.split_len[dir], nt);
+    // split s covers target tiles [s*T/S, (s+1)*T/S): equal work up to one tile
+    const int j0 = (int)((int64_t)split * a.ttiles[dir] / a.splits[dir]) * kTile;
+    const int j1 = min((int)((int64_t)(split + 1) * a.ttiles[dir] / a.splits[dir]) * kTile, nt);
     const int ntiles = (j1 - j0 + kTile - 1) / kTile;  // >= 1 (host guarantees non-empty splits)
 
     if (threadIdx.x == 0) {
@@ -432,15 +433,20 @@ int unfused_ctas_per_sm() {
     return occ;
 }
 
-static int choose_splits(int64_t units, int mt, int ctas_per_sm) {
+// Choose the target-split count S: every (query tile, split) is one CTA; split s covers target
+// tiles [s*T/S, (s+1)*T/S).  Minimise waves(U*S) * (ceil(T/S) + c0), with c0 = per-CTA overhead
+// in tile units, and prefer at least one full wave of CTAs (a partly filled SM is latency-bound).
+static int choose_splits(int64_t units, int ttiles, int ctas_per_sm) {
     const int64_t slots = (int64_t)device_sm_count() * ctas_per_sm;
-    const double c0 = 96.0;
-    const int smax = std::max(1, std::min(64, ceil_div(mt, kTile)));
+    const double c0 = 0.25;
+    const int smax = std::max(1, std::min(64, ttiles));
     int best_s = 1;
     double best_t = 1e300;
     for (int s = 1; s <= smax; ++s) {
-        const double waves = (double)ceil_div(units * s, slots);
-        const double t = waves * ((double)mt / s + c0);
+        const int64_t ctas = units * s;
+        const double waves = (double)ceil_div(ctas, slots);
+        double t = waves * ((double)ceil_div(ttiles, s) + c0);
+        if (ctas < slots && s < smax) t *= 1.15;  // under one wave: idle SM slots
         if (t < best_t * 0.999) {
             best_t = t;
             best_s = s;
@@ -467,12 +473,10 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
         units += (int64_t)B * p.qtiles[d];
     }
     const int occ = mode == kUnfused ? unfused_ctas_per_sm() : fused_ctas_per_sm();
-    const int S = forced_splits > 0 ? forced_splits : choose_splits(units, std::max(N, M), occ);
+    const int S = forced_splits > 0 ? forced_splits : choose_splits(units, ceil_div(std::max(N, M), kTile), occ);
     for (int d = 0; d < 2; ++d) {
-        const int mt = p.npts[1 - d];
-        const int s = std::max(1, std::min(S, ceil_div(mt, kTile)));
-        p.split_len[d] = ceil_div(ceil_div(mt, s), kTile) * kTile;
-        p.splits[d] = ceil_div(mt, p.split_len[d]);  // every split non-empty
+        p.ttiles[d] = ceil_div(p.npts[1 - d], kTile);
+        p.splits[d] = std::max(1, std::min(S, p.ttiles[d]));  // <= T: every split non-empty
         if (p.qtiles[d] == 0) p.splits[d] = 1;
     }
     const int64_t sq = (int64_t)(q1 - q0), sr = (int64_t)(r1 - r0);
@@ -542,7 +546,7 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
                 a.qhi[d] = p.qhi[d];
                 a.qtiles[d] = p.qtiles[d];
                 a.splits[d] = p.splits[d];
-                a.split_len[d] = p.split_len[d];
+                a.ttiles[d] = p.ttiles[d];
                 a.slice_off[d] = p.slice_off[d];
             }
             a.slice_total = p.slice_total;

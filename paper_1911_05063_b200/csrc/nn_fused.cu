@@ -29,7 +29,7 @@ struct FusedArgs {
     const float4* yp;   // packed Y (targets / columns)
     int N, M, xpad, ypad;
     int q0, q1;         // X row slice
-    int qtiles, splits, split_len;
+    int qtiles, splits, ttiles;
     int64_t slice_total;  // B * (q1 - q0)
     float* best_d;      // [splits][B*(q1-q0)]
     int* best_blk;
@@ -47,8 +47,8 @@ __global__ void __launch_bounds__(kFwdThreads, 3) nn_fused_kernel(FusedArgs a) {
     const int split = blockIdx.x - tile * a.splits;
     const float4* __restrict__ Q = a.xp + (int64_t)b * a.xpad;
     const float4* __restrict__ T = a.yp + (int64_t)b * a.ypad;
-    const int j0 = split * a.split_len;
-    const int j1 = min(j0 + a.split_len, a.M);
+    const int j0 = (int)((int64_t)split * a.ttiles / a.splits) * kTile;  // tiles [s*T/S, (s+1)*T/S)
+    const int j1 = min((int)((int64_t)(split + 1) * a.ttiles / a.splits) * kTile, a.M);
     const int ntiles = (j1 - j0 + kTile - 1) / kTile;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -298,7 +298,7 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
     a.q1 = p.qhi[0];
     a.qtiles = p.qtiles[0];
     a.splits = p.splits[0];
-    a.split_len = p.split_len[0];
+    a.ttiles = p.ttiles[0];
     a.slice_total = p.slice_total;
     a.best_d = best_d;
     a.best_blk = best_blk;
