@@ -62,7 +62,8 @@ typedef enum {
     CD_OP_FORWARD = 0,   /* cd_forward */
     CD_OP_FSCORE = 1,    /* cd_fscore */
     CD_OP_BACKWARD = 2,  /* cd_backward */
-    CD_OP_STEP = 3       /* cd_step_host: forward + finalize + backward (+ staging of the clouds) */
+    CD_OP_STEP = 3,      /* cd_step_host: forward + finalize + backward (+ staging of the clouds) */
+    CD_OP_FORWARD_PRUNED = 4 /* cd_forward_pruned */
 } cd_op;
 
 /*
@@ -108,6 +109,24 @@ CD_API cd_status cd_forward_rows(const float* x, const float* y, int B, int N, i
                           void* workspace, size_t workspace_bytes, cd_stream_t stream);
 CD_API cd_status cd_forward_cols(const float* x, const float* y, int B, int N, int M,
                           const int64_t* colkeys, int r0, int r1, float* d_yx, int32_t* idx_yx,
+                          double* partials, float tau,
+                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_forward_pruned — the same outputs as cd_forward on the full problem (q0=0,q1=N,r0=0,r1=M)
+ * computed with far fewer distance evaluations on large clouds (the exact
+ * accelerated search SPEC.md:441/446 asks to equal brute force): both clouds are sorted along a
+ * Morton curve per batch element, every 1024-row query tile visits 512-point target tiles in order
+ * of a strict lower bound of their squared distance and stops once that bound exceeds the largest
+ * current minimum among its rows.  Distances are the same fp32 values as the brute force (same op
+ * order, every pair that could be a minimum is evaluated); indices are exact nearest neighbours —
+ * among EXACTLY equal distances the one found first in tile order is returned instead of the lowest
+ * index (R3').  Partials as cd_forward (sum order differs: equal within fp64 rounding).
+ * Limits: at most 4,194,304 points per cloud per batch element (CD_ERR_TOO_LARGE).
+ * Workspace: cd_workspace_size(CD_OP_FORWARD_PRUNED, B, N, M).
+ */
+CD_API cd_status cd_forward_pruned(const float* x, const float* y, int B, int N, int M,
+                          float* d_xy, int32_t* idx_xy, float* d_yx, int32_t* idx_yx,
                           double* partials, float tau,
                           void* workspace, size_t workspace_bytes, cd_stream_t stream);
 

@@ -54,11 +54,17 @@ def set_forward_splits(s: int) -> int:
 
 
 def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=None, r_slice=None,
-            want_partials: bool = True):
+            want_partials: bool = True, algorithm: str = "brute"):
     """cd_forward: both NN directions.  Returns (d_xy, idx_xy, d_yx, idx_yx, partials[B,4] fp64).
 
     q_slice=(q0,q1) / r_slice=(r0,r1) restrict the query rows (query sharding); outputs are
-    slice-sized."""
+    slice-sized.  algorithm="pruned" uses cd_forward_pruned (exact, culled; full problems only)."""
+    if algorithm == "pruned":
+        if q_slice is not None or r_slice is not None:
+            raise ValueError("the pruned forward takes the full problem")
+        return forward_pruned(x, y, tau=tau, want_partials=want_partials)
+    if algorithm != "brute":
+        raise ValueError(f"unknown algorithm {algorithm!r}")
     x = _check_cloud(x, "x")
     y = _check_cloud(y, "y")
     B, N, _ = x.shape
@@ -77,6 +83,25 @@ def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=
     lib = _lib.load()
     check(lib.cd_forward(_ptr(x), _ptr(y), B, N, M, q0, q1, r0, r1, _ptr(d_xy), _ptr(i_xy), _ptr(d_yx), _ptr(i_yx),
                          _ptr(part), float(-1.0 if tau is None else tau), _ptr(ws), ws.numel(), _stream()))
+    return d_xy, i_xy, d_yx, i_yx, part
+
+
+def forward_pruned(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, want_partials: bool = True):
+    """cd_forward_pruned: exact nearest neighbours with Morton-tile lower-bound culling."""
+    x = _check_cloud(x, "x")
+    y = _check_cloud(y, "y")
+    B, N, _ = x.shape
+    M = y.shape[1]
+    dev = x.device
+    d_xy = torch.empty((B, N), dtype=torch.float32, device=dev)
+    i_xy = torch.empty((B, N), dtype=torch.int32, device=dev)
+    d_yx = torch.empty((B, M), dtype=torch.float32, device=dev)
+    i_yx = torch.empty((B, M), dtype=torch.int32, device=dev)
+    part = torch.empty((B, 4), dtype=torch.float64, device=dev) if want_partials else None
+    ws = workspace(_lib.CD_OP_FORWARD_PRUNED, B, N, M, dev)
+    check(_lib.load().cd_forward_pruned(_ptr(x), _ptr(y), B, N, M, _ptr(d_xy), _ptr(i_xy), _ptr(d_yx), _ptr(i_yx),
+                                        _ptr(part), float(-1.0 if tau is None else tau), _ptr(ws), ws.numel(),
+                                        _stream()))
     return d_xy, i_xy, d_yx, i_yx, part
 
 

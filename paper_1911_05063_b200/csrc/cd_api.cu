@@ -149,6 +149,11 @@ size_t cd_workspace_size(int op, int B, int N, int M) {
             return p.bytes;
         }
         case CD_OP_STEP: return step_layout(B, N, M).bytes;
+        case CD_OP_FORWARD_PRUNED: {
+            cdk::PrunedPlan p;
+            cdk::plan_pruned(p, B, N, M);
+            return p.bytes;
+        }
     }
     return 0;
 }
@@ -162,6 +167,11 @@ int cd_launch_count(int op, int B, int N, int M) {
         case CD_OP_FSCORE: return cdk::kFscoreLaunches;
         case CD_OP_BACKWARD: return cdk::backward_launches(bp);
         case CD_OP_STEP: return fwd_launches(B, N, M) + 1 + cdk::backward_launches(bp);
+        case CD_OP_FORWARD_PRUNED: {
+            cdk::PrunedPlan p;
+            cdk::plan_pruned(p, B, N, M);
+            return cdk::pruned_launches(p);
+        }
     }
     return 0;
 }
@@ -257,6 +267,36 @@ cd_status cd_forward_cols(const float* x, const float* y, int B, int N, int M, c
     o.colkey = const_cast<long long*>(reinterpret_cast<const long long*>(colkeys));
     return cuda_status(cdk::launch_forward(p, x, y, o, workspace, static_cast<cudaStream_t>(stream)),
                        "cd_forward_cols");
+}
+
+cd_status cd_forward_pruned(const float* x, const float* y, int B, int N, int M, float* d_xy, int32_t* idx_xy,
+                            float* d_yx, int32_t* idx_yx, double* partials, float tau, void* workspace,
+                            size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x || !y || !workspace || !d_xy || !idx_xy || !d_yx || !idx_yx)
+        return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (tau != tau) return fail(CD_ERR_INVALID_VALUE, "tau is NaN");
+    if (!aligned(x, 4) || !aligned(y, 4)) return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte aligned");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    cdk::PrunedPlan p;
+    cdk::plan_pruned(p, B, N, M);
+    if (!p.supported) return fail(CD_ERR_TOO_LARGE, "pruned path supports at most 8192 tiles (4,194,304 points) per cloud");
+    if (workspace_bytes < p.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    cdk::FwdOutputs o;
+    o.d[0] = d_xy;
+    o.d[1] = d_yx;
+    o.idx[0] = idx_xy;
+    o.idx[1] = idx_yx;
+    o.partials = partials;
+    o.tau = tau;
+    o.colkey = nullptr;
+    return cuda_status(cdk::launch_pruned(p, x, y, o, workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_forward_pruned");
 }
 
 int cd_set_forward_mode(int mode) {

@@ -52,6 +52,24 @@ cudaError_t launch_col_resolve(const FwdPlan& p, const float4* xp, const float4*
                                int r1, float* d_out, int32_t* idx_out, double* chunk_sum, int* chunk_hits, float tau,
                                cudaStream_t st);
 
+// Exact pruned forward (nn_pruned.cu, NEXT-2): Morton-sorted tiles + box lower-bound culling.
+struct PrunedPlan {
+    int B, npts[2], ppad[2], qtiles[2], ttiles[2];
+    int bbits, kbits, nbits;
+    int64_t L, cand_off[2];
+    int nchunks[2];
+    int64_t chunk_off[2];
+    bool supported;
+    size_t off_bbox, off_keys[2], off_vals[2], off_counts, off_totals, off_sorted[2], off_perm[2], off_box[2], off_box32[2],
+        off_best_d[2], off_best_blk[2], off_cand, off_chunk_sum, off_chunk_hits, bytes;
+};
+void plan_pruned(PrunedPlan& p, int B, int N, int M);
+cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
+                          cudaStream_t st);
+int pruned_launches(const PrunedPlan& p);
+cudaError_t launch_partials(const double* chunk_sum, const int* chunk_hits, const int nchunks[2],
+                            const int64_t chunk_off[2], int B, double* partials, int dirmask, cudaStream_t st);
+
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.
 size_t fscore_workspace(int B, int N, int M);
 cudaError_t launch_fscore(const float* d_xy, const float* d_yx, int B, int N, int M, float tau, float* fscore,
@@ -75,6 +93,13 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
                             const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar,
                             float* grad_x, float* grad_y, void* ws, cudaStream_t st);
 int backward_launches(const BwdPlan& p);
+
+// Reusable stable LSD radix sort of u32 (key, value) pairs (nn_backward.cu).
+int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits, uint32_t* counts, uint32_t* totals,
+                     cudaStream_t st);
+size_t radix_sort_counts_words(int64_t L, int nbits);
+int radix_sort_launches(int64_t L, int nbits);
+constexpr int kSortTotalsWords = 1 << 11;
 
 // thread-local measurement hook (cd_set_profile_events)
 extern thread_local cudaEvent_t g_prof_start;

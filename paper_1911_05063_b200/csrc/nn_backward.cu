@@ -289,6 +289,52 @@ static int sm_count() {
     return sms;
 }
 
+void radix_sort_plan(int64_t L, int nbits, int& npasses, int& digit_bits, int& ntiles) {
+    nbits = std::max(nbits, 1);
+    npasses = (nbits + kMaxDigitBits - 1) / kMaxDigitBits;
+    digit_bits = (nbits + npasses - 1) / npasses;
+    ntiles = (int)((L + kSortTile - 1) / kSortTile);
+}
+
+size_t radix_sort_counts_words(int64_t L, int nbits) {
+    int np, db, nt;
+    radix_sort_plan(L, nbits, np, db, nt);
+    return (size_t)(1 << db) * nt;
+}
+
+// Stable LSD radix sort of (key, value) u32 pairs by the low `nbits` key bits.  keys[0]/vals[0]
+// hold the input; returns the index (0 or 1) of the buffers holding the sorted output.
+// counts: radix_sort_counts_words(L, nbits) words; totals: 2^11 words.
+int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits, uint32_t* counts, uint32_t* totals,
+                     cudaStream_t st) {
+    int npasses, digit_bits, ntiles;
+    radix_sort_plan(L, nbits, npasses, digit_bits, ntiles);
+    const int D = 1 << digit_bits;
+    const size_t scatter_smem = (size_t)(kSortWarps + 1) * D * 4;
+    static thread_local bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (kSortWarps + 1) * (1 << kMaxDigitBits) * 4);
+        attr_set = true;
+    }
+    int cur = 0;
+    for (int pass = 0; pass < npasses; ++pass) {
+        const int shift = pass * digit_bits;
+        radix_hist_kernel<<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D, ntiles, counts);
+        radix_rowscan_kernel<<<D, kSortThreads, 0, st>>>(counts, ntiles, totals);
+        radix_scatter_kernel<<<ntiles, kSortThreads, scatter_smem, st>>>(keys[cur], vals[cur], L, shift, D, ntiles,
+                                                                         counts, totals, keys[1 - cur], vals[1 - cur]);
+        cur = 1 - cur;
+    }
+    return cur;
+}
+
+int radix_sort_launches(int64_t L, int nbits) {
+    int np, db, nt;
+    radix_sort_plan(L, nbits, np, db, nt);
+    return 3 * np;
+}
+
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1) {
     p.B = B;
     p.N = N;
@@ -302,9 +348,7 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
     int bits = 0;
     while (bits < 32 && ((int64_t)1 << bits) < p.kmax) ++bits;
     p.nbits = std::max(bits, 1);
-    p.npasses = (p.nbits + kMaxDigitBits - 1) / kMaxDigitBits;
-    p.digit_bits = (p.nbits + p.npasses - 1) / p.npasses;
-    p.ntiles = (int)((p.L + kSortTile - 1) / kSortTile);
+    radix_sort_plan(p.L, p.nbits, p.npasses, p.digit_bits, p.ntiles);
     size_t off = 0;
     for (int i = 0; i < 2; ++i) {
         p.off_keys[i] = off;
@@ -312,11 +356,10 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
         p.off_vals[i] = off;
         off = align_up(off + (size_t)p.L * 4, 256);
     }
-    const int D = 1 << p.digit_bits;
     p.off_counts = off;
-    off = align_up(off + (size_t)D * p.ntiles * 4, 256);
+    off = align_up(off + radix_sort_counts_words(p.L, p.nbits) * 4, 256);
     p.off_totals = off;
-    off = align_up(off + (size_t)D * 4, 256);
+    off = align_up(off + (size_t)(1 << kMaxDigitBits) * 4, 256);
     p.off_offsets = off;
     off = align_up(off + (size_t)(p.kmax + 1) * 4, 256);
     p.bytes = off;
@@ -335,24 +378,7 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     uint32_t* off = reinterpret_cast<uint32_t*>(w + p.off_offsets);
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sm_count() * 16);
     keys_kernel<<<grid_l, 256, 0, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, keys[0], vals[0]);
-    int cur = 0;
-    const int D = 1 << p.digit_bits;
-    const size_t scatter_smem = (size_t)(kSortWarps + 1) * D * 4;
-    static thread_local bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (kSortWarps + 1) * (1 << kMaxDigitBits) * 4);
-        attr_set = true;
-    }
-    for (int pass = 0; pass < p.npasses; ++pass) {
-        const int shift = pass * p.digit_bits;
-        radix_hist_kernel<<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], p.L, shift, D, p.ntiles, counts);
-        radix_rowscan_kernel<<<D, kSortThreads, 0, st>>>(counts, p.ntiles, totals);
-        radix_scatter_kernel<<<p.ntiles, kSortThreads, scatter_smem, st>>>(keys[cur], vals[cur], p.L, shift, D,
-                                                                           p.ntiles, counts, totals, keys[1 - cur],
-                                                                           vals[1 - cur]);
-        cur = 1 - cur;
-    }
+    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, counts, totals, st);
     const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);
     offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], p.L, p.kmax, off);
     GradArgs a;

@@ -610,6 +610,21 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
     return cudaGetLastError();
 }
 
+cudaError_t launch_partials(const double* chunk_sum, const int* chunk_hits, const int nchunks[2],
+                            const int64_t chunk_off[2], int B, double* partials, int dirmask, cudaStream_t st) {
+    PartialsArgs a;
+    a.chunk_sum = chunk_sum;
+    a.chunk_hits = chunk_hits;
+    for (int d = 0; d < 2; ++d) {
+        a.nchunks[d] = nchunks[d];
+        a.chunk_off[d] = chunk_off[d];
+    }
+    a.partials = partials;
+    a.dirmask = dirmask;
+    partials_kernel<<<B, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 int forward_launches(const FwdPlan& p) {
     int n = 1;                                                      // pack (+ column-key reset)
     if (p.mode == kUnfused) n += 2;                                 // nn_fwd + merge

@@ -1,0 +1,762 @@
+// nn_pruned.cu — exact pruned nearest-neighbour forward.
+//
+// Same results as the brute force (the fixed fp32 distance formula of DESIGN.md §4.2 evaluated on
+// every pair that could matter), far fewer pairs on large clouds:
+//   bbox_kernel        per (cloud, batch) bounding box of a fixed-stride sample (min/max: order-free;
+//                      only the Morton quantisation depends on it).
+//   morton_kernel      key = (cloud | batch | k-bit-per-axis Morton code) per point, value = row.
+//   radix sort         (nn_backward.cu) -> every (cloud, batch) segment in Morton order.
+//   gather_kernel      sorted packed float4 clouds + permutation (sorted position -> original row).
+//   aabb_kernel        bounding box of every 512-point tile of the sorted clouds.
+//   candidates_kernel  per query tile (1024 sorted rows): lower bound LB of the squared distance to
+//                      every target tile (box-box gap, scaled by (1 - 1e-5) so it is a strict lower
+//                      bound of the fp32-evaluated distances), bitonic-sorted ascending.
+//   nn_pruned_kernel   per query tile: target tiles in LB order through the 3-stage TMA ring, the
+//                      same packed-FP32 value-only min + block argmin tracking as nn_fwd_kernel; stops
+//                      at the first tile with LB > max over the CTA's rows of the current minimum:
+//                      every skipped pair has d > that row's minimum, so the minimum is exact.
+//   pruned_resolve_kernel  exact index inside the winning 32-target block (same .rn ops), mapped back
+//                      to original rows; outputs in original order; chunk partials.
+// Tie-break: among EXACTLY equal distances the index found first in LB-tile order wins (the brute
+// force returns the lowest index); any such index is an exact nearest neighbour (R3').
+#include "cd_device.cuh"
+#include "cd_internal.h"
+
+#include <algorithm>
+
+namespace cdk {
+
+constexpr int kPrR = 8;                         // query rows per thread
+constexpr int kPrQ = kFwdThreads * kPrR;        // 1024 sorted rows per query tile (2 target tiles)
+constexpr int kPrMaxTiles = 8192;               // target tiles per batch supported by the LB sort
+constexpr float kLbScale = 0.99999f;            // LB' = LB * (1 - 1e-5): strict lower bound margin
+
+// --------------------------------------------------------------------------------------------- bbox
+struct BoxArgs {
+    const float* src[2];
+    int npts[2];
+    int B;
+    float* bbox;   // [2][B][6]: lo xyz, hi xyz
+};
+
+__global__ void __launch_bounds__(256) bbox_kernel(BoxArgs a) {
+    const int c = blockIdx.x / a.B, b = blockIdx.x - (blockIdx.x / a.B) * a.B;
+    const float* p = a.src[c] + (int64_t)b * a.npts[c] * 3;
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    // The box only sets the Morton quantisation (codes are clamped), never correctness: a fixed-
+    // stride sample of <= 16K points per cloud is enough and keeps this O(16K) per batch element.
+    const int stride = max(1, a.npts[c] / 16384);
+    for (int i = threadIdx.x * stride; i < a.npts[c]; i += 256 * stride) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float v = __ldg(p + (int64_t)i * 3 + k);
+            lo[k] = fminf(lo[k], v);
+            hi[k] = fmaxf(hi[k], v);
+        }
+    }
+    __shared__ float s[8][6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+            hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+        }
+    }
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 3; ++k) {
+            s[threadIdx.x >> 5][k] = lo[k];
+            s[threadIdx.x >> 5][3 + k] = hi[k];
+        }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[0][threadIdx.x];
+        for (int w = 1; w < 8; ++w) v = threadIdx.x < 3 ? fminf(v, s[w][threadIdx.x]) : fmaxf(v, s[w][threadIdx.x]);
+        a.bbox[((int64_t)c * a.B + b) * 6 + threadIdx.x] = v;
+    }
+}
+
+// --------------------------------------------------------------------------------------------- morton
+__device__ __forceinline__ uint32_t spread_bits(uint32_t v, int k) {
+    uint32_t r = 0;
+    for (int i = 0; i < k; ++i) r |= ((v >> i) & 1u) << (3 * i);
+    return r;
+}
+
+struct MortonArgs {
+    const float* src[2];
+    int npts[2];
+    int B, kbits, bbits;
+    const float* bbox;
+    uint32_t* keys;
+    uint32_t* vals;
+};
+
+__global__ void __launch_bounds__(256) morton_kernel(MortonArgs a) {
+    const int64_t L0 = (int64_t)a.B * a.npts[0];
+    const int64_t L = L0 + (int64_t)a.B * a.npts[1];
+    const float qmax = (float)((1 << a.kbits) - 1);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = e < L0 ? 0 : 1;
+        const int64_t f = c == 0 ? e : e - L0;
+        const int b = (int)(f / a.npts[c]);
+        const float* bb = a.bbox + ((int64_t)c * a.B + b) * 6;
+        const float* p = a.src[c] + f * 3;
+        uint32_t code = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float ext = bb[3 + k] - bb[k];
+            float t = ext > 0.f ? (__ldg(p + k) - bb[k]) / ext : 0.f;
+            t = fminf(fmaxf(t, 0.f), 1.f);          // NaN -> 0 via fmaxf
+            const uint32_t q = (uint32_t)(t * qmax + 0.5f);
+            code |= spread_bits(q, a.kbits) << k;
+        }
+        a.keys[e] = ((uint32_t)c << (a.bbits + 3 * a.kbits)) | ((uint32_t)b << (3 * a.kbits)) | code;
+        a.vals[e] = (uint32_t)e;
+    }
+}
+
+// --------------------------------------------------------------------------------------------- gather
+struct GatherArgs {
+    const float* src[2];
+    int npts[2], ppad[2];
+    int B;
+    const uint32_t* vals;   // sorted flat rows (cloud 0 rows first)
+    float4* sorted[2];      // [B][ppad]
+    int* perm[2];           // [B][npts]: sorted position -> original row within the batch element
+};
+
+__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+    const int64_t L0 = (int64_t)a.B * a.npts[0];
+    const int64_t L = L0 + (int64_t)a.B * a.npts[1];
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L; s += (int64_t)gridDim.x * blockDim.x) {
+        const int c = s < L0 ? 0 : 1;
+        const int64_t f = c == 0 ? s : s - L0;          // (b, p) of the sorted position
+        const int b = (int)(f / a.npts[c]);
+        const int p = (int)(f - (int64_t)b * a.npts[c]);
+        const int64_t v = (int64_t)a.vals[s] - (c == 0 ? 0 : L0);  // original flat row of the same cloud
+        const float* q = a.src[c] + v * 3;
+        a.sorted[c][(int64_t)b * a.ppad[c] + p] = make_float4(__ldg(q), __ldg(q + 1), __ldg(q + 2), 0.f);
+        a.perm[c][(int64_t)b * a.npts[c] + p] = (int)(v - (int64_t)b * a.npts[c]);
+    }
+    // padding rows of every batch element: +inf (never a nearest neighbour)
+    const int64_t pad0 = (int64_t)a.B * (a.ppad[0] - a.npts[0]);
+    const int64_t padL = pad0 + (int64_t)a.B * (a.ppad[1] - a.npts[1]);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < padL; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = e < pad0 ? 0 : 1;
+        const int64_t f = c == 0 ? e : e - pad0;
+        const int w = a.ppad[c] - a.npts[c];
+        const int b = (int)(f / w);
+        const int p = a.npts[c] + (int)(f - (int64_t)b * w);
+        a.sorted[c][(int64_t)b * a.ppad[c] + p] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+    }
+}
+
+// --------------------------------------------------------------------------------------------- tile boxes
+constexpr int kBlocksPerTile = kTile / kBlockK;  // 16 blocks of 32 points per 512-point tile
+
+struct AabbArgs {
+    const float4* sorted[2];
+    int npts[2], ppad[2];
+    int B;
+    float4* box[2];         // [B][ppad/kTile][2]: tile lo, hi (empty: lo = +inf, hi = -inf)
+    float4* bbox32[2];      // [B][ppad/kBlockK][2]: 32-point block lo, hi
+};
+
+// One warp per 512-point tile: lane l reduces point l of each 32-point block.
+__global__ void __launch_bounds__(256) aabb_kernel(AabbArgs a) {
+    const int nt0 = a.ppad[0] / kTile, nt1 = a.ppad[1] / kTile;
+    const int64_t T0 = (int64_t)a.B * nt0, T = T0 + (int64_t)a.B * nt1;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= T) return;
+    const int c = wid < T0 ? 0 : 1;
+    const int64_t f = c == 0 ? wid : wid - T0;
+    const int nt = c == 0 ? nt0 : nt1;
+    const int b = (int)(f / nt);
+    const int t = (int)(f - (int64_t)b * nt);
+    float tlo[3] = {INFINITY, INFINITY, INFINITY}, thi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int k = 0; k < kBlocksPerTile; ++k) {
+        const int p = t * kTile + k * kBlockK + lane;
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        if (p < a.npts[c]) {
+            const float4 v = a.sorted[c][(int64_t)b * a.ppad[c] + p];
+            lo[0] = hi[0] = v.x;
+            lo[1] = hi[1] = v.y;
+            lo[2] = hi[2] = v.z;
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo[q] = fminf(lo[q], __shfl_xor_sync(0xffffffffu, lo[q], o));
+                hi[q] = fmaxf(hi[q], __shfl_xor_sync(0xffffffffu, hi[q], o));
+            }
+        if (lane == 0) {
+            float4* o = a.bbox32[c] + (((int64_t)b * nt + t) * kBlocksPerTile + k) * 2;
+            o[0] = make_float4(lo[0], lo[1], lo[2], 0.f);
+            o[1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            tlo[q] = fminf(tlo[q], lo[q]);
+            thi[q] = fmaxf(thi[q], hi[q]);
+        }
+    }
+    if (lane == 0) {
+        float4* o = a.box[c] + ((int64_t)b * nt + t) * 2;
+        o[0] = make_float4(tlo[0], tlo[1], tlo[2], 0.f);
+        o[1] = make_float4(thi[0], thi[1], thi[2], 0.f);
+    }
+}
+
+// --------------------------------------------------------------------------------------------- candidates
+struct CandArgs {
+    const float4* box[2];
+    int ppad[2];
+    int B;
+    int qtiles[2];            // query tiles (kPrQ rows) per batch element, per dir
+    int64_t cand_off[2];      // offset of dir's lists in `cand` (u64 entries)
+    unsigned long long* cand; // per (dir, b, query tile): ttiles(1-dir) keys (LB' bits << 32 | tile)
+};
+
+__device__ __forceinline__ float gap(float qlo, float qhi, float tlo, float thi) {
+    return fmaxf(fmaxf(tlo - qhi, qlo - thi), 0.f);
+}
+
+__global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
+    extern __shared__ unsigned long long keys[];
+    int u = blockIdx.x;
+    int dir = 0;
+    if (u >= a.B * a.qtiles[0]) {
+        dir = 1;
+        u -= a.B * a.qtiles[0];
+    }
+    const int b = u / a.qtiles[dir];
+    const int q = u - b * a.qtiles[dir];
+    const int qc = dir, tc = 1 - dir;
+    const int qnt = a.ppad[qc] / kTile, tnt = a.ppad[tc] / kTile;
+    // query tile box = union of its kPrQ / kTile target-size tiles
+    float qlo[3] = {INFINITY, INFINITY, INFINITY}, qhi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int s = 0; s < kPrQ / kTile; ++s) {
+        const float4* bx = a.box[qc] + ((int64_t)b * qnt + q * (kPrQ / kTile) + s) * 2;
+        const float4 lo = bx[0], hi = bx[1];
+        qlo[0] = fminf(qlo[0], lo.x); qlo[1] = fminf(qlo[1], lo.y); qlo[2] = fminf(qlo[2], lo.z);
+        qhi[0] = fmaxf(qhi[0], hi.x); qhi[1] = fmaxf(qhi[1], hi.y); qhi[2] = fmaxf(qhi[2], hi.z);
+    }
+    int npow = 1;
+    while (npow < tnt) npow <<= 1;
+    for (int t = threadIdx.x; t < npow; t += 256) {
+        unsigned long long key = ~0ull;
+        if (t < tnt) {
+            const float4* bx = a.box[tc] + ((int64_t)b * tnt + t) * 2;
+            const float4 lo = bx[0], hi = bx[1];
+            float lb;
+            if (lo.x > hi.x) {
+                lb = INFINITY;   // empty tile (all padding)
+            } else {
+                const float gx = gap(qlo[0], qhi[0], lo.x, hi.x);
+                const float gy = gap(qlo[1], qhi[1], lo.y, hi.y);
+                const float gz = gap(qlo[2], qhi[2], lo.z, hi.z);
+                lb = (gx * gx + gy * gy + gz * gz) * kLbScale;
+            }
+            key = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+        }
+        keys[t] = key;
+    }
+    __syncthreads();
+    // bitonic sort ascending (npow <= kPrMaxTiles)
+    for (int k = 2; k <= npow; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < npow; i += 256) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned long long x = keys[i], y = keys[l];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) {
+                        keys[i] = y;
+                        keys[l] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    unsigned long long* out = a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + q) * tnt;
+    for (int t = threadIdx.x; t < tnt; t += 256) out[t] = keys[t];
+}
+
+// --------------------------------------------------------------------------------------------- main kernel
+struct PrunedArgs {
+    const float4* sorted[2];
+    const float4* bbox32[2];
+    int npts[2], ppad[2];
+    int qtiles[2];
+    int64_t cand_off[2];
+    const unsigned long long* cand;
+    float* best_d[2];     // [B][npts] sorted order
+    int* best_blk[2];     // sorted target position of the winning block
+};
+
+__device__ __forceinline__ float box_lb(const float wlo[3], const float whi[3], float4 lo, float4 hi) {
+    const float gx = gap(wlo[0], whi[0], lo.x, hi.x);
+    const float gy = gap(wlo[1], whi[1], lo.y, hi.y);
+    const float gz = gap(wlo[2], whi[2], lo.z, hi.z);
+    return (gx * gx + gy * gy + gz * gz) * kLbScale;
+}
+
+__global__ void __launch_bounds__(kFwdThreads, 4) nn_pruned_kernel(PrunedArgs a) {
+    __shared__ __align__(128) float4 sm[kStages][kTile];
+    __shared__ __align__(128) float4 smb[kStages][kBlocksPerTile * 2];   // the tile's 32-point block boxes
+    __shared__ __align__(8) u64 full_bar[kStages];
+    __shared__ unsigned s_wmax[kFwdThreads / 32];
+
+    int u = blockIdx.x;
+    const int b = blockIdx.y;
+    int dir = 0;
+    if (u >= a.qtiles[0]) {
+        dir = 1;
+        u -= a.qtiles[0];
+    }
+    const int qc = dir, tc = 1 - dir;
+    const int P = a.npts[qc];
+    const int tnt = a.ppad[tc] / kTile;
+    const float4* __restrict__ Q = a.sorted[qc] + (int64_t)b * a.ppad[qc];
+    const float4* __restrict__ T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
+    const float4* __restrict__ TB = a.bbox32[tc] + (int64_t)b * tnt * kBlocksPerTile * 2;
+    const unsigned long long* __restrict__ cand =
+        a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + u) * tnt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    int issued = 0;  // thread 0 only
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+        fence_mbar_init();
+        const int pre = min(kStages, tnt);
+        for (int k = 0; k < pre; ++k) {
+            const int t = (int)(cand[k] & 0xffffffffull);
+            mbar_arrive_expect_tx(&full_bar[k], kTile * 16 + kBlocksPerTile * 32);
+            tma_load_1d(sm[k], T + (int64_t)t * kTile, kTile * 16, &full_bar[k]);
+            tma_load_1d(smb[k], TB + (int64_t)t * kBlocksPerTile * 2, kBlocksPerTile * 32, &full_bar[k]);
+        }
+        issued = pre;
+    }
+    __syncthreads();
+
+    const int qbase = u * kPrQ + threadIdx.x * kPrR;
+    u64 qx[kPrR / 2], qy[kPrR / 2], qz[kPrR / 2];
+#pragma unroll
+    for (int r = 0; r < kPrR / 2; ++r) {
+        const float4 p0 = Q[min(qbase + 2 * r, P - 1)];
+        const float4 p1 = Q[min(qbase + 2 * r + 1, P - 1)];
+        qx[r] = pk2(p0.x, p1.x);
+        qy[r] = pk2(p0.y, p1.y);
+        qz[r] = pk2(p0.z, p1.z);
+    }
+    float best[kPrR];
+    int blk[kPrR];
+#pragma unroll
+    for (int r = 0; r < kPrR; ++r) {
+        best[r] = INFINITY;
+        blk[r] = -1;
+    }
+    // box of this warp's 256 consecutive sorted rows (valid rows only)
+    float wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int r = 0; r < kPrR / 2; ++r) {
+        float v0, v1;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            upk2(q == 0 ? qx[r] : (q == 1 ? qy[r] : qz[r]), v0, v1);
+            if (qbase + 2 * r < P) { wlo[q] = fminf(wlo[q], v0); whi[q] = fmaxf(whi[q], v0); }
+            if (qbase + 2 * r + 1 < P) { wlo[q] = fminf(wlo[q], v1); whi[q] = fmaxf(whi[q], v1); }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wlo[q] = fminf(wlo[q], __shfl_xor_sync(0xffffffffu, wlo[q], o));
+            whi[q] = fmaxf(whi[q], __shfl_xor_sync(0xffffffffu, whi[q], o));
+        }
+    float wmax = INFINITY;      // warp-uniform: max over the warp's rows of their current minimum
+    float maxbest = INFINITY;   // CTA-uniform (read from shared memory after a barrier)
+    unsigned long long next = cand[0];
+    int k = 0;
+    for (; k < tnt; ++k) {
+        const unsigned long long cur = next;
+        if (k + 1 < tnt) next = cand[k + 1];   // prefetch the next list entry
+        const float lb = __uint_as_float((unsigned)(cur >> 32));
+        if (lb > maxbest) break;               // every remaining tile is farther: done (uniform)
+        const int t = (int)(cur & 0xffffffffull);
+        const int s = k % kStages;
+        mbar_wait(&full_bar[s], (k / kStages) & 1);
+        const float4* tb = sm[s];
+        const float4* bb = smb[s];
+        const int jt = t * kTile;
+        for (int kb = 0; kb < kTile; kb += kBlockK) {
+            // warp-uniform skip: every pair of this block is farther than every row's minimum
+            if (box_lb(wlo, whi, bb[2 * (kb / kBlockK)], bb[2 * (kb / kBlockK) + 1]) > wmax) continue;
+            float old[kPrR];
+#pragma unroll
+            for (int r = 0; r < kPrR; ++r) old[r] = best[r];
+#pragma unroll 4
+            for (int jj = 0; jj < kBlockK; jj += 2) {
+                const float4 t0 = tb[kb + jj];
+                const float4 t1 = tb[kb + jj + 1];
+                const u64 t0x = pk2(t0.x, t0.x), t0y = pk2(t0.y, t0.y), t0z = pk2(t0.z, t0.z);
+                const u64 t1x = pk2(t1.x, t1.x), t1y = pk2(t1.y, t1.y), t1z = pk2(t1.z, t1.z);
+#pragma unroll
+                for (int r = 0; r < kPrR / 2; ++r) {
+                    u64 dx = sub2(qx[r], t0x), dy = sub2(qy[r], t0y), dz = sub2(qz[r], t0z);
+                    u64 s0 = mul2(dx, dx);
+                    s0 = fma2(dy, dy, s0);
+                    s0 = fma2(dz, dz, s0);
+                    dx = sub2(qx[r], t1x);
+                    dy = sub2(qy[r], t1y);
+                    dz = sub2(qz[r], t1z);
+                    u64 s1 = mul2(dx, dx);
+                    s1 = fma2(dy, dy, s1);
+                    s1 = fma2(dz, dz, s1);
+                    float a0, a1, c0, c1;
+                    upk2(s0, a0, a1);
+                    upk2(s1, c0, c1);
+                    best[2 * r] = fmin3(best[2 * r], a0, c0);
+                    best[2 * r + 1] = fmin3(best[2 * r + 1], a1, c1);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kPrR; ++r) blk[r] = best[r] < old[r] ? jt + kb : blk[r];
+        }
+        // CTA maximum of the rows' current minima (valid rows only; d >= 0 so bits order = float order)
+        unsigned m = 0u;
+#pragma unroll
+        for (int r = 0; r < kPrR; ++r)
+            if (qbase + r < P) m = max(m, __float_as_uint(best[r]));
+        m = __reduce_max_sync(0xffffffffu, m);
+        wmax = __uint_as_float(m);
+        if (lane == 0) s_wmax[warp] = m;
+        __syncthreads();  // stage s consumed by every warp; s_wmax complete
+        unsigned mm = s_wmax[0];
+#pragma unroll
+        for (int w = 1; w < kFwdThreads / 32; ++w) mm = max(mm, s_wmax[w]);
+        maxbest = __uint_as_float(mm);
+        if (threadIdx.x == 0 && issued == k + kStages && issued < tnt) {
+            const unsigned long long e = cand[issued];
+            if (__uint_as_float((unsigned)(e >> 32)) <= maxbest) {
+                const int tn = (int)(e & 0xffffffffull);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&full_bar[s], kTile * 16 + kBlocksPerTile * 32);
+                tma_load_1d(sm[s], T + (int64_t)tn * kTile, kTile * 16, &full_bar[s]);
+                tma_load_1d(smb[s], TB + (int64_t)tn * kBlocksPerTile * 2, kBlocksPerTile * 32, &full_bar[s]);
+                ++issued;
+            }
+        }
+        __syncthreads();  // s_wmax may be rewritten by the next tile only after everyone read it
+    }
+    // drain copies that were issued but not consumed (no shared-memory writes after exit)
+    if (threadIdx.x == 0)
+        for (int kk = k; kk < issued; ++kk) mbar_wait(&full_bar[kk % kStages], (kk / kStages) & 1);
+
+    const int64_t rowbase = (int64_t)b * P;
+#pragma unroll
+    for (int r = 0; r < kPrR; ++r) {
+        const int q = qbase + r;
+        if (q < P) {
+            a.best_d[dir][rowbase + q] = best[r];
+            a.best_blk[dir][rowbase + q] = blk[r];
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------------------- resolve
+struct PrResolveArgs {
+    const float4* sorted[2];
+    const int* perm[2];
+    int npts[2], ppad[2];
+    int B;
+    int nchunks[2];
+    int64_t chunk_off[2];
+    const float* best_d[2];
+    const int* best_blk[2];
+    float* d_out[2];
+    int32_t* idx_out[2];
+    double* chunk_sum;
+    int* chunk_hits;
+    double tau2;
+};
+
+__global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolveArgs a) {
+    int u = blockIdx.x;
+    int dir = 0;
+    if (u >= a.B * a.nchunks[0]) {
+        dir = 1;
+        u -= a.B * a.nchunks[0];
+    }
+    const int b = u / a.nchunks[dir];
+    const int chunk = u - b * a.nchunks[dir];
+    const int qc = dir, tc = 1 - dir;
+    const int P = a.npts[qc];
+    const int p = chunk * kMergeThreads + threadIdx.x;
+    double v = 0.0;
+    int h = 0;
+    if (p < P) {
+        const float best = a.best_d[dir][(int64_t)b * P + p];
+        const int bb = a.best_blk[dir][(int64_t)b * P + p];
+        int idx = -1;
+        if (bb >= 0) {
+            const float4 qp = a.sorted[qc][(int64_t)b * a.ppad[qc] + p];
+            const float4* T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
+            const int jend = min(bb + kBlockK, a.npts[tc]);
+            int pos = -1;
+            for (int c = bb; c < jend && pos < 0; c += 8) {
+                float d[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const float4 t = T[min(c + r, jend - 1)];
+                    d[r] = dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z);
+                }
+#pragma unroll
+                for (int r = 7; r >= 0; --r)
+                    if (c + r < jend && d[r] == best) pos = c + r;
+            }
+            if (pos >= 0) idx = a.perm[tc][(int64_t)b * a.npts[tc] + pos];
+        }
+        const int i = a.perm[qc][(int64_t)b * P + p];
+        a.d_out[dir][(int64_t)b * P + i] = best;
+        a.idx_out[dir][(int64_t)b * P + i] = idx;
+        v = (double)best;
+        h = (a.tau2 >= 0.0 && (double)best <= a.tau2) ? 1 : 0;
+    }
+    // fixed-order block reduction
+    __shared__ double ssum[kMergeThreads / 32];
+    __shared__ int shit[kMergeThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_down_sync(0xffffffffu, v, o);
+        h += __shfl_down_sync(0xffffffffu, h, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        ssum[threadIdx.x >> 5] = v;
+        shit[threadIdx.x >> 5] = h;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        int t = 0;
+        for (int w = 0; w < kMergeThreads / 32; ++w) {
+            s += ssum[w];
+            t += shit[w];
+        }
+        const int64_t c = a.chunk_off[dir] + (int64_t)b * a.nchunks[dir] + chunk;
+        a.chunk_sum[c] = s;
+        a.chunk_hits[c] = t;
+    }
+}
+
+// --------------------------------------------------------------------------------------------- host
+static int cdiv(int64_t x, int64_t y) { return (int)((x + y - 1) / y); }
+
+void plan_pruned(PrunedPlan& p, int B, int N, int M) {
+    p.B = B;
+    p.npts[0] = N;
+    p.npts[1] = M;
+    for (int c = 0; c < 2; ++c) {
+        p.ppad[c] = cdiv(p.npts[c], kPrQ) * kPrQ;
+        p.qtiles[c] = p.ppad[c] / kPrQ;
+        p.ttiles[c] = p.ppad[c] / kTile;
+    }
+    int bb = 0;
+    while ((1 << bb) < B) ++bb;
+    p.bbits = bb;
+    p.kbits = std::max(1, std::min(10, (32 - 1 - bb) / 3));
+    p.nbits = 1 + bb + 3 * p.kbits;
+    p.L = (int64_t)B * (N + M);
+    p.cand_off[0] = 0;
+    p.cand_off[1] = (int64_t)B * p.qtiles[0] * p.ttiles[1];
+    const int64_t ncand = p.cand_off[1] + (int64_t)B * p.qtiles[1] * p.ttiles[0];
+    p.nchunks[0] = cdiv(N, kMergeThreads);
+    p.nchunks[1] = cdiv(M, kMergeThreads);
+    p.chunk_off[0] = 0;
+    p.chunk_off[1] = (int64_t)B * p.nchunks[0];
+    const int64_t chunks = p.chunk_off[1] + (int64_t)B * p.nchunks[1];
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    p.off_bbox = take((size_t)2 * B * 6 * 4);
+    for (int i = 0; i < 2; ++i) {
+        p.off_keys[i] = take((size_t)p.L * 4);
+        p.off_vals[i] = take((size_t)p.L * 4);
+    }
+    p.off_counts = take(radix_sort_counts_words(p.L, p.nbits) * 4);
+    p.off_totals = take((size_t)kSortTotalsWords * 4);
+    for (int c = 0; c < 2; ++c) {
+        p.off_sorted[c] = take((size_t)B * p.ppad[c] * 16);
+        p.off_perm[c] = take((size_t)B * p.npts[c] * 4);
+        p.off_box[c] = take((size_t)B * p.ttiles[c] * 32);
+        p.off_box32[c] = take((size_t)B * p.ttiles[c] * kBlocksPerTile * 32);
+        p.off_best_d[c] = take((size_t)B * p.npts[c] * 4);
+        p.off_best_blk[c] = take((size_t)B * p.npts[c] * 4);
+    }
+    p.off_cand = take((size_t)ncand * 8);
+    p.off_chunk_sum = take((size_t)chunks * 8);
+    p.off_chunk_hits = take((size_t)chunks * 4);
+    p.bytes = off;
+    p.supported = p.ttiles[0] <= kPrMaxTiles && p.ttiles[1] <= kPrMaxTiles;
+}
+
+int pruned_launches(const PrunedPlan& p) { return 2 + radix_sort_launches(p.L, p.nbits) + 6; }
+
+cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
+                          cudaStream_t st) {
+    char* w = static_cast<char*>(ws);
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    float* bbox = reinterpret_cast<float*>(w + p.off_bbox);
+    {
+        BoxArgs a;
+        a.src[0] = x;
+        a.src[1] = y;
+        a.npts[0] = p.npts[0];
+        a.npts[1] = p.npts[1];
+        a.B = p.B;
+        a.bbox = bbox;
+        bbox_kernel<<<2 * p.B, 256, 0, st>>>(a);
+    }
+    uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
+    uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
+    const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);
+    {
+        MortonArgs a;
+        a.src[0] = x;
+        a.src[1] = y;
+        a.npts[0] = p.npts[0];
+        a.npts[1] = p.npts[1];
+        a.B = p.B;
+        a.kbits = p.kbits;
+        a.bbits = p.bbits;
+        a.bbox = bbox;
+        a.keys = keys[0];
+        a.vals = vals[0];
+        morton_kernel<<<grid_l, 256, 0, st>>>(a);
+    }
+    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
+                                     reinterpret_cast<uint32_t*>(w + p.off_totals), st);
+    float4* sorted[2];
+    int* perm[2];
+    float4* box[2];
+    float4* box32[2];
+    for (int c = 0; c < 2; ++c) {
+        sorted[c] = reinterpret_cast<float4*>(w + p.off_sorted[c]);
+        perm[c] = reinterpret_cast<int*>(w + p.off_perm[c]);
+        box[c] = reinterpret_cast<float4*>(w + p.off_box[c]);
+        box32[c] = reinterpret_cast<float4*>(w + p.off_box32[c]);
+    }
+    {
+        GatherArgs a;
+        a.src[0] = x;
+        a.src[1] = y;
+        a.B = p.B;
+        a.vals = vals[cur];
+        for (int c = 0; c < 2; ++c) {
+            a.npts[c] = p.npts[c];
+            a.ppad[c] = p.ppad[c];
+            a.sorted[c] = sorted[c];
+            a.perm[c] = perm[c];
+        }
+        gather_kernel<<<grid_l, 256, 0, st>>>(a);
+    }
+    {
+        AabbArgs a;
+        a.B = p.B;
+        for (int c = 0; c < 2; ++c) {
+            a.sorted[c] = sorted[c];
+            a.npts[c] = p.npts[c];
+            a.ppad[c] = p.ppad[c];
+            a.box[c] = box[c];
+            a.bbox32[c] = box32[c];
+        }
+        const int64_t tiles = (int64_t)p.B * (p.ttiles[0] + p.ttiles[1]);
+        aabb_kernel<<<cdiv(tiles * 32, 256), 256, 0, st>>>(a);
+    }
+    unsigned long long* cand = reinterpret_cast<unsigned long long*>(w + p.off_cand);
+    {
+        CandArgs a;
+        a.B = p.B;
+        for (int c = 0; c < 2; ++c) {
+            a.box[c] = box[c];
+            a.ppad[c] = p.ppad[c];
+            a.qtiles[c] = p.qtiles[c];
+            a.cand_off[c] = p.cand_off[c];
+        }
+        a.cand = cand;
+        int npow = 1;
+        while (npow < std::max(p.ttiles[0], p.ttiles[1])) npow <<= 1;
+        const size_t smem = (size_t)npow * 8;
+        static thread_local bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrMaxTiles * 8);
+            attr = true;
+        }
+        candidates_kernel<<<p.B * (p.qtiles[0] + p.qtiles[1]), 256, smem, st>>>(a);
+    }
+    float* best_d[2];
+    int* best_blk[2];
+    for (int c = 0; c < 2; ++c) {
+        best_d[c] = reinterpret_cast<float*>(w + p.off_best_d[c]);
+        best_blk[c] = reinterpret_cast<int*>(w + p.off_best_blk[c]);
+    }
+    {
+        PrunedArgs a;
+        for (int c = 0; c < 2; ++c) {
+            a.sorted[c] = sorted[c];
+            a.bbox32[c] = box32[c];
+            a.npts[c] = p.npts[c];
+            a.ppad[c] = p.ppad[c];
+            a.qtiles[c] = p.qtiles[c];
+            a.cand_off[c] = p.cand_off[c];
+            a.best_d[c] = best_d[c];
+            a.best_blk[c] = best_blk[c];
+        }
+        a.cand = cand;
+        if (g_prof_start) record_profile_event(g_prof_start, st);
+        nn_pruned_kernel<<<dim3(p.qtiles[0] + p.qtiles[1], p.B), kFwdThreads, 0, st>>>(a);
+        if (g_prof_stop) record_profile_event(g_prof_stop, st);
+    }
+    double* chunk_sum = reinterpret_cast<double*>(w + p.off_chunk_sum);
+    int* chunk_hits = reinterpret_cast<int*>(w + p.off_chunk_hits);
+    {
+        PrResolveArgs a;
+        a.B = p.B;
+        for (int c = 0; c < 2; ++c) {
+            a.sorted[c] = sorted[c];
+            a.perm[c] = perm[c];
+            a.npts[c] = p.npts[c];
+            a.ppad[c] = p.ppad[c];
+            a.nchunks[c] = p.nchunks[c];
+            a.chunk_off[c] = p.chunk_off[c];
+            a.best_d[c] = best_d[c];
+            a.best_blk[c] = best_blk[c];
+            a.d_out[c] = o.d[c];
+            a.idx_out[c] = o.idx[c];
+        }
+        a.chunk_sum = chunk_sum;
+        a.chunk_hits = chunk_hits;
+        a.tau2 = o.tau >= 0.f ? (double)o.tau * (double)o.tau : -1.0;
+        pruned_resolve_kernel<<<p.B * (p.nchunks[0] + p.nchunks[1]), kMergeThreads, 0, st>>>(a);
+    }
+    if (o.partials) {
+        cudaError_t e = launch_partials(chunk_sum, chunk_hits, p.nchunks, p.chunk_off, p.B, o.partials, 3, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace cdk

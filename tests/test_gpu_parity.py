@@ -349,3 +349,75 @@ def test_rows_cols_sharding_emulated(cd, world):
     np.testing.assert_array_equal(torch.cat([i for _, i in cols], 1).cpu().numpy(), full[3])
     np.testing.assert_allclose(part.cpu().numpy(), full[4], rtol=1e-12)
     np.testing.assert_array_equal(part.cpu().numpy()[:, 2:], full[4][:, 2:])
+
+
+# ------------------------------------------------------------------------------ exact pruned path (NEXT-2)
+def _check_pruned_vs_brute(cd, X, Y, tau=0.01):
+    """cd_forward_pruned must give the brute-force distances bit for bit; its indices must equal the
+    brute-force indices except among exactly equal distances, where the returned index must attain
+    the same fp32 distance (R3')."""
+    x, y, brute = _run(cd, X, Y, tau=tau)
+    pr = [t.cpu().numpy() for t in cd.forward(x, y, tau=tau, algorithm="pruned")]
+    torch.cuda.synchronize()
+    for dk, ik, Q, T in ((0, 1, X, Y), (2, 3, Y, X)):
+        np.testing.assert_array_equal(pr[dk].view(np.uint32), brute[dk].view(np.uint32))
+        diff = pr[ik] != brute[ik]
+        if diff.any():
+            rows = np.nonzero(diff.reshape(-1))[0]
+            b = rows // Q.shape[1]
+            q = Q.reshape(-1, 3)[rows][:, None]                      # (n, 1, 3)
+            t = T[b, pr[ik].reshape(-1)[rows]][:, None]              # the pruned path's neighbours
+            d_pair, _ = oracle.mirror_nn_f32(q, t)                   # their fp32 distances (fixed op order)
+            # an exact tie: the returned neighbour attains the same minimum distance
+            np.testing.assert_array_equal(d_pair.reshape(-1), pr[dk].reshape(-1)[rows])
+    np.testing.assert_allclose(pr[4], brute[4], rtol=1e-12)
+    np.testing.assert_array_equal(pr[4][:, 2:], brute[4][:, 2:])
+    return brute, pr
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_pruned_equals_brute_configs(cd, name):
+    X, Y = synth.config_inputs(name)
+    brute, pr = _check_pruned_vs_brute(cd, X, Y)
+    # random surface samples have no exact ties: indices identical
+    np.testing.assert_array_equal(pr[1], brute[1])
+    np.testing.assert_array_equal(pr[3], brute[3])
+
+
+@pytest.mark.parametrize("B,N,M", [(1, 1, 1), (2, 3, 7), (1, 1, 5000), (2, 5000, 1), (3, 2049, 4097),
+                                   (2, 100000, 30000)])
+def test_pruned_ragged(cd, B, N, M):
+    X, Y = synth.shape_pair(B, N, M, config_index=70 + N % 5)
+    _check_pruned_vs_brute(cd, X, Y)
+
+
+def test_pruned_adversarial(cd):
+    rng = np.random.default_rng(12)
+    # uniform cube (poor culling), duplicates (exact ties), clustered far away, identical clouds
+    X, Y = synth.uniform_pair(2, 6000, 5000, seed=5)
+    _check_pruned_vs_brute(cd, X, Y)
+    base = rng.uniform(-0.5, 0.5, size=(1, 3000, 3)).astype(np.float32)
+    _check_pruned_vs_brute(cd, base, np.concatenate([base, base[:, ::-1]], axis=1))
+    Yc = rng.uniform(-0.5, 0.5, size=(1, 4000, 3)).astype(np.float32)
+    Xc = (Yc[:, :1] + 10.0 + rng.normal(scale=1e-3, size=(1, 3000, 3))).astype(np.float32)
+    _check_pruned_vs_brute(cd, Xc, Yc)
+    S, _ = synth.shape_pair(2, 4000, 10, config_index=71)
+    _, pr = _check_pruned_vs_brute(cd, S, S.copy(), tau=0.0)
+    assert np.all(pr[0] == 0)
+    k = np.arange(12)
+    g = (np.stack(np.meshgrid(k, k, k, indexing="ij"), -1).reshape(-1, 3) * 2.0 ** -5)[None].astype(np.float32)
+    _check_pruned_vs_brute(cd, (g[:, :700] + 2.0 ** -6).astype(np.float32), g)   # exact 8-way ties
+
+
+def test_pruned_large_sampled(cd):
+    X, Y = synth.config_inputs("c5")
+    x, y = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    pr = [t.cpu().numpy() for t in cd.forward(x, y, tau=0.01, algorithm="pruned")]
+    B, N, M = X.shape[0], X.shape[1], Y.shape[1]
+    rng = np.random.default_rng(6)
+    rows = np.unique(np.concatenate([rng.choice(B * N, 400, replace=False), [0, N - 1, B * N - 1]]))
+    d1, i1, d2 = oracle.nn(X, Y, rows=rows)
+    dm, im = oracle.mirror_nn_f32(X, Y, rows=rows)
+    np.testing.assert_array_equal(pr[0].reshape(-1)[rows], dm)
+    clear = (d2 - d1) > 1e-6 * d1
+    np.testing.assert_array_equal(pr[1].reshape(-1)[rows][clear], i1[clear])
