@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--no-pruned", action="store_true", help="skip the exact pruned (NEXT-2) comparison")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise the multi-rank "
                     "logic when several ranks share one GPU")
     return ap.parse_args()
@@ -333,6 +334,46 @@ def main():
     value = pairs_total / (ms_per_step * 1e-3)
     loss = float(out["loss"].item())
 
+    # ---------------------------------------------------------------- exact pruned algorithm (NEXT-2)
+    pruned = None
+    if world == 1 and not args.no_pruned:
+        class PrunedEngine:
+            forward = staticmethod(lambda xx, yy, tau=None: cd.forward_pruned(xx, yy, tau=tau))
+            finalize = staticmethod(cd.finalize)
+            backward = staticmethod(cd.backward)
+
+        def pstep():
+            return pdist.batch_sharded_step(PrunedEngine, x, y, B_global, b0, tau=tau, w1=w1, w2=w2)
+
+        for _ in range(args.warmup):
+            pout = pstep()
+        torch.cuda.synchronize()
+        pgraph = None
+        if not args.no_graph:
+            pgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(pgraph):
+                pout = pstep()
+            for _ in range(args.warmup):
+                pgraph.replay()
+        torch.cuda.synchronize()
+        pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            pev[k][0].record()
+            if pgraph is not None:
+                pgraph.replay()
+            else:
+                pout = pstep()
+            pev[k][1].record()
+        torch.cuda.synchronize()
+        pms = sum(a.elapsed_time(b) for a, b in pev) / K
+        ploss = float(pout["loss"].item())
+        pruned = {"ms_per_step": pms, "value_effective": pairs_total / (pms * 1e-3), "unit": UNIT,
+                  "speedup_vs_brute_step": ms_per_step / pms, "loss": ploss,
+                  "loss_rel_diff_vs_brute": abs(ploss - loss) / max(abs(loss), 1e-300),
+                  "note": ("cd_forward_pruned (exact: Morton tiles + lower-bound culling, SURVEY §8.f NEXT-2) "
+                           "+ finalize + backward; effective = the same 2*B*N*M directed pairs / step time")}
+
     # ---------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
@@ -418,6 +459,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "pruned": pruned,
             "gpu_launches": launches * K,
             "gpu_launches_per_step": launches,
             "clocks": clocks,
