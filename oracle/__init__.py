@@ -19,6 +19,10 @@ Every function follows a plain definition, cited:
                   pinned only to the stated definition and hand examples.
 * ``backward``  — SPEC.md:441 "VJP holds the argmin fixed": see oracle_backward in
                   chamfer_oracle.c.
+* ``sample_mesh`` / ``sample_vjp`` — NEXT-4 (SPEC.md:228-245, PAPER.md:196 "differentiable
+                  surface sampling ... reparameterization trick"): area-proportional face choice with
+                  an exact integer CDF (R19), square-root barycentrics (R20),
+                  points (R21) and the VJP with choices fixed (R22), fp64.
 * ``mirror_nn_f32`` — not the oracle; fp32 re-evaluation of DESIGN.md §4.2's fixed op order,
                   used to check GPU distance bits.
 """
@@ -67,6 +71,11 @@ def _load():
             lib.mirror_nn_f32.argtypes = [f32p, f32p, i64, i64, i64, i64p, i64, f32p, i32p, ctypes.c_int]
             lib.mirror_nn_f32.restype = ctypes.c_int
             lib.oracle_max_threads.restype = ctypes.c_int
+            u32p, u64p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64)
+            lib.oracle_sample_mesh.argtypes = [f32p, i32p, i64, i64, i64, i64, u32p, f32p, f64p, i32p, f64p, u64p]
+            lib.oracle_sample_mesh.restype = ctypes.c_int
+            lib.oracle_sample_vjp.argtypes = [f64p, i32p, i32p, i64, i64, i64, i64, f64p, f64p]
+            lib.oracle_sample_vjp.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -237,3 +246,41 @@ def mirror_nn_f32(q, t, rows=None, nthreads: int = 0):
     if rows is None:
         return d.reshape(B, N), idx.reshape(B, N)
     return d, idx
+
+
+def sample_mesh(verts, faces, r_face, r_bary):
+    """NEXT-4 forward (R19-R21).  verts (B,Nv,3) fp32, faces (Nf,3) int32, r_face (B,N) uint32,
+    r_bary (B,N,2) fp32 uniforms.  Returns (points fp64 (B,N,3), face_idx (B,N), bary fp64 (B,N,3),
+    cdf uint64 (B,Nf))."""
+    v = np.ascontiguousarray(verts, np.float32)
+    f = np.ascontiguousarray(faces, np.int32)
+    rf = np.ascontiguousarray(r_face, np.uint32)
+    rb = np.ascontiguousarray(r_bary, np.float32)
+    B, Nv, _ = v.shape
+    Nf = f.shape[0]
+    N = rf.shape[1]
+    pts = np.empty((B, N, 3), np.float64)
+    fi = np.empty((B, N), np.int32)
+    bary = np.empty((B, N, 3), np.float64)
+    cdf = np.empty((B, Nf), np.uint64)
+    rc = _load().oracle_sample_mesh(_ptr(v, ctypes.c_float), _ptr(f, ctypes.c_int32), B, Nv, Nf, N,
+                                    _ptr(rf, ctypes.c_uint32), _ptr(rb, ctypes.c_float), _ptr(pts, ctypes.c_double),
+                                    _ptr(fi, ctypes.c_int32), _ptr(bary, ctypes.c_double), _ptr(cdf, ctypes.c_uint64))
+    if rc != 0:
+        raise ValueError(f"oracle_sample_mesh failed rc={rc}")
+    return pts, fi, bary, cdf
+
+
+def sample_vjp(bary, face_idx, faces, Nv, grad_points):
+    """NEXT-4 VJP (R22): grad w.r.t. the vertices of sum(grad_points * points), choices fixed."""
+    ba = np.ascontiguousarray(bary, np.float64)
+    fi = np.ascontiguousarray(face_idx, np.int32)
+    f = np.ascontiguousarray(faces, np.int32)
+    g = np.ascontiguousarray(grad_points, np.float64)
+    B, N, _ = ba.shape
+    out = np.empty((B, Nv, 3), np.float64)
+    rc = _load().oracle_sample_vjp(_ptr(ba, ctypes.c_double), _ptr(fi, ctypes.c_int32), _ptr(f, ctypes.c_int32), B, Nv,
+                                   f.shape[0], N, _ptr(g, ctypes.c_double), _ptr(out, ctypes.c_double))
+    if rc != 0:
+        raise ValueError(f"oracle_sample_vjp failed rc={rc}")
+    return out

@@ -24,6 +24,9 @@
  *                        (SPEC.md:441), accumulated in the defining order (own term, then
  *                        scatter terms in ascending source index) plus the condition scale
  *                        S = sum |terms| used by the gradient gate (R14).
+ *   oracle_sample_mesh   NEXT-4: area-proportional face choice (exact integer CDF, R19), square-
+ *                        root barycentrics, sampled points — fp64.
+ *   oracle_sample_vjp    NEXT-4: VJP of the sampled points w.r.t. the vertices, choices fixed.
  *   mirror_nn_f32        NOT the oracle: an fp32 re-evaluation of the distance formula in the
  *                        operation order DESIGN.md §4.2 fixes for the kernel
  *                        (dx=x-y; s=dx*dx; s=fma(dy,dy,s); s=fma(dz,dz,s), all IEEE RN),
@@ -37,6 +40,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -206,5 +210,109 @@ int mirror_nn_f32(const float* q, const float* t, int64_t B, int64_t N, int64_t 
         d[r] = best;
         idx[r] = arg;
     }
+    return 0;
+}
+
+/* ====================================================================================== NEXT-4
+ * Differentiable surface sampling ("differentiable surface sampling
+ * ... by application of the reparameterization trick").  Plain definitions in fp64; the random
+ * numbers are inputs (uint32 r_face, fp32 r1, r2 per sample).  Readings R19-R22 in DESIGN.md §11.
+ *
+ * R19 face choice with probability proportional to area, made exactly reproducible:
+ *   e1 = v1 - v0, e2 = v2 - v0 (fp64 from fp32 vertices, exact);
+ *   c  = e1 x e2 (cx = e1y*e2z - e1z*e2y, cy = e1z*e2x - e1x*e2z, cz = e1x*e2y - e1y*e2x);
+ *   area_f = 0.5 * sqrt(cx*cx + cy*cy + cz*cz)              (fp64, this op order, no contraction)
+ *   k = 52 - e where Nf * max_f area_f = m * 2^e, m in [0.5, 1)  (frexp);  q_f = floor(area_f * 2^k)
+ *   P_f = sum_{g <= f} q_g (exact integers), S = P_{Nf-1};  t = (r_face * S) >> 32;
+ *   face = min { f : P_f > t }   (S == 0: face 0)
+ * R20 barycentrics: s = sqrt(r1); (w0, w1, w2) = (1 - s, s (1 - r2), s r2)
+ * R21 point = w0 v_a + w1 v_b + w2 v_c
+ * R22 VJP with face choice and weights fixed: grad_v = sum over (sample i, corner k) with
+ *     faces[face_i][k] == v of w_{i,k} * g_i, accumulated in ascending (i, k) order.
+ */
+static double area64(const float* v, const int32_t* f) {
+    const float* a = v + 3 * (int64_t)f[0];
+    const float* b = v + 3 * (int64_t)f[1];
+    const float* c = v + 3 * (int64_t)f[2];
+    double e1x = (double)b[0] - (double)a[0], e1y = (double)b[1] - (double)a[1], e1z = (double)b[2] - (double)a[2];
+    double e2x = (double)c[0] - (double)a[0], e2y = (double)c[1] - (double)a[1], e2z = (double)c[2] - (double)a[2];
+    double cx = e1y * e2z - e1z * e2y;
+    double cy = e1z * e2x - e1x * e2z;
+    double cz = e1x * e2y - e1y * e2x;
+    return 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+}
+
+/* verts B x Nv x 3 fp32, faces Nf x 3 (shared topology), r_face B x N uint32, r_bary B x N x 2 fp32.
+ * Outputs: points B x N x 3 (fp64), face_idx B x N, bary B x N x 3 (fp64); cdf (B x Nf uint64, may be
+ * NULL) = the inclusive quantised prefix P_f. */
+int oracle_sample_mesh(const float* verts, const int32_t* faces, int64_t B, int64_t Nv, int64_t Nf, int64_t N,
+                       const uint32_t* r_face, const float* r_bary, double* points, int32_t* face_idx,
+                       double* bary, uint64_t* cdf_out) {
+    if (!verts || !faces || !r_face || !r_bary || !points || !face_idx || B < 1 || Nv < 1 || Nf < 1 || N < 1) return 1;
+    uint64_t* P = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)Nf);
+    if (!P) return 3;
+    for (int64_t b = 0; b < B; ++b) {
+        const float* v = verts + 3 * b * Nv;
+        double amax = 0.0;
+        for (int64_t f = 0; f < Nf; ++f) {
+            for (int k = 0; k < 3; ++k)
+                if (faces[3 * f + k] < 0 || faces[3 * f + k] >= Nv) { free(P); return 2; }
+            double a = area64(v, faces + 3 * f);
+            if (a > amax) amax = a;
+        }
+        int e = 0;
+        if (amax > 0.0) frexp(amax * (double)Nf, &e);
+        uint64_t run = 0;
+        for (int64_t f = 0; f < Nf; ++f) {
+            double a = area64(v, faces + 3 * f);
+            uint64_t q = amax > 0.0 ? (uint64_t)floor(ldexp(a, 52 - e)) : 0;
+            run += q;
+            P[f] = run;
+            if (cdf_out) cdf_out[b * Nf + f] = run;
+        }
+        const uint64_t S = run;
+        for (int64_t i = 0; i < N; ++i) {
+            const int64_t s = b * N + i;
+            int64_t face = 0;
+            if (S > 0) {
+                const unsigned __int128 prod = (unsigned __int128)r_face[s] * (unsigned __int128)S;
+                const uint64_t t = (uint64_t)(prod >> 32);
+                /* plain linear scan (the definition: smallest f with P_f > t) */
+                face = 0;
+                while (face < Nf - 1 && !(P[face] > t)) ++face;
+            }
+            face_idx[s] = (int32_t)face;
+            const double r1 = (double)r_bary[2 * s], r2 = (double)r_bary[2 * s + 1];
+            const double sq = sqrt(r1);
+            const double w[3] = {1.0 - sq, sq * (1.0 - r2), sq * r2};
+            for (int c = 0; c < 3; ++c) {
+                double acc = 0.0;
+                for (int k = 0; k < 3; ++k) acc += w[k] * (double)v[3 * (int64_t)faces[3 * face + k] + c];
+                points[3 * s + c] = acc;
+            }
+            if (bary)
+                for (int k = 0; k < 3; ++k) bary[3 * s + k] = w[k];
+        }
+    }
+    free(P);
+    return 0;
+}
+
+/* VJP (R22): bary B x N x 3 (the weights used by the forward), face_idx B x N, grad_points B x N x 3;
+ * output grad_verts B x Nv x 3 (fp64). */
+int oracle_sample_vjp(const double* bary, const int32_t* face_idx, const int32_t* faces, int64_t B, int64_t Nv,
+                      int64_t Nf, int64_t N, const double* grad_points, double* grad_verts) {
+    if (!bary || !face_idx || !faces || !grad_points || !grad_verts) return 1;
+    for (int64_t j = 0; j < B * Nv * 3; ++j) grad_verts[j] = 0.0;
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t i = 0; i < N; ++i) {
+            const int64_t s = b * N + i;
+            const int64_t f = face_idx[s];
+            if (f < 0 || f >= Nf) return 2;
+            for (int k = 0; k < 3; ++k) {
+                const int64_t v = faces[3 * f + k];
+                for (int c = 0; c < 3; ++c) grad_verts[3 * (b * Nv + v) + c] += bary[3 * s + k] * grad_points[3 * s + c];
+            }
+        }
     return 0;
 }

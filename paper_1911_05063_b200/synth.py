@@ -132,3 +132,23 @@ def config_inputs(name: str, b0: int = 0, B: int | None = None):
     c = CONFIGS[name]
     B = c["B"] if B is None else B
     return shape_pair(B, c["N"], c["M"], config_index=c["index"], b0=b0)
+
+
+def mesh_batch(B: int, config_index: int = 100, subdiv: int = 5):
+    """Deformed-icosphere meshes sharing one topology: verts (B,V,3) fp32, faces (F,3) int32."""
+    _, faces = icosphere(subdiv)
+    verts = []
+    for b in range(B):
+        rs, _, _ = _streams(config_index, b)
+        v, _ = random_shape(rs, subdiv)
+        verts.append(v)
+    return np.stack(verts).astype(np.float32), faces.astype(np.int32)
+
+
+def sampling_randoms(B: int, N: int, seed: int = 0):
+    """Random numbers the sampling step draws (passed to both sides as inputs): r_face (B,N) uint32,
+    r_bary (B,N,2) fp32 uniforms in [0, 1)."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([ROOT_SEED, 2000 + seed])))
+    r_face = rng.integers(0, 2 ** 32, size=(B, N), dtype=np.uint64).astype(np.uint32)
+    r_bary = rng.random(size=(B, N, 2), dtype=np.float32)
+    return r_face, r_bary
