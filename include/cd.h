@@ -63,7 +63,9 @@ typedef enum {
     CD_OP_FSCORE = 1,    /* cd_fscore */
     CD_OP_BACKWARD = 2,  /* cd_backward */
     CD_OP_STEP = 3,      /* cd_step_host: forward + finalize + backward (+ staging of the clouds) */
-    CD_OP_FORWARD_PRUNED = 4 /* cd_forward_pruned */
+    CD_OP_FORWARD_PRUNED = 4, /* cd_forward_pruned */
+    CD_OP_SAMPLE = 5,          /* cd_sample_mesh (cd_sample_workspace_size) */
+    CD_OP_SAMPLE_BACKWARD = 6  /* cd_sample_mesh_backward (cd_sample_workspace_size) */
 } cd_op;
 
 /*
@@ -185,6 +187,35 @@ CD_API cd_status cd_step_host(const float* x_host, const float* y_host, int B, i
                        float tau, float w1, float w2,
                        float* loss_host, float* fscore_host, float* grad_x_host, float* grad_y_host,
                        void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_sample_mesh — differentiable surface sampling, the step before the Chamfer path
+ * ("differentiable surface sampling ... by
+ * application of the reparameterization trick").  B meshes sharing one topology:
+ *   verts [B x Nv x 3] fp32, faces [Nf x 3] int32 (vertex indices, clamped to [0, Nv) if outside);
+ *   random inputs (drawn by the caller): r_face [B x N] uint32, r_bary [B x N x 2] fp32 in [0, 1).
+ *   Face choice with probability proportional to area, as an exact integer decision (R19):
+ *     area_f in fp64 (fixed op order), q_f = floor(area_f * 2^k), k = 52 - e with
+ *     Nf * max_f area_f = m 2^e (m in [0.5,1)); P = inclusive prefix of q; t = (r_face * P_last) >> 32;
+ *     face = min { f : P_f > t } (face 0 when every area is 0).
+ *   Barycentrics (R20): s = sqrt(r1), w = (1 - s, s (1 - r2), s r2) in fp32 .rn;
+ *   point = (w0 v_a + w1 v_b) + w2 v_c (fp32 .rn, R21).
+ *   Outputs: points [B x N x 3], face_idx [B x N], bary [B x N x 3] (may be NULL; needed by the
+ *   backward).  Workspace: cd_sample_workspace_size(CD_OP_SAMPLE, ...).
+ * cd_sample_mesh_backward — VJP with the face choice and weights fixed (R22):
+ *   grad_verts[b, v] = sum over (sample i, corner k) with faces[face_i][k] == v of
+ *   bary[i][k] * grad_points[i], accumulated in fp64 in ascending (i, k) order (stable radix sort,
+ *   no floating-point atomics); grad_verts [B x Nv x 3] is fully written (0 for unsampled vertices).
+ */
+CD_API cd_status cd_sample_mesh(const float* verts, const int32_t* faces, int B, int Nv, int Nf, int N,
+                         const uint32_t* r_face, const float* r_bary,
+                         float* points, int32_t* face_idx, float* bary,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream);
+CD_API cd_status cd_sample_mesh_backward(const int32_t* faces, const int32_t* face_idx, const float* bary,
+                         int B, int Nv, int Nf, int N, const float* grad_points, float* grad_verts,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream);
+CD_API size_t cd_sample_workspace_size(int op, int B, int Nv, int Nf, int N);
+CD_API int cd_sample_launch_count(int op, int B, int Nv, int Nf, int N);
 
 /* Workspace bytes needed by an operation for these sizes (full slices).  0 on invalid sizes. */
 CD_API size_t cd_workspace_size(int op, int B, int N, int M);

@@ -289,3 +289,75 @@ def set_profile_events(start=None, stop=None):
     """Record torch.cuda.Events around the nn_fwd_kernel of subsequent forwards (None disables)."""
     _lib.load().cd_set_profile_events(ctypes.c_void_p(start.cuda_event) if start is not None else None,
                                       ctypes.c_void_p(stop.cuda_event) if stop is not None else None)
+
+
+
+# ---------------------------------------------------------------------------------------- NEXT-4
+def _sample_ws(op, B, Nv, Nf, N, device):
+    lib = _lib.load()
+    n = int(lib.cd_sample_workspace_size(op, B, Nv, Nf, N))
+    if n == 0:
+        raise _lib.CdError(1, f"invalid sizes B={B} Nv={Nv} Nf={Nf} N={N}")
+    key = (str(device), op, B, Nv, Nf, N)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(n, dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def sample_mesh(verts: torch.Tensor, faces: torch.Tensor, r_face: torch.Tensor, r_bary: torch.Tensor):
+    """cd_sample_mesh: (points [B,N,3], face_idx [B,N], bary [B,N,3]) for B meshes sharing `faces`."""
+    if not verts.is_cuda or verts.dtype != torch.float32 or verts.dim() != 3:
+        raise TypeError("verts must be CUDA fp32 (B, Nv, 3)")
+    verts = verts.contiguous()
+    faces = faces.to(torch.int32).contiguous()
+    B, Nv, _ = verts.shape
+    Nf = faces.shape[0]
+    N = r_face.shape[1]
+    dev = verts.device
+    pts = torch.empty((B, N, 3), dtype=torch.float32, device=dev)
+    fi = torch.empty((B, N), dtype=torch.int32, device=dev)
+    ba = torch.empty((B, N, 3), dtype=torch.float32, device=dev)
+    ws = _sample_ws(_lib.CD_OP_SAMPLE, B, Nv, Nf, N, dev)
+    check(_lib.load().cd_sample_mesh(_ptr(verts), _ptr(faces), B, Nv, Nf, N, _ptr(r_face.contiguous()),
+                                     _ptr(r_bary.contiguous()), _ptr(pts), _ptr(fi), _ptr(ba), _ptr(ws), ws.numel(),
+                                     _stream()))
+    return pts, fi, ba
+
+
+def sample_mesh_backward(faces: torch.Tensor, face_idx: torch.Tensor, bary: torch.Tensor, Nv: int,
+                         grad_points: torch.Tensor):
+    """cd_sample_mesh_backward: gradient w.r.t. the vertices (choices fixed)."""
+    faces = faces.to(torch.int32).contiguous()
+    B, N = face_idx.shape
+    Nf = faces.shape[0]
+    dev = bary.device
+    gv = torch.empty((B, Nv, 3), dtype=torch.float32, device=dev)
+    ws = _sample_ws(_lib.CD_OP_SAMPLE_BACKWARD, B, Nv, Nf, N, dev)
+    check(_lib.load().cd_sample_mesh_backward(_ptr(faces), _ptr(face_idx.contiguous()), _ptr(bary.contiguous()), B,
+                                              Nv, Nf, N, _ptr(grad_points.contiguous().float()), _ptr(gv), _ptr(ws),
+                                              ws.numel(), _stream()))
+    return gv
+
+
+class SampleMeshFunction(torch.autograd.Function):
+    """points = sample(verts; faces, randoms) with the reparameterisation gradient."""
+
+    @staticmethod
+    def forward(ctx, verts, faces, r_face, r_bary):
+        pts, fi, ba = sample_mesh(verts, faces, r_face, r_bary)
+        ctx.save_for_backward(faces, fi, ba)
+        ctx.Nv = verts.shape[1]
+        ctx.mark_non_differentiable(fi)
+        return pts, fi
+
+    @staticmethod
+    def backward(ctx, grad_points, _grad_fi):
+        faces, fi, ba = ctx.saved_tensors
+        return sample_mesh_backward(faces, fi, ba, ctx.Nv, grad_points), None, None, None
+
+
+def sample_points(verts, faces, r_face, r_bary):
+    """Differentiable surface sampling: returns (points, face_idx); points carry gradients to verts."""
+    return SampleMeshFunction.apply(verts, faces, r_face, r_bary)

@@ -299,6 +299,60 @@ cd_status cd_forward_pruned(const float* x, const float* y, int B, int N, int M,
                        "cd_forward_pruned");
 }
 
+cd_status cd_sample_mesh(const float* verts, const int32_t* faces, int B, int Nv, int Nf, int N,
+                         const uint32_t* r_face, const float* r_bary, float* points, int32_t* face_idx, float* bary,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    if (B < 1 || Nv < 3 || Nf < 1 || N < 1)
+        return fail(CD_ERR_INVALID_VALUE, "need B >= 1, Nv >= 3, Nf >= 1, N >= 1 (got %d %d %d %d)", B, Nv, Nf, N);
+    if ((long long)B * N * 3 > 0x7fffffffLL || (long long)B * Nv > 0x7fffffffLL)
+        return fail(CD_ERR_TOO_LARGE, "B*N*3 or B*Nv exceeds 2^31-1");
+    if (!verts || !faces || !r_face || !r_bary || !points || !face_idx || !workspace)
+        return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const size_t need = cdk::sample_workspace(B, Nv, Nf, N);
+    if (workspace_bytes < need) return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu", workspace_bytes, need);
+    cd_status s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_sample(verts, faces, B, Nv, Nf, N, r_face, r_bary, points, face_idx, bary, workspace,
+                                          static_cast<cudaStream_t>(stream)),
+                       "cd_sample_mesh");
+}
+
+cd_status cd_sample_mesh_backward(const int32_t* faces, const int32_t* face_idx, const float* bary, int B, int Nv,
+                                  int Nf, int N, const float* grad_points, float* grad_verts, void* workspace,
+                                  size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    if (B < 1 || Nv < 3 || Nf < 1 || N < 1)
+        return fail(CD_ERR_INVALID_VALUE, "need B >= 1, Nv >= 3, Nf >= 1, N >= 1 (got %d %d %d %d)", B, Nv, Nf, N);
+    if ((long long)B * N * 3 > 0x7fffffffLL || (long long)B * Nv > 0x7fffffffLL)
+        return fail(CD_ERR_TOO_LARGE, "B*N*3 or B*Nv exceeds 2^31-1");
+    if (!faces || !face_idx || !bary || !grad_points || !grad_verts || !workspace)
+        return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const size_t need = cdk::sample_backward_workspace(B, Nv, Nf, N);
+    if (workspace_bytes < need) return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu", workspace_bytes, need);
+    cd_status s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_sample_backward(faces, face_idx, bary, B, Nv, Nf, N, grad_points, grad_verts,
+                                                   workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_sample_mesh_backward");
+}
+
+size_t cd_sample_workspace_size(int op, int B, int Nv, int Nf, int N) {
+    if (B < 1 || Nv < 3 || Nf < 1 || N < 1) return 0;
+    if (op == CD_OP_SAMPLE) return cdk::sample_workspace(B, Nv, Nf, N);
+    if (op == CD_OP_SAMPLE_BACKWARD) return cdk::sample_backward_workspace(B, Nv, Nf, N);
+    return 0;
+}
+
+int cd_sample_launch_count(int op, int B, int Nv, int Nf, int N) {
+    if (B < 1 || Nv < 3 || Nf < 1 || N < 1) return 0;
+    if (op == CD_OP_SAMPLE) return 2;
+    if (op == CD_OP_SAMPLE_BACKWARD) return cdk::sample_backward_launches(B, Nv, Nf, N);
+    return 0;
+}
+
 int cd_set_forward_mode(int mode) {
     int old = g_forward_mode;
     g_forward_mode = (mode == 1 || mode == 2) ? mode : 0;

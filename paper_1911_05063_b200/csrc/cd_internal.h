@@ -70,6 +70,15 @@ int pruned_launches(const PrunedPlan& p);
 cudaError_t launch_partials(const double* chunk_sum, const int* chunk_hits, const int nchunks[2],
                             const int64_t chunk_off[2], int B, double* partials, int dirmask, cudaStream_t st);
 
+// Differentiable mesh surface sampling (mesh_sample.cu, NEXT-4).
+size_t sample_workspace(int B, int Nv, int Nf, int N);
+cudaError_t launch_sample(const float* verts, const int* faces, int B, int Nv, int Nf, int N, const unsigned* r_face,
+                          const float* r_bary, float* points, int* face_idx, float* bary, void* ws, cudaStream_t st);
+size_t sample_backward_workspace(int B, int Nv, int Nf, int N);
+int sample_backward_launches(int B, int Nv, int Nf, int N);
+cudaError_t launch_sample_backward(const int* faces, const int* face_idx, const float* bary, int B, int Nv, int Nf,
+                                   int N, const float* grad_points, float* grad_verts, void* ws, cudaStream_t st);
+
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.
 size_t fscore_workspace(int B, int N, int M);
 cudaError_t launch_fscore(const float* d_xy, const float* d_yx, int B, int N, int M, float tau, float* fscore,
