@@ -23,6 +23,11 @@ Every function follows a plain definition, cited:
                   surface sampling ... reparameterization trick"): area-proportional face choice with
                   an exact integer CDF (R19), square-root barycentrics (R20),
                   points (R21) and the VJP with choices fixed (R22), fp64.
+* ``p2s`` / ``p2s_loss`` — NEXT-3 point-to-surface ("the point-to-surface loss [GEOMetrics]
+                  for Meshes"): closest triangle by brute force with the region
+                  decomposition of the closest point, loss = mean_b mean_i d, VJP 2 g (p - closest)
+                  w.r.t. the points and, through the closest point's barycentrics, w.r.t. the vertices
+                  (R23-R25).
 * ``mirror_nn_f32`` — not the oracle; fp32 re-evaluation of DESIGN.md §4.2's fixed op order,
                   used to check GPU distance bits.
 """
@@ -76,6 +81,9 @@ def _load():
             lib.oracle_sample_mesh.restype = ctypes.c_int
             lib.oracle_sample_vjp.argtypes = [f64p, i32p, i32p, i64, i64, i64, i64, f64p, f64p]
             lib.oracle_sample_vjp.restype = ctypes.c_int
+            lib.oracle_p2s.argtypes = [f32p, f32p, i32p, i64, i64, i64, i64, i64p, i64, f64p, i32p, f64p, f64p, f64p,
+                                       ctypes.c_int]
+            lib.oracle_p2s.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -284,3 +292,50 @@ def sample_vjp(bary, face_idx, faces, Nv, grad_points):
     if rc != 0:
         raise ValueError(f"oracle_sample_vjp failed rc={rc}")
     return out
+
+
+def p2s(points, verts, faces, rows=None, nthreads: int = 0):
+    """NEXT-3: per point min squared distance to the mesh (B,N), face (lowest on ties), second-best d,
+    closest point (B,N,3) and its barycentrics (B,N,3) — fp64 brute force."""
+    P = np.ascontiguousarray(points, np.float32)
+    V = np.ascontiguousarray(verts, np.float32)
+    F = np.ascontiguousarray(faces, np.int32)
+    B, N, _ = P.shape
+    Nv = V.shape[1]
+    Nf = F.shape[0]
+    if rows is not None:
+        rows = np.ascontiguousarray(rows, np.int64)
+        n = rows.shape[0]
+    else:
+        n = B * N
+    d = np.empty(n, np.float64)
+    fi = np.empty(n, np.int32)
+    d2 = np.empty(n, np.float64)
+    cl = np.empty((n, 3), np.float64)
+    la = np.empty((n, 3), np.float64)
+    rc = _load().oracle_p2s(_ptr(P, ctypes.c_float), _ptr(V, ctypes.c_float), _ptr(F, ctypes.c_int32), B, N, Nv, Nf,
+                            _ptr(rows, ctypes.c_int64), n if rows is not None else 0, _ptr(d, ctypes.c_double),
+                            _ptr(fi, ctypes.c_int32), _ptr(d2, ctypes.c_double), _ptr(cl, ctypes.c_double),
+                            _ptr(la, ctypes.c_double), int(nthreads))
+    if rc != 0:
+        raise ValueError(f"oracle_p2s failed rc={rc}")
+    if rows is None:
+        return d.reshape(B, N), fi.reshape(B, N), d2.reshape(B, N), cl.reshape(B, N, 3), la.reshape(B, N, 3)
+    return d, fi, d2, cl, la
+
+
+def p2s_loss(d):
+    """loss = mean_b mean_i d ("mean over points", batch mean as R1)."""
+    d = np.asarray(d, np.float64)
+    return math.fsum((math.fsum(row.tolist()) / d.shape[1] for row in d)) / d.shape[0]
+
+
+def p2s_grads(points, verts, faces, face, closest, lam, g):
+    """VJP of sum_i g_i d_i with the closest point held fixed (SPEC.md:468): grad_p = 2 g (p - c);
+    grad_v = sum over (point, corner) of -2 g (p - c) lam_k (R25).  Returns (grad_p, grad_v) fp64."""
+    P = np.asarray(points, np.float64)
+    g = np.asarray(g, np.float64)
+    diff = P - np.asarray(closest, np.float64)
+    gp = 2.0 * g[..., None] * diff
+    gv = sample_vjp(np.asarray(lam, np.float64), face, faces, np.asarray(verts).shape[1], -gp)
+    return gp, gv

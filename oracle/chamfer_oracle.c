@@ -27,6 +27,9 @@
  *   oracle_sample_mesh   NEXT-4: area-proportional face choice (exact integer CDF, R19), square-
  *                        root barycentrics, sampled points — fp64.
  *   oracle_sample_vjp    NEXT-4: VJP of the sampled points w.r.t. the vertices, choices fixed.
+ *   oracle_p2s           NEXT-3: point-to-surface: squared distance to the closest
+ *                        triangle (region decomposition), lowest face on ties, closest point + its
+ *                        barycentric coordinates — fp64.
  *   mirror_nn_f32        NOT the oracle: an fp32 re-evaluation of the distance formula in the
  *                        operation order DESIGN.md §4.2 fixes for the kernel
  *                        (dx=x-y; s=dx*dx; s=fma(dy,dy,s); s=fma(dz,dz,s), all IEEE RN),
@@ -314,5 +317,106 @@ int oracle_sample_vjp(const double* bary, const int32_t* face_idx, const int32_t
                 for (int c = 0; c < 3; ++c) grad_verts[3 * (b * Nv + v) + c] += bary[3 * s + k] * grad_points[3 * s + c];
             }
         }
+    return 0;
+}
+
+/* ====================================================================================== NEXT-3
+ * Point-to-surface loss ("the point-to-surface loss [GEOMetrics] for Meshes";
+ * "mean over points of squared distance to the closest triangle; VJP: 2(p - closest)/P
+ * per point, closest point held fixed").  fp64, brute force over all faces (plain definition).
+ * Closest point on a triangle: the standard region decomposition (Voronoi regions of the vertices,
+ * edges and face), written out below.  Readings R23-R25 in DESIGN.md §11.
+ */
+static void closest_on_triangle(const double p[3], const double a[3], const double b[3], const double c[3],
+                                double out[3], double lam[3]) {
+    double ab[3], ac[3], ap[3], bp[3], cp[3];
+    for (int k = 0; k < 3; ++k) {
+        ab[k] = b[k] - a[k];
+        ac[k] = c[k] - a[k];
+        ap[k] = p[k] - a[k];
+        bp[k] = p[k] - b[k];
+        cp[k] = p[k] - c[k];
+    }
+    const double d1 = ab[0] * ap[0] + ab[1] * ap[1] + ab[2] * ap[2];
+    const double d2 = ac[0] * ap[0] + ac[1] * ap[1] + ac[2] * ap[2];
+    const double d3 = ab[0] * bp[0] + ab[1] * bp[1] + ab[2] * bp[2];
+    const double d4 = ac[0] * bp[0] + ac[1] * bp[1] + ac[2] * bp[2];
+    const double d5 = ab[0] * cp[0] + ab[1] * cp[1] + ab[2] * cp[2];
+    const double d6 = ac[0] * cp[0] + ac[1] * cp[1] + ac[2] * cp[2];
+    const double vc = d1 * d4 - d3 * d2;
+    const double vb = d5 * d2 - d1 * d6;
+    const double va = d3 * d6 - d5 * d4;
+    double l0, l1, l2;
+    if (d1 <= 0.0 && d2 <= 0.0) {                                  /* vertex region A */
+        l0 = 1.0; l1 = 0.0; l2 = 0.0;
+    } else if (d3 >= 0.0 && d4 <= d3) {                           /* vertex region B */
+        l0 = 0.0; l1 = 1.0; l2 = 0.0;
+    } else if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {             /* edge AB */
+        const double v = d1 / (d1 - d3);
+        l0 = 1.0 - v; l1 = v; l2 = 0.0;
+    } else if (d6 >= 0.0 && d5 <= d6) {                           /* vertex region C */
+        l0 = 0.0; l1 = 0.0; l2 = 1.0;
+    } else if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {             /* edge AC */
+        const double w = d2 / (d2 - d6);
+        l0 = 1.0 - w; l1 = 0.0; l2 = w;
+    } else if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) { /* edge BC */
+        const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        l0 = 0.0; l1 = 1.0 - w; l2 = w;
+    } else {                                                       /* face interior */
+        const double den = va + vb + vc;
+        const double v = vb / den, w = vc / den;
+        l0 = 1.0 - v - w; l1 = v; l2 = w;
+    }
+    for (int k = 0; k < 3; ++k) out[k] = l0 * a[k] + l1 * b[k] + l2 * c[k];
+    lam[0] = l0; lam[1] = l1; lam[2] = l2;
+}
+
+/* points B x N x 3 fp32; verts B x Nv x 3 fp32; faces Nf x 3 (shared topology).
+ * Outputs (per evaluated row; rows == NULL means all B*N): d (min squared distance), face (lowest
+ * face index attaining it), d2 (second-smallest over other faces; +inf if Nf == 1), closest point
+ * (3) and its barycentric coordinates on that face (3). */
+int oracle_p2s(const float* points, const float* verts, const int32_t* faces, int64_t B, int64_t N, int64_t Nv,
+               int64_t Nf, const int64_t* rows, int64_t nrows, double* d, int32_t* face, double* d2,
+               double* closest, double* lam_out, int nthreads) {
+    if (!points || !verts || !faces || !d || !face || B < 1 || N < 1 || Nv < 1 || Nf < 1) return 1;
+    for (int64_t f = 0; f < Nf; ++f)
+        for (int k = 0; k < 3; ++k)
+            if (faces[3 * f + k] < 0 || faces[3 * f + k] >= Nv) return 2;
+    int64_t total = rows ? nrows : B * N;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t r = 0; r < total; ++r) {
+        const int64_t s = rows ? rows[r] : r;
+        const int64_t b = s / N;
+        const double p[3] = {points[3 * s], points[3 * s + 1], points[3 * s + 2]};
+        const float* v = verts + 3 * b * Nv;
+        double best = INFINITY, second = INFINITY, bc[3] = {0, 0, 0}, bl[3] = {0, 0, 0};
+        int32_t arg = -1;
+        for (int64_t f = 0; f < Nf; ++f) {
+            double A[3], Bq[3], C[3], q[3], l[3];
+            for (int k = 0; k < 3; ++k) {
+                A[k] = v[3 * (int64_t)faces[3 * f] + k];
+                Bq[k] = v[3 * (int64_t)faces[3 * f + 1] + k];
+                C[k] = v[3 * (int64_t)faces[3 * f + 2] + k];
+            }
+            closest_on_triangle(p, A, Bq, C, q, l);
+            const double e = (p[0] - q[0]) * (p[0] - q[0]) + (p[1] - q[1]) * (p[1] - q[1]) + (p[2] - q[2]) * (p[2] - q[2]);
+            if (e < best) {
+                second = best;
+                best = e;
+                arg = (int32_t)f;
+                for (int k = 0; k < 3; ++k) { bc[k] = q[k]; bl[k] = l[k]; }
+            } else if (e < second) {
+                second = e;
+            }
+        }
+        d[r] = best;
+        face[r] = arg;
+        if (d2) d2[r] = second;
+        if (closest) for (int k = 0; k < 3; ++k) closest[3 * r + k] = bc[k];
+        if (lam_out) for (int k = 0; k < 3; ++k) lam_out[3 * r + k] = bl[k];
+    }
     return 0;
 }
