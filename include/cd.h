@@ -65,7 +65,9 @@ typedef enum {
     CD_OP_STEP = 3,      /* cd_step_host: forward + finalize + backward (+ staging of the clouds) */
     CD_OP_FORWARD_PRUNED = 4, /* cd_forward_pruned */
     CD_OP_SAMPLE = 5,          /* cd_sample_mesh (cd_sample_workspace_size) */
-    CD_OP_SAMPLE_BACKWARD = 6  /* cd_sample_mesh_backward (cd_sample_workspace_size) */
+    CD_OP_SAMPLE_BACKWARD = 6, /* cd_sample_mesh_backward (cd_sample_workspace_size) */
+    CD_OP_P2S = 7,             /* cd_p2s_forward (cd_p2s_workspace_size) */
+    CD_OP_P2S_BACKWARD = 8     /* cd_p2s_backward (cd_p2s_workspace_size) */
 } cd_op;
 
 /*
@@ -216,6 +218,31 @@ CD_API cd_status cd_sample_mesh_backward(const int32_t* faces, const int32_t* fa
                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
 CD_API size_t cd_sample_workspace_size(int op, int B, int Nv, int Nf, int N);
 CD_API int cd_sample_launch_count(int op, int B, int Nv, int Nf, int N);
+
+/*
+ * cd_p2s_forward — point-to-surface loss ("the point-to-surface
+ * loss [GEOMetrics] for Meshes").  points [B x N x 3], verts [B x Nv x 3] fp32,
+ * faces [Nf x 3] int32 shared by the B meshes.  Per point (brute force over all faces):
+ *   d[b,i] = min_f dist^2(p, triangle f), face[b,i] = lowest f attaining the fp32 minimum of the hot
+ *   loop's formulation (R24: plane distance when the projection is inside, else the nearest
+ *   edge); d, closest [B x N x 3] and bary [B x N x 3] (barycentrics of the closest point on that
+ *   face) are then evaluated in fp64 with the region decomposition and stored as fp32.
+ *   per_batch[b] = mean_i d (may be NULL), loss[0] = mean_b per_batch (may be NULL).
+ *   closest / bary may be NULL (both are needed by the backward).
+ * cd_p2s_backward — VJP of sum_i g_i d_i with the closest point fixed (R25):
+ *   grad_points = 2 g (p - c) [B x N x 3] (may be NULL); grad_verts [B x Nv x 3] (may be NULL) =
+ *   sum over (point, corner) of bary * (-2 g (p - c)) through the deterministic vertex scatter of
+ *   cd_sample_mesh_backward.  g [B x N] or NULL (then g_scalar for every point).
+ */
+CD_API cd_status cd_p2s_forward(const float* points, const float* verts, const int32_t* faces,
+                         int B, int N, int Nv, int Nf, float* d, int32_t* face, float* closest,
+                         float* bary, float* per_batch, float* loss,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream);
+CD_API cd_status cd_p2s_backward(const float* points, const float* closest, const int32_t* face,
+                         const float* bary, const int32_t* faces, int B, int N, int Nv, int Nf,
+                         const float* g, float g_scalar, float* grad_points, float* grad_verts,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream);
+CD_API size_t cd_p2s_workspace_size(int op, int B, int N, int Nv, int Nf);
 
 /* Workspace bytes needed by an operation for these sizes (full slices).  0 on invalid sizes. */
 CD_API size_t cd_workspace_size(int op, int B, int N, int M);

@@ -8,7 +8,7 @@ There is no CPU fallback: without a built libcd.so and an sm_100 GPU every compu
 """
 from . import synth  # noqa: F401  (seeded inputs; no method arithmetic)
 
-__all__ = ["sample_mesh", "sample_mesh_backward", "sample_points", "SampleMeshFunction", "forward_pruned",
+__all__ = ["p2s_forward", "p2s_backward", "point_to_surface", "PointToSurfaceFunction", "sample_mesh", "sample_mesh_backward", "sample_points", "SampleMeshFunction", "forward_pruned",
            "forward", "forward_rows", "forward_cols", "set_forward_mode", "finalize", "fscore", "fscore_from_distances", "backward", "chamfer", "step_host",
            "set_forward_splits", "ChamferFunction", "synth"]
 

@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "cd.h")
 
 CD_OK = 0
 CD_OP_FORWARD, CD_OP_FSCORE, CD_OP_BACKWARD, CD_OP_STEP, CD_OP_FORWARD_PRUNED = 0, 1, 2, 3, 4
-CD_OP_SAMPLE, CD_OP_SAMPLE_BACKWARD = 5, 6
+CD_OP_SAMPLE, CD_OP_SAMPLE_BACKWARD, CD_OP_P2S, CD_OP_P2S_BACKWARD = 5, 6, 7, 8
 STATUS_NAMES = {0: "CD_OK", 1: "CD_ERR_INVALID_VALUE", 2: "CD_ERR_MISALIGNED", 3: "CD_ERR_TOO_LARGE",
                 4: "CD_ERR_UNSUPPORTED_DEVICE", 5: "CD_ERR_CUDA"}
 
@@ -47,6 +47,9 @@ _SIGS = {
     "cd_sample_mesh_backward": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp], i32),
     "cd_sample_workspace_size": ([i32, i32, i32, i32, i32], sz),
     "cd_sample_launch_count": ([i32, i32, i32, i32, i32], i32),
+    "cd_p2s_forward": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "cd_p2s_backward": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, f32, vp, vp, vp, sz, vp], i32),
+    "cd_p2s_workspace_size": ([i32, i32, i32, i32, i32], sz),
     "cd_forward_rows": ([vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, f32, vp, sz, vp], i32),
     "cd_forward_cols": ([vp, vp, i32, i32, i32, vp, i32, i32, vp, vp, vp, f32, vp, sz, vp], i32),
 }

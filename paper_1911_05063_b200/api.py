@@ -361,3 +361,80 @@ class SampleMeshFunction(torch.autograd.Function):
 def sample_points(verts, faces, r_face, r_bary):
     """Differentiable surface sampling: returns (points, face_idx); points carry gradients to verts."""
     return SampleMeshFunction.apply(verts, faces, r_face, r_bary)
+
+
+
+# ---------------------------------------------------------------------------------------- NEXT-3
+def _p2s_ws(op, B, N, Nv, Nf, device):
+    n = int(_lib.load().cd_p2s_workspace_size(op, B, N, Nv, Nf))
+    if n == 0:
+        raise _lib.CdError(1, f"invalid sizes B={B} N={N} Nv={Nv} Nf={Nf}")
+    key = (str(device), op, B, N, Nv, Nf)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(n, dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def p2s_forward(points: torch.Tensor, verts: torch.Tensor, faces: torch.Tensor):
+    """cd_p2s_forward: (d [B,N], face [B,N], closest [B,N,3], bary [B,N,3], per_batch [B], loss [1])."""
+    points = _check_cloud(points, "points")
+    verts = _check_cloud(verts, "verts")
+    faces = faces.to(torch.int32).contiguous()
+    B, N, _ = points.shape
+    Nv = verts.shape[1]
+    Nf = faces.shape[0]
+    dev = points.device
+    d = torch.empty((B, N), dtype=torch.float32, device=dev)
+    fi = torch.empty((B, N), dtype=torch.int32, device=dev)
+    cl = torch.empty((B, N, 3), dtype=torch.float32, device=dev)
+    ba = torch.empty((B, N, 3), dtype=torch.float32, device=dev)
+    pb = torch.empty(B, dtype=torch.float32, device=dev)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    ws = _p2s_ws(_lib.CD_OP_P2S, B, N, Nv, Nf, dev)
+    check(_lib.load().cd_p2s_forward(_ptr(points), _ptr(verts), _ptr(faces), B, N, Nv, Nf, _ptr(d), _ptr(fi), _ptr(cl),
+                                     _ptr(ba), _ptr(pb), _ptr(loss), _ptr(ws), ws.numel(), _stream()))
+    return d, fi, cl, ba, pb, loss
+
+
+def p2s_backward(points, closest, face, bary, faces, Nv: int, g=None, g_scalar: float = 0.0,
+                 want_points: bool = True, want_verts: bool = True):
+    """cd_p2s_backward: (grad_points or None, grad_verts or None)."""
+    faces = faces.to(torch.int32).contiguous()
+    B, N, _ = points.shape
+    Nf = faces.shape[0]
+    dev = points.device
+    gp = torch.empty((B, N, 3), dtype=torch.float32, device=dev) if want_points else None
+    gv = torch.empty((B, Nv, 3), dtype=torch.float32, device=dev) if want_verts else None
+    ws = _p2s_ws(_lib.CD_OP_P2S_BACKWARD, B, N, Nv, Nf, dev)
+    check(_lib.load().cd_p2s_backward(_ptr(points.contiguous()), _ptr(closest.contiguous()), _ptr(face.contiguous()),
+                                      _ptr(bary.contiguous()), _ptr(faces), B, N, Nv, Nf,
+                                      _ptr(g.contiguous().float()) if g is not None else None, float(g_scalar),
+                                      _ptr(gp), _ptr(gv), _ptr(ws), ws.numel(), _stream()))
+    return gp, gv
+
+
+class PointToSurfaceFunction(torch.autograd.Function):
+    """loss = mean_b mean_i min_f dist^2(p_i, face f); gradients to points and mesh vertices."""
+
+    @staticmethod
+    def forward(ctx, points, verts, faces):
+        d, fi, cl, ba, pb, loss = p2s_forward(points, verts, faces)
+        ctx.save_for_backward(points, cl, fi, ba, faces)
+        ctx.Nv = verts.shape[1]
+        return loss[0]
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        points, cl, fi, ba, faces = ctx.saved_tensors
+        B, N = fi.shape
+        g = (grad_out.reshape(1).float() / (B * N)).expand(B, N)
+        gp, gv = p2s_backward(points, cl, fi, ba, faces, ctx.Nv, g=g, want_points=ctx.needs_input_grad[0],
+                              want_verts=ctx.needs_input_grad[1])
+        return gp, gv, None
+
+
+def point_to_surface(points, verts, faces):
+    """Differentiable point-to-surface loss (GEOMetrics)."""
+    return PointToSurfaceFunction.apply(points, verts, faces)

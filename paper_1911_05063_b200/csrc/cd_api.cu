@@ -353,6 +353,57 @@ int cd_sample_launch_count(int op, int B, int Nv, int Nf, int N) {
     return 0;
 }
 
+static cd_status check_p2s_sizes(int B, int N, int Nv, int Nf) {
+    if (B < 1 || N < 1 || Nv < 3 || Nf < 1)
+        return fail(CD_ERR_INVALID_VALUE, "need B, N, Nf >= 1 and Nv >= 3 (got %d %d %d %d)", B, N, Nv, Nf);
+    if ((long long)B * N * 3 > 0x7fffffffLL || (long long)B * Nv > 0x7fffffffLL || (long long)B * Nf * 24 > 0x7fffffffLL)
+        return fail(CD_ERR_TOO_LARGE, "problem too large for 32-bit indexing");
+    return CD_OK;
+}
+
+cd_status cd_p2s_forward(const float* points, const float* verts, const int32_t* faces, int B, int N, int Nv, int Nf,
+                         float* d, int32_t* face, float* closest, float* bary, float* per_batch, float* loss,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_p2s_sizes(B, N, Nv, Nf);
+    if (s != CD_OK) return s;
+    if (!points || !verts || !faces || !d || !face || !workspace) return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const size_t need = cdk::p2s_workspace(B, N, Nv, Nf);
+    if (workspace_bytes < need) return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu", workspace_bytes, need);
+    s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_p2s(points, verts, faces, B, N, Nv, Nf, d, face, closest, bary, per_batch, loss,
+                                       workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_p2s_forward");
+}
+
+cd_status cd_p2s_backward(const float* points, const float* closest, const int32_t* face, const float* bary,
+                          const int32_t* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
+                          float* grad_points, float* grad_verts, void* workspace, size_t workspace_bytes,
+                          cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_p2s_sizes(B, N, Nv, Nf);
+    if (s != CD_OK) return s;
+    if (!points || !closest || !face || !faces || !workspace || (grad_verts && !bary))
+        return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const size_t need = cdk::p2s_backward_workspace(B, N, Nv, Nf);
+    if (workspace_bytes < need) return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu", workspace_bytes, need);
+    s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_p2s_backward(points, closest, face, bary, faces, B, N, Nv, Nf, g, g_scalar,
+                                                grad_points, grad_verts, workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_p2s_backward");
+}
+
+size_t cd_p2s_workspace_size(int op, int B, int N, int Nv, int Nf) {
+    if (B < 1 || N < 1 || Nv < 3 || Nf < 1) return 0;
+    if (op == CD_OP_P2S) return cdk::p2s_workspace(B, N, Nv, Nf);
+    if (op == CD_OP_P2S_BACKWARD) return cdk::p2s_backward_workspace(B, N, Nv, Nf);
+    return 0;
+}
+
 int cd_set_forward_mode(int mode) {
     int old = g_forward_mode;
     g_forward_mode = (mode == 1 || mode == 2) ? mode : 0;

@@ -79,6 +79,17 @@ int sample_backward_launches(int B, int Nv, int Nf, int N);
 cudaError_t launch_sample_backward(const int* faces, const int* face_idx, const float* bary, int B, int Nv, int Nf,
                                    int N, const float* grad_points, float* grad_verts, void* ws, cudaStream_t st);
 
+// Point-to-surface loss (p2s.cu, NEXT-3).
+size_t p2s_workspace(int B, int N, int Nv, int Nf);
+size_t p2s_backward_workspace(int B, int N, int Nv, int Nf);
+cudaError_t launch_p2s(const float* points, const float* verts, const int* faces, int B, int N, int Nv, int Nf,
+                       float* d, int* face, float* closest, float* bary, float* per_batch, float* loss, void* ws,
+                       cudaStream_t st);
+cudaError_t launch_p2s_backward(const float* points, const float* closest, const int* face, const float* bary,
+                                const int* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
+                                float* grad_points, float* grad_verts, void* ws, cudaStream_t st);
+int p2s_launches();
+
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.
 size_t fscore_workspace(int B, int N, int M);
 cudaError_t launch_fscore(const float* d_xy, const float* d_yx, int B, int N, int M, float tau, float* fscore,

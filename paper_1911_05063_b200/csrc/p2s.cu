@@ -1,0 +1,567 @@
+// p2s.cu — point-to-surface loss ("the point-to-surface loss
+// [GEOMetrics] for Meshes"): for every point the squared distance to the closest
+// triangle of its batch element's mesh, loss = mean_b mean_i d, VJP with the closest point fixed.
+// Readings R23-R25.  Same tile engine as the Chamfer forward:
+//
+//   p2s_prep_kernel   per (b, face): the face's fixed-order fp32 data (a, e0 = b-a, e1 = c-a,
+//                     e2 = c-b, unit normal, 1/|e|^2, inverse Gram matrix) packed as 24 floats; the
+//                     face list is padded to the tile size by repeating the last face (same distance,
+//                     higher index: never the argmin).
+//   p2s_kernel        CTA = 1024 points (8 per thread as 4 packed f32x2 pairs) x a split of the faces,
+//                     face tiles staged by 1-D TMA bulk copies; per (point, face)
+//                       d = min( inside ? (ap.n)^2 : +inf, |ap - sat(ap.e0/|e0|^2) e0|^2,
+//                                |ap - sat(ap.e1/|e1|^2) e1|^2, |bp - sat(bp.e2/|e2|^2) e2|^2 )
+//                     (R24: the distance to the triangle = the plane distance when the projection is
+//                     inside, else the nearest edge); value-only running minimum + 32-face block
+//                     argmin tracking exactly as nn_fwd_kernel.
+//   p2s_merge_kernel  merges the splits, re-scans the winning block with the same fp32 ops (lowest
+//                     face with the minimum), then evaluates the closest point on that face in fp64 with
+//                     the region decomposition (d, closest point, barycentrics), fp64 chunk sums.
+//   p2s_finalize_kernel  loss = (1/B) sum_b (1/N) sum_i d.
+//   backward          grad_p = 2 g (p - c); grad_verts through the barycentrics of c with the
+//                     deterministic vertex scatter of mesh_sample.cu (R25).
+#include "cd_device.cuh"
+#include "cd_internal.h"
+
+#include <algorithm>
+
+namespace cdk {
+
+constexpr int kP2sR = 8;                           // points per thread
+constexpr int kP2sQ = kFwdThreads * kP2sR;         // 1024 points per CTA
+constexpr int kFaceTile = 128;                     // faces per shared-memory stage (12 KB)
+constexpr int kFaceFloats = 24;                    // packed face record
+constexpr int kP2sStages = 3;
+
+// face record layout (floats): 0-2 a, 3-5 -e0, 6-8 -e1, 9-11 -e2 (negated edges: every "x - t e"
+// is one fma with a positive operand), 12-14 n (unit), 15-17 -1/|e0|^2, -1/|e1|^2, -1/|e2|^2,
+// 18-20 -g11/det, g01/det, -g00/det (inverse Gram of e0, e1 applied to -s, -t), 21 u/v offset
+// (-1 for a degenerate face: its projection is never "inside"), 22-23 pad
+struct PrepArgs {
+    const float* verts;
+    const int* faces;
+    int B, Nv, Nf, Nfpad;
+    float* fd;   // [B][Nfpad][24]
+};
+
+__global__ void __launch_bounds__(256) p2s_prep_kernel(PrepArgs a) {
+    const int64_t total = (int64_t)a.B * a.Nfpad;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(e / a.Nfpad);
+        const int f = min((int)(e - (int64_t)b * a.Nfpad), a.Nf - 1);
+        const float* v = a.verts + (int64_t)b * a.Nv * 3;
+        const int ia = min(max(a.faces[3 * f], 0), a.Nv - 1);
+        const int ib = min(max(a.faces[3 * f + 1], 0), a.Nv - 1);
+        const int ic = min(max(a.faces[3 * f + 2], 0), a.Nv - 1);
+        float A[3], e0[3], e1[3], e2[3];
+        for (int k = 0; k < 3; ++k) {
+            A[k] = v[3 * ia + k];
+            e0[k] = __fsub_rn(v[3 * ib + k], A[k]);
+            e1[k] = __fsub_rn(v[3 * ic + k], A[k]);
+            e2[k] = __fsub_rn(v[3 * ic + k], v[3 * ib + k]);
+        }
+        // normal and Gram matrix in fp64, rounded once (better-conditioned face data)
+        const double n0 = (double)e0[1] * e1[2] - (double)e0[2] * e1[1];
+        const double n1 = (double)e0[2] * e1[0] - (double)e0[0] * e1[2];
+        const double n2 = (double)e0[0] * e1[1] - (double)e0[1] * e1[0];
+        const double nl = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+        const double g00 = (double)e0[0] * e0[0] + (double)e0[1] * e0[1] + (double)e0[2] * e0[2];
+        const double g01 = (double)e0[0] * e1[0] + (double)e0[1] * e1[1] + (double)e0[2] * e1[2];
+        const double g11 = (double)e1[0] * e1[0] + (double)e1[1] * e1[1] + (double)e1[2] * e1[2];
+        const double g22 = (double)e2[0] * e2[0] + (double)e2[1] * e2[1] + (double)e2[2] * e2[2];
+        const double det = g00 * g11 - g01 * g01;
+        float* o = a.fd + e * kFaceFloats;
+        for (int k = 0; k < 3; ++k) {
+            o[k] = A[k];
+            o[3 + k] = -e0[k];
+            o[6 + k] = -e1[k];
+            o[9 + k] = -e2[k];
+        }
+        const bool nondeg = nl > 0.0 && det > 0.0;
+        o[12] = nondeg ? (float)(n0 / nl) : 0.f;
+        o[13] = nondeg ? (float)(n1 / nl) : 0.f;
+        o[14] = nondeg ? (float)(n2 / nl) : 0.f;
+        o[15] = g00 > 0.0 ? (float)(-1.0 / g00) : 0.f;
+        o[16] = g11 > 0.0 ? (float)(-1.0 / g11) : 0.f;
+        o[17] = g22 > 0.0 ? (float)(-1.0 / g22) : 0.f;
+        // degenerate face: inside test always false (u = v = -1): only the edge distances count
+        o[18] = nondeg ? (float)(-g11 / det) : 0.f;
+        o[19] = nondeg ? (float)(g01 / det) : 0.f;
+        o[20] = nondeg ? (float)(-g00 / det) : 0.f;
+        o[21] = nondeg ? 0.f : -1.f;
+        o[22] = 0.f;
+        o[23] = 0.f;
+    }
+}
+
+// clamp(a * b, 0, 1) per lane: f32x2 has no .sat, two scalar FMUL.SAT cost the same two dispatch cycles
+__device__ __forceinline__ u64 sat_mul2(u64 a, u64 b) {
+    float a0, a1, b0, b1;
+    upk2(a, a0, a1);
+    upk2(b, b0, b1);
+    return pk2(__saturatef(__fmul_rn(a0, b0)), __saturatef(__fmul_rn(a1, b1)));
+}
+__device__ __forceinline__ u64 bc2(float x) { return pk2(x, x); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// Packed squared distance of two points (qx, qy, qz lanes) to one face record (R24, fixed op order).
+// With ne = -e: s' = ap.ne0 = -ap.e0, t0 = sat(s' * (-1/|e0|^2)), x - t0 e0 = fma(t0, ne0, ap).
+__device__ __forceinline__ void face_dist2(const float* f, u64 qx, u64 qy, u64 qz, float& d0, float& d1) {
+    const u64 ax = sub2(qx, bc2(f[0])), ay = sub2(qy, bc2(f[1])), az = sub2(qz, bc2(f[2]));
+    u64 s = mul2(ax, bc2(f[3]));
+    s = fma2(ay, bc2(f[4]), s);
+    s = fma2(az, bc2(f[5]), s);
+    u64 t = mul2(ax, bc2(f[6]));
+    t = fma2(ay, bc2(f[7]), t);
+    t = fma2(az, bc2(f[8]), t);
+    // in-plane coordinates of the projection
+    u64 u = fma2(s, bc2(f[18]), bc2(f[21]));
+    u = fma2(t, bc2(f[19]), u);
+    u64 v = fma2(s, bc2(f[19]), bc2(f[21]));
+    v = fma2(t, bc2(f[20]), v);
+    // plane distance
+    u64 h = mul2(ax, bc2(f[12]));
+    h = fma2(ay, bc2(f[13]), h);
+    h = fma2(az, bc2(f[14]), h);
+    const u64 pl = mul2(h, h);
+    // edge a-b
+    const u64 t0 = sat_mul2(s, bc2(f[15]));
+    u64 dx = fma2(t0, bc2(f[3]), ax), dy = fma2(t0, bc2(f[4]), ay), dz = fma2(t0, bc2(f[5]), az);
+    u64 dab = mul2(dx, dx);
+    dab = fma2(dy, dy, dab);
+    dab = fma2(dz, dz, dab);
+    // edge a-c
+    const u64 t1 = sat_mul2(t, bc2(f[16]));
+    dx = fma2(t1, bc2(f[6]), ax);
+    dy = fma2(t1, bc2(f[7]), ay);
+    dz = fma2(t1, bc2(f[8]), az);
+    u64 dac = mul2(dx, dx);
+    dac = fma2(dy, dy, dac);
+    dac = fma2(dz, dz, dac);
+    // edge b-c: bp = ap - e0 = ap + ne0
+    const u64 bx = add2(ax, bc2(f[3])), by = add2(ay, bc2(f[4])), bz = add2(az, bc2(f[5]));
+    u64 s2 = mul2(bx, bc2(f[9]));
+    s2 = fma2(by, bc2(f[10]), s2);
+    s2 = fma2(bz, bc2(f[11]), s2);
+    const u64 t2 = sat_mul2(s2, bc2(f[17]));
+    dx = fma2(t2, bc2(f[9]), bx);
+    dy = fma2(t2, bc2(f[10]), by);
+    dz = fma2(t2, bc2(f[11]), bz);
+    u64 dbc = mul2(dx, dx);
+    dbc = fma2(dy, dy, dbc);
+    dbc = fma2(dz, dz, dbc);
+    float u0, u1, v0, v1, p0, p1, ab0, ab1, ac0, ac1, bc0, bc1;
+    upk2(u, u0, u1);
+    upk2(v, v0, v1);
+    upk2(pl, p0, p1);
+    upk2(dab, ab0, ab1);
+    upk2(dac, ac0, ac1);
+    upk2(dbc, bc0, bc1);
+    const float w0 = __fsub_rn(__fsub_rn(1.0f, u0), v0), w1 = __fsub_rn(__fsub_rn(1.0f, u1), v1);
+    const bool in0 = fmin3(u0, v0, w0) >= 0.0f, in1 = fmin3(u1, v1, w1) >= 0.0f;
+    d0 = fmin3(ab0, ac0, fminf(bc0, in0 ? p0 : INFINITY));
+    d1 = fmin3(ab1, ac1, fminf(bc1, in1 ? p1 : INFINITY));
+}
+
+struct P2sArgs {
+    const float4* pts;      // packed points [B][Ppad]
+    const float* fd;        // [B][Nfpad][24]
+    int N, Ppad, Nf, Nfpad;
+    int qtiles, splits, ftiles;
+    int64_t total;          // B * N
+    float* best_d;          // [splits][B*N]
+    int* best_blk;
+};
+
+__global__ void __launch_bounds__(kFwdThreads, 3) p2s_kernel(P2sArgs a) {
+    __shared__ __align__(128) float sm[kP2sStages][kFaceTile * kFaceFloats];
+    __shared__ __align__(8) u64 full_bar[kP2sStages];
+    const int b = blockIdx.y;
+    const int tile = blockIdx.x / a.splits;
+    const int split = blockIdx.x - tile * a.splits;
+    const int t0 = (int)((int64_t)split * a.ftiles / a.splits), t1 = (int)((int64_t)(split + 1) * a.ftiles / a.splits);
+    const int ntiles = t1 - t0;
+    const float* FD = a.fd + (int64_t)b * a.Nfpad * kFaceFloats;
+    const uint32_t bytes = kFaceTile * kFaceFloats * 4;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kP2sStages; ++s) mbar_init(&full_bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int k = 0; k < min(kP2sStages, ntiles); ++k) {
+            mbar_arrive_expect_tx(&full_bar[k], bytes);
+            tma_load_1d(sm[k], FD + (int64_t)(t0 + k) * kFaceTile * kFaceFloats, bytes, &full_bar[k]);
+        }
+    const float4* P = a.pts + (int64_t)b * a.Ppad;
+    const int qbase = tile * kP2sQ + threadIdx.x * kP2sR;
+    u64 qx[kP2sR / 2], qy[kP2sR / 2], qz[kP2sR / 2];
+#pragma unroll
+    for (int r = 0; r < kP2sR / 2; ++r) {
+        const float4 p0 = P[min(qbase + 2 * r, a.N - 1)], p1 = P[min(qbase + 2 * r + 1, a.N - 1)];
+        qx[r] = pk2(p0.x, p1.x);
+        qy[r] = pk2(p0.y, p1.y);
+        qz[r] = pk2(p0.z, p1.z);
+    }
+    float best[kP2sR];
+    int blk[kP2sR];
+#pragma unroll
+    for (int r = 0; r < kP2sR; ++r) {
+        best[r] = INFINITY;
+        blk[r] = -1;
+    }
+    for (int k = 0; k < ntiles; ++k) {
+        const int s = k % kP2sStages;
+        mbar_wait(&full_bar[s], (k / kP2sStages) & 1);
+        const float* tb = sm[s];
+        const int ft = (t0 + k) * kFaceTile;
+        for (int kb = 0; kb < kFaceTile; kb += kBlockK) {
+            float old[kP2sR];
+#pragma unroll
+            for (int r = 0; r < kP2sR; ++r) old[r] = best[r];
+#pragma unroll 1
+            for (int j = 0; j < kBlockK; ++j) {
+                const float* f = tb + (kb + j) * kFaceFloats;
+#pragma unroll
+                for (int r = 0; r < kP2sR / 2; ++r) {
+                    float d0, d1;
+                    face_dist2(f, qx[r], qy[r], qz[r], d0, d1);
+                    best[2 * r] = fminf(best[2 * r], d0);
+                    best[2 * r + 1] = fminf(best[2 * r + 1], d1);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kP2sR; ++r) blk[r] = best[r] < old[r] ? ft + kb : blk[r];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && k + kP2sStages < ntiles) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], bytes);
+            tma_load_1d(sm[s], FD + (int64_t)(t0 + k + kP2sStages) * kFaceTile * kFaceFloats, bytes, &full_bar[s]);
+        }
+    }
+    const int64_t rowbase = (int64_t)split * a.total + (int64_t)b * a.N;
+#pragma unroll
+    for (int r = 0; r < kP2sR; ++r) {
+        const int q = qbase + r;
+        if (q < a.N) {
+            a.best_d[rowbase + q] = best[r];
+            a.best_blk[rowbase + q] = blk[r];
+        }
+    }
+}
+
+// fp64 closest point on triangle (region decomposition; the same case order as the definition)
+__device__ void closest64(const double p[3], const double A[3], const double Bv[3], const double C[3], double out[3],
+                          double lam[3]) {
+    double ab[3], ac[3], ap[3], bp[3], cp[3];
+    for (int k = 0; k < 3; ++k) {
+        ab[k] = Bv[k] - A[k];
+        ac[k] = C[k] - A[k];
+        ap[k] = p[k] - A[k];
+        bp[k] = p[k] - Bv[k];
+        cp[k] = p[k] - C[k];
+    }
+    auto dot = [](const double* x, const double* y) { return x[0] * y[0] + x[1] * y[1] + x[2] * y[2]; };
+    const double d1 = dot(ab, ap), d2 = dot(ac, ap), d3 = dot(ab, bp), d4 = dot(ac, bp), d5 = dot(ab, cp),
+                 d6 = dot(ac, cp);
+    const double vc = d1 * d4 - d3 * d2, vb = d5 * d2 - d1 * d6, va = d3 * d6 - d5 * d4;
+    double l0, l1, l2;
+    if (d1 <= 0.0 && d2 <= 0.0) {
+        l0 = 1; l1 = 0; l2 = 0;
+    } else if (d3 >= 0.0 && d4 <= d3) {
+        l0 = 0; l1 = 1; l2 = 0;
+    } else if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        const double v = d1 / (d1 - d3);
+        l0 = 1 - v; l1 = v; l2 = 0;
+    } else if (d6 >= 0.0 && d5 <= d6) {
+        l0 = 0; l1 = 0; l2 = 1;
+    } else if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        const double w = d2 / (d2 - d6);
+        l0 = 1 - w; l1 = 0; l2 = w;
+    } else if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+        const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        l0 = 0; l1 = 1 - w; l2 = w;
+    } else {
+        const double den = va + vb + vc;
+        const double v = vb / den, w = vc / den;
+        l0 = 1 - v - w; l1 = v; l2 = w;
+    }
+    for (int k = 0; k < 3; ++k) out[k] = l0 * A[k] + l1 * Bv[k] + l2 * C[k];
+    lam[0] = l0;
+    lam[1] = l1;
+    lam[2] = l2;
+}
+
+struct P2sMergeArgs {
+    const float4* pts;
+    const float* fd;
+    const float* verts;
+    const int* faces;
+    int B, N, Ppad, Nv, Nf, Nfpad, splits, nchunks;
+    int64_t total;
+    const float* best_d;
+    const int* best_blk;
+    float* d_out;       // [B][N]
+    int* face_out;      // [B][N]
+    float* closest;     // [B][N][3] (may be null)
+    float* bary;        // [B][N][3] (may be null)
+    double* chunk_sum;  // [B][nchunks]
+};
+
+__global__ void __launch_bounds__(kMergeThreads) p2s_merge_kernel(P2sMergeArgs a) {
+    const int b = blockIdx.x / a.nchunks;
+    const int chunk = blockIdx.x - b * a.nchunks;
+    const int i = chunk * kMergeThreads + threadIdx.x;
+    double v = 0.0;
+    if (i < a.N) {
+        const int64_t row = (int64_t)b * a.N + i;
+        float best = INFINITY;
+        int bb = -1;
+        for (int s = 0; s < a.splits; ++s) {
+            const float d = a.best_d[(int64_t)s * a.total + row];
+            if (d < best) {
+                best = d;
+                bb = a.best_blk[(int64_t)s * a.total + row];
+            }
+        }
+        const float4 pp = a.pts[(int64_t)b * a.Ppad + i];
+        int face = 0;
+        if (bb >= 0) {
+            const u64 qx = pk2(pp.x, pp.x), qy = pk2(pp.y, pp.y), qz = pk2(pp.z, pp.z);
+            const float* FD = a.fd + (int64_t)b * a.Nfpad * kFaceFloats;
+            const int fend = min(bb + kBlockK, a.Nf);
+            face = -1;
+            for (int f = bb; f < fend; ++f) {
+                float d0, d1;
+                face_dist2(FD + (int64_t)f * kFaceFloats, qx, qy, qz, d0, d1);
+                if (d0 == best) {
+                    face = f;
+                    break;
+                }
+            }
+            if (face < 0) face = bb;
+        }
+        // fp64 closest point on the chosen face
+        const float* vv = a.verts + (int64_t)b * a.Nv * 3;
+        double A[3], Bv[3], C[3], p[3] = {pp.x, pp.y, pp.z}, c[3], lam[3];
+        const int ia = min(max(a.faces[3 * face], 0), a.Nv - 1), ib = min(max(a.faces[3 * face + 1], 0), a.Nv - 1),
+                  ic = min(max(a.faces[3 * face + 2], 0), a.Nv - 1);
+        for (int k = 0; k < 3; ++k) {
+            A[k] = vv[3 * ia + k];
+            Bv[k] = vv[3 * ib + k];
+            C[k] = vv[3 * ic + k];
+        }
+        closest64(p, A, Bv, C, c, lam);
+        const double dd = (p[0] - c[0]) * (p[0] - c[0]) + (p[1] - c[1]) * (p[1] - c[1]) + (p[2] - c[2]) * (p[2] - c[2]);
+        a.d_out[row] = (float)dd;
+        a.face_out[row] = face;
+        if (a.closest)
+            for (int k = 0; k < 3; ++k) a.closest[3 * row + k] = (float)c[k];
+        if (a.bary)
+            for (int k = 0; k < 3; ++k) a.bary[3 * row + k] = (float)lam[k];
+        v = (double)(float)dd;
+    }
+    __shared__ double ssum[kMergeThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) ssum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kMergeThreads / 32; ++w) s += ssum[w];
+        a.chunk_sum[(int64_t)b * a.nchunks + chunk] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) p2s_finalize_kernel(const double* chunk_sum, int B, int N, int nchunks,
+                                                           float* per_batch, float* loss) {
+    __shared__ double sl[256];
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < B; b += 256) {
+        double s = 0.0;
+        for (int c = 0; c < nchunks; ++c) s += chunk_sum[(int64_t)b * nchunks + c];
+        const double m = s / N;
+        if (per_batch) per_batch[b] = (float)m;
+        acc += m;
+    }
+    sl[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sl[threadIdx.x] += sl[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && loss) loss[0] = (float)(sl[0] / B);
+}
+
+struct P2sPackArgs {
+    const float* src;
+    float4* dst;
+    int N, Ppad, B;
+};
+
+__global__ void __launch_bounds__(256) p2s_pack_kernel(P2sPackArgs a) {
+    const int64_t total = (int64_t)a.B * a.Ppad;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / a.Ppad;
+        const int i = (int)(e - b * a.Ppad);
+        const int j = min(i, a.N - 1);
+        const float* s = a.src + (b * a.N + j) * 3;
+        a.dst[e] = make_float4(s[0], s[1], s[2], 0.f);
+    }
+}
+
+__global__ void __launch_bounds__(256) p2s_grad_points_kernel(const float* pts, const float* closest, const float* g,
+                                                              float g_scalar, int64_t total, float* grad_points,
+                                                              float* upstream_verts) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const double gi = g ? (double)g[e] : (double)g_scalar;
+        for (int k = 0; k < 3; ++k) {
+            const double t = __dmul_rn(__dmul_rn(2.0, gi), __dsub_rn((double)pts[3 * e + k], (double)closest[3 * e + k]));
+            if (grad_points) grad_points[3 * e + k] = (float)t;
+            upstream_verts[3 * e + k] = (float)(-t);   // d/dc of |p - c|^2 = -2 (p - c)
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------ host
+static int cdiv(int64_t x, int64_t y) { return (int)((x + y - 1) / y); }
+
+struct P2sPlan {
+    int B, N, Nv, Nf, Ppad, Nfpad, qtiles, ftiles, splits, nchunks;
+    size_t off_pts, off_fd, off_best_d, off_best_blk, off_chunk, bytes;
+};
+
+static void plan_p2s(P2sPlan& p, int B, int N, int Nv, int Nf) {
+    p.B = B;
+    p.N = N;
+    p.Nv = Nv;
+    p.Nf = Nf;
+    p.Ppad = cdiv(N, kP2sQ) * kP2sQ;
+    p.Nfpad = cdiv(Nf, kFaceTile) * kFaceTile;
+    p.qtiles = p.Ppad / kP2sQ;
+    p.ftiles = p.Nfpad / kFaceTile;
+    int sms = 148;
+    const int64_t units = (int64_t)B * p.qtiles, slots = (int64_t)sms * 3;
+    int best = 1;
+    double bt = 1e300;
+    for (int s = 1; s <= std::min(64, p.ftiles); ++s) {
+        const double t = (double)cdiv(units * s, slots) * ((double)cdiv(p.ftiles, s) + 0.25) *
+                         ((units * s < slots && s < std::min(64, p.ftiles)) ? 1.15 : 1.0);
+        if (t < bt * 0.999) {
+            bt = t;
+            best = s;
+        }
+    }
+    p.splits = best;
+    p.nchunks = cdiv(N, kMergeThreads);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    p.off_pts = take((size_t)B * p.Ppad * 16);
+    p.off_fd = take((size_t)B * p.Nfpad * kFaceFloats * 4);
+    p.off_best_d = take((size_t)p.splits * B * N * 4);
+    p.off_best_blk = take((size_t)p.splits * B * N * 4);
+    p.off_chunk = take((size_t)B * p.nchunks * 8);
+    p.bytes = off;
+}
+
+size_t p2s_workspace(int B, int N, int Nv, int Nf) {
+    P2sPlan p;
+    plan_p2s(p, B, N, Nv, Nf);
+    return p.bytes;
+}
+
+size_t p2s_backward_workspace(int B, int N, int Nv, int Nf) {
+    return align_up((size_t)B * N * 12, 256) + sample_backward_workspace(B, Nv, Nf, N);
+}
+
+cudaError_t launch_p2s(const float* points, const float* verts, const int* faces, int B, int N, int Nv, int Nf,
+                       float* d, int* face, float* closest, float* bary, float* per_batch, float* loss, void* ws,
+                       cudaStream_t st) {
+    P2sPlan p;
+    plan_p2s(p, B, N, Nv, Nf);
+    char* w = static_cast<char*>(ws);
+    float4* pts = reinterpret_cast<float4*>(w + p.off_pts);
+    float* fd = reinterpret_cast<float*>(w + p.off_fd);
+    float* best_d = reinterpret_cast<float*>(w + p.off_best_d);
+    int* best_blk = reinterpret_cast<int*>(w + p.off_best_blk);
+    double* chunk = reinterpret_cast<double*>(w + p.off_chunk);
+    {
+        P2sPackArgs a{points, pts, N, p.Ppad, B};
+        p2s_pack_kernel<<<std::min(cdiv((int64_t)B * p.Ppad, 256), 148 * 16), 256, 0, st>>>(a);
+    }
+    {
+        PrepArgs a{verts, faces, B, Nv, Nf, p.Nfpad, fd};
+        p2s_prep_kernel<<<std::min(cdiv((int64_t)B * p.Nfpad, 256), 148 * 16), 256, 0, st>>>(a);
+    }
+    {
+        P2sArgs a;
+        a.pts = pts;
+        a.fd = fd;
+        a.N = N;
+        a.Ppad = p.Ppad;
+        a.Nf = Nf;
+        a.Nfpad = p.Nfpad;
+        a.qtiles = p.qtiles;
+        a.splits = p.splits;
+        a.ftiles = p.ftiles;
+        a.total = (int64_t)B * N;
+        a.best_d = best_d;
+        a.best_blk = best_blk;
+        if (g_prof_start) record_profile_event(g_prof_start, st);
+        p2s_kernel<<<dim3(p.qtiles * p.splits, B), kFwdThreads, 0, st>>>(a);
+        if (g_prof_stop) record_profile_event(g_prof_stop, st);
+    }
+    {
+        P2sMergeArgs a;
+        a.pts = pts;
+        a.fd = fd;
+        a.verts = verts;
+        a.faces = faces;
+        a.B = B;
+        a.N = N;
+        a.Ppad = p.Ppad;
+        a.Nv = Nv;
+        a.Nf = Nf;
+        a.Nfpad = p.Nfpad;
+        a.splits = p.splits;
+        a.nchunks = p.nchunks;
+        a.total = (int64_t)B * N;
+        a.best_d = best_d;
+        a.best_blk = best_blk;
+        a.d_out = d;
+        a.face_out = face;
+        a.closest = closest;
+        a.bary = bary;
+        a.chunk_sum = chunk;
+        p2s_merge_kernel<<<B * p.nchunks, kMergeThreads, 0, st>>>(a);
+    }
+    if (per_batch || loss) p2s_finalize_kernel<<<1, 256, 0, st>>>(chunk, B, N, p.nchunks, per_batch, loss);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p2s_backward(const float* points, const float* closest, const int* face, const float* bary,
+                                const int* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
+                                float* grad_points, float* grad_verts, void* ws, cudaStream_t st) {
+    char* w = static_cast<char*>(ws);
+    float* up = reinterpret_cast<float*>(w);
+    const int64_t total = (int64_t)B * N;
+    p2s_grad_points_kernel<<<std::min(cdiv(total, 256), 148 * 16), 256, 0, st>>>(points, closest, g, g_scalar, total,
+                                                                                 grad_points, up);
+    if (grad_verts)
+        return launch_sample_backward(faces, face, bary, B, Nv, Nf, N, up, grad_verts,
+                                      w + align_up((size_t)B * N * 12, 256), st);
+    return cudaGetLastError();
+}
+
+int p2s_launches() { return 5; }
+
+}  // namespace cdk
