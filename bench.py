@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-pruned", action="store_true", help="skip the exact pruned (NEXT-2) comparison")
+    ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-3 / NEXT-4 workload lines")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise the multi-rank "
                     "logic when several ranks share one GPU")
     return ap.parse_args()
@@ -219,6 +220,95 @@ def _traffic(kernel, cfg):
         return None
 
 
+P2S_OPS_PER_PAIR = 44   # FP32-pipe lane ops per (point, face) of the p2s hot loop
+
+
+def _timed(torch, fn, flush, K, warmup=2, graph=True):
+    """Mean device ms of fn() over K replays (CUDA graph when possible), L2 flushed between steps."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    g = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record()
+        if g is not None:
+            g.replay()
+        else:
+            fn()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev) / K
+
+
+def measure_extras(cd, torch, dev, flush, args, K_extra):
+    """NEXT-3 (point-to-surface loss fwd+bwd) and NEXT-4 (mesh -> sample -> Chamfer -> grad to
+    vertices) steps on ShapeNet-like meshes (icosphere subdivision 5: 10,242 vertices, 20,480 faces)."""
+    out = {}
+    # NEXT-3: B=8 meshes, N=16,384 points each (c3-sized clouds), loss + grads to points and vertices
+    B, N = 8, 16384
+    V, F = synth.mesh_batch(B, subdiv=5, config_index=200)
+    P = synth.shape_pair(B, N, 8, config_index=201)[0]
+    v, f, p = torch.from_numpy(V).to(dev), torch.from_numpy(F).to(dev), torch.from_numpy(P).to(dev)
+    Nv, Nf = V.shape[1], F.shape[0]
+
+    def p2s_step():
+        d, fi, cl, ba, pb, loss = cd.p2s_forward(p, v, f)
+        cd.p2s_backward(p, cl, fi, ba, f, Nv, g=None, g_scalar=1.0 / (B * N))
+        return loss
+
+    ms = _timed(torch, p2s_step, flush, K_extra)
+    fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fa.record()
+    fb.record()
+    torch.cuda.synchronize()
+    cd.set_profile_events(fa, fb)
+    cd.p2s_forward(p, v, f)
+    cd.set_profile_events(None, None)
+    torch.cuda.synchronize()
+    kms = fa.elapsed_time(fb)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 128 * 1965e6 / 1e12
+    pairs = B * N * Nf
+    ach = P2S_OPS_PER_PAIR * pairs / (kms * 1e-3) / 1e12
+    out["next3_point_to_surface"] = {
+        "workload": f"B={B} meshes (icosphere-5: {Nv} verts, {Nf} faces) x N={N} points; loss + grads to points and vertices",
+        "ms_per_step": ms, "point_face_pairs_per_s": pairs / (ms * 1e-3),
+        "kernel": "p2s_kernel", "kernel_ms": kms,
+        "roofline": {"bound": "alu", "unit": "Tops/s (FP32-pipe lane ops)", "achieved": ach, "peak": peak,
+                     "frac": ach / peak, "algorithmic": f"{P2S_OPS_PER_PAIR} FP32-pipe ops per (point, face)"},
+    }
+    # NEXT-4: B=32 meshes -> N=16,384 samples each -> Chamfer vs Y (M=16,384) -> grad to vertices
+    B, N, M = 32, 16384, 16384
+    V, F = synth.mesh_batch(B, subdiv=5, config_index=210)
+    Y = synth.shape_pair(B, 8, M, config_index=211)[1]
+    rf, rb = synth.sampling_randoms(B, N, seed=212)
+    v, f, y = torch.from_numpy(V).to(dev), torch.from_numpy(F).to(dev), torch.from_numpy(Y).to(dev)
+    rft, rbt = torch.from_numpy(rf).to(dev), torch.from_numpy(rb).to(dev)
+    Nv = V.shape[1]
+
+    def pipe_step():
+        pts, fi, ba = cd.sample_mesh(v, f, rft, rbt)
+        d_xy, i_xy, d_yx, i_yx, part = cd.forward(pts, y, tau=0.01)
+        _, loss, F1, _, _ = cd.finalize(part, N, M)
+        gx, _ = cd.backward(pts, y, i_xy, i_yx, g_scalar=1.0 / (B * N), h_scalar=1.0 / (B * M))
+        return cd.sample_mesh_backward(f, fi, ba, Nv, gx)
+
+    ms = _timed(torch, pipe_step, flush, K_extra)
+    out["next4_sample_chamfer"] = {
+        "workload": f"B={B} meshes (icosphere-5) -> N={N} samples -> Chamfer + F@0.01 vs M={M} -> grad to vertices",
+        "ms_per_step": ms, "directed_pairs_per_s": 2 * B * N * M / (ms * 1e-3),
+    }
+    return out
+
+
 # ------------------------------------------------------------------------------------------ ours
 def main():
     args = parse()
@@ -374,6 +464,11 @@ def main():
                   "note": ("cd_forward_pruned (exact: Morton tiles + lower-bound culling, SURVEY §8.f NEXT-2) "
                            "+ finalize + backward; effective = the same 2*B*N*M directed pairs / step time")}
 
+    # ---------------------------------------------------------------- NEXT-3 / NEXT-4 workloads
+    extras = None
+    if world == 1 and not args.no_extras:
+        extras = measure_extras(cd, torch, dev, flush, args, K_extra=max(3, min(K, 50)))
+
     # ---------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
@@ -460,6 +555,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pruned": pruned,
+            "next_rows": extras,
             "gpu_launches": launches * K,
             "gpu_launches_per_step": launches,
             "clocks": clocks,

@@ -6,7 +6,7 @@ for c in ${CFGS:-c1 c2 c3 c4 c5}; do
   python bench.py --config $c > gpurun_out/bench_${TAG}_$c.json 2> gpurun_out/bench_${TAG}_$c.err; echo "$c rc=$?"
   python - <<PY
 import json; d=json.load(open("gpurun_out/bench_${TAG}_$c.json"))
-r=d["roofline"]; pr=d.get("pruned") or {}; print("$c pruned ms %.4f eff %.4g speedup %.2f lossdiff %.2g" % (pr.get("ms_per_step",0), pr.get("value_effective",0), pr.get("speedup_vs_brute_step",0), pr.get("loss_rel_diff_vs_brute",0))); print("$c value %.4g ms/step %.4f kernel_ms %.4f frac %.3f eff%% %.1f e2e %.4g cpu %.4g launch %s clocks %s" % (d["value"], d["ms_per_step"], r["kernel_ms"], r["frac"], d["pct_fp32_fma_peak_effective"], (d.get("e2e") or {}).get("value") or 0, (d.get("cpu_baseline") or {}).get("value") or 0, d["config"].get("launch"), d.get("clocks")))
+r=d["roofline"]; pr=d.get("pruned") or {}; print("$c next", json.dumps(d.get("next_rows"))); print("$c pruned ms %.4f eff %.4g speedup %.2f lossdiff %.2g" % (pr.get("ms_per_step",0), pr.get("value_effective",0), pr.get("speedup_vs_brute_step",0), pr.get("loss_rel_diff_vs_brute",0))); print("$c value %.4g ms/step %.4f kernel_ms %.4f frac %.3f eff%% %.1f e2e %.4g cpu %.4g launch %s clocks %s" % (d["value"], d["ms_per_step"], r["kernel_ms"], r["frac"], d["pct_fp32_fma_peak_effective"], (d.get("e2e") or {}).get("value") or 0, (d.get("cpu_baseline") or {}).get("value") or 0, d["config"].get("launch"), d.get("clocks")))
 PY
 done
 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --config c3 --steps 10 --warmup 3 --dist-backend gloo --no-cpu-baseline > gpurun_out/bench_${TAG}_dist_c3.json 2> gpurun_out/bench_${TAG}_dist_c3.err; echo "dist c3 rc=$?"; cut -c1-400 gpurun_out/bench_${TAG}_dist_c3.json
