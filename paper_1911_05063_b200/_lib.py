@@ -12,6 +12,9 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libcd.so")
+# experiment hook: load another in-tree build (e.g. a tuning variant); the product default is above
+if os.environ.get("CD_LIB_VARIANT"):
+    LIB_PATH = os.path.join(HERE, "lib", f"libcd_{os.environ['CD_LIB_VARIANT']}.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "cd.h")
 
 CD_OK = 0
