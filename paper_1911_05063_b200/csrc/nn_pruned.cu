@@ -8,7 +8,7 @@
 //   radix sort         (nn_backward.cu) -> every (cloud, batch) segment in Morton order.
 //   gather_kernel      sorted packed float4 clouds + permutation (sorted position -> original row).
 //   aabb_kernel        bounding box of every 512-point tile of the sorted clouds.
-//   candidates_kernel  per query tile (1024 sorted rows): lower bound LB of the squared distance to
+//   candidates_kernel  per query tile (256 sorted rows): lower bound LB of the squared distance to
 //                      every target tile (box-box gap, scaled by (1 - 1e-5) so it is a strict lower
 //                      bound of the fp32-evaluated distances), bitonic-sorted ascending.
 //   nn_pruned_kernel   per query tile: target tiles in LB order through the 3-stage TMA ring, the
@@ -26,8 +26,9 @@
 
 namespace cdk {
 
-constexpr int kPrR = 8;                         // query rows per thread
-constexpr int kPrQ = kFwdThreads * kPrR;        // 1024 sorted rows per query tile (2 target tiles)
+constexpr int kPrR = 2;                         // query rows per thread (one packed f32x2 pair)
+constexpr int kPrThreads = 128;                 // threads per query-tile CTA
+constexpr int kPrQ = kPrThreads * kPrR;         // 256 sorted rows per query tile: tight boxes
 constexpr int kPrMaxTiles = 8192;               // target tiles per batch supported by the LB sort
 constexpr float kLbScale = 0.99999f;            // LB' = LB * (1 - 1e-5): strict lower bound margin
 
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(256) aabb_kernel(AabbArgs a) {
 // --------------------------------------------------------------------------------------------- candidates
 struct CandArgs {
     const float4* box[2];
+    const float4* box32[2];   // 32-point block boxes: the query tile box is their union
     int ppad[2];
     int B;
     int qtiles[2];            // query tiles (kPrQ rows) per batch element, per dir
@@ -236,10 +238,10 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
     const int q = u - b * a.qtiles[dir];
     const int qc = dir, tc = 1 - dir;
     const int qnt = a.ppad[qc] / kTile, tnt = a.ppad[tc] / kTile;
-    // query tile box = union of its kPrQ / kTile target-size tiles
+    // query tile box = union of its kPrQ / kBlockK 32-point block boxes
     float qlo[3] = {INFINITY, INFINITY, INFINITY}, qhi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int s = 0; s < kPrQ / kTile; ++s) {
-        const float4* bx = a.box[qc] + ((int64_t)b * qnt + q * (kPrQ / kTile) + s) * 2;
+    for (int s = 0; s < kPrQ / kBlockK; ++s) {
+        const float4* bx = a.box32[qc] + ((int64_t)b * qnt * kBlocksPerTile + q * (kPrQ / kBlockK) + s) * 2;
         const float4 lo = bx[0], hi = bx[1];
         qlo[0] = fminf(qlo[0], lo.x); qlo[1] = fminf(qlo[1], lo.y); qlo[2] = fminf(qlo[2], lo.z);
         qhi[0] = fmaxf(qhi[0], hi.x); qhi[1] = fmaxf(qhi[1], hi.y); qhi[2] = fmaxf(qhi[2], hi.z);
@@ -305,11 +307,11 @@ __device__ __forceinline__ float box_lb(const float wlo[3], const float whi[3], 
     return (gx * gx + gy * gy + gz * gz) * kLbScale;
 }
 
-__global__ void __launch_bounds__(kFwdThreads, 4) nn_pruned_kernel(PrunedArgs a) {
+__global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) {
     __shared__ __align__(128) float4 sm[kStages][kTile];
     __shared__ __align__(128) float4 smb[kStages][kBlocksPerTile * 2];   // the tile's 32-point block boxes
     __shared__ __align__(8) u64 full_bar[kStages];
-    __shared__ unsigned s_wmax[kFwdThreads / 32];
+    __shared__ unsigned s_wmax[kPrThreads / 32];
 
     int u = blockIdx.x;
     const int b = blockIdx.y;
@@ -439,7 +441,7 @@ __global__ void __launch_bounds__(kFwdThreads, 4) nn_pruned_kernel(PrunedArgs a)
         __syncthreads();  // stage s consumed by every warp; s_wmax complete
         unsigned mm = s_wmax[0];
 #pragma unroll
-        for (int w = 1; w < kFwdThreads / 32; ++w) mm = max(mm, s_wmax[w]);
+        for (int w = 1; w < kPrThreads / 32; ++w) mm = max(mm, s_wmax[w]);
         maxbest = __uint_as_float(mm);
         if (threadIdx.x == 0 && issued == k + kStages && issued < tnt) {
             const unsigned long long e = cand[issued];
@@ -562,8 +564,9 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
     p.npts[0] = N;
     p.npts[1] = M;
     for (int c = 0; c < 2; ++c) {
-        p.ppad[c] = cdiv(p.npts[c], kPrQ) * kPrQ;
-        p.qtiles[c] = p.ppad[c] / kPrQ;
+        const int unit = std::max(kPrQ, kTile);
+        p.ppad[c] = cdiv(p.npts[c], unit) * unit;
+        p.qtiles[c] = cdiv(p.npts[c], kPrQ);
         p.ttiles[c] = p.ppad[c] / kTile;
     }
     int bb = 0;
@@ -692,6 +695,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         a.B = p.B;
         for (int c = 0; c < 2; ++c) {
             a.box[c] = box[c];
+            a.box32[c] = box32[c];
             a.ppad[c] = p.ppad[c];
             a.qtiles[c] = p.qtiles[c];
             a.cand_off[c] = p.cand_off[c];
@@ -727,7 +731,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         }
         a.cand = cand;
         if (g_prof_start) record_profile_event(g_prof_start, st);
-        nn_pruned_kernel<<<dim3(p.qtiles[0] + p.qtiles[1], p.B), kFwdThreads, 0, st>>>(a);
+        nn_pruned_kernel<<<dim3(p.qtiles[0] + p.qtiles[1], p.B), kPrThreads, 0, st>>>(a);
         if (g_prof_stop) record_profile_event(g_prof_stop, st);
     }
     double* chunk_sum = reinterpret_cast<double*>(w + p.off_chunk_sum);
