@@ -48,9 +48,7 @@ int unfused_ctas_per_sm();
 // fused kernels (nn_fused.cu)
 cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey, float* best_d,
                               int* best_blk, cudaStream_t st);
-cudaError_t launch_col_resolve(const FwdPlan& p, const float4* xp, const float4* yp, const long long* colkey, int r0,
-                               int r1, float* d_out, int32_t* idx_out, double* chunk_sum, int* chunk_hits, float tau,
-                               cudaStream_t st);
+
 
 // Exact pruned forward (nn_pruned.cu, NEXT-2): Morton-sorted tiles + box lower-bound culling.
 struct PrunedPlan {
@@ -116,7 +114,8 @@ int backward_launches(const BwdPlan& p);
 
 // Reusable stable LSD radix sort of u32 (key, value) pairs (nn_backward.cu).
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits, uint32_t* counts, uint32_t* totals,
-                     cudaStream_t st);
+                     cudaStream_t st, bool first_hist_done = false);
+int radix_digit_bits(int64_t L, int nbits);
 size_t radix_sort_counts_words(int64_t L, int nbits);
 int radix_sort_launches(int64_t L, int nbits);
 constexpr int kSortTotalsWords = 1 << 11;

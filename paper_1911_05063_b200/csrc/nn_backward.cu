@@ -1,9 +1,9 @@
 // nn_backward.cu — backward of the Chamfer per-point distances, argmin held fixed
 // (SURVEY.md §8.a.6-a.8).  Deterministic and free of floating-point atomics:
 //
-//   keys_kernel      one (key, value) pair per NN edge: xy edge i -> a_i gets key b*M + a_i,
+//   keys_hist_kernel one (key, value) pair per NN edge: xy edge i -> a_i gets key b*M + a_i,
 //                    yx edge j -> b_j gets key B*M + b*N + b_j; value = the source row.  Built in
-//                    ascending source order.
+//                    ascending source order; also the first radix pass's per-tile histogram.
 //   radix passes     stable LSD radix sort by key, digits of <= 11 bits (2 passes up to 2^22
 //                    keys), reduce-then-scan:
 //                      radix_hist_kernel   per-tile digit histograms (shared-memory integer adds)
@@ -29,28 +29,43 @@ constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements per tile (512 per warp)
 constexpr int kMaxDigitBits = 11;                     // digits of up to 11 bits: 2 passes cover 2^22 keys
 
-__global__ void __launch_bounds__(256) keys_kernel(const int32_t* __restrict__ idx_xy,
-                                                   const int32_t* __restrict__ idx_yx, int B, int N, int M,
-                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+// Edge keys fused with the first radix pass's per-tile histogram: one CTA per sort
+// tile writes its 4096 (key, value) pairs and counts digit 0 (saves a launch and a read of the keys).
+__global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(const int32_t* __restrict__ idx_xy,
+                                                                 const int32_t* __restrict__ idx_yx, int B, int N,
+                                                                 int M, int D, int ntiles, uint32_t* __restrict__ keys,
+                                                                 uint32_t* __restrict__ vals,
+                                                                 uint32_t* __restrict__ counts) {
+    extern __shared__ uint32_t hist[];
+    for (int d = threadIdx.x; d < D; d += kSortThreads) hist[d] = 0;
+    __syncthreads();
     const int64_t L0 = (int64_t)B * N;
     const int64_t L = L0 + (int64_t)B * M;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L; p += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t key, val;
-        if (p < L0) {
-            const int64_t b = p / N;
-            const int a = min(max(idx_xy[p], 0), M - 1);
-            key = (uint32_t)(b * M + a);
-            val = (uint32_t)p;
-        } else {
-            const int64_t q = p - L0;
-            const int64_t b = q / M;
-            const int a = min(max(idx_yx[q], 0), N - 1);
-            key = (uint32_t)((int64_t)B * M + b * N + a);
-            val = (uint32_t)q;
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+    for (int k = 0; k < kSortItems; ++k) {
+        const int64_t p = base + (int64_t)k * kSortThreads + threadIdx.x;
+        if (p < L) {
+            uint32_t key, val;
+            if (p < L0) {
+                const int64_t b = p / N;
+                const int a = min(max(idx_xy[p], 0), M - 1);
+                key = (uint32_t)(b * M + a);
+                val = (uint32_t)p;
+            } else {
+                const int64_t q = p - L0;
+                const int64_t b = q / M;
+                const int a = min(max(idx_yx[q], 0), N - 1);
+                key = (uint32_t)((int64_t)B * M + b * N + a);
+                val = (uint32_t)q;
+            }
+            keys[p] = key;
+            vals[p] = val;
+            atomicAdd(&hist[key & (D - 1)], 1u);  // integer adds: order-free
         }
-        keys[p] = key;
-        vals[p] = val;
     }
+    __syncthreads();
+    for (int d = threadIdx.x; d < D; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
 }
 
 // counts[digit * ntiles + tile]; D = 1 << digit bits (dynamic shared memory: D words)
@@ -306,7 +321,7 @@ size_t radix_sort_counts_words(int64_t L, int nbits) {
 // hold the input; returns the index (0 or 1) of the buffers holding the sorted output.
 // counts: radix_sort_counts_words(L, nbits) words; totals: 2^11 words.
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits, uint32_t* counts, uint32_t* totals,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool first_hist_done) {
     int npasses, digit_bits, ntiles;
     radix_sort_plan(L, nbits, npasses, digit_bits, ntiles);
     const int D = 1 << digit_bits;
@@ -320,7 +335,8 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits,
     int cur = 0;
     for (int pass = 0; pass < npasses; ++pass) {
         const int shift = pass * digit_bits;
-        radix_hist_kernel<<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D, ntiles, counts);
+        if (!(pass == 0 && first_hist_done))
+            radix_hist_kernel<<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D, ntiles, counts);
         radix_rowscan_kernel<<<D, kSortThreads, 0, st>>>(counts, ntiles, totals);
         radix_scatter_kernel<<<ntiles, kSortThreads, scatter_smem, st>>>(keys[cur], vals[cur], L, shift, D, ntiles,
                                                                          counts, totals, keys[1 - cur], vals[1 - cur]);
@@ -333,6 +349,12 @@ int radix_sort_launches(int64_t L, int nbits) {
     int np, db, nt;
     radix_sort_plan(L, nbits, np, db, nt);
     return 3 * np;
+}
+
+int radix_digit_bits(int64_t L, int nbits) {
+    int np, db, nt;
+    radix_sort_plan(L, nbits, np, db, nt);
+    return db;
 }
 
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1) {
@@ -365,7 +387,7 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
     p.bytes = off;
 }
 
-int backward_launches(const BwdPlan& p) { return 1 + 3 * p.npasses + 2; }
+int backward_launches(const BwdPlan& p) { return 3 * p.npasses + 2; }  // keys fused with pass-0 hist
 
 cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, const int32_t* idx_xy,
                             const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar,
@@ -376,9 +398,12 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     uint32_t* counts = reinterpret_cast<uint32_t*>(w + p.off_counts);
     uint32_t* totals = reinterpret_cast<uint32_t*>(w + p.off_totals);
     uint32_t* off = reinterpret_cast<uint32_t*>(w + p.off_offsets);
-    const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sm_count() * 16);
-    keys_kernel<<<grid_l, 256, 0, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, keys[0], vals[0]);
-    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, counts, totals, st);
+    {
+        const int D = 1 << p.digit_bits;
+        keys_hist_kernel<<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles,
+                                                                        keys[0], vals[0], counts);
+    }
+    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, counts, totals, st, /*first_hist_done=*/true);
     const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);
     offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], p.L, p.kmax, off);
     GradArgs a;

@@ -233,8 +233,8 @@ struct MergeArgs {
     double tau2;  // < 0: no hits
 };
 
-__global__ void __launch_bounds__(kMergeThreads) nn_merge_kernel(MergeArgs a) {
-    int u = blockIdx.x;
+__device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
+    int u = blk;
     int dir = 0;
     if (u >= a.B * a.nchunks[0]) {
         dir = 1;
@@ -290,6 +290,77 @@ __global__ void __launch_bounds__(kMergeThreads) nn_merge_kernel(MergeArgs a) {
         a.chunk_sum[c] = s;
         a.chunk_hits[c] = t;
     }
+}
+
+struct ResolveArgs {
+    const float4* xp;
+    const float4* yp;
+    int N, M, xpad, ypad;
+    int q0, q1;            // X rows that took part in the column minima
+    int r0, r1;            // Y rows to resolve
+    int B, nchunks;
+    const long long* colkey;
+    float* d_out;          // [B][r1-r0]
+    int32_t* idx_out;
+    double* chunk_sum;     // dir-1 chunk partials
+    int* chunk_hits;
+    double tau2;
+};
+
+// column direction of the fused forward: per Y row, unpack the key and re-evaluate the winning
+// thread's 16 rows with the same .rn ops (lowest index with d == min); `blk` = this CTA's chunk.
+__device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk) {
+    const int b = blk / a.nchunks;
+    const int chunk = blk - b * a.nchunks;
+    const int slen = a.r1 - a.r0;
+    const int sj = chunk * kMergeThreads + threadIdx.x;
+    double v = 0.0;
+    int h = 0;
+    if (sj < slen) {
+        const int j = a.r0 + sj;
+        const unsigned long long key = (unsigned long long)a.colkey[(int64_t)b * a.M + j];
+        float m = INFINITY;
+        int idx = -1;
+        if ((long long)key != kColKeyEmpty) {
+            m = __uint_as_float((unsigned)(key >> 32));
+            const int i0 = (int)(unsigned)(key & 0xffffffffull);
+            const float4 t = a.yp[(int64_t)b * a.ypad + j];
+            const float4* X = a.xp + (int64_t)b * a.xpad;
+            const int iend = min(i0 + kR, a.q1);
+            float d[kR];
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                const float4 q = X[min(i0 + r, a.q1 - 1)];
+                d[r] = dist_rn(q.x, q.y, q.z, t.x, t.y, t.z);  // same operand order as the kernel
+            }
+#pragma unroll
+            for (int r = kR - 1; r >= 0; --r)
+                if (i0 + r < iend && d[r] == m) idx = i0 + r;
+            if (idx < 0) m = INFINITY;  // only when every distance was NaN
+        }
+        a.d_out[(int64_t)b * slen + sj] = m;
+        a.idx_out[(int64_t)b * slen + sj] = idx;
+        v = (double)m;
+        h = (a.tau2 >= 0.0 && (double)m <= a.tau2) ? 1 : 0;
+    }
+    double s;
+    int t;
+    block_sum_hits(v, h, &s, &t);
+    if (threadIdx.x == 0) {
+        a.chunk_sum[(int64_t)b * a.nchunks + chunk] = s;
+        a.chunk_hits[(int64_t)b * a.nchunks + chunk] = t;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+
+// a.4 epilogue of the forward in ONE launch: blocks [0, merge_blocks) merge the row splits, the rest
+// resolve the fused kernel's column keys (independent work, so the two overlap on the GPU).
+__global__ void __launch_bounds__(kMergeThreads) nn_epilogue_kernel(MergeArgs m, ResolveArgs r, int merge_blocks) {
+    if ((int)blockIdx.x < merge_blocks)
+        row_merge_block(m, blockIdx.x);
+    else
+        col_resolve_block(r, blockIdx.x - merge_blocks);
 }
 
 // Per-chunk stats of given distance arrays (cd_fscore path).
@@ -562,39 +633,57 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
     }
     double* chunk_sum = reinterpret_cast<double*>(w + p.off_chunk_sum);
     int* chunk_hits = reinterpret_cast<int*>(w + p.off_chunk_hits);
-    // rows (and, unfused, both directions): merge splits + exact index re-scan + chunk partials
+    // rows (and, unfused, both directions): merge splits + exact index re-scan + chunk partials;
+    // columns of the fused modes: resolve the Y rows from the (reduced) column keys — one launch
     const int64_t merge_chunks = p.mode == kUnfused ? p.chunk_total : (int64_t)p.B * p.nchunks[0];
-    if (merge_chunks > 0) {
-        MergeArgs a;
-        a.pack[0] = pack0;
-        a.pack[1] = pack1;
-        for (int d = 0; d < 2; ++d) {
-            a.npts[d] = p.npts[d];
-            a.ppad[d] = p.ppad[d];
-            a.qlo[d] = p.qlo[d];
-            a.qhi[d] = p.qhi[d];
-            a.splits[d] = p.splits[d];
-            a.slice_off[d] = p.slice_off[d];
-            a.nchunks[d] = p.nchunks[d];
-            a.chunk_off[d] = p.chunk_off[d];
-            a.d_out[d] = o.d[d];
-            a.idx_out[d] = o.idx[d];
-        }
-        a.slice_total = p.slice_total;
-        a.B = p.B;
-        a.best_d = best_d;
-        a.best_blk = best_blk;
-        a.chunk_sum = chunk_sum;
-        a.chunk_hits = chunk_hits;
-        a.tau2 = o.tau >= 0.f ? (double)o.tau * (double)o.tau : -1.0;
-        nn_merge_kernel<<<(unsigned)merge_chunks, kMergeThreads, 0, st>>>(a);
+    MergeArgs ma;
+    ma.pack[0] = pack0;
+    ma.pack[1] = pack1;
+    for (int d = 0; d < 2; ++d) {
+        ma.npts[d] = p.npts[d];
+        ma.ppad[d] = p.ppad[d];
+        ma.qlo[d] = p.qlo[d];
+        ma.qhi[d] = p.qhi[d];
+        ma.splits[d] = p.splits[d];
+        ma.slice_off[d] = p.slice_off[d];
+        ma.nchunks[d] = p.nchunks[d];
+        ma.chunk_off[d] = p.chunk_off[d];
+        ma.d_out[d] = o.d[d];
+        ma.idx_out[d] = o.idx[d];
     }
-    // columns of the fused modes: resolve the Y rows from the (reduced) column keys
+    ma.slice_total = p.slice_total;
+    ma.B = p.B;
+    ma.best_d = best_d;
+    ma.best_blk = best_blk;
+    ma.chunk_sum = chunk_sum;
+    ma.chunk_hits = chunk_hits;
+    ma.tau2 = o.tau >= 0.f ? (double)o.tau * (double)o.tau : -1.0;
+    ResolveArgs ra;
+    int64_t resolve_chunks = 0;
     if ((p.mode == kFusedFull || p.mode == kFusedCols) && p.nchunks[1] > 0) {
-        cudaError_t e = launch_col_resolve(p, pack0, pack1, colkey, p.qlo[1], p.qhi[1], o.d[1], o.idx[1],
-                                           chunk_sum + p.chunk_off[1], chunk_hits + p.chunk_off[1], o.tau, st);
-        if (e != cudaSuccess) return e;
+        ra.xp = pack0;
+        ra.yp = pack1;
+        ra.N = p.npts[0];
+        ra.M = p.npts[1];
+        ra.xpad = p.ppad[0];
+        ra.ypad = p.ppad[1];
+        ra.q0 = 0;
+        ra.q1 = p.npts[0];
+        ra.r0 = p.qlo[1];
+        ra.r1 = p.qhi[1];
+        ra.B = p.B;
+        ra.nchunks = p.nchunks[1];
+        ra.colkey = colkey;
+        ra.d_out = o.d[1];
+        ra.idx_out = o.idx[1];
+        ra.chunk_sum = chunk_sum + p.chunk_off[1];
+        ra.chunk_hits = chunk_hits + p.chunk_off[1];
+        ra.tau2 = ma.tau2;
+        resolve_chunks = (int64_t)p.B * p.nchunks[1];
     }
+    if (merge_chunks + resolve_chunks > 0)
+        nn_epilogue_kernel<<<(unsigned)(merge_chunks + resolve_chunks), kMergeThreads, 0, st>>>(ma, ra,
+                                                                                                (int)merge_chunks);
     if (o.partials) {
         PartialsArgs a;
         a.chunk_sum = chunk_sum;
@@ -627,10 +716,10 @@ cudaError_t launch_partials(const double* chunk_sum, const int* chunk_hits, cons
 
 int forward_launches(const FwdPlan& p) {
     int n = 1;                                                      // pack (+ column-key reset)
-    if (p.mode == kUnfused) n += 2;                                 // nn_fwd + merge
-    if (p.mode == kFusedFull) n += 3;                               // fused + merge + resolve
-    if (p.mode == kFusedRows) n += 2;                               // fused + merge
-    if (p.mode == kFusedCols) n += 1;                               // resolve
+    if (p.mode == kUnfused) n += 2;                                 // nn_fwd + epilogue (merge)
+    if (p.mode == kFusedFull) n += 2;                               // fused + epilogue (merge | resolve)
+    if (p.mode == kFusedRows) n += 2;                               // fused + epilogue (merge)
+    if (p.mode == kFusedCols) n += 1;                               // epilogue (resolve)
     return n + 1;                                                   // partials
 }
 

@@ -188,90 +188,6 @@ __global__ void __launch_bounds__(kFwdThreads, 3) nn_fused_kernel(FusedArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------------
-struct ResolveArgs {
-    const float4* xp;
-    const float4* yp;
-    int N, M, xpad, ypad;
-    int q0, q1;            // X rows that took part in the column minima
-    int r0, r1;            // Y rows to resolve
-    int B, nchunks;
-    const long long* colkey;
-    float* d_out;          // [B][r1-r0]
-    int32_t* idx_out;
-    double* chunk_sum;     // dir-1 chunk partials
-    int* chunk_hits;
-    double tau2;
-};
-
-__device__ void block_sum_hits_fused(double v, int h, double* out_sum, int* out_hits) {
-    __shared__ double ssum[kMergeThreads / 32];
-    __shared__ int shit[kMergeThreads / 32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        v += __shfl_down_sync(0xffffffffu, v, o);
-        h += __shfl_down_sync(0xffffffffu, h, o);
-    }
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) {
-        ssum[w] = v;
-        shit[w] = h;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        int t = 0;
-        for (int i = 0; i < kMergeThreads / 32; ++i) {
-            s += ssum[i];
-            t += shit[i];
-        }
-        *out_sum = s;
-        *out_hits = t;
-    }
-}
-
-__global__ void __launch_bounds__(kMergeThreads) nn_col_resolve_kernel(ResolveArgs a) {
-    const int b = blockIdx.x / a.nchunks;
-    const int chunk = blockIdx.x - b * a.nchunks;
-    const int slen = a.r1 - a.r0;
-    const int sj = chunk * kMergeThreads + threadIdx.x;
-    double v = 0.0;
-    int h = 0;
-    if (sj < slen) {
-        const int j = a.r0 + sj;
-        const unsigned long long key = (unsigned long long)a.colkey[(int64_t)b * a.M + j];
-        float m = INFINITY;
-        int idx = -1;
-        if ((long long)key != kColKeyEmpty) {
-            m = __uint_as_float((unsigned)(key >> 32));
-            const int i0 = (int)(unsigned)(key & 0xffffffffull);
-            const float4 t = a.yp[(int64_t)b * a.ypad + j];
-            const float4* X = a.xp + (int64_t)b * a.xpad;
-            const int iend = min(i0 + kR, a.q1);
-            float d[kR];
-#pragma unroll
-            for (int r = 0; r < kR; ++r) {
-                const float4 q = X[min(i0 + r, a.q1 - 1)];
-                d[r] = dist_rn(q.x, q.y, q.z, t.x, t.y, t.z);  // same operand order as the kernel
-            }
-#pragma unroll
-            for (int r = kR - 1; r >= 0; --r)
-                if (i0 + r < iend && d[r] == m) idx = i0 + r;
-            if (idx < 0) m = INFINITY;  // only when every distance was NaN
-        }
-        a.d_out[(int64_t)b * slen + sj] = m;
-        a.idx_out[(int64_t)b * slen + sj] = idx;
-        v = (double)m;
-        h = (a.tau2 >= 0.0 && (double)m <= a.tau2) ? 1 : 0;
-    }
-    double s;
-    int t;
-    block_sum_hits_fused(v, h, &s, &t);
-    if (threadIdx.x == 0) {
-        a.chunk_sum[(int64_t)b * a.nchunks + chunk] = s;
-        a.chunk_hits[(int64_t)b * a.nchunks + chunk] = t;
-    }
-}
-
 // ------------------------------------------------------------------------------------------------
 int fused_ctas_per_sm() {
     static thread_local int occ = 0;
@@ -309,32 +225,6 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
         nn_fused_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
         if (g_prof_stop) record_profile_event(g_prof_stop, st);
     }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_col_resolve(const FwdPlan& p, const float4* xp, const float4* yp, const long long* colkey, int r0,
-                               int r1, float* d_out, int32_t* idx_out, double* chunk_sum, int* chunk_hits, float tau,
-                               cudaStream_t st) {
-    ResolveArgs a;
-    a.xp = xp;
-    a.yp = yp;
-    a.N = p.npts[0];
-    a.M = p.npts[1];
-    a.xpad = p.ppad[0];
-    a.ypad = p.ppad[1];
-    a.q0 = 0;
-    a.q1 = p.npts[0];
-    a.r0 = r0;
-    a.r1 = r1;
-    a.B = p.B;
-    a.nchunks = (r1 - r0 + kMergeThreads - 1) / kMergeThreads;
-    a.colkey = colkey;
-    a.d_out = d_out;
-    a.idx_out = idx_out;
-    a.chunk_sum = chunk_sum;
-    a.chunk_hits = chunk_hits;
-    a.tau2 = tau >= 0.f ? (double)tau * (double)tau : -1.0;
-    if (a.nchunks > 0) nn_col_resolve_kernel<<<p.B * a.nchunks, kMergeThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -53,13 +53,13 @@ def test_workspace_sizes(lib):
 
 
 def test_launch_counts(lib):
-    # fused forward: pack + fused + row merge + column resolve + partials
-    assert lib.cd_launch_count(0, 32, 16384, 16384) == 5
-    # backward: keys + 2 radix passes (11-bit digits cover 2^20 keys) x 3 kernels + offsets + grad
-    assert lib.cd_launch_count(2, 32, 16384, 16384) == 1 + 2 * 3 + 2
-    assert lib.cd_launch_count(3, 32, 16384, 16384) == 5 + 1 + 9
+    # fused forward: pack + fused + epilogue (row merge | column resolve) + partials
+    assert lib.cd_launch_count(0, 32, 16384, 16384) == 4
+    # backward: keys+hist, 2 radix passes (11-bit digits cover 2^20 keys) x 3 kernels - 1 hist, offsets, grad
+    assert lib.cd_launch_count(2, 32, 16384, 16384) == 2 * 3 + 2
+    assert lib.cd_launch_count(3, 32, 16384, 16384) == 4 + 1 + 8
     # c5: 2^23 keys -> 3 passes
-    assert lib.cd_launch_count(2, 4, 1 << 20, 1 << 20) == 1 + 3 * 3 + 2
+    assert lib.cd_launch_count(2, 4, 1 << 20, 1 << 20) == 3 * 3 + 2
 
 
 def _forward(lib, B=1, N=8, M=8, q=(0, 8), r=(0, 8), x=4, y=4, ws=256, wsb=1 << 30, tau=-1.0, dxy=64, ixy=64,
