@@ -66,6 +66,13 @@ __device__ __forceinline__ float dist_rn(float qx, float qy, float qz, float tx,
     return s;
 }
 
+// Row key merged over target splits with a 64-bit atomicMin: the distance bits (d >= 0, so unsigned
+// order is float order) then the block start (lowest block among equal minima); blk = -1 (no finite
+// distance) becomes 0xffffffff.  Keys are >= 0 as signed 64-bit integers.
+__device__ __forceinline__ long long row_key(float best, int blk) {
+    return (long long)(((unsigned long long)__float_as_uint(best) << 32) | (unsigned long long)(unsigned)blk);
+}
+
 // ---------------------------------------------------------------- mbarrier + TMA bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -28,7 +28,7 @@ struct FwdPlan {
     int64_t chunk_off[2];
     int64_t chunk_total;
     // workspace carve (byte offsets)
-    size_t off_pack[2], off_best_d, off_best_blk, off_chunk_sum, off_chunk_hits, off_colkey, bytes;
+    size_t off_pack[2], off_rowkey, off_chunk_sum, off_chunk_hits, off_colkey, bytes;
 };
 
 struct FwdOutputs {
@@ -46,8 +46,8 @@ int forward_launches(const FwdPlan& p);
 int fused_ctas_per_sm();
 int unfused_ctas_per_sm();
 // fused kernels (nn_fused.cu)
-cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey, float* best_d,
-                              int* best_blk, cudaStream_t st);
+cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey,
+                              long long* rowkey, cudaStream_t st);
 
 
 // Exact pruned forward (nn_pruned.cu, NEXT-2): Morton-sorted tiles + box lower-bound culling.

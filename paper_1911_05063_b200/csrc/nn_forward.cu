@@ -34,6 +34,8 @@ struct PackArgs {
     int B;
     long long* colkey;   // optional: column keys to reset to the identity of min (fused modes)
     int64_t ncolkey;
+    long long* rowkey;   // row keys (min over target splits) to reset
+    int64_t nrowkey;
 };
 
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
@@ -58,6 +60,9 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.ncolkey;
          e += (int64_t)gridDim.x * blockDim.x)
         a.colkey[e] = kColKeyEmpty;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.nrowkey;
+         e += (int64_t)gridDim.x * blockDim.x)
+        a.rowkey[e] = kColKeyEmpty;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -67,8 +72,7 @@ struct FwdArgs {
     int qlo[2], qhi[2];
     int qtiles[2], splits[2], ttiles[2];
     int64_t slice_off[2], slice_total;
-    float* best_d;
-    int* best_blk;
+    long long* rowkey;   // [slice_total]: min over splits of (best bits << 32 | block start)
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 4) nn_fwd_kernel(FwdArgs a) {
@@ -174,15 +178,11 @@ __global__ void __launch_bounds__(kFwdThreads, 4) nn_fwd_kernel(FwdArgs a) {
 
     const int qhi = a.qhi[dir];
     const int slen = qhi - a.qlo[dir];
-    const int64_t rowbase = (int64_t)split * a.slice_total + a.slice_off[dir] + (int64_t)b * slen;
+    const int64_t rowbase = a.slice_off[dir] + (int64_t)b * slen;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
         const int q = qbase + r;
-        if (q < qhi) {
-            const int64_t o = rowbase + (q - a.qlo[dir]);
-            a.best_d[o] = best[r];
-            a.best_blk[o] = blk[r];
-        }
+        if (q < qhi) atomicMin(&a.rowkey[rowbase + (q - a.qlo[dir])], row_key(best[r], blk[r]));
     }
 }
 
@@ -224,8 +224,7 @@ struct MergeArgs {
     int nchunks[2];
     int64_t chunk_off[2];
     int B;
-    const float* best_d;
-    const int* best_blk;
+    const long long* rowkey;   // [slice_total] merged (over splits) row keys
     float* d_out[2];
     int32_t* idx_out[2];
     double* chunk_sum;
@@ -249,15 +248,10 @@ __device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
     int h = 0;
     if (valid) {
         const int64_t row = a.slice_off[dir] + (int64_t)b * slen + sq;
-        float best = INFINITY;
-        int bb = -1;
-        for (int s = 0; s < a.splits[dir]; ++s) {
-            const float d = a.best_d[(int64_t)s * a.slice_total + row];
-            if (d < best) {  // strict <: the earliest split (lowest target indices) keeps ties
-                best = d;
-                bb = a.best_blk[(int64_t)s * a.slice_total + row];
-            }
-        }
+        // the atomicMin over splits kept the smallest distance, then the lowest block start
+        const unsigned long long key = (unsigned long long)a.rowkey[row];
+        const float best = __uint_as_float((unsigned)(key >> 32));
+        const int bb = (int)(unsigned)(key & 0xffffffffull);   // 0xffffffff -> -1: no finite distance
         int idx = -1;
         if (bb >= 0) {
             const int tdir = 1 - dir;
@@ -565,10 +559,9 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
         p.off_pack[d] = off;
         off = align_up(off + (size_t)B * p.ppad[d] * 16, 256);
     }
-    p.off_best_d = off;
-    off = align_up(off + (size_t)smax * p.slice_total * 4, 256);
-    p.off_best_blk = off;
-    off = align_up(off + (size_t)smax * p.slice_total * 4, 256);
+    (void)smax;
+    p.off_rowkey = off;
+    off = align_up(off + (size_t)std::max<int64_t>(p.slice_total, 1) * 8, 256);
     p.off_chunk_sum = off;
     off = align_up(off + (size_t)std::max<int64_t>(p.chunk_total, 1) * 8, 256);
     p.off_chunk_hits = off;
@@ -584,6 +577,7 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
     float4* pack0 = reinterpret_cast<float4*>(w + p.off_pack[0]);
     float4* pack1 = reinterpret_cast<float4*>(w + p.off_pack[1]);
     long long* colkey = p.mode == kFusedFull ? reinterpret_cast<long long*>(w + p.off_colkey) : o.colkey;
+    long long* rowkey = reinterpret_cast<long long*>(w + p.off_rowkey);
     {
         PackArgs a;
         a.src[0] = x;
@@ -598,12 +592,12 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
         const bool init = p.mode == kFusedFull || p.mode == kFusedRows;
         a.colkey = init ? colkey : nullptr;
         a.ncolkey = init ? (int64_t)p.B * p.npts[1] : 0;
+        a.rowkey = rowkey;
+        a.nrowkey = p.mode == kFusedCols ? 0 : p.slice_total;
         const int64_t total = (int64_t)p.B * (p.ppad[0] + p.ppad[1]);
         const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)device_sm_count() * 16);
         pack_kernel<<<grid, 256, 0, st>>>(a);
     }
-    float* best_d = reinterpret_cast<float*>(w + p.off_best_d);
-    int* best_blk = reinterpret_cast<int*>(w + p.off_best_blk);
     if (p.mode == kUnfused) {
         const int gx = p.qtiles[0] * p.splits[0] + p.qtiles[1] * p.splits[1];
         if (gx > 0) {
@@ -621,14 +615,13 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
                 a.slice_off[d] = p.slice_off[d];
             }
             a.slice_total = p.slice_total;
-            a.best_d = best_d;
-            a.best_blk = best_blk;
+            a.rowkey = rowkey;
             if (g_prof_start) record_profile_event(g_prof_start, st);
             nn_fwd_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
             if (g_prof_stop) record_profile_event(g_prof_stop, st);
         }
     } else if (p.mode == kFusedFull || p.mode == kFusedRows) {
-        cudaError_t e = launch_fused_rows(p, pack0, pack1, colkey, best_d, best_blk, st);
+        cudaError_t e = launch_fused_rows(p, pack0, pack1, colkey, rowkey, st);
         if (e != cudaSuccess) return e;
     }
     double* chunk_sum = reinterpret_cast<double*>(w + p.off_chunk_sum);
@@ -653,8 +646,7 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
     }
     ma.slice_total = p.slice_total;
     ma.B = p.B;
-    ma.best_d = best_d;
-    ma.best_blk = best_blk;
+    ma.rowkey = rowkey;
     ma.chunk_sum = chunk_sum;
     ma.chunk_hits = chunk_hits;
     ma.tau2 = o.tau >= 0.f ? (double)o.tau * (double)o.tau : -1.0;

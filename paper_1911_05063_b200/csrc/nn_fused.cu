@@ -31,8 +31,7 @@ struct FusedArgs {
     int q0, q1;         // X row slice
     int qtiles, splits, ttiles;
     int64_t slice_total;  // B * (q1 - q0)
-    float* best_d;      // [splits][B*(q1-q0)]
-    int* best_blk;
+    long long* rowkey;  // [B*(q1-q0)]: min over splits of (best bits << 32 | block start)
     long long* colkey;  // [B][M], non-negative keys; kColKeyEmpty = none
 };
 
@@ -175,15 +174,11 @@ __global__ void __launch_bounds__(kFwdThreads, 3) nn_fused_kernel(FusedArgs a) {
     }
 
     const int slen = a.q1 - a.q0;
-    const int64_t rowbase = (int64_t)split * a.slice_total + (int64_t)b * slen;
+    const int64_t rowbase = (int64_t)b * slen;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
         const int q = qbase + r;
-        if (q < a.q1) {
-            const int64_t o = rowbase + (q - a.q0);
-            a.best_d[o] = best[r];
-            a.best_blk[o] = blk[r];
-        }
+        if (q < a.q1) atomicMin(&a.rowkey[rowbase + (q - a.q0)], row_key(best[r], blk[r]));
     }
 }
 
@@ -201,8 +196,8 @@ int fused_ctas_per_sm() {
     return occ;
 }
 
-cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey, float* best_d,
-                              int* best_blk, cudaStream_t st) {
+cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey,
+                              long long* rowkey, cudaStream_t st) {
     FusedArgs a;
     a.xp = xp;
     a.yp = yp;
@@ -216,8 +211,7 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
     a.splits = p.splits[0];
     a.ttiles = p.ttiles[0];
     a.slice_total = p.slice_total;
-    a.best_d = best_d;
-    a.best_blk = best_blk;
+    a.rowkey = rowkey;
     a.colkey = colkey;
     const int gx = p.qtiles[0] * p.splits[0];
     if (gx > 0) {
