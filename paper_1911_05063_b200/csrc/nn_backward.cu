@@ -128,24 +128,29 @@ __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* _
 // Stable scatter of one tile.  Warp w owns elements [w*512, (w+1)*512) of the tile (16 rounds of
 // 32), so tile order = (warp, round, lane).  Phase 1: per-warp digit counters in shared memory give
 // every element its rank among equal digits of its warp (warp match; only the warp's own counter row
-// is touched, no block barrier per round).  Phase 2: per digit, exclusive prefix over the warps plus
-// the digit's global base (exclusive scan of the digit totals) plus this tile's row-scan offset.
-// Phase 3: scatter.  Dynamic shared memory: (kSortWarps + 1) * D words.
+// is touched, no block barrier per round).  Phase 2: per digit, the tile-local start (exclusive scan
+// of the tile's digit counts) plus the prefix over the warps; delta[d] = global base - local start.
+// Phase 3: the tile is re-ordered by digit in shared memory, then written out so that consecutive
+// threads write consecutive addresses of each digit's run (coalesced stores).
+// Dynamic shared memory: (kSortWarps + 2) * D + 2 * kSortTile words.
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int D, int ntiles,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout) {
     extern __shared__ uint32_t smem[];
-    uint32_t* wcnt = smem;                      // [kSortWarps][D]
-    uint32_t* dbase = smem + kSortWarps * D;    // [D]
+    uint32_t* wcnt = smem;                       // [kSortWarps][D]
+    uint32_t* dbase = smem + kSortWarps * D;     // [D] global base of digit d for this tile
+    uint32_t* delta = dbase + D;                 // [D] global base - tile-local start
+    uint32_t* skey = delta + D;                  // [kSortTile] tile re-ordered by digit
+    uint32_t* sval = skey + kSortTile;
     __shared__ uint32_t warp_tot[kSortWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    const int per = (D + kSortThreads - 1) / kSortThreads;   // digits owned by this thread in the scans
+    const int d0 = threadIdx.x * per;
     for (int i = threadIdx.x; i < kSortWarps * D; i += kSortThreads) wcnt[i] = 0;
-    // global digit bases: exclusive scan of totals[0..D), each thread owns D/256 consecutive digits
+    // global digit bases: exclusive scan of totals[0..D), plus this tile's row-scan offset
     {
-        const int per = (D + kSortThreads - 1) / kSortThreads;
-        const int d0 = threadIdx.x * per;
         uint32_t loc = 0;
         for (int d = d0; d < min(d0 + per, D); ++d) loc += totals[d];
         uint32_t tot;
@@ -157,15 +162,22 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     }
     __syncthreads();
     const uint32_t lt_mask = (1u << lane) - 1u;
-    const int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * (kSortItems * 32);
+    const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
+    const int64_t wbase = tbase + (int64_t)warp * (kSortItems * 32);
     uint32_t kk[kSortItems], vv[kSortItems], rk[kSortItems];
     uint32_t* my = wcnt + warp * D;
+    // all 16 loads first (independent: full memory-level parallelism), then the ranking rounds
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
         const int64_t e = wbase + k * 32 + lane;
         const bool valid = e < L;
         kk[k] = valid ? kin[e] : 0u;
         vv[k] = valid ? vin[e] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+        const int64_t e = wbase + k * 32 + lane;
+        const bool valid = e < L;
         const int digit = valid ? (int)((kk[k] >> shift) & (D - 1)) : D;  // D: sentinel group
         const uint32_t peers = __match_any_sync(0xffffffffu, digit);
         const uint32_t before = valid ? my[digit] : 0u;
@@ -175,24 +187,39 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
         __syncwarp();
     }
     __syncthreads();
-    // per digit: prefix over warps (warp order = element order), plus the digit base
-    for (int d = threadIdx.x; d < D; d += kSortThreads) {
-        uint32_t run = dbase[d];
-        for (int w = 0; w < kSortWarps; ++w) {
-            const uint32_t t = wcnt[w * D + d];
-            wcnt[w * D + d] = run;
-            run += t;
+    // tile-local digit starts (exclusive scan of the tile's digit counts) and warp prefixes
+    {
+        uint32_t loc = 0;
+        for (int d = d0; d < min(d0 + per, D); ++d)
+            for (int w = 0; w < kSortWarps; ++w) loc += wcnt[w * D + d];
+        uint32_t tot;
+        uint32_t run = block_exclusive_scan(loc, warp_tot, tot);
+        for (int d = d0; d < min(d0 + per, D); ++d) {
+            delta[d] = dbase[d] - run;
+            for (int w = 0; w < kSortWarps; ++w) {
+                const uint32_t t = wcnt[w * D + d];
+                wcnt[w * D + d] = run;
+                run += t;
+            }
         }
     }
     __syncthreads();
+    const int nvalid = (int)min((int64_t)kSortTile, L - tbase);
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
         const int64_t e = wbase + k * 32 + lane;
         if (e < L) {
-            const uint32_t pos = my[(kk[k] >> shift) & (D - 1)] + rk[k];
-            kout[pos] = kk[k];
-            vout[pos] = vv[k];
+            const uint32_t lp = my[(kk[k] >> shift) & (D - 1)] + rk[k];
+            skey[lp] = kk[k];
+            sval[lp] = vv[k];
         }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nvalid; i += kSortThreads) {
+        const uint32_t key = skey[i];
+        const uint32_t pos = (uint32_t)i + delta[(key >> shift) & (D - 1)];
+        kout[pos] = key;
+        vout[pos] = sval[i];
     }
 }
 
@@ -325,11 +352,11 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits,
     int npasses, digit_bits, ntiles;
     radix_sort_plan(L, nbits, npasses, digit_bits, ntiles);
     const int D = 1 << digit_bits;
-    const size_t scatter_smem = (size_t)(kSortWarps + 1) * D * 4;
+    const size_t scatter_smem = ((size_t)(kSortWarps + 2) * D + 2 * kSortTile) * 4;
     static thread_local bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (kSortWarps + 1) * (1 << kMaxDigitBits) * 4);
+                             ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile) * 4);
         attr_set = true;
     }
     int cur = 0;
