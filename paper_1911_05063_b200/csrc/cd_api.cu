@@ -348,7 +348,7 @@ size_t cd_sample_workspace_size(int op, int B, int Nv, int Nf, int N) {
 
 int cd_sample_launch_count(int op, int B, int Nv, int Nf, int N) {
     if (B < 1 || Nv < 3 || Nf < 1 || N < 1) return 0;
-    if (op == CD_OP_SAMPLE) return 2;
+    if (op == CD_OP_SAMPLE) return 3;
     if (op == CD_OP_SAMPLE_BACKWARD) return cdk::sample_backward_launches(B, Nv, Nf, N);
     return 0;
 }

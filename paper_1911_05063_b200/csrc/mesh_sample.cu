@@ -2,10 +2,11 @@
 // ("differentiable surface sampling ... by
 // application of the reparameterization trick").  Readings R19-R22:
 //
-//   mesh_cdf_kernel     one CTA per batch element: fp64 face areas (fixed op order, no contraction),
-//                       quantised to integers q_f = floor(area_f * 2^k) with k = 52 - e,
-//                       Nf * max area = m 2^e; exact uint64 inclusive prefix (order-free integers),
-//                       so the face choice is the same integer decision on every implementation.
+//   mesh_area_kernel    fp64 face areas (fixed op order, no contraction) on every SM, per-CTA max.
+//   mesh_cdf_kernel     one CTA per batch element: areas quantised to integers q_f = floor(area_f * 2^k)
+//                       with k = 52 - e, Nf * max area = m 2^e; exact uint64 inclusive prefix
+//                       (order-free integers), so the face choice is the same integer decision on
+//                       every implementation.
 //   mesh_sample_kernel  per sample: t = (r_face * S) >> 32 exactly, face = upper_bound(prefix, t),
 //                       square-root barycentrics and the point, fp32 .rn ops.
 //   backward            keys (b*Nv + corner vertex) for every (sample, corner), the stable radix sort
@@ -35,21 +36,49 @@ __device__ __forceinline__ double face_area64(const float* v, int fa, int fb, in
 struct CdfArgs {
     const float* verts;   // [B][Nv][3]
     const int* faces;     // [Nf][3]
-    int Nv, Nf;
+    int Nv, Nf, nblk;
+    double* areas;        // [B][Nf] scratch
+    double* blkmax;       // [B][nblk] scratch
     unsigned long long* cdf;  // [B][Nf] inclusive prefix of the quantised areas
 };
 
+constexpr int kAreaThreads = 256;
+
+// (1) fp64 areas of every face (all SMs), per-CTA maximum (fixed-order, no atomics)
+__global__ void __launch_bounds__(kAreaThreads) mesh_area_kernel(CdfArgs a) {
+    const int b = blockIdx.y;
+    const float* v = a.verts + (int64_t)b * a.Nv * 3;
+    const int f = blockIdx.x * kAreaThreads + threadIdx.x;
+    double ar = 0.0;
+    if (f < a.Nf) {
+        const int ia = min(max(a.faces[3 * f], 0), a.Nv - 1), ib = min(max(a.faces[3 * f + 1], 0), a.Nv - 1),
+                  ic = min(max(a.faces[3 * f + 2], 0), a.Nv - 1);
+        ar = face_area64(v, ia, ib, ic);
+        a.areas[(int64_t)b * a.Nf + f] = ar;
+    }
+    __shared__ double sm[kAreaThreads / 32];
+    double m = ar;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = 0.0;
+        for (int w = 0; w < kAreaThreads / 32; ++w) mm = fmax(mm, sm[w]);
+        a.blkmax[(int64_t)b * a.nblk + blockIdx.x] = mm;
+    }
+}
+
+// (2) one CTA per batch element: max -> exponent, quantise, exact uint64 inclusive prefix
+// (each thread a contiguous run of faces, one block scan of the run totals)
 __global__ void __launch_bounds__(kCdfThreads) mesh_cdf_kernel(CdfArgs a) {
     const int b = blockIdx.x;
-    const float* v = a.verts + (int64_t)b * a.Nv * 3;
     __shared__ double smax[kCdfThreads / 32];
     __shared__ unsigned long long wtot[kCdfThreads / 32];
     __shared__ int s_e;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    auto clampv = [&](int i) { return min(max(i, 0), a.Nv - 1); };
     double m = 0.0;
-    for (int f = threadIdx.x; f < a.Nf; f += kCdfThreads)
-        m = fmax(m, face_area64(v, clampv(a.faces[3 * f]), clampv(a.faces[3 * f + 1]), clampv(a.faces[3 * f + 2])));
+    for (int i = threadIdx.x; i < a.nblk; i += kCdfThreads) m = fmax(m, a.blkmax[(int64_t)b * a.nblk + i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) smax[warp] = m;
@@ -63,30 +92,28 @@ __global__ void __launch_bounds__(kCdfThreads) mesh_cdf_kernel(CdfArgs a) {
     }
     __syncthreads();
     const int e = s_e;
-    unsigned long long carry = 0;
-    for (int base = 0; base < a.Nf; base += kCdfThreads) {
-        const int f = base + threadIdx.x;
-        unsigned long long q = 0;
-        if (f < a.Nf && e != 1000) {
-            const double ar = face_area64(v, clampv(a.faces[3 * f]), clampv(a.faces[3 * f + 1]), clampv(a.faces[3 * f + 2]));
-            q = (unsigned long long)ldexp(ar, 52 - e);   // exact scaling, truncation = floor (ar >= 0)
-        }
-        unsigned long long incl = q;
+    const double* ar = a.areas + (int64_t)b * a.Nf;
+    const int per = (a.Nf + kCdfThreads - 1) / kCdfThreads;
+    const int f0 = threadIdx.x * per, f1 = min(f0 + per, a.Nf);
+    auto quant = [&](int f) -> unsigned long long {
+        return e == 1000 ? 0ull : (unsigned long long)ldexp(ar[f], 52 - e);  // exact scaling, floor
+    };
+    unsigned long long loc = 0;
+    for (int f = f0; f < f1; ++f) loc += quant(f);
+    unsigned long long incl = loc;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) wtot[warp] = incl;
-        __syncthreads();
-        unsigned long long before = 0, all = 0;
-        for (int w = 0; w < kCdfThreads / 32; ++w) {
-            before += w < warp ? wtot[w] : 0ull;
-            all += wtot[w];
-        }
-        if (f < a.Nf) a.cdf[(int64_t)b * a.Nf + f] = carry + before + incl;
-        carry += all;
-        __syncthreads();
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    unsigned long long run = incl - loc;
+    for (int w = 0; w < warp; ++w) run += wtot[w];
+    unsigned long long* out = a.cdf + (int64_t)b * a.Nf;
+    for (int f = f0; f < f1; ++f) {
+        run += quant(f);
+        out[f] = run;
     }
 }
 
@@ -189,21 +216,28 @@ __global__ void __launch_bounds__(256) vertex_grad_kernel(const uint32_t* __rest
 // ------------------------------------------------------------------------------------------ host
 static int ceil_div64(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+static int area_blocks(int Nf) { return (Nf + kAreaThreads - 1) / kAreaThreads; }
+
 size_t sample_workspace(int B, int Nv, int Nf, int N) {
     (void)Nv;
     (void)N;
-    return align_up((size_t)B * Nf * 8, 256);
+    return align_up((size_t)B * Nf * 8, 256) * 2 + align_up((size_t)B * area_blocks(Nf) * 8, 256);
 }
 
 cudaError_t launch_sample(const float* verts, const int* faces, int B, int Nv, int Nf, int N, const unsigned* r_face,
                           const float* r_bary, float* points, int* face_idx, float* bary, void* ws, cudaStream_t st) {
-    unsigned long long* cdf = static_cast<unsigned long long*>(ws);
+    char* w = static_cast<char*>(ws);
+    unsigned long long* cdf = reinterpret_cast<unsigned long long*>(w);
     CdfArgs c;
     c.verts = verts;
     c.faces = faces;
     c.Nv = Nv;
     c.Nf = Nf;
+    c.nblk = area_blocks(Nf);
     c.cdf = cdf;
+    c.areas = reinterpret_cast<double*>(w + align_up((size_t)B * Nf * 8, 256));
+    c.blkmax = reinterpret_cast<double*>(w + 2 * align_up((size_t)B * Nf * 8, 256));
+    mesh_area_kernel<<<dim3(c.nblk, B), kAreaThreads, 0, st>>>(c);
     mesh_cdf_kernel<<<B, kCdfThreads, 0, st>>>(c);
     SampleArgs s;
     s.verts = verts;
