@@ -244,6 +244,22 @@ CD_API cd_status cd_p2s_backward(const float* points, const float* closest, cons
                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
 CD_API size_t cd_p2s_workspace_size(int op, int B, int N, int Nv, int Nf);
 
+/*
+ * cd_step_host_overlapped — cd_step_host with the host->device copies overlapped with the compute:
+ * the clouds are copied in `nchunks` batch ranges on `copy_stream`; the forward of range c runs on
+ * `stream` as soon as range c has landed (cudaStreamWaitEvent), while later ranges are still in
+ * flight; finalize, backward and the D2H copies follow on `stream`.  Results are identical to
+ * cd_step_host (per-batch outputs do not depend on the chunking).  events: nchunks + 1 cudaEvent_t
+ * created by the caller (disable-timing events are fine); events[nchunks] is recorded at the end of
+ * the step, and the next call's copies wait on it before overwriting the staging buffers.
+ * nchunks in [1, B].  Workspace: cd_workspace_size(CD_OP_STEP).
+ */
+CD_API cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int B, int N, int M,
+                       float tau, float w1, float w2,
+                       float* loss_host, float* fscore_host, float* grad_x_host, float* grad_y_host,
+                       int nchunks, void* workspace, size_t workspace_bytes,
+                       cd_stream_t stream, cd_stream_t copy_stream, void* const* events);
+
 /* Workspace bytes needed by an operation for these sizes (full slices).  0 on invalid sizes. */
 CD_API size_t cd_workspace_size(int op, int B, int N, int M);
 

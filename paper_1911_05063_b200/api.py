@@ -236,6 +236,36 @@ def step_host(x_host: np.ndarray, y_host: np.ndarray, tau: float | None = None, 
     return out
 
 
+class HostStepper:
+    """End-to-end steps from pinned host clouds with the H2D copies overlapped with the compute
+    (cd_step_host_overlapped).  Owns a copy stream and nchunks + 1 events; outputs land in pinned
+    host tensors.  step() is asynchronous: call synchronize() (or read after the stream syncs)."""
+
+    def __init__(self, B: int, N: int, M: int, tau: float | None = None, w1: float = 1.0, w2: float = 1.0,
+                 nchunks: int | None = None, device=None):
+        self.B, self.N, self.M, self.tau, self.w1, self.w2 = B, N, M, tau, w1, w2
+        self.nchunks = nchunks or (4 if B >= 8 else 1)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.ws = workspace(_lib.CD_OP_STEP, B, N, M, self.device)
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.events = [torch.cuda.Event() for _ in range(self.nchunks + 1)]
+        for ev in self.events:       # materialise the cudaEvent handles
+            ev.record()
+        torch.cuda.synchronize(self.device)
+        self._evp = (ctypes.c_void_p * (self.nchunks + 1))(*[ev.cuda_event for ev in self.events])
+        self.loss = pinned_empty((1,))
+        self.fscore = pinned_empty((B,))
+
+    def step(self, x_host: torch.Tensor, y_host: torch.Tensor):
+        check(_lib.load().cd_step_host_overlapped(
+            _host_ptr(x_host), _host_ptr(y_host), self.B, self.N, self.M,
+            float(-1.0 if self.tau is None else self.tau), float(self.w1), float(self.w2),
+            _host_ptr(self.loss), _host_ptr(self.fscore) if self.tau is not None else None, None, None,
+            self.nchunks, _ptr(self.ws), self.ws.numel(), _stream(),
+            ctypes.c_void_p(self.copy_stream.cuda_stream), self._evp))
+        return self.loss, self.fscore
+
+
 def _host_ptr(t):
     if t is None:
         return None

@@ -514,4 +514,78 @@ cd_status cd_step_host(const float* x_host, const float* y_host, int B, int N, i
     return cuda_status(e, "cd_step_host D2H");
 }
 
+cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int B, int N, int M, float tau, float w1,
+                                  float w2, float* loss_host, float* fscore_host, float* grad_x_host,
+                                  float* grad_y_host, int nchunks, void* workspace, size_t workspace_bytes,
+                                  cd_stream_t stream, cd_stream_t copy_stream, void* const* events) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x_host || !y_host || !loss_host || !workspace || !events || !copy_stream)
+        return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (nchunks < 1 || nchunks > B) return fail(CD_ERR_INVALID_VALUE, "nchunks must be in [1, B] (got %d)", nchunks);
+    for (int c = 0; c <= nchunks; ++c)
+        if (!events[c]) return fail(CD_ERR_INVALID_VALUE, "events[%d] is null", c);
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const StepLayout L = step_layout(B, N, M);
+    if (workspace_bytes < L.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, L.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaStream_t cs = static_cast<cudaStream_t>(copy_stream);
+    char* w = static_cast<char*>(workspace);
+    float* x = reinterpret_cast<float*>(w + L.x);
+    float* y = reinterpret_cast<float*>(w + L.y);
+    float* dxy = reinterpret_cast<float*>(w + L.dxy);
+    int32_t* ixy = reinterpret_cast<int32_t*>(w + L.ixy);
+    float* dyx = reinterpret_cast<float*>(w + L.dyx);
+    int32_t* iyx = reinterpret_cast<int32_t*>(w + L.iyx);
+    double* part = reinterpret_cast<double*>(w + L.part);
+    float* loss = reinterpret_cast<float*>(w + L.loss);
+    float* fs = reinterpret_cast<float*>(w + L.fs);
+    float* gx = reinterpret_cast<float*>(w + L.gx);
+    float* gy = reinterpret_cast<float*>(w + L.gy);
+    void* inner = w + L.inner;
+    cudaEvent_t done = static_cast<cudaEvent_t>(events[nchunks]);
+    // the staging buffers are free once the previous step on `stream` is done (never-recorded: no-op)
+    cudaError_t e = cudaStreamWaitEvent(cs, done, 0);
+    for (int c = 0; c < nchunks && e == cudaSuccess; ++c) {
+        const int b0 = (int)((int64_t)B * c / nchunks), b1 = (int)((int64_t)B * (c + 1) / nchunks);
+        e = cudaMemcpyAsync(x + (size_t)b0 * N * 3, x_host + (size_t)b0 * N * 3, (size_t)(b1 - b0) * N * 12,
+                            cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(y + (size_t)b0 * M * 3, y_host + (size_t)b0 * M * 3, (size_t)(b1 - b0) * M * 12,
+                                cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(static_cast<cudaEvent_t>(events[c]), cs);
+    }
+    if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped H2D");
+    // chunk c's forward starts as soon as its clouds have landed; later chunks copy meanwhile
+    for (int c = 0; c < nchunks; ++c) {
+        const int b0 = (int)((int64_t)B * c / nchunks), b1 = (int)((int64_t)B * (c + 1) / nchunks);
+        e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(events[c]), 0);
+        if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped wait");
+        s = cd_forward(x + (size_t)b0 * N * 3, y + (size_t)b0 * M * 3, b1 - b0, N, M, 0, N, 0, M,
+                       dxy + (size_t)b0 * N, ixy + (size_t)b0 * N, dyx + (size_t)b0 * M, iyx + (size_t)b0 * M,
+                       part + 4 * (size_t)b0, tau, inner, L.inner_bytes, stream);
+        if (s != CD_OK) return s;
+    }
+    s = cd_finalize(part, B, N, M, w1, w2, nullptr, loss, tau >= 0.f ? fs : nullptr, nullptr, nullptr, stream);
+    if (s != CD_OK) return s;
+    const float gs = (float)((double)w1 / ((double)B * N));
+    const float hs = (float)((double)w2 / ((double)B * M));
+    s = cd_backward(x, y, B, N, M, ixy, iyx, nullptr, nullptr, gs, hs, 0, N, 0, M, gx, gy, inner, L.inner_bytes,
+                    stream);
+    if (s != CD_OK) return s;
+    e = cudaMemcpyAsync(loss_host, loss, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && fscore_host && tau >= 0.f)
+        e = cudaMemcpyAsync(fscore_host, fs, (size_t)B * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && grad_x_host)
+        e = cudaMemcpyAsync(grad_x_host, gx, (size_t)B * N * 12, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && grad_y_host)
+        e = cudaMemcpyAsync(grad_y_host, gy, (size_t)B * M * 12, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaEventRecord(done, st);
+    return cuda_status(e, "cd_step_host_overlapped D2H");
+}
+
 }  // extern "C"

@@ -421,3 +421,16 @@ def test_pruned_large_sampled(cd):
     np.testing.assert_array_equal(pr[0].reshape(-1)[rows], dm)
     clear = (d2 - d1) > 1e-6 * d1
     np.testing.assert_array_equal(pr[1].reshape(-1)[rows][clear], i1[clear])
+
+
+def test_step_host_overlapped_equals_step_host(cd):
+    X, Y = synth.shape_pair(8, 3000, 2500, config_index=29)
+    xh, yh = cd.pinned_copy(X), cd.pinned_copy(Y)
+    ref = cd.step_host(xh.numpy(), yh.numpy(), tau=0.01, want_grads=False)
+    for nchunks in (1, 3, 8):
+        st = cd.HostStepper(8, 3000, 2500, tau=0.01, nchunks=nchunks)
+        for _ in range(2):                      # back-to-back steps reuse the staging buffers
+            loss, fs = st.step(xh, yh)
+        torch.cuda.synchronize()
+        assert float(loss[0]) == float(ref["loss"][0])
+        np.testing.assert_array_equal(fs.numpy(), ref["fscore"].numpy())
