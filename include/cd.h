@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define CD_ABI_VERSION 2
+#define CD_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define CD_API __attribute__((visibility("default")))
@@ -67,7 +67,8 @@ typedef enum {
     CD_OP_SAMPLE = 5,          /* cd_sample_mesh (cd_sample_workspace_size) */
     CD_OP_SAMPLE_BACKWARD = 6, /* cd_sample_mesh_backward (cd_sample_workspace_size) */
     CD_OP_P2S = 7,             /* cd_p2s_forward (cd_p2s_workspace_size) */
-    CD_OP_P2S_BACKWARD = 8     /* cd_p2s_backward (cd_p2s_workspace_size) */
+    CD_OP_P2S_BACKWARD = 8,    /* cd_p2s_backward (cd_p2s_workspace_size) */
+    CD_OP_P2S_PRUNED = 9       /* cd_p2s_forward_pruned (cd_p2s_workspace_size) */
 } cd_op;
 
 /*
@@ -243,6 +244,23 @@ CD_API cd_status cd_p2s_backward(const float* points, const float* closest, cons
                          const float* g, float g_scalar, float* grad_points, float* grad_verts,
                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
 CD_API size_t cd_p2s_workspace_size(int op, int B, int N, int Nv, int Nf);
+CD_API int cd_p2s_launch_count(int op, int B, int N, int Nv, int Nf);
+
+/*
+ * cd_p2s_forward_pruned — cd_p2s_forward with culling (R26): points and face centroids
+ * are Morton-sorted per batch element; 256-point query tiles visit 128-face tiles in ascending order
+ * of a box lower bound and stop once the bound exceeds every point's current minimum; 32-face blocks
+ * are skipped per warp the same way.  Boxes are widened by 2^-14 max|coord| so that the bound also
+ * holds for the fp32-evaluated distances of the hot loop (R26): the minimum is the brute force's.
+ * Same arguments and outputs as cd_p2s_forward except the tie rule: among faces with EXACTLY equal
+ * fp32 minima the first found in the visiting order is returned (any of them is a closest face).
+ * Workspace: cd_p2s_workspace_size(CD_OP_P2S_PRUNED, ...); 0 = unsupported size (more than
+ * 8192 face tiles, i.e. Nf > 1048576, or B*(N+Nf) >= 2^31) and the call returns CD_ERR_TOO_LARGE.
+ */
+CD_API cd_status cd_p2s_forward_pruned(const float* points, const float* verts, const int32_t* faces,
+                         int B, int N, int Nv, int Nf, float* d, int32_t* face, float* closest,
+                         float* bary, float* per_batch, float* loss,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream);
 
 /*
  * cd_step_host_overlapped — cd_step_host with the host->device copies overlapped with the compute:

@@ -19,7 +19,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "cd.h")
 
 CD_OK = 0
 CD_OP_FORWARD, CD_OP_FSCORE, CD_OP_BACKWARD, CD_OP_STEP, CD_OP_FORWARD_PRUNED = 0, 1, 2, 3, 4
-CD_OP_SAMPLE, CD_OP_SAMPLE_BACKWARD, CD_OP_P2S, CD_OP_P2S_BACKWARD = 5, 6, 7, 8
+CD_OP_SAMPLE, CD_OP_SAMPLE_BACKWARD, CD_OP_P2S, CD_OP_P2S_BACKWARD, CD_OP_P2S_PRUNED = 5, 6, 7, 8, 9
 STATUS_NAMES = {0: "CD_OK", 1: "CD_ERR_INVALID_VALUE", 2: "CD_ERR_MISALIGNED", 3: "CD_ERR_TOO_LARGE",
                 4: "CD_ERR_UNSUPPORTED_DEVICE", 5: "CD_ERR_CUDA"}
 
@@ -55,6 +55,8 @@ _SIGS = {
     "cd_p2s_forward": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "cd_p2s_backward": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, f32, vp, vp, vp, sz, vp], i32),
     "cd_p2s_workspace_size": ([i32, i32, i32, i32, i32], sz),
+    "cd_p2s_launch_count": ([i32, i32, i32, i32, i32], i32),
+    "cd_p2s_forward_pruned": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "cd_forward_rows": ([vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, f32, vp, sz, vp], i32),
     "cd_forward_cols": ([vp, vp, i32, i32, i32, vp, i32, i32, vp, vp, vp, f32, vp, sz, vp], i32),
 }
@@ -86,7 +88,7 @@ def load():
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res
-            if lib.cd_abi_version() != 2:
+            if lib.cd_abi_version() != 3:
                 raise RuntimeError("libcd ABI version mismatch")
             _lib = lib
     return _lib

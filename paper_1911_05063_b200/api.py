@@ -407,8 +407,11 @@ def _p2s_ws(op, B, N, Nv, Nf, device):
     return buf
 
 
-def p2s_forward(points: torch.Tensor, verts: torch.Tensor, faces: torch.Tensor):
-    """cd_p2s_forward: (d [B,N], face [B,N], closest [B,N,3], bary [B,N,3], per_batch [B], loss [1])."""
+def p2s_forward(points: torch.Tensor, verts: torch.Tensor, faces: torch.Tensor, algorithm: str = "brute"):
+    """cd_p2s_forward (algorithm="brute") or cd_p2s_forward_pruned (algorithm="pruned", R26):
+    (d [B,N], face [B,N], closest [B,N,3], bary [B,N,3], per_batch [B], loss [1])."""
+    if algorithm not in ("brute", "pruned"):
+        raise ValueError(f"algorithm must be 'brute' or 'pruned', got {algorithm!r}")
     points = _check_cloud(points, "points")
     verts = _check_cloud(verts, "verts")
     faces = faces.to(torch.int32).contiguous()
@@ -422,9 +425,11 @@ def p2s_forward(points: torch.Tensor, verts: torch.Tensor, faces: torch.Tensor):
     ba = torch.empty((B, N, 3), dtype=torch.float32, device=dev)
     pb = torch.empty(B, dtype=torch.float32, device=dev)
     loss = torch.empty(1, dtype=torch.float32, device=dev)
-    ws = _p2s_ws(_lib.CD_OP_P2S, B, N, Nv, Nf, dev)
-    check(_lib.load().cd_p2s_forward(_ptr(points), _ptr(verts), _ptr(faces), B, N, Nv, Nf, _ptr(d), _ptr(fi), _ptr(cl),
-                                     _ptr(ba), _ptr(pb), _ptr(loss), _ptr(ws), ws.numel(), _stream()))
+    op = _lib.CD_OP_P2S if algorithm == "brute" else _lib.CD_OP_P2S_PRUNED
+    fn = _lib.load().cd_p2s_forward if algorithm == "brute" else _lib.load().cd_p2s_forward_pruned
+    ws = _p2s_ws(op, B, N, Nv, Nf, dev)
+    check(fn(_ptr(points), _ptr(verts), _ptr(faces), B, N, Nv, Nf, _ptr(d), _ptr(fi), _ptr(cl),
+             _ptr(ba), _ptr(pb), _ptr(loss), _ptr(ws), ws.numel(), _stream()))
     return d, fi, cl, ba, pb, loss
 
 
@@ -449,8 +454,8 @@ class PointToSurfaceFunction(torch.autograd.Function):
     """loss = mean_b mean_i min_f dist^2(p_i, face f); gradients to points and mesh vertices."""
 
     @staticmethod
-    def forward(ctx, points, verts, faces):
-        d, fi, cl, ba, pb, loss = p2s_forward(points, verts, faces)
+    def forward(ctx, points, verts, faces, algorithm="brute"):
+        d, fi, cl, ba, pb, loss = p2s_forward(points, verts, faces, algorithm=algorithm)
         ctx.save_for_backward(points, cl, fi, ba, faces)
         ctx.Nv = verts.shape[1]
         return loss[0]
@@ -462,9 +467,10 @@ class PointToSurfaceFunction(torch.autograd.Function):
         g = (grad_out.reshape(1).float() / (B * N)).expand(B, N)
         gp, gv = p2s_backward(points, cl, fi, ba, faces, ctx.Nv, g=g, want_points=ctx.needs_input_grad[0],
                               want_verts=ctx.needs_input_grad[1])
-        return gp, gv, None
+        return gp, gv, None, None
 
 
-def point_to_surface(points, verts, faces):
-    """Differentiable point-to-surface loss (GEOMetrics)."""
-    return PointToSurfaceFunction.apply(points, verts, faces)
+def point_to_surface(points, verts, faces, algorithm: str = "brute"):
+    """Differentiable point-to-surface loss (GEOMetrics); algorithm "pruned" culls
+    faces (R26) with the same minimum."""
+    return PointToSurfaceFunction.apply(points, verts, faces, algorithm)

@@ -401,7 +401,34 @@ size_t cd_p2s_workspace_size(int op, int B, int N, int Nv, int Nf) {
     if (B < 1 || N < 1 || Nv < 3 || Nf < 1) return 0;
     if (op == CD_OP_P2S) return cdk::p2s_workspace(B, N, Nv, Nf);
     if (op == CD_OP_P2S_BACKWARD) return cdk::p2s_backward_workspace(B, N, Nv, Nf);
+    if (op == CD_OP_P2S_PRUNED) return cdk::p2s_pruned_workspace(B, N, Nv, Nf);
     return 0;
+}
+
+int cd_p2s_launch_count(int op, int B, int N, int Nv, int Nf) {
+    if (B < 1 || N < 1 || Nv < 3 || Nf < 1) return 0;
+    if (op == CD_OP_P2S) return cdk::p2s_launches();
+    if (op == CD_OP_P2S_BACKWARD) return 1 + cdk::sample_backward_launches(B, Nv, Nf, N);
+    if (op == CD_OP_P2S_PRUNED) return cdk::p2s_pruned_workspace(B, N, Nv, Nf) ? cdk::p2s_pruned_launches(B, N, Nv, Nf) : 0;
+    return 0;
+}
+
+cd_status cd_p2s_forward_pruned(const float* points, const float* verts, const int32_t* faces, int B, int N, int Nv,
+                                int Nf, float* d, int32_t* face, float* closest, float* bary, float* per_batch,
+                                float* loss, void* workspace, size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_p2s_sizes(B, N, Nv, Nf);
+    if (s != CD_OK) return s;
+    if (!points || !verts || !faces || !d || !face || !workspace) return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    const size_t need = cdk::p2s_pruned_workspace(B, N, Nv, Nf);
+    if (need == 0) return fail(CD_ERR_TOO_LARGE, "pruned point-to-surface: unsupported size (Nf %d, B %d, N %d)", Nf, B, N);
+    if (workspace_bytes < need) return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu", workspace_bytes, need);
+    s = check_device();
+    if (s != CD_OK) return s;
+    return cuda_status(cdk::launch_p2s_pruned(points, verts, faces, B, N, Nv, Nf, d, face, closest, bary, per_batch,
+                                              loss, workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_p2s_forward_pruned");
 }
 
 int cd_set_forward_mode(int mode) {

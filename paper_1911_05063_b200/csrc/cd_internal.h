@@ -87,6 +87,16 @@ cudaError_t launch_p2s_backward(const float* points, const float* closest, const
                                 const int* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
                                 float* grad_points, float* grad_verts, void* ws, cudaStream_t st);
 int p2s_launches();
+void launch_p2s_finalize(const double* chunk_sum, int B, int N, int nchunks, float* per_batch, float* loss,
+                         cudaStream_t st);
+// Culled point-to-surface forward (p2s_pruned.cu, R26); workspace 0 = unsupported size.
+size_t p2s_pruned_workspace(int B, int N, int Nv, int Nf);
+int p2s_pruned_launches(int B, int N, int Nv, int Nf);
+cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int* faces, int B, int N, int Nv, int Nf,
+                              float* d, int* face, float* closest, float* bary, float* per_batch, float* loss,
+                              void* ws, cudaStream_t st);
+// Per-(cloud, batch) sample bounding boxes [2][B][6] (nn_pruned.cu).
+void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, float* bbox, cudaStream_t st);
 
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.
 size_t fscore_workspace(int B, int N, int M);

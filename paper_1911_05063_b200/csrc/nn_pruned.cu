@@ -77,6 +77,17 @@ __global__ void __launch_bounds__(256) bbox_kernel(BoxArgs a) {
     }
 }
 
+void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, float* bbox, cudaStream_t st) {
+    BoxArgs a;
+    a.src[0] = src0;
+    a.src[1] = src1;
+    a.npts[0] = n0;
+    a.npts[1] = n1;
+    a.B = B;
+    a.bbox = bbox;
+    bbox_kernel<<<2 * B, 256, 0, st>>>(a);
+}
+
 // --------------------------------------------------------------------------------------------- morton
 __device__ __forceinline__ uint32_t spread_bits(uint32_t v, int k) {
     uint32_t r = 0;
@@ -623,16 +634,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     float* bbox = reinterpret_cast<float*>(w + p.off_bbox);
-    {
-        BoxArgs a;
-        a.src[0] = x;
-        a.src[1] = y;
-        a.npts[0] = p.npts[0];
-        a.npts[1] = p.npts[1];
-        a.B = p.B;
-        a.bbox = bbox;
-        bbox_kernel<<<2 * p.B, 256, 0, st>>>(a);
-    }
+    launch_bbox(x, p.npts[0], y, p.npts[1], p.B, bbox, st);
     uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);

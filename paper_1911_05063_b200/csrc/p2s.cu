@@ -232,6 +232,11 @@ __global__ void __launch_bounds__(256) p2s_finalize_kernel(const double* chunk_s
     if (threadIdx.x == 0 && loss) loss[0] = (float)(sl[0] / B);
 }
 
+void launch_p2s_finalize(const double* chunk_sum, int B, int N, int nchunks, float* per_batch, float* loss,
+                         cudaStream_t st) {
+    p2s_finalize_kernel<<<1, 256, 0, st>>>(chunk_sum, B, N, nchunks, per_batch, loss);
+}
+
 struct P2sPackArgs {
     const float* src;
     float4* dst;

@@ -1,0 +1,638 @@
+// p2s_pruned.cu — culled point-to-surface forward (SURVEY.md §8.f NEXT-3 at scale).
+//
+// The same outputs as p2s.cu (cd_p2s_forward) with far fewer (point, face) evaluations, built from
+// the pruned nearest-neighbour machinery of nn_pruned.cu (R26):
+//   bbox (nn_pruned.cu)  per batch element: sample boxes of the points and of the vertices (they only
+//                        set the Morton quantisation).
+//   ps_morton_kernel     key = (set | batch | Morton code) for every point (set 0) and every face
+//                        centroid (set 1); value = flat row.
+//   radix sort           (nn_backward.cu)
+//   ps_gather_kernel     Morton-sorted packed points + permutation; face order (sorted pos -> face).
+//   ps_prep_kernel       the 24-float face records (p2s_common.cuh) in Morton face order, padded to
+//                        the 128-face tile by repeating the last sorted face.
+//   ps_aabb_kernel       boxes of every 256-point query tile and of every 128-face tile and 32-face
+//                        block (over the faces' vertices), each widened by delta = 2^-14 max|coord| of
+//                        the box so that a box gap bounds the fp32-evaluated distances (R26).
+//   ps_candidates_kernel per query tile: LB = gap^2 (1 - 1e-5) to every face tile, bitonic-sorted.
+//   p2s_pruned_kernel    face tiles in LB order through a 3-stage TMA ring; per 32-face block a
+//                        warp-uniform skip test against the warp's point box; value-only running
+//                        minimum of face_dist2 + block argmin; the CTA stops at the first tile whose LB
+//                        exceeds every row's current minimum.
+//   ps_resolve_kernel    exact face inside the winning block (same fp32 ops; first in sorted order),
+//                        fp64 closest point / barycentrics / distance on that face, outputs in the
+//                        original point order, fp64 chunk sums; then p2s_finalize (p2s.cu).
+#include "cd_internal.h"
+#include "p2s_common.cuh"
+
+#include <algorithm>
+
+namespace cdk {
+
+constexpr int kPsR = 2;                          // points per thread (one packed pair)
+constexpr int kPsThreads = 128;
+constexpr int kPsQ = kPsThreads * kPsR;          // 256 sorted points per query tile
+constexpr int kPsBlocks = kFaceTile / kBlockK;   // 4 blocks of 32 faces per 128-face tile
+constexpr int kPsMaxTiles = 8192;                // face tiles per batch element (LB sort in smem)
+constexpr float kPsLbScale = 0.99999f;
+constexpr float kPsMargin = 1.0f / 16384.0f;     // delta = 2^-14 * max |coord| of the box
+
+// ------------------------------------------------------------------------------------------ morton
+__device__ __forceinline__ uint32_t ps_spread(uint32_t v, int k) {
+    uint32_t r = 0;
+    for (int i = 0; i < k; ++i) r |= ((v >> i) & 1u) << (3 * i);
+    return r;
+}
+
+struct PsMortonArgs {
+    const float* points;
+    const float* verts;
+    const int* faces;
+    int B, N, Nv, Nf, kbits, bbits;
+    const float* bbox;   // [2][B][6]
+    uint32_t* keys;
+    uint32_t* vals;
+};
+
+__global__ void __launch_bounds__(256) ps_morton_kernel(PsMortonArgs a) {
+    const int64_t L0 = (int64_t)a.B * a.N;
+    const int64_t L = L0 + (int64_t)a.B * a.Nf;
+    const float qmax = (float)((1 << a.kbits) - 1);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = e < L0 ? 0 : 1;
+        float p[3];
+        int b;
+        if (c == 0) {
+            b = (int)(e / a.N);
+            for (int k = 0; k < 3; ++k) p[k] = __ldg(a.points + e * 3 + k);
+        } else {
+            const int64_t f = e - L0;
+            b = (int)(f / a.Nf);
+            const int fi = (int)(f - (int64_t)b * a.Nf);
+            const float* v = a.verts + (int64_t)b * a.Nv * 3;
+            const int i0 = min(max(a.faces[3 * fi], 0), a.Nv - 1), i1 = min(max(a.faces[3 * fi + 1], 0), a.Nv - 1),
+                      i2 = min(max(a.faces[3 * fi + 2], 0), a.Nv - 1);
+            for (int k = 0; k < 3; ++k) p[k] = (__ldg(v + 3 * i0 + k) + __ldg(v + 3 * i1 + k) + __ldg(v + 3 * i2 + k)) * (1.0f / 3.0f);
+        }
+        const float* bb = a.bbox + ((int64_t)c * a.B + b) * 6;
+        uint32_t code = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float ext = bb[3 + k] - bb[k];
+            float t = ext > 0.f ? (p[k] - bb[k]) / ext : 0.f;
+            t = fminf(fmaxf(t, 0.f), 1.f);
+            code |= ps_spread((uint32_t)(t * qmax + 0.5f), a.kbits) << k;
+        }
+        a.keys[e] = ((uint32_t)c << (a.bbits + 3 * a.kbits)) | ((uint32_t)b << (3 * a.kbits)) | code;
+        a.vals[e] = (uint32_t)e;
+    }
+}
+
+// ------------------------------------------------------------------------------------------ gather
+struct PsGatherArgs {
+    const float* points;
+    int B, N, Nf;
+    const uint32_t* vals;
+    float4* spts;    // [B][N] sorted points
+    int* perm_p;     // [B][N] sorted position -> original point
+    int* perm_f;     // [B][Nf] sorted position -> face
+};
+
+__global__ void __launch_bounds__(256) ps_gather_kernel(PsGatherArgs a) {
+    const int64_t L0 = (int64_t)a.B * a.N;
+    const int64_t L = L0 + (int64_t)a.B * a.Nf;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = a.vals[s];
+        if (s < L0) {
+            const int b = (int)(s / a.N);
+            const float* q = a.points + v * 3;
+            a.spts[s] = make_float4(__ldg(q), __ldg(q + 1), __ldg(q + 2), 0.f);
+            a.perm_p[s] = (int)(v - (int64_t)b * a.N);
+        } else {
+            const int64_t f = s - L0;
+            const int b = (int)(f / a.Nf);
+            a.perm_f[f] = (int)(v - L0 - (int64_t)b * a.Nf);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------ face records
+struct PsPrepArgs {
+    const float* verts;
+    const int* faces;
+    const int* perm_f;
+    int B, Nv, Nf, Fpad;
+    float* fd;   // [B][Fpad][24] in sorted face order
+};
+
+__global__ void __launch_bounds__(256) ps_prep_kernel(PsPrepArgs a) {
+    const int64_t total = (int64_t)a.B * a.Fpad;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(e / a.Fpad);
+        const int pos = min((int)(e - (int64_t)b * a.Fpad), a.Nf - 1);
+        const int f = a.perm_f[(int64_t)b * a.Nf + pos];
+        write_face_record(a.verts + (int64_t)b * a.Nv * 3, a.Nv, a.faces, f, a.fd + e * kFaceFloats);
+    }
+}
+
+// ------------------------------------------------------------------------------------------ boxes
+__device__ __forceinline__ void warp_box(float lo[3], float hi[3]) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[q] = fminf(lo[q], __shfl_xor_sync(0xffffffffu, lo[q], o));
+            hi[q] = fmaxf(hi[q], __shfl_xor_sync(0xffffffffu, hi[q], o));
+        }
+}
+
+// widen a (non-empty) box by delta = 2^-14 * max |coord| (R26); an empty box stays empty
+__device__ __forceinline__ void widen(float lo[3], float hi[3]) {
+    if (!(lo[0] <= hi[0])) return;
+    float m = 0.f;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) m = fmaxf(m, fmaxf(fabsf(lo[q]), fabsf(hi[q])));
+    const float d = m * kPsMargin + 1e-30f;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        lo[q] -= d;
+        hi[q] += d;
+    }
+}
+
+struct PsAabbArgs {
+    const float4* spts;
+    const float* verts;
+    const int* faces;
+    const int* perm_f;
+    int B, N, Nv, Nf, qtiles, ftiles;
+    float4* qbox;     // [B][qtiles][2]
+    float4* fbox;     // [B][ftiles][2]
+    float4* fbox32;   // [B][ftiles*4][2]
+};
+
+// One warp per 256-point query tile (lane reduces 8 points) or per 128-face tile (4 blocks of 32).
+__global__ void __launch_bounds__(256) ps_aabb_kernel(PsAabbArgs a) {
+    const int64_t TQ = (int64_t)a.B * a.qtiles, T = TQ + (int64_t)a.B * a.ftiles;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= T) return;
+    if (wid < TQ) {
+        const int b = (int)(wid / a.qtiles), t = (int)(wid - (int64_t)b * a.qtiles);
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int k = 0; k < kPsQ / 32; ++k) {
+            const int p = t * kPsQ + k * 32 + lane;
+            if (p < a.N) {
+                const float4 v = a.spts[(int64_t)b * a.N + p];
+                lo[0] = fminf(lo[0], v.x); hi[0] = fmaxf(hi[0], v.x);
+                lo[1] = fminf(lo[1], v.y); hi[1] = fmaxf(hi[1], v.y);
+                lo[2] = fminf(lo[2], v.z); hi[2] = fmaxf(hi[2], v.z);
+            }
+        }
+        warp_box(lo, hi);
+        widen(lo, hi);
+        if (lane == 0) {
+            float4* o = a.qbox + wid * 2;
+            o[0] = make_float4(lo[0], lo[1], lo[2], 0.f);
+            o[1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+        }
+        return;
+    }
+    const int64_t f = wid - TQ;
+    const int b = (int)(f / a.ftiles), t = (int)(f - (int64_t)b * a.ftiles);
+    const float* vv = a.verts + (int64_t)b * a.Nv * 3;
+    float tlo[3] = {INFINITY, INFINITY, INFINITY}, thi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int k = 0; k < kPsBlocks; ++k) {
+        const int pos = t * kFaceTile + k * kBlockK + lane;
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        if (pos < a.Nf) {
+            const int fi = a.perm_f[(int64_t)b * a.Nf + pos];
+            for (int c = 0; c < 3; ++c) {
+                const int vi = min(max(a.faces[3 * fi + c], 0), a.Nv - 1);
+                for (int q = 0; q < 3; ++q) {
+                    const float x = vv[3 * vi + q];
+                    lo[q] = fminf(lo[q], x);
+                    hi[q] = fmaxf(hi[q], x);
+                }
+            }
+        }
+        warp_box(lo, hi);
+        widen(lo, hi);
+        if (lane == 0) {
+            float4* o = a.fbox32 + ((int64_t)b * a.ftiles * kPsBlocks + t * kPsBlocks + k) * 2;
+            o[0] = make_float4(lo[0], lo[1], lo[2], 0.f);
+            o[1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            tlo[q] = fminf(tlo[q], lo[q]);
+            thi[q] = fmaxf(thi[q], hi[q]);
+        }
+    }
+    if (lane == 0) {
+        float4* o = a.fbox + f * 2;
+        o[0] = make_float4(tlo[0], tlo[1], tlo[2], 0.f);
+        o[1] = make_float4(thi[0], thi[1], thi[2], 0.f);
+    }
+}
+
+__device__ __forceinline__ float ps_gap(float qlo, float qhi, float tlo, float thi) {
+    return fmaxf(fmaxf(tlo - qhi, qlo - thi), 0.f);
+}
+// squared box-box gap scaled down by 1e-5 (empty target box: +inf)
+__device__ __forceinline__ float ps_box_lb(const float qlo[3], const float qhi[3], float4 lo, float4 hi) {
+    if (lo.x > hi.x) return INFINITY;
+    const float gx = ps_gap(qlo[0], qhi[0], lo.x, hi.x);
+    const float gy = ps_gap(qlo[1], qhi[1], lo.y, hi.y);
+    const float gz = ps_gap(qlo[2], qhi[2], lo.z, hi.z);
+    return (gx * gx + gy * gy + gz * gz) * kPsLbScale;
+}
+
+// ------------------------------------------------------------------------------------------ candidates
+struct PsCandArgs {
+    const float4* qbox;
+    const float4* fbox;
+    int qtiles, ftiles;
+    unsigned long long* cand;   // [B][qtiles][ftiles]: (LB bits << 32) | face tile, ascending
+};
+
+__global__ void __launch_bounds__(256) ps_candidates_kernel(PsCandArgs a) {
+    extern __shared__ unsigned long long keys[];
+    const int u = blockIdx.x;
+    const int b = u / a.qtiles;
+    const float4 ql = a.qbox[(int64_t)u * 2], qh = a.qbox[(int64_t)u * 2 + 1];
+    const float qlo[3] = {ql.x, ql.y, ql.z}, qhi[3] = {qh.x, qh.y, qh.z};
+    int npow = 1;
+    while (npow < a.ftiles) npow <<= 1;
+    for (int t = threadIdx.x; t < npow; t += 256) {
+        unsigned long long key = ~0ull;
+        if (t < a.ftiles) {
+            const float4* bx = a.fbox + ((int64_t)b * a.ftiles + t) * 2;
+            const float lb = ps_box_lb(qlo, qhi, bx[0], bx[1]);
+            key = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+        }
+        keys[t] = key;
+    }
+    __syncthreads();
+    for (int k = 2; k <= npow; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < npow; i += 256) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned long long x = keys[i], y = keys[l];
+                    if ((x > y) == ((i & k) == 0)) {
+                        keys[i] = y;
+                        keys[l] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    unsigned long long* out = a.cand + (int64_t)u * a.ftiles;
+    for (int t = threadIdx.x; t < a.ftiles; t += 256) out[t] = keys[t];
+}
+
+// ------------------------------------------------------------------------------------------ main kernel
+struct PsArgs {
+    const float4* spts;
+    const float* fd;        // [B][Fpad][24] sorted faces
+    const float4* fbox32;
+    const unsigned long long* cand;
+    int N, Fpad, qtiles, ftiles;
+    float* best_d;          // [B][N] sorted order
+    int* best_blk;          // sorted face position of the winning block
+};
+
+__global__ void __launch_bounds__(kPsThreads, 4) p2s_pruned_kernel(PsArgs a) {
+    __shared__ __align__(128) float sm[kP2sStages][kFaceTile * kFaceFloats];
+    __shared__ __align__(128) float4 smb[kP2sStages][kPsBlocks * 2];
+    __shared__ __align__(8) u64 full_bar[kP2sStages];
+    __shared__ unsigned s_wmax[kPsThreads / 32];
+
+    const int u = blockIdx.x, b = blockIdx.y;
+    const int nt = a.ftiles;
+    const float* FD = a.fd + (int64_t)b * a.Fpad * kFaceFloats;
+    const float4* FB = a.fbox32 + (int64_t)b * nt * kPsBlocks * 2;
+    const unsigned long long* __restrict__ cand = a.cand + ((int64_t)b * a.qtiles + u) * nt;
+    const uint32_t fbytes = kFaceTile * kFaceFloats * 4, bbytes = kPsBlocks * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    int issued = 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kP2sStages; ++s) mbar_init(&full_bar[s], 1);
+        fence_mbar_init();
+        const int pre = min(kP2sStages, nt);
+        for (int k = 0; k < pre; ++k) {
+            const int t = (int)(cand[k] & 0xffffffffull);
+            mbar_arrive_expect_tx(&full_bar[k], fbytes + bbytes);
+            tma_load_1d(sm[k], FD + (int64_t)t * kFaceTile * kFaceFloats, fbytes, &full_bar[k]);
+            tma_load_1d(smb[k], FB + (int64_t)t * kPsBlocks * 2, bbytes, &full_bar[k]);
+        }
+        issued = pre;
+    }
+    __syncthreads();
+
+    const int P = a.N;
+    const float4* Q = a.spts + (int64_t)b * P;
+    const int qbase = u * kPsQ + threadIdx.x * kPsR;
+    const float4 p0 = Q[min(qbase, P - 1)], p1 = Q[min(qbase + 1, P - 1)];
+    const u64 qx = pk2(p0.x, p1.x), qy = pk2(p0.y, p1.y), qz = pk2(p0.z, p1.z);
+    float best0 = INFINITY, best1 = INFINITY;
+    int blk0 = -1, blk1 = -1;
+    // widened box of the warp's 64 sorted points (valid rows only)
+    float wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    if (qbase < P) {
+        wlo[0] = fminf(wlo[0], p0.x); whi[0] = fmaxf(whi[0], p0.x);
+        wlo[1] = fminf(wlo[1], p0.y); whi[1] = fmaxf(whi[1], p0.y);
+        wlo[2] = fminf(wlo[2], p0.z); whi[2] = fmaxf(whi[2], p0.z);
+    }
+    if (qbase + 1 < P) {
+        wlo[0] = fminf(wlo[0], p1.x); whi[0] = fmaxf(whi[0], p1.x);
+        wlo[1] = fminf(wlo[1], p1.y); whi[1] = fmaxf(whi[1], p1.y);
+        wlo[2] = fminf(wlo[2], p1.z); whi[2] = fmaxf(whi[2], p1.z);
+    }
+    warp_box(wlo, whi);
+    widen(wlo, whi);
+
+    float wmax = INFINITY, maxbest = INFINITY;
+    unsigned long long next = cand[0];
+    int k = 0;
+    for (; k < nt; ++k) {
+        const unsigned long long cur = next;
+        if (k + 1 < nt) next = cand[k + 1];
+        const float lb = __uint_as_float((unsigned)(cur >> 32));
+        if (lb > maxbest) break;
+        const int t = (int)(cur & 0xffffffffull);
+        const int s = k % kP2sStages;
+        mbar_wait(&full_bar[s], (k / kP2sStages) & 1);
+        const float* tb = sm[s];
+        const float4* bb = smb[s];
+        const int ft = t * kFaceTile;
+        for (int kb = 0; kb < kPsBlocks; ++kb) {
+            if (ps_box_lb(wlo, whi, bb[2 * kb], bb[2 * kb + 1]) > wmax) continue;
+            const float o0 = best0, o1 = best1;
+#pragma unroll 2
+            for (int j = 0; j < kBlockK; ++j) {
+                float d0, d1;
+                face_dist2(tb + (kb * kBlockK + j) * kFaceFloats, qx, qy, qz, d0, d1);
+                best0 = fminf(best0, d0);
+                best1 = fminf(best1, d1);
+            }
+            blk0 = best0 < o0 ? ft + kb * kBlockK : blk0;
+            blk1 = best1 < o1 ? ft + kb * kBlockK : blk1;
+        }
+        unsigned m = 0u;
+        if (qbase < P) m = __float_as_uint(best0);
+        if (qbase + 1 < P) m = max(m, __float_as_uint(best1));
+        m = __reduce_max_sync(0xffffffffu, m);
+        wmax = __uint_as_float(m);
+        if (lane == 0) s_wmax[warp] = m;
+        __syncthreads();
+        unsigned mm = s_wmax[0];
+#pragma unroll
+        for (int w = 1; w < kPsThreads / 32; ++w) mm = max(mm, s_wmax[w]);
+        maxbest = __uint_as_float(mm);
+        if (threadIdx.x == 0 && issued == k + kP2sStages && issued < nt) {
+            const unsigned long long e = cand[issued];
+            if (__uint_as_float((unsigned)(e >> 32)) <= maxbest) {
+                const int tn = (int)(e & 0xffffffffull);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&full_bar[s], fbytes + bbytes);
+                tma_load_1d(sm[s], FD + (int64_t)tn * kFaceTile * kFaceFloats, fbytes, &full_bar[s]);
+                tma_load_1d(smb[s], FB + (int64_t)tn * kPsBlocks * 2, bbytes, &full_bar[s]);
+                ++issued;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int kk = k; kk < issued; ++kk) mbar_wait(&full_bar[kk % kP2sStages], (kk / kP2sStages) & 1);
+
+    const int64_t rowbase = (int64_t)b * P;
+    if (qbase < P) {
+        a.best_d[rowbase + qbase] = best0;
+        a.best_blk[rowbase + qbase] = blk0;
+    }
+    if (qbase + 1 < P) {
+        a.best_d[rowbase + qbase + 1] = best1;
+        a.best_blk[rowbase + qbase + 1] = blk1;
+    }
+}
+
+// ------------------------------------------------------------------------------------------ resolve
+struct PsResolveArgs {
+    const float4* spts;
+    const int* perm_p;
+    const int* perm_f;
+    const float* fd;
+    const float* verts;
+    const int* faces;
+    int B, N, Nv, Nf, Fpad, nchunks;
+    const float* best_d;
+    const int* best_blk;
+    float* d_out;
+    int* face_out;
+    float* closest;
+    float* bary;
+    double* chunk_sum;
+};
+
+__global__ void __launch_bounds__(kMergeThreads) ps_resolve_kernel(PsResolveArgs a) {
+    const int b = blockIdx.x / a.nchunks;
+    const int chunk = blockIdx.x - b * a.nchunks;
+    const int p = chunk * kMergeThreads + threadIdx.x;
+    double v = 0.0;
+    if (p < a.N) {
+        const int64_t srow = (int64_t)b * a.N + p;
+        const float best = a.best_d[srow];
+        const int bb = a.best_blk[srow];
+        const float4 pp = a.spts[srow];
+        int face = a.perm_f[(int64_t)b * a.Nf];
+        if (bb >= 0) {
+            const u64 qx = pk2(pp.x, pp.x), qy = pk2(pp.y, pp.y), qz = pk2(pp.z, pp.z);
+            const float* FD = a.fd + (int64_t)b * a.Fpad * kFaceFloats;
+            const int fend = min(bb + kBlockK, a.Nf);
+            int pos = bb;
+            for (int f = bb; f < fend; ++f) {
+                float d0, d1;
+                face_dist2(FD + (int64_t)f * kFaceFloats, qx, qy, qz, d0, d1);
+                if (d0 == best) {
+                    pos = f;
+                    break;
+                }
+            }
+            face = a.perm_f[(int64_t)b * a.Nf + min(pos, a.Nf - 1)];
+        }
+        const float* vv = a.verts + (int64_t)b * a.Nv * 3;
+        double A[3], Bv[3], C[3], q[3] = {pp.x, pp.y, pp.z}, c[3], lam[3];
+        const int ia = min(max(a.faces[3 * face], 0), a.Nv - 1), ib = min(max(a.faces[3 * face + 1], 0), a.Nv - 1),
+                  ic = min(max(a.faces[3 * face + 2], 0), a.Nv - 1);
+        for (int k = 0; k < 3; ++k) {
+            A[k] = vv[3 * ia + k];
+            Bv[k] = vv[3 * ib + k];
+            C[k] = vv[3 * ic + k];
+        }
+        closest64(q, A, Bv, C, c, lam);
+        const double dd = (q[0] - c[0]) * (q[0] - c[0]) + (q[1] - c[1]) * (q[1] - c[1]) + (q[2] - c[2]) * (q[2] - c[2]);
+        const int64_t row = (int64_t)b * a.N + a.perm_p[srow];
+        a.d_out[row] = (float)dd;
+        a.face_out[row] = face;
+        if (a.closest)
+            for (int k = 0; k < 3; ++k) a.closest[3 * row + k] = (float)c[k];
+        if (a.bary)
+            for (int k = 0; k < 3; ++k) a.bary[3 * row + k] = (float)lam[k];
+        v = (double)(float)dd;
+    }
+    __shared__ double ssum[kMergeThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) ssum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kMergeThreads / 32; ++w) s += ssum[w];
+        a.chunk_sum[(int64_t)b * a.nchunks + chunk] = s;
+    }
+}
+
+// ------------------------------------------------------------------------------------------ host
+static int ps_cdiv(int64_t x, int64_t y) { return (int)((x + y - 1) / y); }
+
+struct PsPlan {
+    int B, N, Nv, Nf, Fpad, qtiles, ftiles, nchunks, bbits, kbits, nbits;
+    int64_t L;
+    size_t off_bbox, off_keys[2], off_vals[2], off_counts, off_totals, off_spts, off_perm_p, off_perm_f, off_fd,
+        off_qbox, off_fbox, off_fbox32, off_cand, off_best_d, off_best_blk, off_chunk, bytes;
+    bool supported;
+};
+
+static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
+    p.B = B;
+    p.N = N;
+    p.Nv = Nv;
+    p.Nf = Nf;
+    p.Fpad = ps_cdiv(Nf, kFaceTile) * kFaceTile;
+    p.qtiles = ps_cdiv(N, kPsQ);
+    p.ftiles = p.Fpad / kFaceTile;
+    p.nchunks = ps_cdiv(N, kMergeThreads);
+    int bb = 0;
+    while ((1 << bb) < B) ++bb;
+    p.bbits = bb;
+    p.kbits = std::max(1, std::min(10, (32 - 1 - bb) / 3));
+    p.nbits = 1 + bb + 3 * p.kbits;
+    p.L = (int64_t)B * N + (int64_t)B * Nf;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    p.off_bbox = take((size_t)2 * B * 6 * 4);
+    for (int i = 0; i < 2; ++i) {
+        p.off_keys[i] = take((size_t)p.L * 4);
+        p.off_vals[i] = take((size_t)p.L * 4);
+    }
+    p.off_counts = take(radix_sort_counts_words(p.L, p.nbits) * 4);
+    p.off_totals = take((size_t)kSortTotalsWords * 4);
+    p.off_spts = take((size_t)B * N * 16);
+    p.off_perm_p = take((size_t)B * N * 4);
+    p.off_perm_f = take((size_t)B * Nf * 4);
+    p.off_fd = take((size_t)B * p.Fpad * kFaceFloats * 4);
+    p.off_qbox = take((size_t)B * p.qtiles * 32);
+    p.off_fbox = take((size_t)B * p.ftiles * 32);
+    p.off_fbox32 = take((size_t)B * p.ftiles * kPsBlocks * 32);
+    p.off_cand = take((size_t)B * p.qtiles * p.ftiles * 8);
+    p.off_best_d = take((size_t)B * N * 4);
+    p.off_best_blk = take((size_t)B * N * 4);
+    p.off_chunk = take((size_t)B * p.nchunks * 8);
+    p.bytes = off;
+    p.supported = p.ftiles <= kPsMaxTiles && p.L <= 0x7fffffffLL;
+}
+
+size_t p2s_pruned_workspace(int B, int N, int Nv, int Nf) {
+    PsPlan p;
+    plan_ps(p, B, N, Nv, Nf);
+    return p.supported ? p.bytes : 0;
+}
+
+int p2s_pruned_launches(int B, int N, int Nv, int Nf) {
+    PsPlan p;
+    plan_ps(p, B, N, Nv, Nf);
+    return 2 + radix_sort_launches(p.L, p.nbits) + 6 + 1;   // + finalize
+}
+
+cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int* faces, int B, int N, int Nv, int Nf,
+                              float* d, int* face, float* closest, float* bary, float* per_batch, float* loss,
+                              void* ws, cudaStream_t st) {
+    PsPlan p;
+    plan_ps(p, B, N, Nv, Nf);
+    if (!p.supported) return cudaErrorInvalidValue;
+    char* w = static_cast<char*>(ws);
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    float* bbox = reinterpret_cast<float*>(w + p.off_bbox);
+    launch_bbox(points, N, verts, Nv, B, bbox, st);
+    uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
+    uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
+    const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);
+    {
+        PsMortonArgs a{points, verts, faces, B, N, Nv, Nf, p.kbits, p.bbits, bbox, keys[0], vals[0]};
+        ps_morton_kernel<<<grid_l, 256, 0, st>>>(a);
+    }
+    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
+                                     reinterpret_cast<uint32_t*>(w + p.off_totals), st);
+    float4* spts = reinterpret_cast<float4*>(w + p.off_spts);
+    int* perm_p = reinterpret_cast<int*>(w + p.off_perm_p);
+    int* perm_f = reinterpret_cast<int*>(w + p.off_perm_f);
+    float* fd = reinterpret_cast<float*>(w + p.off_fd);
+    float4* qbox = reinterpret_cast<float4*>(w + p.off_qbox);
+    float4* fbox = reinterpret_cast<float4*>(w + p.off_fbox);
+    float4* fbox32 = reinterpret_cast<float4*>(w + p.off_fbox32);
+    unsigned long long* cand = reinterpret_cast<unsigned long long*>(w + p.off_cand);
+    float* best_d = reinterpret_cast<float*>(w + p.off_best_d);
+    int* best_blk = reinterpret_cast<int*>(w + p.off_best_blk);
+    double* chunk = reinterpret_cast<double*>(w + p.off_chunk);
+    {
+        PsGatherArgs a{points, B, N, Nf, vals[cur], spts, perm_p, perm_f};
+        ps_gather_kernel<<<grid_l, 256, 0, st>>>(a);
+    }
+    {
+        PsPrepArgs a{verts, faces, perm_f, B, Nv, Nf, p.Fpad, fd};
+        ps_prep_kernel<<<std::min(ps_cdiv((int64_t)B * p.Fpad, 256), sms * 16), 256, 0, st>>>(a);
+    }
+    {
+        PsAabbArgs a{spts, verts, faces, perm_f, B, N, Nv, Nf, p.qtiles, p.ftiles, qbox, fbox, fbox32};
+        const int64_t tasks = (int64_t)B * (p.qtiles + p.ftiles);
+        ps_aabb_kernel<<<ps_cdiv(tasks * 32, 256), 256, 0, st>>>(a);
+    }
+    {
+        PsCandArgs a{qbox, fbox, p.qtiles, p.ftiles, cand};
+        int npow = 1;
+        while (npow < p.ftiles) npow <<= 1;
+        static thread_local bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(ps_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPsMaxTiles * 8);
+            attr = true;
+        }
+        ps_candidates_kernel<<<B * p.qtiles, 256, (size_t)npow * 8, st>>>(a);
+    }
+    {
+        PsArgs a{spts, fd, fbox32, cand, N, p.Fpad, p.qtiles, p.ftiles, best_d, best_blk};
+        if (g_prof_start) record_profile_event(g_prof_start, st);
+        p2s_pruned_kernel<<<dim3(p.qtiles, B), kPsThreads, 0, st>>>(a);
+        if (g_prof_stop) record_profile_event(g_prof_stop, st);
+    }
+    {
+        PsResolveArgs a{spts, perm_p, perm_f, fd, verts, faces, B, N, Nv, Nf, p.Fpad, p.nchunks,
+                        best_d, best_blk, d, face, closest, bary, chunk};
+        ps_resolve_kernel<<<B * p.nchunks, kMergeThreads, 0, st>>>(a);
+    }
+    launch_p2s_finalize(chunk, B, N, p.nchunks, per_batch, loss, st);
+    return cudaGetLastError();
+}
+
+}  // namespace cdk

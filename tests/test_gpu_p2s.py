@@ -130,3 +130,87 @@ def test_p2s_autograd(cd):
     err = np.abs(p.grad.cpu().numpy() - gp_ref)
     assert np.quantile(err / (np.abs(gp_ref) + 1e-9), 0.99) < 1e-4
     assert np.linalg.norm(v.grad.cpu().numpy() - gv_ref) <= 1e-4 * np.linalg.norm(gv_ref)
+
+
+# ---------------------------------------------------------------------------------- culled path (R26)
+def _pruned_vs_brute(cd, P, V, F, rows=None, min_clear=0.3):
+    """The culled forward against the oracle (same gate) and against the brute-force kernel: the
+    same face wherever the brute force's choice is unique up to fp32 ties, and then bit-identical
+    d / closest / bary (both evaluate the chosen face with the same fp64 code)."""
+    outp = cd.p2s_forward(_t(P), _t(V), _t(F), algorithm="pruned")
+    outb = cd.p2s_forward(_t(P), _t(V), _t(F))
+    torch.cuda.synchronize()
+    d1, f1, clear = _gate(P, V, F, outp, rows=rows, min_clear=min_clear)
+    dp, fp, cp, bp = (o.cpu().numpy() for o in outp[:4])
+    db, fb, cb, bb = (o.cpu().numpy() for o in outb[:4])
+    # exact fp32 ties are common (a shared closest vertex evaluated through two faces with the same
+    # corner role): there the culled path keeps the first face in its visiting order (R26)
+    same = fp == fb
+    assert same.mean() > 0.5
+    np.testing.assert_array_equal(dp[same], db[same])
+    np.testing.assert_array_equal(cp[same], cb[same])
+    np.testing.assert_array_equal(bp[same], bb[same])
+    # a different face only on (near-)ties: the two fp64 distances agree to the fp32 band
+    R = max(np.abs(P).max(), np.abs(V).max())
+    np.testing.assert_allclose(dp[~same], db[~same], rtol=1e-5, atol=2.0 ** -22 * R * R)
+    # loss: fp64 sums of the per-point d (summation order differs from the brute force)
+    assert abs(outp[5].item() - dp.astype(np.float64).mean()) <= 1e-6 * dp.mean() + 1e-30
+    np.testing.assert_allclose(outp[4].cpu().numpy(), dp.astype(np.float64).mean(1), rtol=1e-6)
+    return outp
+
+
+@pytest.mark.parametrize("B,N,subdiv,near", [(1, 1, 0, False), (2, 3000, 3, False), (2, 2000, 3, True),
+                                             (1, 5000, 1, False), (3, 777, 2, True), (2, 4097, 4, True)])
+def test_p2s_pruned_parity(cd, B, N, subdiv, near):
+    V, F = synth.mesh_batch(B, subdiv=subdiv, config_index=130)
+    if near:
+        rf, rb = synth.sampling_randoms(B, N, seed=11)
+        P, _, _, _ = oracle.sample_mesh(V, F, rf, rb)
+        P = (P + np.random.default_rng(4).normal(scale=1e-3, size=P.shape)).astype(np.float32)
+    else:
+        P = synth.shape_pair(B, N, 8, config_index=131)[0]
+    rows = None if B * N <= 6000 else np.random.default_rng(5).choice(B * N, 2000, replace=False)
+    _pruned_vs_brute(cd, P, V, F, rows=rows, min_clear=0.0 if N == 1 else 0.3)
+
+
+def test_p2s_pruned_far_and_exact_surface(cd):
+    """Points far outside the mesh (little culling) and points exactly on faces (d = 0 ties between
+    neighbouring faces at shared edges)."""
+    B, N = 2, 3000
+    V, F = synth.mesh_batch(B, subdiv=3, config_index=132)
+    Pfar = (synth.shape_pair(B, N, 8, config_index=133)[0] * 5.0 + 3.0).astype(np.float32)
+    _pruned_vs_brute(cd, Pfar, V, F, min_clear=0.0)   # mostly vertex-closest: ties
+    rf, rb = synth.sampling_randoms(B, N, seed=12)
+    Pon, _, _, _ = oracle.sample_mesh(V, F, rf, rb)
+    _pruned_vs_brute(cd, Pon.astype(np.float32), V, F, min_clear=0.0)
+
+
+def test_p2s_pruned_bench_config_sampled(cd):
+    """The bench's NEXT-3 workload (B=8, icosphere-5 with 20480 faces, 16384 points per mesh):
+    the culled path agrees with the brute-force kernel everywhere and with the oracle on samples."""
+    B, N = 8, 16384
+    V, F = synth.mesh_batch(B, subdiv=5, config_index=134)
+    rf, rb = synth.sampling_randoms(B, N, seed=13)
+    P, _, _, _ = oracle.sample_mesh(V, F, rf, rb)
+    P = (P + np.random.default_rng(6).normal(scale=1e-2, size=P.shape)).astype(np.float32)
+    rows = np.random.default_rng(7).choice(B * N, 1500, replace=False)
+    _pruned_vs_brute(cd, P, V, F, rows=rows)
+
+
+def test_p2s_pruned_autograd(cd):
+    B, N = 2, 3000
+    V, F = synth.mesh_batch(B, subdiv=3, config_index=135)
+    P = synth.shape_pair(B, N, 8, config_index=136)[0]
+    p = _t(P).requires_grad_(True)
+    v = _t(V).requires_grad_(True)
+    loss = cd.point_to_surface(p, v, _t(F), algorithm="pruned")
+    loss.backward()
+    p2 = _t(P).requires_grad_(True)
+    v2 = _t(V).requires_grad_(True)
+    loss2 = cd.point_to_surface(p2, v2, _t(F))
+    loss2.backward()
+    assert abs(loss.item() - loss2.item()) <= 1e-6 * abs(loss2.item())
+    # equal except on fp32 near-ties (a different closest face / point): as the brute force vs oracle
+    gp, gb = p.grad.cpu().numpy(), p2.grad.cpu().numpy()
+    assert np.quantile(np.abs(gp - gb) / (np.abs(gb) + 1e-9), 0.99) < 1e-6
+    assert np.linalg.norm(v.grad.cpu().numpy() - v2.grad.cpu().numpy()) <= 1e-4 * np.linalg.norm(v2.grad.cpu().numpy())
