@@ -25,15 +25,39 @@
 #include "p2s_common.cuh"
 
 #include <algorithm>
+#include <cstdio>
 
 namespace cdk {
 
 constexpr int kPsR = 2;                          // points per thread (one packed pair)
-constexpr int kPsThreads = 128;
+#ifndef CD_PS_THREADS
+#define CD_PS_THREADS 128
+#endif
+#ifndef CD_PS_STAGES
+#define CD_PS_STAGES 3
+#endif
+#ifndef CD_PS_TILE
+#define CD_PS_TILE 128
+#endif
+#ifndef CD_PS_MINB
+#define CD_PS_MINB 4
+#endif
+constexpr int kPsThreads = CD_PS_THREADS;
+constexpr int kPsStages = CD_PS_STAGES;          // TMA ring depth
+constexpr int kPsTile = CD_PS_TILE;              // faces per shared-memory stage
 constexpr int kPsQ = kPsThreads * kPsR;          // 256 sorted points per query tile
-constexpr int kPsBlocks = kFaceTile / kBlockK;   // 4 blocks of 32 faces per 128-face tile
+constexpr int kPsBlocks = kPsTile / kBlockK;   // blocks of 32 faces per face tile
 constexpr int kPsMaxTiles = 8192;                // face tiles per batch element (LB sort in smem)
 constexpr float kPsLbScale = 0.99999f;
+#ifndef CD_PS_FIRST
+#define CD_PS_FIRST 4
+#endif
+#ifndef CD_PS_CHUNK
+#define CD_PS_CHUNK 8
+#endif
+constexpr int kPsFirst = CD_PS_FIRST;            // phase-0 face tiles per query tile
+constexpr int kPsChunk = CD_PS_CHUNK;            // phase-1 face tiles per CTA (at least)
+constexpr int kPsMaxChunks = 32;                 // phase-1 CTAs per query tile (at most)
 constexpr float kPsMargin = 1.0f / 16384.0f;     // delta = 2^-14 * max |coord| of the box
 
 // ------------------------------------------------------------------------------------------ morton
@@ -202,7 +226,7 @@ __global__ void __launch_bounds__(256) ps_aabb_kernel(PsAabbArgs a) {
     const float* vv = a.verts + (int64_t)b * a.Nv * 3;
     float tlo[3] = {INFINITY, INFINITY, INFINITY}, thi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int k = 0; k < kPsBlocks; ++k) {
-        const int pos = t * kFaceTile + k * kBlockK + lane;
+        const int pos = t * kPsTile + k * kBlockK + lane;
         float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
         if (pos < a.Nf) {
             const int fi = a.perm_f[(int64_t)b * a.Nf + pos];
@@ -293,42 +317,47 @@ __global__ void __launch_bounds__(256) ps_candidates_kernel(PsCandArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------ main kernel
+#ifdef CD_PS_STATS   // experiment build only: visit statistics
+__device__ unsigned long long g_ps_stats[4];
+#endif
 struct PsArgs {
     const float4* spts;
     const float* fd;        // [B][Fpad][24] sorted faces
+    const float4* fbox;     // [B][ftiles][2] face tile boxes
     const float4* fbox32;
     const unsigned long long* cand;
     int N, Fpad, qtiles, ftiles;
-    float* best_d;          // [B][N] sorted order
-    int* best_blk;          // sorted face position of the winning block
+    int k0, klen, nchunk;   // candidate range of chunk c: [k0 + c klen, k0 + (c+1) klen)
+    int phase;              // 0: first tiles, plain store of the row keys; 1: refine from the row keys
+    long long* rowkey;      // [B][N] sorted order: (best bits << 32) | sorted block position
 };
 
-__global__ void __launch_bounds__(kPsThreads, 4) p2s_pruned_kernel(PsArgs a) {
-    __shared__ __align__(128) float sm[kP2sStages][kFaceTile * kFaceFloats];
-    __shared__ __align__(128) float4 smb[kP2sStages][kPsBlocks * 2];
-    __shared__ __align__(8) u64 full_bar[kP2sStages];
+// Per-lane lower bound: the lane's two points (widened box) against a face box; a tile or block is
+// evaluated iff some thread of the CTA / lane of the warp may still improve (LB <= its own max best).
+__device__ __forceinline__ float lane_lb(const float llo[3], const float lhi[3], float4 lo, float4 hi) {
+    return ps_box_lb(llo, lhi, lo, hi);
+}
+
+__global__ void __launch_bounds__(kPsThreads, CD_PS_MINB) p2s_pruned_kernel(PsArgs a) {
+    __shared__ __align__(128) float sm[kPsStages][kPsTile * kFaceFloats];
+    __shared__ __align__(128) float4 smb[kPsStages][kPsBlocks * 2];
+    __shared__ __align__(8) u64 full_bar[kPsStages];
     __shared__ unsigned s_wmax[kPsThreads / 32];
 
-    const int u = blockIdx.x, b = blockIdx.y;
+    const int u = blockIdx.x / a.nchunk, chunk = blockIdx.x - (blockIdx.x / a.nchunk) * a.nchunk;
+    const int b = blockIdx.y;
     const int nt = a.ftiles;
+    const int kbeg = min(nt, a.k0 + chunk * a.klen), kend = min(nt, kbeg + a.klen);
     const float* FD = a.fd + (int64_t)b * a.Fpad * kFaceFloats;
     const float4* FB = a.fbox32 + (int64_t)b * nt * kPsBlocks * 2;
+    const float4* FT = a.fbox + (int64_t)b * nt * 2;
     const unsigned long long* __restrict__ cand = a.cand + ((int64_t)b * a.qtiles + u) * nt;
-    const uint32_t fbytes = kFaceTile * kFaceFloats * 4, bbytes = kPsBlocks * 32;
+    const uint32_t fbytes = kPsTile * kFaceFloats * 4, bbytes = kPsBlocks * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    int issued = 0;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kP2sStages; ++s) mbar_init(&full_bar[s], 1);
+        for (int s = 0; s < kPsStages; ++s) mbar_init(&full_bar[s], 1);
         fence_mbar_init();
-        const int pre = min(kP2sStages, nt);
-        for (int k = 0; k < pre; ++k) {
-            const int t = (int)(cand[k] & 0xffffffffull);
-            mbar_arrive_expect_tx(&full_bar[k], fbytes + bbytes);
-            tma_load_1d(sm[k], FD + (int64_t)t * kFaceTile * kFaceFloats, fbytes, &full_bar[k]);
-            tma_load_1d(smb[k], FB + (int64_t)t * kPsBlocks * 2, bbytes, &full_bar[k]);
-        }
-        issued = pre;
     }
     __syncthreads();
 
@@ -338,38 +367,98 @@ __global__ void __launch_bounds__(kPsThreads, 4) p2s_pruned_kernel(PsArgs a) {
     const float4 p0 = Q[min(qbase, P - 1)], p1 = Q[min(qbase + 1, P - 1)];
     const u64 qx = pk2(p0.x, p1.x), qy = pk2(p0.y, p1.y), qz = pk2(p0.z, p1.z);
     float best0 = INFINITY, best1 = INFINITY;
+    const int64_t rowbase = (int64_t)b * P;
+    if (a.phase == 1) {   // refine: start from the first phase's minima (upper bounds of the final ones)
+        if (qbase < P) best0 = __uint_as_float((unsigned)((unsigned long long)a.rowkey[rowbase + qbase] >> 32));
+        if (qbase + 1 < P) best1 = __uint_as_float((unsigned)((unsigned long long)a.rowkey[rowbase + qbase + 1] >> 32));
+    }
+    if (qbase >= P) best0 = -1.0f;       // padding rows: never need anything
+    if (qbase + 1 >= P) best1 = -1.0f;
+    const float init0 = best0, init1 = best1;
     int blk0 = -1, blk1 = -1;
-    // widened box of the warp's 64 sorted points (valid rows only)
-    float wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    // widened box of the lane's (valid) points
+    float llo[3] = {INFINITY, INFINITY, INFINITY}, lhi[3] = {-INFINITY, -INFINITY, -INFINITY};
     if (qbase < P) {
-        wlo[0] = fminf(wlo[0], p0.x); whi[0] = fmaxf(whi[0], p0.x);
-        wlo[1] = fminf(wlo[1], p0.y); whi[1] = fmaxf(whi[1], p0.y);
-        wlo[2] = fminf(wlo[2], p0.z); whi[2] = fmaxf(whi[2], p0.z);
+        llo[0] = p0.x; llo[1] = p0.y; llo[2] = p0.z;
+        lhi[0] = p0.x; lhi[1] = p0.y; lhi[2] = p0.z;
     }
     if (qbase + 1 < P) {
-        wlo[0] = fminf(wlo[0], p1.x); whi[0] = fmaxf(whi[0], p1.x);
-        wlo[1] = fminf(wlo[1], p1.y); whi[1] = fmaxf(whi[1], p1.y);
-        wlo[2] = fminf(wlo[2], p1.z); whi[2] = fmaxf(whi[2], p1.z);
+        llo[0] = fminf(llo[0], p1.x); lhi[0] = fmaxf(lhi[0], p1.x);
+        llo[1] = fminf(llo[1], p1.y); lhi[1] = fmaxf(lhi[1], p1.y);
+        llo[2] = fminf(llo[2], p1.z); lhi[2] = fmaxf(lhi[2], p1.z);
     }
-    warp_box(wlo, whi);
-    widen(wlo, whi);
+    widen(llo, lhi);
 
-    float wmax = INFINITY, maxbest = INFINITY;
-    unsigned long long next = cand[0];
-    int k = 0;
-    for (; k < nt; ++k) {
-        const unsigned long long cur = next;
-        if (k + 1 < nt) next = cand[k + 1];
-        const float lb = __uint_as_float((unsigned)(cur >> 32));
-        if (lb > maxbest) break;
-        const int t = (int)(cur & 0xffffffffull);
-        const int s = k % kP2sStages;
-        mbar_wait(&full_bar[s], (k / kP2sStages) & 1);
+    // next face tile that some thread may still need, in the query tile's LB order (-1: none).  Block-
+    // uniform: every thread walks the same list; one barrier per candidate considered.
+    int pos = kbeg;
+    auto advance = [&]() -> int {
+        // CTA maximum of the rows' current minima: the sorted list ends the walk once LB exceeds it
+        unsigned m = __float_as_uint(fmaxf(fmaxf(best0, best1), 0.f));
+        m = __reduce_max_sync(0xffffffffu, m);
+        if (lane == 0) s_wmax[warp] = m;
+        __syncthreads();
+        unsigned mm = s_wmax[0];
+#pragma unroll
+        for (int w = 1; w < kPsThreads / 32; ++w) mm = max(mm, s_wmax[w]);
+        const float maxbest = __uint_as_float(mm);
+        const float mine = fmaxf(best0, best1);
+        int found = -1;
+        while (pos < kend) {
+            const unsigned long long e = cand[pos];
+            if (__uint_as_float((unsigned)(e >> 32)) > maxbest) {
+                pos = kend;
+                break;
+            }
+            const int t = (int)(e & 0xffffffffull);
+            ++pos;
+            const bool need = lane_lb(llo, lhi, FT[2 * t], FT[2 * t + 1]) <= mine;
+            if (__syncthreads_or(need)) {
+                found = t;
+                break;
+            }
+        }
+        __syncthreads();   // s_wmax reuse
+        return found;
+    };
+
+    int tiles[kPsStages];
+    int tail = 0;
+#ifdef CD_PS_STATS
+    unsigned long long nblk_stat = 0;
+#endif
+#pragma unroll
+    for (int k = 0; k < kPsStages; ++k) {
+        const int t = advance();
+        tiles[k] = t;
+        if (t < 0) break;
+        if (threadIdx.x == 0) {
+            mbar_arrive_expect_tx(&full_bar[k], fbytes + bbytes);
+            tma_load_1d(sm[k], FD + (int64_t)t * kPsTile * kFaceFloats, fbytes, &full_bar[k]);
+            tma_load_1d(smb[k], FB + (int64_t)t * kPsBlocks * 2, bbytes, &full_bar[k]);
+        }
+        ++tail;
+    }
+    for (int head = 0; head < tail; ++head) {
+        const int s = head % kPsStages;
+        int t = tiles[0];
+#pragma unroll
+        for (int q = 1; q < kPsStages; ++q) t = s == q ? tiles[q] : t;
+        mbar_wait(&full_bar[s], (head / kPsStages) & 1);
+#ifdef CD_PS_STATS
+        if (threadIdx.x == 0) atomicAdd(&g_ps_stats[0], 1ull);
+#endif
         const float* tb = sm[s];
         const float4* bb = smb[s];
-        const int ft = t * kFaceTile;
+        const int ft = t * kPsTile;
+        const float mine = fmaxf(best0, best1);
         for (int kb = 0; kb < kPsBlocks; ++kb) {
-            if (ps_box_lb(wlo, whi, bb[2 * kb], bb[2 * kb + 1]) > wmax) continue;
+            const bool need = lane_lb(llo, lhi, bb[2 * kb], bb[2 * kb + 1]) <= mine;
+            if (!__any_sync(0xffffffffu, need)) continue;
+#ifdef CD_PS_STATS
+            if (lane == 0) atomicAdd(&g_ps_stats[1], 1ull);
+            ++nblk_stat;
+#endif
             const float o0 = best0, o1 = best1;
 #pragma unroll 2
             for (int j = 0; j < kBlockK; ++j) {
@@ -381,41 +470,32 @@ __global__ void __launch_bounds__(kPsThreads, 4) p2s_pruned_kernel(PsArgs a) {
             blk0 = best0 < o0 ? ft + kb * kBlockK : blk0;
             blk1 = best1 < o1 ? ft + kb * kBlockK : blk1;
         }
-        unsigned m = 0u;
-        if (qbase < P) m = __float_as_uint(best0);
-        if (qbase + 1 < P) m = max(m, __float_as_uint(best1));
-        m = __reduce_max_sync(0xffffffffu, m);
-        wmax = __uint_as_float(m);
-        if (lane == 0) s_wmax[warp] = m;
-        __syncthreads();
-        unsigned mm = s_wmax[0];
+        __syncthreads();   // stage s consumed by every warp
+        const int tn = advance();
+        if (tn >= 0) {
 #pragma unroll
-        for (int w = 1; w < kPsThreads / 32; ++w) mm = max(mm, s_wmax[w]);
-        maxbest = __uint_as_float(mm);
-        if (threadIdx.x == 0 && issued == k + kP2sStages && issued < nt) {
-            const unsigned long long e = cand[issued];
-            if (__uint_as_float((unsigned)(e >> 32)) <= maxbest) {
-                const int tn = (int)(e & 0xffffffffull);
+            for (int q = 0; q < kPsStages; ++q) tiles[q] = s == q ? tn : tiles[q];
+            if (threadIdx.x == 0) {
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(&full_bar[s], fbytes + bbytes);
-                tma_load_1d(sm[s], FD + (int64_t)tn * kFaceTile * kFaceFloats, fbytes, &full_bar[s]);
+                tma_load_1d(sm[s], FD + (int64_t)tn * kPsTile * kFaceFloats, fbytes, &full_bar[s]);
                 tma_load_1d(smb[s], FB + (int64_t)tn * kPsBlocks * 2, bbytes, &full_bar[s]);
-                ++issued;
             }
+            ++tail;
         }
-        __syncthreads();
     }
-    if (threadIdx.x == 0)
-        for (int kk = k; kk < issued; ++kk) mbar_wait(&full_bar[kk % kP2sStages], (kk / kP2sStages) & 1);
+#ifdef CD_PS_STATS
+    if (threadIdx.x == 0) atomicMax(&g_ps_stats[2], (unsigned long long)tail);
+    if (lane == 0) atomicMax(&g_ps_stats[3], nblk_stat);
+#endif
 
-    const int64_t rowbase = (int64_t)b * P;
-    if (qbase < P) {
-        a.best_d[rowbase + qbase] = best0;
-        a.best_blk[rowbase + qbase] = blk0;
-    }
-    if (qbase + 1 < P) {
-        a.best_d[rowbase + qbase + 1] = best1;
-        a.best_blk[rowbase + qbase + 1] = blk1;
+    if (a.phase == 0) {
+        if (qbase < P) a.rowkey[rowbase + qbase] = row_key(best0, blk0);
+        if (qbase + 1 < P) a.rowkey[rowbase + qbase + 1] = row_key(best1, blk1);
+    } else {
+        // strictly improved rows only; the 64-bit minimum over chunks is order-independent
+        if (qbase < P && best0 < init0) atomicMin(a.rowkey + rowbase + qbase, row_key(best0, blk0));
+        if (qbase + 1 < P && best1 < init1) atomicMin(a.rowkey + rowbase + qbase + 1, row_key(best1, blk1));
     }
 }
 
@@ -428,8 +508,7 @@ struct PsResolveArgs {
     const float* verts;
     const int* faces;
     int B, N, Nv, Nf, Fpad, nchunks;
-    const float* best_d;
-    const int* best_blk;
+    const long long* rowkey;
     float* d_out;
     int* face_out;
     float* closest;
@@ -444,8 +523,9 @@ __global__ void __launch_bounds__(kMergeThreads) ps_resolve_kernel(PsResolveArgs
     double v = 0.0;
     if (p < a.N) {
         const int64_t srow = (int64_t)b * a.N + p;
-        const float best = a.best_d[srow];
-        const int bb = a.best_blk[srow];
+        const unsigned long long key = (unsigned long long)a.rowkey[srow];
+        const float best = __uint_as_float((unsigned)(key >> 32));
+        const int bb = (int)(unsigned)(key & 0xffffffffull);   // 0xffffffff -> -1
         const float4 pp = a.spts[srow];
         int face = a.perm_f[(int64_t)b * a.Nf];
         if (bb >= 0) {
@@ -502,7 +582,8 @@ struct PsPlan {
     int B, N, Nv, Nf, Fpad, qtiles, ftiles, nchunks, bbits, kbits, nbits;
     int64_t L;
     size_t off_bbox, off_keys[2], off_vals[2], off_counts, off_totals, off_spts, off_perm_p, off_perm_f, off_fd,
-        off_qbox, off_fbox, off_fbox32, off_cand, off_best_d, off_best_blk, off_chunk, bytes;
+        off_qbox, off_fbox, off_fbox32, off_cand, off_rowkey, off_chunk, bytes;
+    int k_first, klen, nchunk;   // phase 0: candidates [0, k_first); phase 1: nchunk chunks of klen
     bool supported;
 };
 
@@ -511,9 +592,9 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
     p.N = N;
     p.Nv = Nv;
     p.Nf = Nf;
-    p.Fpad = ps_cdiv(Nf, kFaceTile) * kFaceTile;
+    p.Fpad = ps_cdiv(Nf, kPsTile) * kPsTile;
     p.qtiles = ps_cdiv(N, kPsQ);
-    p.ftiles = p.Fpad / kFaceTile;
+    p.ftiles = p.Fpad / kPsTile;
     p.nchunks = ps_cdiv(N, kMergeThreads);
     int bb = 0;
     while ((1 << bb) < B) ++bb;
@@ -542,10 +623,16 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
     p.off_fbox = take((size_t)B * p.ftiles * 32);
     p.off_fbox32 = take((size_t)B * p.ftiles * kPsBlocks * 32);
     p.off_cand = take((size_t)B * p.qtiles * p.ftiles * 8);
-    p.off_best_d = take((size_t)B * N * 4);
-    p.off_best_blk = take((size_t)B * N * 4);
+    p.off_rowkey = take((size_t)B * N * 8);
     p.off_chunk = take((size_t)B * p.nchunks * 8);
     p.bytes = off;
+    // phase 0 visits each query tile's nearest kPsFirst face tiles (tight upper bounds for most rows);
+    // phase 1 spreads the rest of every list over chunks of klen tiles, one CTA each (load balance:
+    // the work of a far or straddling query tile is split instead of serialised in one CTA)
+    p.k_first = std::min(p.ftiles, kPsFirst);
+    const int rest = p.ftiles - p.k_first;
+    p.klen = std::max(kPsChunk, ps_cdiv(rest, kPsMaxChunks));
+    p.nchunk = rest > 0 ? ps_cdiv(rest, p.klen) : 0;
     p.supported = p.ftiles <= kPsMaxTiles && p.L <= 0x7fffffffLL;
 }
 
@@ -558,7 +645,7 @@ size_t p2s_pruned_workspace(int B, int N, int Nv, int Nf) {
 int p2s_pruned_launches(int B, int N, int Nv, int Nf) {
     PsPlan p;
     plan_ps(p, B, N, Nv, Nf);
-    return 2 + radix_sort_launches(p.L, p.nbits) + 6 + 1;   // + finalize
+    return 2 + radix_sort_launches(p.L, p.nbits) + 6 + (p.nchunk > 0 ? 1 : 0) + 1;   // + finalize
 }
 
 cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int* faces, int B, int N, int Nv, int Nf,
@@ -593,8 +680,7 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
     float4* fbox = reinterpret_cast<float4*>(w + p.off_fbox);
     float4* fbox32 = reinterpret_cast<float4*>(w + p.off_fbox32);
     unsigned long long* cand = reinterpret_cast<unsigned long long*>(w + p.off_cand);
-    float* best_d = reinterpret_cast<float*>(w + p.off_best_d);
-    int* best_blk = reinterpret_cast<int*>(w + p.off_best_blk);
+    long long* rowkey = reinterpret_cast<long long*>(w + p.off_rowkey);
     double* chunk = reinterpret_cast<double*>(w + p.off_chunk);
     {
         PsGatherArgs a{points, B, N, Nf, vals[cur], spts, perm_p, perm_f};
@@ -621,14 +707,30 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
         ps_candidates_kernel<<<B * p.qtiles, 256, (size_t)npow * 8, st>>>(a);
     }
     {
-        PsArgs a{spts, fd, fbox32, cand, N, p.Fpad, p.qtiles, p.ftiles, best_d, best_blk};
+        PsArgs a{spts, fd, fbox, fbox32, cand, N, p.Fpad, p.qtiles, p.ftiles, 0, p.k_first, 1, 0, rowkey};
         if (g_prof_start) record_profile_event(g_prof_start, st);
         p2s_pruned_kernel<<<dim3(p.qtiles, B), kPsThreads, 0, st>>>(a);
+        if (p.nchunk > 0) {
+            a.k0 = p.k_first;
+            a.klen = p.klen;
+            a.nchunk = p.nchunk;
+            a.phase = 1;
+            p2s_pruned_kernel<<<dim3(p.qtiles * p.nchunk, B), kPsThreads, 0, st>>>(a);
+        }
         if (g_prof_stop) record_profile_event(g_prof_stop, st);
+#ifdef CD_PS_STATS
+        unsigned long long h[4];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_ps_stats, sizeof(h));
+        printf("ps_stats tiles=%llu warp_blocks=%llu maxtiles=%llu maxwarpblocks=%llu ctas=%d ftiles=%d (full warp_blocks=%lld)\n", h[0], h[1], h[2], h[3],
+               p.qtiles * B, p.ftiles, (long long)p.qtiles * B * p.ftiles * kPsBlocks * (kPsThreads / 32));
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_ps_stats, z, sizeof(z));
+#endif
     }
     {
         PsResolveArgs a{spts, perm_p, perm_f, fd, verts, faces, B, N, Nv, Nf, p.Fpad, p.nchunks,
-                        best_d, best_blk, d, face, closest, bary, chunk};
+                        rowkey, d, face, closest, bary, chunk};
         ps_resolve_kernel<<<B * p.nchunks, kMergeThreads, 0, st>>>(a);
     }
     launch_p2s_finalize(chunk, B, N, p.nchunks, per_batch, loss, st);
