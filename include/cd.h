@@ -248,14 +248,15 @@ CD_API int cd_p2s_launch_count(int op, int B, int N, int Nv, int Nf);
 
 /*
  * cd_p2s_forward_pruned — cd_p2s_forward with culling (R26): points and face centroids
- * are Morton-sorted per batch element; 256-point query tiles visit 128-face tiles in ascending order
- * of a box lower bound and stop once the bound exceeds every point's current minimum; 32-face blocks
- * are skipped per warp the same way.  Boxes are widened by 2^-14 max|coord| so that the bound also
+ * are Morton-sorted per batch element; 64-point query tiles visit 64-face tiles in ascending order
+ * of a box lower bound and stop once the bound exceeds every point's current minimum; tiles and
+ * 32-face blocks no lane can improve on are skipped.  Boxes are widened by 2^-14 max|coord| so that the bound also
  * holds for the fp32-evaluated distances of the hot loop (R26): the minimum is the brute force's.
  * Same arguments and outputs as cd_p2s_forward except the tie rule: among faces with EXACTLY equal
- * fp32 minima the first found in the visiting order is returned (any of them is a closest face).
- * Workspace: cd_p2s_workspace_size(CD_OP_P2S_PRUNED, ...); 0 = unsupported size (more than
- * 8192 face tiles, i.e. Nf > 1048576, or B*(N+Nf) >= 2^31) and the call returns CD_ERR_TOO_LARGE.
+ * fp32 minima one is returned deterministically, not necessarily the lowest index (any of them is a
+ * closest face; R26).  Workspace: cd_p2s_workspace_size(CD_OP_P2S_PRUNED, ...); 0 = unsupported
+ * size (Nf > 524288, B*(N+Nf) >= 2^31, or per-query-tile candidate lists B*ceil(N/64)*ceil(Nf/64)*8
+ * bytes > 4 GiB) and the call returns CD_ERR_TOO_LARGE.
  */
 CD_API cd_status cd_p2s_forward_pruned(const float* points, const float* verts, const int32_t* faces,
                          int B, int N, int Nv, int Nf, float* d, int32_t* face, float* closest,

@@ -9,15 +9,21 @@
 //   radix sort           (nn_backward.cu)
 //   ps_gather_kernel     Morton-sorted packed points + permutation; face order (sorted pos -> face).
 //   ps_prep_kernel       the 24-float face records (p2s_common.cuh) in Morton face order, padded to
-//                        the 128-face tile by repeating the last sorted face.
-//   ps_aabb_kernel       boxes of every 256-point query tile and of every 128-face tile and 32-face
+//                        the 64-face tile by repeating the last sorted face.
+//   ps_aabb_kernel       boxes of every 64-point query tile and of every 64-face tile and 32-face
 //                        block (over the faces' vertices), each widened by delta = 2^-14 max|coord| of
 //                        the box so that a box gap bounds the fp32-evaluated distances (R26).
 //   ps_candidates_kernel per query tile: LB = gap^2 (1 - 1e-5) to every face tile, bitonic-sorted.
-//   p2s_pruned_kernel    face tiles in LB order through a 3-stage TMA ring; per 32-face block a
-//                        warp-uniform skip test against the warp's point box; value-only running
-//                        minimum of face_dist2 + block argmin; the CTA stops at the first tile whose LB
-//                        exceeds every row's current minimum.
+//   p2s_pruned_kernel    one warp per query tile (2 points per lane), face tiles in LB order through a
+//                        2-stage TMA ring.  A tile is fetched, and a 32-face block evaluated, only if
+//                        some lane may still improve: LB(lane's 2-point box, face box) <= the lane's
+//                        current maximum (a vote); value-only running minimum of face_dist2 + block
+//                        argmin.  Two phases for load balance: phase 0 visits each list's first
+//                        kPsFirst tiles (tight upper bounds for most rows) and stores 64-bit row keys
+//                        (distance bits << 32 | block); phase 1 splits the rest of every list into
+//                        chunks, one CTA each, that start from those bounds, stop once the list's LB
+//                        exceeds every row's bound and merge improvements with atomicMin on the keys
+//                        (order-independent: deterministic).
 //   ps_resolve_kernel    exact face inside the winning block (same fp32 ops; first in sorted order),
 //                        fp64 closest point / barycentrics / distance on that face, outputs in the
 //                        original point order, fp64 chunk sums; then p2s_finalize (p2s.cu).
@@ -31,29 +37,29 @@ namespace cdk {
 
 constexpr int kPsR = 2;                          // points per thread (one packed pair)
 #ifndef CD_PS_THREADS
-#define CD_PS_THREADS 128
+#define CD_PS_THREADS 32
 #endif
 #ifndef CD_PS_STAGES
-#define CD_PS_STAGES 3
+#define CD_PS_STAGES 2
 #endif
 #ifndef CD_PS_TILE
-#define CD_PS_TILE 128
+#define CD_PS_TILE 64
 #endif
 #ifndef CD_PS_MINB
-#define CD_PS_MINB 4
+#define CD_PS_MINB 16
 #endif
 constexpr int kPsThreads = CD_PS_THREADS;
 constexpr int kPsStages = CD_PS_STAGES;          // TMA ring depth
 constexpr int kPsTile = CD_PS_TILE;              // faces per shared-memory stage
-constexpr int kPsQ = kPsThreads * kPsR;          // 256 sorted points per query tile
+constexpr int kPsQ = kPsThreads * kPsR;          // 64 sorted points per query tile
 constexpr int kPsBlocks = kPsTile / kBlockK;   // blocks of 32 faces per face tile
 constexpr int kPsMaxTiles = 8192;                // face tiles per batch element (LB sort in smem)
 constexpr float kPsLbScale = 0.99999f;
 #ifndef CD_PS_FIRST
-#define CD_PS_FIRST 4
+#define CD_PS_FIRST 16
 #endif
 #ifndef CD_PS_CHUNK
-#define CD_PS_CHUNK 8
+#define CD_PS_CHUNK 16
 #endif
 constexpr int kPsFirst = CD_PS_FIRST;            // phase-0 face tiles per query tile
 constexpr int kPsChunk = CD_PS_CHUNK;            // phase-1 face tiles per CTA (at least)
@@ -194,7 +200,7 @@ struct PsAabbArgs {
     float4* fbox32;   // [B][ftiles*4][2]
 };
 
-// One warp per 256-point query tile (lane reduces 8 points) or per 128-face tile (4 blocks of 32).
+// One warp per query tile (lane reduces kPsQ / 32 points) or per face tile (kPsBlocks blocks of 32).
 __global__ void __launch_bounds__(256) ps_aabb_kernel(PsAabbArgs a) {
     const int64_t TQ = (int64_t)a.B * a.qtiles, T = TQ + (int64_t)a.B * a.ftiles;
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -633,7 +639,7 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
     const int rest = p.ftiles - p.k_first;
     p.klen = std::max(kPsChunk, ps_cdiv(rest, kPsMaxChunks));
     p.nchunk = rest > 0 ? ps_cdiv(rest, p.klen) : 0;
-    p.supported = p.ftiles <= kPsMaxTiles && p.L <= 0x7fffffffLL;
+    p.supported = (double)B * p.qtiles * p.ftiles * 8.0 <= 4294967296.0 && p.ftiles <= kPsMaxTiles && p.L <= 0x7fffffffLL;
 }
 
 size_t p2s_pruned_workspace(int B, int N, int Nv, int Nf) {
