@@ -96,6 +96,7 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
                               float* d, int* face, float* closest, float* bary, float* per_batch, float* loss,
                               void* ws, cudaStream_t st);
 // Per-(cloud, batch) sample bounding boxes [2][B][6] (nn_pruned.cu).
+int morton_bits(int bbits, int nmax);
 void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, float* bbox, cudaStream_t st);
 
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.

@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(256) bbox_kernel(BoxArgs a) {
     const float* p = a.src[c] + (int64_t)b * a.npts[c] * 3;
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     // The box only sets the Morton quantisation (codes are clamped), never correctness: a fixed-
-    // stride sample of <= 16K points per cloud is enough and keeps this O(16K) per batch element.
-    const int stride = max(1, a.npts[c] / 16384);
+    // stride sample of ~4K points per cloud is enough and keeps this O(4K) per batch element.
+    const int stride = max(1, a.npts[c] / 4096);
     for (int i = threadIdx.x * stride; i < a.npts[c]; i += 256 * stride) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -568,6 +568,17 @@ __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolve
 }
 
 // --------------------------------------------------------------------------------------------- host
+// Bits per axis of the Morton codes (key = set | batch | code).  A 2-pass radix sort (<= 22 key bits)
+// when it still leaves <= ~8 points per occupied surface cell (4^k >= n / 48); else up to 10 bits
+// (3 passes).  The order only affects how much is culled, never the results.
+int morton_bits(int bbits, int nmax) {
+    const int k2 = (21 - bbits) / 3;
+    int need = 1;
+    while (((int64_t)1 << (2 * need)) * 48 < (int64_t)nmax) ++need;
+    if (k2 >= need) return std::max(1, k2);
+    return std::max(1, std::min(10, (32 - 1 - bbits) / 3));
+}
+
 static int cdiv(int64_t x, int64_t y) { return (int)((x + y - 1) / y); }
 
 void plan_pruned(PrunedPlan& p, int B, int N, int M) {
@@ -583,7 +594,7 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
     int bb = 0;
     while ((1 << bb) < B) ++bb;
     p.bbits = bb;
-    p.kbits = std::max(1, std::min(10, (32 - 1 - bb) / 3));
+    p.kbits = morton_bits(bb, std::max(N, M));
     p.nbits = 1 + bb + 3 * p.kbits;
     p.L = (int64_t)B * (N + M);
     p.cand_off[0] = 0;

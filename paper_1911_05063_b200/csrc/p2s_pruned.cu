@@ -605,7 +605,7 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
     int bb = 0;
     while ((1 << bb) < B) ++bb;
     p.bbits = bb;
-    p.kbits = std::max(1, std::min(10, (32 - 1 - bb) / 3));
+    p.kbits = morton_bits(bb, std::max(N, Nf));
     p.nbits = 1 + bb + 3 * p.kbits;
     p.L = (int64_t)B * N + (int64_t)B * Nf;
     size_t off = 0;
