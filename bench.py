@@ -278,12 +278,23 @@ def measure_extras(cd, torch, dev, flush, args, K_extra):
     peak = sms * 128 * 1965e6 / 1e12
     pairs = B * N * Nf
     ach = P2S_OPS_PER_PAIR * pairs / (kms * 1e-3) / 1e12
+
+    def p2s_step_pruned():
+        d, fi, cl, ba, pb, loss = cd.p2s_forward(p, v, f, algorithm="pruned")
+        cd.p2s_backward(p, cl, fi, ba, f, Nv, g=None, g_scalar=1.0 / (B * N))
+        return loss
+
+    ms_pr = _timed(torch, p2s_step_pruned, flush, K_extra)
     out["next3_point_to_surface"] = {
         "workload": f"B={B} meshes (icosphere-5: {Nv} verts, {Nf} faces) x N={N} points; loss + grads to points and vertices",
         "ms_per_step": ms, "point_face_pairs_per_s": pairs / (ms * 1e-3),
         "kernel": "p2s_kernel", "kernel_ms": kms,
         "roofline": {"bound": "alu", "unit": "Tops/s (FP32-pipe lane ops)", "achieved": ach, "peak": peak,
                      "frac": ach / peak, "algorithmic": f"{P2S_OPS_PER_PAIR} FP32-pipe ops per (point, face)"},
+        "pruned": {"ms_per_step": ms_pr, "point_face_pairs_per_s_effective": pairs / (ms_pr * 1e-3),
+                   "speedup_vs_brute": ms / ms_pr,
+                   "note": "cd_p2s_forward_pruned (R26): same minima as the brute force; work-efficient, so "
+                           "its rate is quoted in brute-force pairs per second"},
     }
     # NEXT-4: B=32 meshes -> N=16,384 samples each -> Chamfer vs Y (M=16,384) -> grad to vertices
     B, N, M = 32, 16384, 16384
