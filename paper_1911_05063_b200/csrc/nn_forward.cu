@@ -1,19 +1,24 @@
 // nn_forward.cu — forward of the batched exact nearest-neighbour search.
 //
 // Kernels (one launch each, on the caller's stream):
-//   pack_kernel      AoS (x,y,z) fp32 clouds -> padded float4 clouds in the workspace (a.1).
-//   nn_fwd_kernel    the hot loop (a.2 + a.3, both directions in one grid): every thread keeps
-//                    kR = 16 queries in packed f32x2 registers and sweeps the targets of its split,
-//                    staged through a 3-stage shared-memory ring by 1-D TMA bulk copies
-//                    (cp.async.bulk + mbarrier).  Distances use FADD2/FMUL2/FFMA2 with the target
-//                    coordinate as broadcast operand; the running minimum is value-only (FMNMX3
-//                    folding two targets per op) and the argmin is tracked per block of kBlockK
-//                    targets (the block where the minimum last strictly decreased).
-//   nn_merge_kernel  merges the target splits (lowest split wins ties), re-scans the winning block
-//                    with the same .rn ops to recover the exact lowest index, writes d / idx and
-//                    per-chunk fp64 sums + hit counts (a.4).
+//   pack_kernel      AoS (x,y,z) fp32 clouds -> padded float4 clouds in the workspace (a.1); also
+//                    resets the 64-bit row / column keys to the identity of min.
+//   nn_fused_kernel  (nn_fused.cu) the default hot loop for full problems: both directions from one
+//                    evaluation of every distance.
+//   nn_fwd_kernel    the per-direction hot loop (query slices; a.2 + a.3, both directions in one
+//                    grid): every thread keeps kR = 16 queries in packed f32x2 registers and sweeps
+//                    the targets of its split, staged through a 3-stage shared-memory ring by 1-D TMA
+//                    bulk copies (cp.async.bulk + mbarrier).  Distances use FADD2/FMUL2/FFMA2 with
+//                    the target coordinate as broadcast operand; the running minimum is value-only
+//                    (FMNMX3 folding two targets per op) and the argmin is tracked per block of kBlockK
+//                    targets (the block where the minimum last strictly decreased).  Splits merge with
+//                    a 64-bit atomicMin on (distance bits << 32 | block start): order-independent.
+//   nn_epilogue_kernel  one launch for both directions' epilogues (a.4): row blocks re-scan the
+//                    winning 32-target block with the same .rn ops (exact lowest index), column blocks
+//                    re-scan the winning 16-row group of the fused kernel's column keys; d / idx
+//                    stores and per-chunk fp64 sums + hit counts.
 //   partials_kernel  fixed-order reduction of the chunk partials into partials[B][4] (a.4/a.5).
-// plus finalize_kernel (cd_finalize, a.5) and the cd_fscore path.
+// plus finalize_kernel (cd_finalize, a.5) and the cd_fscore path (stats_kernel).
 #include "cd_device.cuh"
 #include "cd_internal.h"
 
