@@ -307,8 +307,9 @@ CD_API void cd_set_profile_events(void* start, void* stop);
 /*
  * Test hook: forward kernel selection for cd_forward on the calling thread.  0 = automatic (the
  * fused bidirectional kernel for full problems, the per-direction kernel for query slices),
- * 1 = always the per-direction kernel, 2 = automatic (reserved).  Returns the previous value.
- * Both kernels produce bit-identical outputs.
+ * 1 = always the per-direction kernel, 2 = the fused kernel (full problems), 3 = the tensor-core
+ * filter + exact re-scan forward (nn_tc.cu, R27; full problems).  Returns the
+ * previous value.  All produce bit-identical outputs.
  */
 CD_API int cd_set_forward_mode(int mode);
 

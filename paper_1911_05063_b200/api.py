@@ -107,7 +107,8 @@ def forward_pruned(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, w
 
 def set_forward_mode(mode: int) -> int:
     """Test hook: 0 = automatic (fused bidirectional kernel for full problems), 1 = per-direction
-    kernel always.  Returns the previous value."""
+    kernel always, 2 = fused, 3 = tensor-core filter + exact re-scan (full problems).
+    Returns the previous value."""
     return int(_lib.load().cd_set_forward_mode(int(mode)))
 
 

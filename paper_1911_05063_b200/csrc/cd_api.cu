@@ -13,11 +13,12 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_forced_splits = 0;
-thread_local int g_forward_mode = 0;  // 0 auto (fused for full problems), 1 unfused, 2 fused
+thread_local int g_forward_mode = 0;  // 0 auto, 1 unfused, 2 fused (FP32 pipe), 3 tensor-core filter
 
 int auto_mode(int N, int M, int q0, int q1, int r0, int r1) {
     const bool full = q0 == 0 && q1 == N && r0 == 0 && r1 == M;
     if (g_forward_mode == 1 || !full) return cdk::kUnfused;
+    if (g_forward_mode == 3) return cdk::kTensor;
     return cdk::kFusedFull;
 }
 
@@ -65,7 +66,13 @@ size_t forward_ws(int B, int N, int M, int q0, int q1, int r0, int r1) {
     cdk::FwdPlan p, u;
     cdk::plan_forward(p, cdk::kFusedFull, B, N, M, q0, q1, r0, r1, g_forced_splits);
     cdk::plan_forward(u, cdk::kUnfused, B, N, M, q0, q1, r0, r1, g_forced_splits);
-    return std::max(p.bytes, u.bytes);
+    size_t bytes = std::max(p.bytes, u.bytes);
+    if (q0 == 0 && q1 == N && r0 == 0 && r1 == M) {
+        cdk::FwdPlan t;
+        cdk::plan_forward(t, cdk::kTensor, B, N, M, q0, q1, r0, r1, g_forced_splits);
+        bytes = std::max(bytes, t.bytes);
+    }
+    return bytes;
 }
 
 int fwd_launches(int B, int N, int M) {
@@ -433,7 +440,7 @@ cd_status cd_p2s_forward_pruned(const float* points, const float* verts, const i
 
 int cd_set_forward_mode(int mode) {
     int old = g_forward_mode;
-    g_forward_mode = (mode == 1 || mode == 2) ? mode : 0;
+    g_forward_mode = (mode >= 1 && mode <= 3) ? mode : 0;
     return old;
 }
 

@@ -8,7 +8,7 @@ namespace cdk {
 
 // Forward modes: the unfused kernel searches each direction separately (any query slices); the
 // fused kernel evaluates every distance once for both directions.
-enum FwdMode { kUnfused = 0, kFusedFull = 1, kFusedRows = 2, kFusedCols = 3 };
+enum FwdMode { kUnfused = 0, kFusedFull = 1, kFusedRows = 2, kFusedCols = 3, kTensor = 4 };
 // identity of the column-key min: larger than every key (keys are non-negative int64)
 constexpr long long kColKeyEmpty = 0x7fffffffffffffffLL;
 
@@ -29,6 +29,7 @@ struct FwdPlan {
     int64_t chunk_total;
     // workspace carve (byte offsets)
     size_t off_pack[2], off_rowkey, off_chunk_sum, off_chunk_hits, off_colkey, bytes;
+    int forced_splits;   // 0: automatic
 };
 
 struct FwdOutputs {
@@ -38,6 +39,17 @@ struct FwdOutputs {
     float tau;          // < 0: no hits
     long long* colkey;  // fused rows/cols modes: caller's B x M column keys (out / in)
 };
+
+// Tensor-core forward (nn_tc.cu, R27): full problems only.
+struct TcPlan {
+    int B, npts[2], ppad[2], qblocks, ttiles, splits, nchunks[2];
+    int64_t chunk_off[2];
+    size_t off_box, off_pack[2], off_op[2], off_rowsum, off_colsum, off_fb, off_chunk_sum, off_chunk_hits, bytes;
+};
+void plan_tc(TcPlan& p, int B, int N, int M, int forced_splits);
+int tc_launches(const TcPlan& p);
+struct FwdOutputs;
+cudaError_t launch_tc(const TcPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws, cudaStream_t st);
 
 void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits);
 cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,

@@ -320,7 +320,8 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
         const unsigned long long key = (unsigned long long)a.colkey[(int64_t)b * a.M + j];
         float m = INFINITY;
         int idx = -1;
-        if ((long long)key != kColKeyEmpty) {
+        // a +inf minimum is no finite candidate (R6): (+inf, -1) like the row direction
+        if ((long long)key != kColKeyEmpty && __uint_as_float((unsigned)(key >> 32)) < INFINITY) {
             m = __uint_as_float((unsigned)(key >> 32));
             const int i0 = (int)(unsigned)(key & 0xffffffffull);
             const float4 t = a.yp[(int64_t)b * a.ypad + j];
@@ -526,7 +527,17 @@ static int choose_splits(int64_t units, int ttiles, int ctas_per_sm) {
 }
 
 void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits) {
+    if (mode == kTensor) {   // full problems only (q = [0,N), r = [0,M)); the tensor plan carves its own workspace
+        plan_forward(p, kFusedFull, B, N, M, q0, q1, r0, r1, forced_splits);
+        TcPlan t;
+        plan_tc(t, B, N, M, forced_splits);
+        p.mode = kTensor;
+        p.bytes = t.bytes;
+        p.forced_splits = forced_splits;
+        return;
+    }
     p.mode = mode;
+    p.forced_splits = forced_splits;
     p.B = B;
     p.npts[0] = N;
     p.npts[1] = M;
@@ -578,6 +589,11 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
 
 cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
                            cudaStream_t st) {
+    if (p.mode == kTensor) {
+        TcPlan t;
+        plan_tc(t, p.B, p.npts[0], p.npts[1], p.forced_splits);
+        return launch_tc(t, x, y, o, ws, st);
+    }
     char* w = static_cast<char*>(ws);
     float4* pack0 = reinterpret_cast<float4*>(w + p.off_pack[0]);
     float4* pack1 = reinterpret_cast<float4*>(w + p.off_pack[1]);
@@ -712,6 +728,11 @@ cudaError_t launch_partials(const double* chunk_sum, const int* chunk_hits, cons
 }
 
 int forward_launches(const FwdPlan& p) {
+    if (p.mode == kTensor) {
+        TcPlan t;
+        plan_tc(t, p.B, p.npts[0], p.npts[1], p.forced_splits);
+        return tc_launches(t);
+    }
     int n = 1;                                                      // pack (+ column-key reset)
     if (p.mode == kUnfused) n += 2;                                 // nn_fwd + epilogue (merge)
     if (p.mode == kFusedFull) n += 2;                               // fused + epilogue (merge | resolve)
