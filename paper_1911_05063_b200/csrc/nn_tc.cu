@@ -301,9 +301,13 @@ __device__ __forceinline__ void tc_step_min(uint32_t tl, int step, u64* tfull, u
     uint32_t v[64];
 #pragma unroll
     for (int h = 0; h < 2 / kTcHalves; ++h) {
+#ifdef CD_TC_NOLD
+        v[0] = tl + h; v[63] = step;
+#else
         tmem_ld32(tl + buf * 256 + 64 * h, v);
         tmem_ld32(tl + buf * 256 + 64 * h + 32, v + 32);
         tmem_wait_ld();
+#endif
 #ifdef CD_TC_NOCOMPUTE
         c[h] = __uint_as_float(v[0] ^ v[63]);
 #else
