@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-pruned", action="store_true", help="skip the exact pruned (NEXT-2) comparison")
+    ap.add_argument("--no-tc", action="store_true", help="skip the tensor-core forward (mode 3) comparison")
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-3 / NEXT-4 workload lines")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise the multi-rank "
                     "logic when several ranks share one GPU")
@@ -475,6 +476,25 @@ def main():
                   "note": ("cd_forward_pruned (exact: Morton tiles + lower-bound culling, SURVEY §8.f NEXT-2) "
                            "+ finalize + backward; effective = the same 2*B*N*M directed pairs / step time")}
 
+    # ---------------------------------------------------------------- tensor-core forward (mode 3)
+    tcf = None
+    if world == 1 and not args.no_tc and not query_sharded:
+        outs = {}
+        times = {}
+        for mode in (2, 3):
+            old_mode = cd.set_forward_mode(mode)
+            try:
+                times[mode] = _timed(torch, lambda: cd.forward(x, y, tau=tau), flush, max(3, min(K, 50)))
+                outs[mode] = cd.forward(x, y, tau=tau)
+                torch.cuda.synchronize()
+            finally:
+                cd.set_forward_mode(old_mode)
+        same = all(bool(torch.equal(a, b)) for a, b in zip(outs[2], outs[3]))
+        tcf = {"forward_ms_tensor_core": times[3], "forward_ms_fp32_fused": times[2],
+               "bit_identical_outputs": same,
+               "note": ("cd_set_forward_mode(3): tcgen05 fp16-split MMA filter + exact fp32 re-scan (DESIGN.md "
+                        "4.7, R27); not the default (its exactness rests on the measured tensor-core accumulation)")}
+
     # ---------------------------------------------------------------- NEXT-3 / NEXT-4 workloads
     extras = None
     if world == 1 and not args.no_extras:
@@ -561,6 +581,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pruned": pruned,
+            "tensor_core_forward": tcf,
             "next_rows": extras,
             "gpu_launches": launches * K,
             "gpu_launches_per_step": launches,
