@@ -52,7 +52,7 @@ constexpr int kTcStages = 3;                     // target tile ring
 #endif
 constexpr int kTcHalves = CD_TC_HALVES;          // column halves per lane quarter (1: a warp reads all 128 columns)
 constexpr int kTcEpiWarps = 8 * kTcHalves;       // 2 groups (rows, columns) x 4 lane quarters x halves
-constexpr int kTcThreads = 32 * (2 + kTcEpiWarps);   // + TMA warp + MMA warp
+constexpr int kTcThreads = 32 * (3 + kTcEpiWarps);   // + TMA warp + 2 MMA warps (one per group)
 constexpr int kTcTileBytes = kTcRows * 32;       // 128 rows x 16 fp16
 constexpr int kTcChunk = 64;                     // targets / queries per tracked chunk (block)
 constexpr float kTcErel = 1.6e-5f;               // R27: E = kTcErel * U^2 (4e-6 at U = 1/2: 2x the derived bound)
@@ -304,8 +304,8 @@ __device__ __forceinline__ void tc_step_min(uint32_t tl, int step, u64* tfull, u
 #ifdef CD_TC_NOLD
         v[0] = tl + h; v[63] = step;
 #else
-        tmem_ld32(tl + buf * 256 + 64 * h, v);
-        tmem_ld32(tl + buf * 256 + 64 * h + 32, v + 32);
+        tmem_ld32(tl + buf * 128 + 64 * h, v);
+        tmem_ld32(tl + buf * 128 + 64 * h + 32, v + 32);
         tmem_wait_ld();
 #endif
 #ifdef CD_TC_NOCOMPUTE
@@ -329,9 +329,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(TcArgs a) {
     unsigned char* st = tc_smem + kTcSub * kTcTileBytes;          // target tile ring
     u64* full_bar = reinterpret_cast<u64*>(st + kTcStages * kTcTileBytes);
     u64* empty_bar = full_bar + kTcStages;
-    u64* tfull = empty_bar + kTcStages;    // [2]
-    u64* tempty = tfull + 2;               // [2]
-    u64* qbar = tempty + 2;
+    u64* tfull = empty_bar + kTcStages;    // [2 groups][2 buffers]
+    u64* tempty = tfull + 4;               // [2 groups][2 buffers]
+    u64* qbar = tempty + 4;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qbar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -343,11 +343,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(TcArgs a) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
+            mbar_init(&empty_bar[s], 2);   // released by both groups' MMA commits
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < 4; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], kTcEpiWarps);
+            mbar_init(&tempty[s], kTcEpiWarps / 2);
         }
         mbar_init(qbar, 1);
         fence_mbar_init();
@@ -374,8 +374,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(TcArgs a) {
                 tma_load_1d(st + s * kTcTileBytes, T + (int64_t)k * kTcTileBytes, kTcTileBytes, &full_bar[s]);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {   // MMA issuer
+    } else if (warp == 1 || warp == 2) {
+        if (lane == 0) {   // MMA issuer of group g: g = 0 -> D1 = Q_q T^T (lane = query), 1 -> D2 = T Q_q^T
+            const int g = warp - 1;
             const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcRows >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
             mbar_wait(qbar, 0);
             tc_fence_after();
@@ -388,14 +389,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(TcArgs a) {
                 for (int q = 0; q < kTcSub; ++q) {
                     const int buf = q & 1;
                     const int use = k * (kTcSub / 2) + (q >> 1);   // n-th use of this buffer
-                    if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);
+                    if (use > 0) mbar_wait(&tempty[2 * g + buf], (use - 1) & 1);
                     tc_fence_after();
                     const uint64_t dq = tc_desc(smem_u32(sq + q * kTcTileBytes));
 #ifndef CD_TC_NOMMA
-                    tc_mma(tmem + buf * 256, dq, dt, idesc);          // D1 = Q_q T^T (lane = query)
-                    tc_mma(tmem + buf * 256 + 128, dt, dq, idesc);    // D2 = T Q_q^T (lane = target)
+                    if (g == 0) tc_mma(tmem + buf * 128, dq, dt, idesc);
+                    else tc_mma(tmem + 256 + buf * 128, dt, dq, idesc);
 #endif
-                    tc_commit(&tfull[buf]);
+                    tc_commit(&tfull[2 * g + buf]);
                 }
                 tc_commit(&empty_bar[s]);
             }
@@ -404,12 +405,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(TcArgs a) {
         // epilogue: warps 2-9 = rows (D1), 10-17 = columns (D2); a warp reads the TMEM lane quarter
         // warp % 4 (hardware rule) and the column half (warp - 2) / 4 % 2 of its group's accumulator:
         // one 64-column chunk per step.  The two halves of a lane quarter merge through shared memory.
-        const int w = warp - 2;
+        const int w = warp - 3;
         const int group = w / (4 * kTcHalves);
         const int half = kTcHalves == 1 ? 0 : (w >> 2) & 1;
         const int lbase = 32 * (warp & 3);
         const int r = lbase + lane;
-        const uint32_t tl = tmem + ((uint32_t)lbase << 16) + (group ? 128u : 0u) + 64u * half;
+        const uint32_t tl = tmem + ((uint32_t)lbase << 16) + (group ? 256u : 0u) + 64u * half;
         constexpr int CPS = 2 / kTcHalves;   // 64-column chunks per warp and step
         const int N = a.npts[0], M = a.npts[1];
         const int64_t BN = (int64_t)gridDim.y * N, BM = (int64_t)gridDim.y * M;
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(TcArgs a) {
         for (int step = 0; step < nt * kTcSub; ++step) {
             const int k = step / kTcSub, q = step - k * kTcSub;
             float c[CPS];
-            tc_step_min(tl, step, tfull, tempty, lane, c);
+            tc_step_min(tl, step, tfull + 2 * group, tempty + 2 * group, lane, c);
             if (group == 0) {
                 float m1 = RS(0, q), m2 = RS(1, q), m3 = RS(2, q);
                 int b1 = __float_as_int(RS(3, q)), b2 = __float_as_int(RS(4, q));
