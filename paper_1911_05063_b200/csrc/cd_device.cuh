@@ -73,6 +73,42 @@ __device__ __forceinline__ long long row_key(float best, int blk) {
     return (long long)(((unsigned long long)__float_as_uint(best) << 32) | (unsigned long long)(unsigned)blk);
 }
 
+// 3-D Hilbert index of the cell (x[0], x[1], x[2]) of a 2^k grid (3k bits; Skilling's transpose
+// algorithm, then bit interleave).  Space-filling order for the pruned paths: consecutive runs are
+// more compact than Morton (Z-order) runs, so tile and block boxes are tighter.
+__device__ __forceinline__ uint32_t hilbert3(uint32_t x0, uint32_t x1, uint32_t x2, int k) {
+    uint32_t X[3] = {x0, x1, x2};
+    const uint32_t M = 1u << (k - 1);
+    for (uint32_t Q = M; Q > 1; Q >>= 1) {
+        const uint32_t P = Q - 1;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (X[i] & Q) {
+                X[0] ^= P;
+            } else {
+                const uint32_t t = (X[0] ^ X[i]) & P;
+                X[0] ^= t;
+                X[i] ^= t;
+            }
+        }
+    }
+    X[1] ^= X[0];
+    X[2] ^= X[1];
+    uint32_t t = 0;
+    for (uint32_t Q = M; Q > 1; Q >>= 1)
+        if (X[2] & Q) t ^= Q - 1;
+    X[0] ^= t;
+    X[1] ^= t;
+    X[2] ^= t;
+    uint32_t code = 0;
+    for (int bit = k - 1; bit >= 0; --bit) {
+        code = (code << 1) | ((X[0] >> bit) & 1u);
+        code = (code << 1) | ((X[1] >> bit) & 1u);
+        code = (code << 1) | ((X[2] >> bit) & 1u);
+    }
+    return code;
+}
+
 // ---------------------------------------------------------------- mbarrier + TMA bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

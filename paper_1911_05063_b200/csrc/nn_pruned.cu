@@ -89,11 +89,6 @@ void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, fl
 }
 
 // --------------------------------------------------------------------------------------------- morton
-__device__ __forceinline__ uint32_t spread_bits(uint32_t v, int k) {
-    uint32_t r = 0;
-    for (int i = 0; i < k; ++i) r |= ((v >> i) & 1u) << (3 * i);
-    return r;
-}
 
 struct MortonArgs {
     const float* src[2];
@@ -114,15 +109,15 @@ __global__ void __launch_bounds__(256) morton_kernel(MortonArgs a) {
         const int b = (int)(f / a.npts[c]);
         const float* bb = a.bbox + ((int64_t)c * a.B + b) * 6;
         const float* p = a.src[c] + f * 3;
-        uint32_t code = 0;
+        uint32_t q[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const float ext = bb[3 + k] - bb[k];
             float t = ext > 0.f ? (__ldg(p + k) - bb[k]) / ext : 0.f;
             t = fminf(fmaxf(t, 0.f), 1.f);          // NaN -> 0 via fmaxf
-            const uint32_t q = (uint32_t)(t * qmax + 0.5f);
-            code |= spread_bits(q, a.kbits) << k;
+            q[k] = (uint32_t)(t * qmax + 0.5f);
         }
+        const uint32_t code = hilbert3(q[0], q[1], q[2], a.kbits);
         a.keys[e] = ((uint32_t)c << (a.bbits + 3 * a.kbits)) | ((uint32_t)b << (3 * a.kbits)) | code;
         a.vals[e] = (uint32_t)e;
     }

@@ -67,11 +67,6 @@ constexpr int kPsMaxChunks = 32;                 // phase-1 CTAs per query tile 
 constexpr float kPsMargin = 1.0f / 16384.0f;     // delta = 2^-14 * max |coord| of the box
 
 // ------------------------------------------------------------------------------------------ morton
-__device__ __forceinline__ uint32_t ps_spread(uint32_t v, int k) {
-    uint32_t r = 0;
-    for (int i = 0; i < k; ++i) r |= ((v >> i) & 1u) << (3 * i);
-    return r;
-}
 
 struct PsMortonArgs {
     const float* points;
@@ -104,14 +99,15 @@ __global__ void __launch_bounds__(256) ps_morton_kernel(PsMortonArgs a) {
             for (int k = 0; k < 3; ++k) p[k] = (__ldg(v + 3 * i0 + k) + __ldg(v + 3 * i1 + k) + __ldg(v + 3 * i2 + k)) * (1.0f / 3.0f);
         }
         const float* bb = a.bbox + ((int64_t)c * a.B + b) * 6;
-        uint32_t code = 0;
+        uint32_t q[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const float ext = bb[3 + k] - bb[k];
             float t = ext > 0.f ? (p[k] - bb[k]) / ext : 0.f;
             t = fminf(fmaxf(t, 0.f), 1.f);
-            code |= ps_spread((uint32_t)(t * qmax + 0.5f), a.kbits) << k;
+            q[k] = (uint32_t)(t * qmax + 0.5f);
         }
+        const uint32_t code = hilbert3(q[0], q[1], q[2], a.kbits);
         a.keys[e] = ((uint32_t)c << (a.bbits + 3 * a.kbits)) | ((uint32_t)b << (3 * a.kbits)) | code;
         a.vals[e] = (uint32_t)e;
     }
