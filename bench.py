@@ -209,6 +209,18 @@ def run_reference(args):
         dist.destroy_process_group()
 
 
+def _measured_peak(key, fallback):
+    """(value, source) from the driver-written MEASURED_PEAKS.json, else the profiling guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            v = json.load(f).get(key)
+        if v:
+            return float(v), f"MEASURED_PEAKS.json {key}"
+    except (OSError, ValueError):
+        pass
+    return fallback, "fallback (B200_PROFILING.md)"
+
+
 def _traffic(kernel, cfg):
     """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -476,6 +488,23 @@ def main():
                   "note": ("cd_forward_pruned (exact: Morton tiles + lower-bound culling, SURVEY §8.f NEXT-2) "
                            "+ finalize + backward; effective = the same 2*B*N*M directed pairs / step time")}
 
+    # ---------------------------------------------------------------- backward vs HBM roofline
+    bwd_roof = None
+    if not query_sharded:
+        d_xy0, i_xy0, d_yx0, i_yx0, _ = cd.forward(x, y, tau=tau)
+        torch.cuda.synchronize()
+        bms = _timed(torch, lambda: cd.backward(x, y, i_xy0, i_yx0, g_scalar=w1 / (B_global * N),
+                                                h_scalar=w2 / (B_global * M)), flush, max(3, min(K, 50)))
+        pts = B_local * (N + M)
+        alg = 28 * pts   # read both clouds (12 B) + both index arrays (4 B) + write both gradients (12 B)
+        hbm_peak = _measured_peak("hbm_gbs", 7700.0)
+        bwd_roof = {"bound": "hbm", "kernel": "cd_backward (keys+hist, radix passes, offsets, grad: "
+                    f"{cd.launch_count(_lib.CD_OP_BACKWARD, B_local, N, M)} launches)", "ms": bms,
+                    "achieved": alg / (bms * 1e-3) / 1e9, "peak": hbm_peak[0], "unit": "GB/s",
+                    "frac": alg / (bms * 1e-3) / 1e9 / hbm_peak[0], "peak_source": hbm_peak[1],
+                    "algorithmic": "28 B per point (clouds 12 + indices 4 + gradients 12); the sort's key/value "
+                                   "passes and the partner gathers are extra traffic"}
+
     # ---------------------------------------------------------------- tensor-core forward (mode 3)
     tcf = None
     if world == 1 and not args.no_tc and not query_sharded:
@@ -578,6 +607,7 @@ def main():
             "pct_fp32_fma_peak_effective": 100.0 * FP32_OPS_PER_PAIR * pairs_total / world / (ms_per_step * 1e-3) /
                                            (sms * 128 * sm_max * 1e6),
             "roofline": roofline,
+            "roofline_backward": bwd_roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pruned": pruned,
