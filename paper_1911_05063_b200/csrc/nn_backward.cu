@@ -25,8 +25,14 @@ namespace cdk {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements per tile (512 per warp)
+#ifndef CD_SORT_ITEMS
+#define CD_SORT_ITEMS 16
+#endif
+#ifndef CD_SORT_MINB
+#define CD_SORT_MINB 1
+#endif
+constexpr int kSortItems = CD_SORT_ITEMS;
+constexpr int kSortTile = kSortThreads * kSortItems;  // elements per tile (kSortItems * 32 per warp)
 constexpr int kMaxDigitBits = 11;                     // digits of up to 11 bits: 2 passes cover 2^22 keys
 
 // Edge keys fused with the first radix pass's per-tile histogram: one CTA per sort
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* _
 // Phase 3: the tile is re-ordered by digit in shared memory, then written out so that consecutive
 // threads write consecutive addresses of each digit's run (coalesced stores).
 // Dynamic shared memory: (kSortWarps + 2) * D + 2 * kSortTile words.
-__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+__global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int D, int ntiles,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout) {
