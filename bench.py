@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-pruned", action="store_true", help="skip the exact pruned (NEXT-2) comparison")
     ap.add_argument("--no-tc", action="store_true", help="skip the tensor-core forward (mode 3) comparison")
+    ap.add_argument("--no-bwd-roofline", action="store_true", help="skip the separate backward timing")
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-3 / NEXT-4 workload lines")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise the multi-rank "
                     "logic when several ranks share one GPU")
@@ -490,7 +491,7 @@ def main():
 
     # ---------------------------------------------------------------- backward vs HBM roofline
     bwd_roof = None
-    if not query_sharded:
+    if not query_sharded and not args.no_bwd_roofline:
         d_xy0, i_xy0, d_yx0, i_yx0, _ = cd.forward(x, y, tau=tau)
         torch.cuda.synchronize()
         bms = _timed(torch, lambda: cd.backward(x, y, i_xy0, i_yx0, g_scalar=w1 / (B_global * N),

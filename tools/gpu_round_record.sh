@@ -7,4 +7,6 @@ CFGS=${CFGS:-c1 c2 c3 c4 c5} tools/gpu_allcfg.sh $TAG
 tools/gpu_launches.sh ${TAG}_l c3
 tools/gpu_ncu_full.sh ${TAG}_fused c3 nn_fused
 tools/gpu_ncu_kernel.sh ${TAG}_pruned nn_pruned 1 tools/run_forward.py c4 pruned 2
-tools/gpu_ncu_kernel.sh ${TAG}_p2s p2s_kernel 1 tools/run_p2s.py
+tools/gpu_ncu_kernel.sh ${TAG}_p2s p2s_kernel 1 tools/run_p2s.py brute
+tools/gpu_ncu_kernel.sh ${TAG}_p2sp p2s_pruned_kernel 1 tools/run_p2s.py pruned
+tools/gpu_ncu_kernel.sh ${TAG}_tc nn_tc_kernel 0 tools/run_tc.py c3 1
