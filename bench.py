@@ -486,7 +486,7 @@ def main():
         pruned = {"ms_per_step": pms, "value_effective": pairs_total / (pms * 1e-3), "unit": UNIT,
                   "speedup_vs_brute_step": ms_per_step / pms, "loss": ploss,
                   "loss_rel_diff_vs_brute": abs(ploss - loss) / max(abs(loss), 1e-300),
-                  "note": ("cd_forward_pruned (exact: Morton tiles + lower-bound culling, SURVEY §8.f NEXT-2) "
+                  "note": ("cd_forward_pruned (exact: Hilbert-ordered tiles + lower-bound culling, SURVEY §8.f NEXT-2) "
                            "+ finalize + backward; effective = the same 2*B*N*M directed pairs / step time")}
 
     # ---------------------------------------------------------------- backward vs HBM roofline

@@ -121,12 +121,13 @@ CD_API cd_status cd_forward_cols(const float* x, const float* y, int B, int N, i
  * cd_forward_pruned — the same outputs as cd_forward on the full problem (q0=0,q1=N,r0=0,r1=M)
  * computed with far fewer distance evaluations on large clouds (the exact
  * accelerated search SPEC.md:441/446 asks to equal brute force): both clouds are sorted along a
- * Morton curve per batch element, every 1024-row query tile visits 512-point target tiles in order
+ * Hilbert curve per batch element, every 256-row query tile visits 512-point target tiles in order
  * of a strict lower bound of their squared distance and stops once that bound exceeds the largest
  * current minimum among its rows.  Distances are the same fp32 values as the brute force (same op
- * order, every pair that could be a minimum is evaluated); indices are exact nearest neighbours —
- * among EXACTLY equal distances the one found first in tile order is returned instead of the lowest
- * index (R3').  Partials as cd_forward (sum order differs: equal within fp64 rounding).
+ * order, every pair that could be a minimum is evaluated) and so are the indices: the lowest index
+ * among exactly equal distances (ties inside one 32-point block are settled by the re-scan, ties
+ * across blocks by a full scan of the row; R3').  Partials as cd_forward (sum order
+ * differs: equal within fp64 rounding).
  * Limits: at most 4,194,304 points per cloud per batch element (CD_ERR_TOO_LARGE).
  * Workspace: cd_workspace_size(CD_OP_FORWARD_PRUNED, B, N, M).
  */
@@ -248,7 +249,7 @@ CD_API int cd_p2s_launch_count(int op, int B, int N, int Nv, int Nf);
 
 /*
  * cd_p2s_forward_pruned — cd_p2s_forward with culling (R26): points and face centroids
- * are Morton-sorted per batch element; 64-point query tiles visit 64-face tiles in ascending order
+ * are Hilbert-sorted per batch element; 64-point query tiles visit 64-face tiles in ascending order
  * of a box lower bound and stop once the bound exceeds every point's current minimum; tiles and
  * 32-face blocks no lane can improve on are skipped.  Boxes are widened by 2^-14 max|coord| so that the bound also
  * holds for the fp32-evaluated distances of the hot loop (R26): the minimum is the brute force's.

@@ -87,7 +87,7 @@ def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=
 
 
 def forward_pruned(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, want_partials: bool = True):
-    """cd_forward_pruned: exact nearest neighbours with Morton-tile lower-bound culling."""
+    """cd_forward_pruned: exact nearest neighbours with Hilbert-ordered tiles and lower-bound culling (same results as the brute force)."""
     x = _check_cloud(x, "x")
     y = _check_cloud(y, "y")
     B, N, _ = x.shape

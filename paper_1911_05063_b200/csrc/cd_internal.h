@@ -62,7 +62,7 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
                               long long* rowkey, cudaStream_t st);
 
 
-// Exact pruned forward (nn_pruned.cu, NEXT-2): Morton-sorted tiles + box lower-bound culling.
+// Exact pruned forward (nn_pruned.cu, NEXT-2): Hilbert-sorted tiles + box lower-bound culling.
 struct PrunedPlan {
     int B, npts[2], ppad[2], qtiles[2], ttiles[2];
     int bbits, kbits, nbits;
@@ -71,7 +71,7 @@ struct PrunedPlan {
     int64_t chunk_off[2];
     bool supported;
     size_t off_bbox, off_keys[2], off_vals[2], off_counts, off_totals, off_sorted[2], off_perm[2], off_box[2], off_box32[2],
-        off_best_d[2], off_best_blk[2], off_cand, off_chunk_sum, off_chunk_hits, bytes;
+        off_best_d[2], off_best_blk[2], off_cand, off_chunk_sum, off_chunk_hits, off_fb, bytes;
 };
 void plan_pruned(PrunedPlan& p, int B, int N, int M);
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
@@ -108,7 +108,7 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
                               float* d, int* face, float* closest, float* bary, float* per_batch, float* loss,
                               void* ws, cudaStream_t st);
 // Per-(cloud, batch) sample bounding boxes [2][B][6] (nn_pruned.cu).
-int morton_bits(int bbits, int nmax);
+int hilbert_bits(int bbits, int nmax);
 void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, float* bbox, cudaStream_t st);
 
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.

@@ -3,9 +3,9 @@
 // Same results as the brute force (the fixed fp32 distance formula of DESIGN.md §4.2 evaluated on
 // every pair that could matter), far fewer pairs on large clouds:
 //   bbox_kernel        per (cloud, batch) bounding box of a fixed-stride sample (min/max: order-free;
-//                      only the Morton quantisation depends on it).
-//   morton_kernel      key = (cloud | batch | k-bit-per-axis Morton code) per point, value = row.
-//   radix sort         (nn_backward.cu) -> every (cloud, batch) segment in Morton order.
+//                      only the Hilbert quantisation depends on it).
+//   hilbert_kernel      key = (cloud | batch | 3k-bit Hilbert index) per point, value = row.
+//   radix sort         (nn_backward.cu) -> every (cloud, batch) segment in Hilbert order.
 //   gather_kernel      sorted packed float4 clouds + permutation (sorted position -> original row).
 //   aabb_kernel        bounding box of every 512-point tile of the sorted clouds.
 //   candidates_kernel  per query tile (256 sorted rows): lower bound LB of the squared distance to
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) bbox_kernel(BoxArgs a) {
     const int c = blockIdx.x / a.B, b = blockIdx.x - (blockIdx.x / a.B) * a.B;
     const float* p = a.src[c] + (int64_t)b * a.npts[c] * 3;
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    // The box only sets the Morton quantisation (codes are clamped), never correctness: a fixed-
+    // The box only sets the Hilbert quantisation (codes are clamped), never correctness: a fixed-
     // stride sample of ~4K points per cloud is enough and keeps this O(4K) per batch element.
     const int stride = max(1, a.npts[c] / 4096);
     for (int i = threadIdx.x * stride; i < a.npts[c]; i += 256 * stride) {
@@ -88,18 +88,20 @@ void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, fl
     bbox_kernel<<<2 * B, 256, 0, st>>>(a);
 }
 
-// --------------------------------------------------------------------------------------------- morton
+// --------------------------------------------------------------------------------------------- hilbert keys
 
-struct MortonArgs {
+struct HilbertArgs {
     const float* src[2];
     int npts[2];
     int B, kbits, bbits;
     const float* bbox;
     uint32_t* keys;
     uint32_t* vals;
+    unsigned* fb_count;   // tie queue of the resolve, reset here
 };
 
-__global__ void __launch_bounds__(256) morton_kernel(MortonArgs a) {
+__global__ void __launch_bounds__(256) hilbert_kernel(HilbertArgs a) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.fb_count) *a.fb_count = 0u;
     const int64_t L0 = (int64_t)a.B * a.npts[0];
     const int64_t L = L0 + (int64_t)a.B * a.npts[1];
     const float qmax = (float)((1 << a.kbits) - 1);
@@ -363,10 +365,12 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
     }
     float best[kPrR];
     int blk[kPrR];
+    bool tie[kPrR];
 #pragma unroll
     for (int r = 0; r < kPrR; ++r) {
         best[r] = INFINITY;
         blk[r] = -1;
+        tie[r] = false;
     }
     // box of this warp's 256 consecutive sorted rows (valid rows only)
     float wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -405,9 +409,9 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         for (int kb = 0; kb < kTile; kb += kBlockK) {
             // warp-uniform skip: every pair of this block is farther than every row's minimum
             if (box_lb(wlo, whi, bb[2 * (kb / kBlockK)], bb[2 * (kb / kBlockK) + 1]) > wmax) continue;
-            float old[kPrR];
+            float cur[kPrR];   // this block's minimum per row
 #pragma unroll
-            for (int r = 0; r < kPrR; ++r) old[r] = best[r];
+            for (int r = 0; r < kPrR; ++r) cur[r] = INFINITY;
 #pragma unroll 4
             for (int jj = 0; jj < kBlockK; jj += 2) {
                 const float4 t0 = tb[kb + jj];
@@ -429,12 +433,20 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
                     float a0, a1, c0, c1;
                     upk2(s0, a0, a1);
                     upk2(s1, c0, c1);
-                    best[2 * r] = fmin3(best[2 * r], a0, c0);
-                    best[2 * r + 1] = fmin3(best[2 * r + 1], a1, c1);
+                    cur[2 * r] = fmin3(cur[2 * r], a0, c0);
+                    cur[2 * r + 1] = fmin3(cur[2 * r + 1], a1, c1);
                 }
             }
+            // a strictly smaller block minimum takes over; an EQUAL finite one is an exact tie across
+            // blocks (Hilbert order is not index order): flagged, the resolve then scans the row
 #pragma unroll
-            for (int r = 0; r < kPrR; ++r) blk[r] = best[r] < old[r] ? jt + kb : blk[r];
+            for (int r = 0; r < kPrR; ++r) {
+                const bool lt = cur[r] < best[r];
+                const bool eq = cur[r] == best[r] && cur[r] < INFINITY;
+                blk[r] = lt ? jt + kb : blk[r];
+                tie[r] = lt ? false : (eq || tie[r]);
+                best[r] = fminf(best[r], cur[r]);
+            }
         }
         // CTA maximum of the rows' current minima (valid rows only; d >= 0 so bits order = float order)
         unsigned m = 0u;
@@ -472,7 +484,7 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         const int q = qbase + r;
         if (q < P) {
             a.best_d[dir][rowbase + q] = best[r];
-            a.best_blk[dir][rowbase + q] = blk[r];
+            a.best_blk[dir][rowbase + q] = (blk[r] >= 0 && tie[r]) ? (blk[r] | (int)0x80000000) : blk[r];
         }
     }
 }
@@ -492,6 +504,8 @@ struct PrResolveArgs {
     double* chunk_sum;
     int* chunk_hits;
     double tau2;
+    unsigned* fb_count;    // rows with an exact tie across blocks (full scan: lowest original index)
+    unsigned* fb_list;     // (dir << 31) | b * P + p
 };
 
 __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolveArgs a) {
@@ -510,14 +524,17 @@ __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolve
     int h = 0;
     if (p < P) {
         const float best = a.best_d[dir][(int64_t)b * P + p];
-        const int bb = a.best_blk[dir][(int64_t)b * P + p];
+        const int bbt = a.best_blk[dir][(int64_t)b * P + p];
+        const bool tie = bbt != -1 && (bbt & (int)0x80000000) != 0;
+        const int bb = bbt == -1 ? -1 : (bbt & 0x7fffffff);
         int idx = -1;
         if (bb >= 0) {
+            // the lowest ORIGINAL index among the block's targets at the minimum distance
             const float4 qp = a.sorted[qc][(int64_t)b * a.ppad[qc] + p];
             const float4* T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
+            const int* PT = a.perm[tc] + (int64_t)b * a.npts[tc];
             const int jend = min(bb + kBlockK, a.npts[tc]);
-            int pos = -1;
-            for (int c = bb; c < jend && pos < 0; c += 8) {
+            for (int c = bb; c < jend; c += 8) {
                 float d[8];
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
@@ -525,10 +542,16 @@ __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolve
                     d[r] = dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z);
                 }
 #pragma unroll
-                for (int r = 7; r >= 0; --r)
-                    if (c + r < jend && d[r] == best) pos = c + r;
+                for (int r = 0; r < 8; ++r)
+                    if (c + r < jend && d[r] == best) {
+                        const int o = PT[c + r];
+                        idx = (idx < 0 || o < idx) ? o : idx;
+                    }
             }
-            if (pos >= 0) idx = a.perm[tc][(int64_t)b * a.npts[tc] + pos];
+            if (tie) {
+                const unsigned slot = atomicAdd(a.fb_count, 1u);
+                a.fb_list[slot] = ((unsigned)dir << 31) | (unsigned)((int64_t)b * P + p);
+            }
         }
         const int i = a.perm[qc][(int64_t)b * P + p];
         a.d_out[dir][(int64_t)b * P + i] = best;
@@ -562,11 +585,48 @@ __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolve
     }
 }
 
+// Rows whose minimum is attained in more than one block: scan every target (sorted clouds) for the
+// lowest original index at the minimum distance (the distance itself is already final).  One CTA
+// per queued row.
+__global__ void __launch_bounds__(256) pruned_tie_kernel(PrResolveArgs a) {
+    const unsigned count = *a.fb_count;
+    __shared__ int sidx[8];
+    for (unsigned w = blockIdx.x; w < count; w += gridDim.x) {
+        const unsigned item = a.fb_list[w];
+        const int dir = (int)(item >> 31);
+        const int64_t g = item & 0x7fffffffu;
+        const int qc = dir, tc = 1 - dir;
+        const int P = a.npts[qc];
+        const int b = (int)(g / P);
+        const int p = (int)(g - (int64_t)b * P);
+        const float best = a.best_d[dir][g];
+        const float4 qp = a.sorted[qc][(int64_t)b * a.ppad[qc] + p];
+        const float4* T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
+        const int* PT = a.perm[tc] + (int64_t)b * a.npts[tc];
+        const int nT = a.npts[tc];
+        int idx = 0x7fffffff;
+        for (int j = threadIdx.x; j < nT; j += blockDim.x) {
+            const float4 t = T[j];
+            if (dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z) == best) idx = min(idx, PT[j]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(0xffffffffu, idx, o));
+        if ((threadIdx.x & 31) == 0) sidx[threadIdx.x >> 5] = idx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < (int)(blockDim.x >> 5); ++k) idx = min(idx, sidx[k]);
+            const int i = a.perm[qc][(int64_t)b * P + p];
+            if (idx != 0x7fffffff) a.idx_out[dir][(int64_t)b * P + i] = idx;
+        }
+        __syncthreads();
+    }
+}
+
 // --------------------------------------------------------------------------------------------- host
-// Bits per axis of the Morton codes (key = set | batch | code).  A 2-pass radix sort (<= 22 key bits)
+// Bits per axis of the Hilbert codes (key = set | batch | code).  A 2-pass radix sort (<= 22 key bits)
 // when it still leaves <= ~8 points per occupied surface cell (4^k >= n / 48); else up to 10 bits
 // (3 passes).  The order only affects how much is culled, never the results.
-int morton_bits(int bbits, int nmax) {
+int hilbert_bits(int bbits, int nmax) {
     const int k2 = (21 - bbits) / 3;
     int need = 1;
     while (((int64_t)1 << (2 * need)) * 48 < (int64_t)nmax) ++need;
@@ -589,7 +649,7 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
     int bb = 0;
     while ((1 << bb) < B) ++bb;
     p.bbits = bb;
-    p.kbits = morton_bits(bb, std::max(N, M));
+    p.kbits = hilbert_bits(bb, std::max(N, M));
     p.nbits = 1 + bb + 3 * p.kbits;
     p.L = (int64_t)B * (N + M);
     p.cand_off[0] = 0;
@@ -624,11 +684,12 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
     p.off_cand = take((size_t)ncand * 8);
     p.off_chunk_sum = take((size_t)chunks * 8);
     p.off_chunk_hits = take((size_t)chunks * 4);
+    p.off_fb = take(256 + (size_t)p.L * 4);
     p.bytes = off;
     p.supported = p.ttiles[0] <= kPrMaxTiles && p.ttiles[1] <= kPrMaxTiles;
 }
 
-int pruned_launches(const PrunedPlan& p) { return 2 + radix_sort_launches(p.L, p.nbits) + 6; }
+int pruned_launches(const PrunedPlan& p) { return 2 + radix_sort_launches(p.L, p.nbits) + 7; }
 
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
                           cudaStream_t st) {
@@ -645,7 +706,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);
     {
-        MortonArgs a;
+        HilbertArgs a;
         a.src[0] = x;
         a.src[1] = y;
         a.npts[0] = p.npts[0];
@@ -656,7 +717,8 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         a.bbox = bbox;
         a.keys = keys[0];
         a.vals = vals[0];
-        morton_kernel<<<grid_l, 256, 0, st>>>(a);
+        a.fb_count = reinterpret_cast<unsigned*>(w + p.off_fb);
+        hilbert_kernel<<<grid_l, 256, 0, st>>>(a);
     }
     const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
                                      reinterpret_cast<uint32_t*>(w + p.off_totals), st);
@@ -762,7 +824,10 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         a.chunk_sum = chunk_sum;
         a.chunk_hits = chunk_hits;
         a.tau2 = o.tau >= 0.f ? (double)o.tau * (double)o.tau : -1.0;
+        a.fb_count = reinterpret_cast<unsigned*>(w + p.off_fb);
+        a.fb_list = a.fb_count + 64;
         pruned_resolve_kernel<<<p.B * (p.nchunks[0] + p.nchunks[1]), kMergeThreads, 0, st>>>(a);
+        pruned_tie_kernel<<<sms * 4, 256, 0, st>>>(a);
     }
     if (o.partials) {
         cudaError_t e = launch_partials(chunk_sum, chunk_hits, p.nchunks, p.chunk_off, p.B, o.partials, 3, st);

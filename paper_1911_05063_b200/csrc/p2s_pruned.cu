@@ -3,12 +3,12 @@
 // The same outputs as p2s.cu (cd_p2s_forward) with far fewer (point, face) evaluations, built from
 // the pruned nearest-neighbour machinery of nn_pruned.cu (R26):
 //   bbox (nn_pruned.cu)  per batch element: sample boxes of the points and of the vertices (they only
-//                        set the Morton quantisation).
-//   ps_morton_kernel     key = (set | batch | Morton code) for every point (set 0) and every face
+//                        set the Hilbert quantisation).
+//   ps_hilbert_kernel     key = (set | batch | Hilbert code) for every point (set 0) and every face
 //                        centroid (set 1); value = flat row.
 //   radix sort           (nn_backward.cu)
-//   ps_gather_kernel     Morton-sorted packed points + permutation; face order (sorted pos -> face).
-//   ps_prep_kernel       the 24-float face records (p2s_common.cuh) in Morton face order, padded to
+//   ps_gather_kernel     Hilbert-sorted packed points + permutation; face order (sorted pos -> face).
+//   ps_prep_kernel       the 24-float face records (p2s_common.cuh) in Hilbert face order, padded to
 //                        the 64-face tile by repeating the last sorted face.
 //   ps_aabb_kernel       boxes of every 64-point query tile and of every 64-face tile and 32-face
 //                        block (over the faces' vertices), each widened by delta = 2^-14 max|coord| of
@@ -66,9 +66,9 @@ constexpr int kPsChunk = CD_PS_CHUNK;            // phase-1 face tiles per CTA (
 constexpr int kPsMaxChunks = 32;                 // phase-1 CTAs per query tile (at most)
 constexpr float kPsMargin = 1.0f / 16384.0f;     // delta = 2^-14 * max |coord| of the box
 
-// ------------------------------------------------------------------------------------------ morton
+// ------------------------------------------------------------------------------------------ hilbert keys
 
-struct PsMortonArgs {
+struct PsHilbertArgs {
     const float* points;
     const float* verts;
     const int* faces;
@@ -78,7 +78,7 @@ struct PsMortonArgs {
     uint32_t* vals;
 };
 
-__global__ void __launch_bounds__(256) ps_morton_kernel(PsMortonArgs a) {
+__global__ void __launch_bounds__(256) ps_hilbert_kernel(PsHilbertArgs a) {
     const int64_t L0 = (int64_t)a.B * a.N;
     const int64_t L = L0 + (int64_t)a.B * a.Nf;
     const float qmax = (float)((1 << a.kbits) - 1);
@@ -601,7 +601,7 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
     int bb = 0;
     while ((1 << bb) < B) ++bb;
     p.bbits = bb;
-    p.kbits = morton_bits(bb, std::max(N, Nf));
+    p.kbits = hilbert_bits(bb, std::max(N, Nf));
     p.nbits = 1 + bb + 3 * p.kbits;
     p.L = (int64_t)B * N + (int64_t)B * Nf;
     size_t off = 0;
@@ -669,8 +669,8 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);
     {
-        PsMortonArgs a{points, verts, faces, B, N, Nv, Nf, p.kbits, p.bbits, bbox, keys[0], vals[0]};
-        ps_morton_kernel<<<grid_l, 256, 0, st>>>(a);
+        PsHilbertArgs a{points, verts, faces, B, N, Nv, Nf, p.kbits, p.bbits, bbox, keys[0], vals[0]};
+        ps_hilbert_kernel<<<grid_l, 256, 0, st>>>(a);
     }
     const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
                                      reinterpret_cast<uint32_t*>(w + p.off_totals), st);
