@@ -23,6 +23,7 @@
 #include "cd_internal.h"
 
 #include <algorithm>
+#include <cstdio>
 
 namespace cdk {
 
@@ -227,7 +228,8 @@ struct CandArgs {
     int B;
     int qtiles[2];            // query tiles (kPrQ rows) per batch element, per dir
     int64_t cand_off[2];      // offset of dir's lists in `cand` (u64 entries)
-    unsigned long long* cand; // per (dir, b, query tile): ttiles(1-dir) keys (LB' bits << 32 | tile)
+    unsigned long long* cand; // per (dir, b, query tile): up to ttiles(1-dir) keys (LB' bits << 32 | tile)
+    int* ccount;              // per list: number of entries (LB <= UB), lists of dir 1 after dir 0's
 };
 
 __device__ __forceinline__ float gap(float qlo, float qhi, float tlo, float thi) {
@@ -254,26 +256,50 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
         qlo[0] = fminf(qlo[0], lo.x); qlo[1] = fminf(qlo[1], lo.y); qlo[2] = fminf(qlo[2], lo.z);
         qhi[0] = fmaxf(qhi[0], hi.x); qhi[1] = fmaxf(qhi[1], hi.y); qhi[2] = fmaxf(qhi[2], hi.z);
     }
-    int npow = 1;
-    while (npow < tnt) npow <<= 1;
-    for (int t = threadIdx.x; t < npow; t += 256) {
-        unsigned long long key = ~0ull;
-        if (t < tnt) {
-            const float4* bx = a.box[tc] + ((int64_t)b * tnt + t) * 2;
-            const float4 lo = bx[0], hi = bx[1];
-            float lb;
-            if (lo.x > hi.x) {
-                lb = INFINITY;   // empty tile (all padding)
-            } else {
-                const float gx = gap(qlo[0], qhi[0], lo.x, hi.x);
-                const float gy = gap(qlo[1], qhi[1], lo.y, hi.y);
-                const float gz = gap(qlo[2], qhi[2], lo.z, hi.z);
-                lb = (gx * gx + gy * gy + gz * gz) * kLbScale;
-            }
-            key = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+    // Upper bound UB of every row's final minimum: each row's nearest target is at most as far as any
+    // point of any non-empty tile, i.e. the farthest box-to-box corner distance (x (1 + 1e-5): an
+    // upper bound of the fp32-evaluated distance too).  Tiles with LB > UB can never be visited
+    // (the kernel stops at LB > max over rows of the current minimum <= UB): the list keeps only
+    // LB <= UB, compacted, then sorted (keys are unique, so the order is deterministic).
+    __shared__ float s_ub[8];
+    __shared__ int s_cnt;
+    float ub = INFINITY;
+    for (int t = threadIdx.x; t < tnt; t += 256) {
+        const float4* bx = a.box[tc] + ((int64_t)b * tnt + t) * 2;
+        const float4 lo = bx[0], hi = bx[1];
+        if (lo.x <= hi.x) {
+            const float fx = fmaxf(fabsf(hi.x - qlo[0]), fabsf(qhi[0] - lo.x));
+            const float fy = fmaxf(fabsf(hi.y - qlo[1]), fabsf(qhi[1] - lo.y));
+            const float fz = fmaxf(fabsf(hi.z - qlo[2]), fabsf(qhi[2] - lo.z));
+            ub = fminf(ub, (fx * fx + fy * fy + fz * fz) * 1.00001f);
         }
-        keys[t] = key;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ub = fminf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+    if ((threadIdx.x & 31) == 0) s_ub[threadIdx.x >> 5] = ub;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    ub = s_ub[0];
+    for (int w = 1; w < 8; ++w) ub = fminf(ub, s_ub[w]);
+    for (int t = threadIdx.x; t < tnt; t += 256) {
+        const float4* bx = a.box[tc] + ((int64_t)b * tnt + t) * 2;
+        const float4 lo = bx[0], hi = bx[1];
+        float lb;
+        if (lo.x > hi.x) {
+            lb = INFINITY;   // empty tile (all padding)
+        } else {
+            const float gx = gap(qlo[0], qhi[0], lo.x, hi.x);
+            const float gy = gap(qlo[1], qhi[1], lo.y, hi.y);
+            const float gz = gap(qlo[2], qhi[2], lo.z, hi.z);
+            lb = (gx * gx + gy * gy + gz * gz) * kLbScale;
+        }
+        if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+    }
+    __syncthreads();
+    const int n = s_cnt;
+    int npow = 1;
+    while (npow < n) npow <<= 1;
+    for (int t = n + threadIdx.x; t < npow; t += 256) keys[t] = ~0ull;
     __syncthreads();
     // bitonic sort ascending (npow <= kPrMaxTiles)
     for (int k = 2; k <= npow; k <<= 1) {
@@ -292,8 +318,10 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
             __syncthreads();
         }
     }
+    const int64_t list = (int64_t)(dir == 0 ? 0 : a.B * a.qtiles[0]) + (int64_t)b * a.qtiles[dir] + q;
     unsigned long long* out = a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + q) * tnt;
-    for (int t = threadIdx.x; t < tnt; t += 256) out[t] = keys[t];
+    for (int t = threadIdx.x; t < n; t += 256) out[t] = keys[t];
+    if (threadIdx.x == 0) a.ccount[list] = n;
 }
 
 // --------------------------------------------------------------------------------------------- main kernel
@@ -304,6 +332,7 @@ struct PrunedArgs {
     int qtiles[2];
     int64_t cand_off[2];
     const unsigned long long* cand;
+    const int* ccount;    // entries per list (candidates_kernel)
     float* best_d[2];     // [B][npts] sorted order
     int* best_blk[2];     // sorted target position of the winning block
 };
@@ -336,13 +365,14 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
     const float4* __restrict__ TB = a.bbox32[tc] + (int64_t)b * tnt * kBlocksPerTile * 2;
     const unsigned long long* __restrict__ cand =
         a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + u) * tnt;
+    const int ncand = a.ccount[(int64_t)(dir == 0 ? 0 : (int64_t)gridDim.y * a.qtiles[0]) + (int64_t)b * a.qtiles[dir] + u];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     int issued = 0;  // thread 0 only
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
         fence_mbar_init();
-        const int pre = min(kStages, tnt);
+        const int pre = min(kStages, ncand);
         for (int k = 0; k < pre; ++k) {
             const int t = (int)(cand[k] & 0xffffffffull);
             mbar_arrive_expect_tx(&full_bar[k], kTile * 16 + kBlocksPerTile * 32);
@@ -395,9 +425,9 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
     float maxbest = INFINITY;   // CTA-uniform (read from shared memory after a barrier)
     unsigned long long next = cand[0];
     int k = 0;
-    for (; k < tnt; ++k) {
+    for (; k < ncand; ++k) {
         const unsigned long long cur = next;
-        if (k + 1 < tnt) next = cand[k + 1];   // prefetch the next list entry
+        if (k + 1 < ncand) next = cand[k + 1];   // prefetch the next list entry
         const float lb = __uint_as_float((unsigned)(cur >> 32));
         if (lb > maxbest) break;               // every remaining tile is farther: done (uniform)
         const int t = (int)(cur & 0xffffffffull);
@@ -461,7 +491,7 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
 #pragma unroll
         for (int w = 1; w < kPrThreads / 32; ++w) mm = max(mm, s_wmax[w]);
         maxbest = __uint_as_float(mm);
-        if (threadIdx.x == 0 && issued == k + kStages && issued < tnt) {
+        if (threadIdx.x == 0 && issued == k + kStages && issued < ncand) {
             const unsigned long long e = cand[issued];
             if (__uint_as_float((unsigned)(e >> 32)) <= maxbest) {
                 const int tn = (int)(e & 0xffffffffull);
@@ -589,34 +619,45 @@ __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolve
 // lowest original index at the minimum distance (the distance itself is already final).  One CTA
 // per queued row.
 __global__ void __launch_bounds__(256) pruned_tie_kernel(PrResolveArgs a) {
+    constexpr int kChunk = 256 * 16;   // targets per work item (16 per thread)
     const unsigned count = *a.fb_count;
+    const int nchunk = (max(a.npts[0], a.npts[1]) + kChunk - 1) / kChunk;
     __shared__ int sidx[8];
-    for (unsigned w = blockIdx.x; w < count; w += gridDim.x) {
-        const unsigned item = a.fb_list[w];
+    for (int64_t w = blockIdx.x; w < (int64_t)count * nchunk; w += gridDim.x) {
+        const unsigned item = a.fb_list[w / nchunk];
+        const int c = (int)(w % nchunk);
         const int dir = (int)(item >> 31);
         const int64_t g = item & 0x7fffffffu;
         const int qc = dir, tc = 1 - dir;
         const int P = a.npts[qc];
         const int b = (int)(g / P);
         const int p = (int)(g - (int64_t)b * P);
+        const int nT = a.npts[tc];
+        const int j0 = c * kChunk;
+        if (j0 >= nT) continue;   // uniform across the CTA
         const float best = a.best_d[dir][g];
         const float4 qp = a.sorted[qc][(int64_t)b * a.ppad[qc] + p];
         const float4* T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
         const int* PT = a.perm[tc] + (int64_t)b * a.npts[tc];
-        const int nT = a.npts[tc];
         int idx = 0x7fffffff;
-        for (int j = threadIdx.x; j < nT; j += blockDim.x) {
-            const float4 t = T[j];
-            if (dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z) == best) idx = min(idx, PT[j]);
+        float4 t[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) t[u] = T[min(j0 + 256 * u + (int)threadIdx.x, nT - 1)];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int j = j0 + 256 * u + (int)threadIdx.x;
+            if (j < nT && dist_rn(qp.x, qp.y, qp.z, t[u].x, t[u].y, t[u].z) == best) idx = min(idx, PT[j]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(0xffffffffu, idx, o));
         if ((threadIdx.x & 31) == 0) sidx[threadIdx.x >> 5] = idx;
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int k = 1; k < (int)(blockDim.x >> 5); ++k) idx = min(idx, sidx[k]);
+            for (int k = 1; k < 8; ++k) idx = min(idx, sidx[k]);
             const int i = a.perm[qc][(int64_t)b * P + p];
-            if (idx != 0x7fffffff) a.idx_out[dir][(int64_t)b * P + i] = idx;
+            // the resolve stored a tie index of the winning block; the minimum over all chunks is the
+            // lowest original index at the minimum distance (integer min: order-independent)
+            if (idx != 0x7fffffff) atomicMin(&a.idx_out[dir][(int64_t)b * P + i], idx);
         }
         __syncthreads();
     }
@@ -682,6 +723,7 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
         p.off_best_blk[c] = take((size_t)B * p.npts[c] * 4);
     }
     p.off_cand = take((size_t)ncand * 8);
+    p.off_ccount = take((size_t)B * (p.qtiles[0] + p.qtiles[1]) * 4);
     p.off_chunk_sum = take((size_t)chunks * 8);
     p.off_chunk_hits = take((size_t)chunks * 4);
     p.off_fb = take(256 + (size_t)p.L * 4);
@@ -771,6 +813,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
             a.cand_off[c] = p.cand_off[c];
         }
         a.cand = cand;
+        a.ccount = reinterpret_cast<int*>(w + p.off_ccount);
         int npow = 1;
         while (npow < std::max(p.ttiles[0], p.ttiles[1])) npow <<= 1;
         const size_t smem = (size_t)npow * 8;
@@ -800,6 +843,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
             a.best_blk[c] = best_blk[c];
         }
         a.cand = cand;
+        a.ccount = reinterpret_cast<const int*>(w + p.off_ccount);
         if (g_prof_start) record_profile_event(g_prof_start, st);
         nn_pruned_kernel<<<dim3(p.qtiles[0] + p.qtiles[1], p.B), kPrThreads, 0, st>>>(a);
         if (g_prof_stop) record_profile_event(g_prof_stop, st);
@@ -828,6 +872,12 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         a.fb_list = a.fb_count + 64;
         pruned_resolve_kernel<<<p.B * (p.nchunks[0] + p.nchunks[1]), kMergeThreads, 0, st>>>(a);
         pruned_tie_kernel<<<sms * 4, 256, 0, st>>>(a);
+#ifdef CD_PR_STATS
+        unsigned h = 0;
+        cudaStreamSynchronize(st);
+        cudaMemcpy(&h, a.fb_count, 4, cudaMemcpyDeviceToHost);
+        printf("pruned tie rows: %u of %lld\n", h, (long long)p.L);
+#endif
     }
     if (o.partials) {
         cudaError_t e = launch_partials(chunk_sum, chunk_hits, p.nchunks, p.chunk_off, p.B, o.partials, 3, st);
