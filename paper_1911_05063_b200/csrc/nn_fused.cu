@@ -24,6 +24,11 @@
 
 namespace cdk {
 
+#ifndef CD_FUSED_UNROLL
+#define CD_FUSED_UNROLL 2
+#endif
+constexpr int kFusedUnroll = CD_FUSED_UNROLL;   // target pairs per inner-loop body
+
 struct FusedArgs {
     const float4* xp;   // packed X (rows)
     const float4* yp;   // packed Y (targets / columns)
@@ -35,7 +40,10 @@ struct FusedArgs {
     long long* colkey;  // [B][M], non-negative keys; kColKeyEmpty = none
 };
 
-__global__ void __launch_bounds__(kFwdThreads, 3) nn_fused_kernel(FusedArgs a) {
+#ifndef CD_FUSED_MINB
+#define CD_FUSED_MINB 3
+#endif
+__global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(FusedArgs a) {
     __shared__ __align__(128) float4 sm[kStages][kTile];
     __shared__ float colv[2][kFwdThreads / 32][kTile];
     __shared__ unsigned char coll[2][kFwdThreads / 32][kTile];
@@ -98,13 +106,17 @@ __global__ void __launch_bounds__(kFwdThreads, 3) nn_fused_kernel(FusedArgs a) {
 #pragma unroll
             for (int r = 0; r < kR; ++r) old[r] = best[r];
             unsigned keep_m = 0x7f800000u, keep_e = 0u;  // this lane's target (kb + lane) results
-#pragma unroll 2
+#pragma unroll kFusedUnroll
             for (int jj = 0; jj < kBlockK; jj += 2) {
                 const float4 t0 = tb[kb + jj];
                 const float4 t1 = tb[kb + jj + 1];
                 const u64 t0x = pk2(t0.x, t0.x), t0y = pk2(t0.y, t0.y), t0z = pk2(t0.z, t0.z);
                 const u64 t1x = pk2(t1.x, t1.x), t1y = pk2(t1.y, t1.y), t1z = pk2(t1.z, t1.z);
+#ifndef CD_COLMIN_TREE
+                float ca[2], cb[2];   // column partials: two FMNMX3 accumulators per target (depth 4)
+#else
                 float ca[kR / 2], cb[kR / 2];
+#endif
 #pragma unroll
                 for (int r = 0; r < kR / 2; ++r) {
                     u64 dx = sub2(qx[r], t0x), dy = sub2(qy[r], t0y), dz = sub2(qz[r], t0z);
@@ -122,12 +134,26 @@ __global__ void __launch_bounds__(kFwdThreads, 3) nn_fused_kernel(FusedArgs a) {
                     upk2(s1, b0, b1);
                     best[2 * r] = fmin3(best[2 * r], a0, b0);      // row mins
                     best[2 * r + 1] = fmin3(best[2 * r + 1], a1, b1);
+#ifndef CD_COLMIN_TREE
+                    if (r < 2) {
+                        ca[r] = fminf(a0, a1);
+                        cb[r] = fminf(b0, b1);
+                    } else {
+                        ca[r & 1] = fmin3(ca[r & 1], a0, a1);
+                        cb[r & 1] = fmin3(cb[r & 1], b0, b1);
+                    }
+#else
                     ca[r] = fminf(a0, a1);                           // column partials (tree below)
                     cb[r] = fminf(b0, b1);
+#endif
                 }
+#ifndef CD_COLMIN_TREE
+                const float c0 = fminf(ca[0], ca[1]), c1 = fminf(cb[0], cb[1]);
+#else
                 // column min over this thread's 16 rows: FMNMX3 tree (depth 2 instead of a chain)
                 const float c0 = fmin3(fmin3(ca[0], ca[1], ca[2]), fmin3(ca[3], ca[4], ca[5]), fminf(ca[6], ca[7]));
                 const float c1 = fmin3(fmin3(cb[0], cb[1], cb[2]), fmin3(cb[3], cb[4], cb[5]), fminf(cb[6], cb[7]));
+#endif
                 // warp min (REDUX on the bits: d >= 0, so unsigned order == float order, NaN > inf)
                 const unsigned u0 = __float_as_uint(c0), u1 = __float_as_uint(c1);
                 const unsigned m0 = __reduce_min_sync(0xffffffffu, u0);
