@@ -30,6 +30,7 @@ struct FwdPlan {
     // workspace carve (byte offsets)
     size_t off_pack[2], off_rowkey, off_chunk_sum, off_chunk_hits, off_colkey, bytes;
     int forced_splits;   // 0: automatic
+    int split_unit;      // fused kernel: targets per split unit (kTile, or kBlockK for small M)
 };
 
 struct FwdOutputs {

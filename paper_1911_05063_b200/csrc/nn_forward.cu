@@ -526,6 +526,27 @@ static int choose_splits(int64_t units, int ttiles, int ctas_per_sm) {
     return best_s;
 }
 
+// Block-granular version for the fused kernel: a CTA's work is ceil(nb/S) 32-target blocks (plus a
+// fixed overhead of ~4 tiles' worth: the 2048-row load, the per-tile column combine, the row keys).
+static int choose_splits_blocks(int64_t units, int nb, int ctas_per_sm) {
+    const int64_t slots = (int64_t)device_sm_count() * ctas_per_sm;
+    const double c0 = 4.0;   // in blocks
+    const int smax = std::max(1, std::min(128, nb));
+    int best_s = 1;
+    double best_t = 1e300;
+    for (int s = 1; s <= smax; ++s) {
+        const int64_t ctas = units * s;
+        const double waves = (double)ceil_div(ctas, slots);
+        double t = waves * ((double)ceil_div(nb, s) + c0);
+        if (ctas < slots && s < smax) t *= 1.15;
+        if (t < best_t * 0.999) {
+            best_t = t;
+            best_s = s;
+        }
+    }
+    return best_s;
+}
+
 void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits) {
     if (mode == kTensor) {   // full problems only (q = [0,N), r = [0,M)); the tensor plan carves its own workspace
         plan_forward(p, kFusedFull, B, N, M, q0, q1, r0, r1, forced_splits);
@@ -538,6 +559,7 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
     }
     p.mode = mode;
     p.forced_splits = forced_splits;
+    p.split_unit = kTile;
     p.B = B;
     p.npts[0] = N;
     p.npts[1] = M;
@@ -554,11 +576,27 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
         units += (int64_t)B * p.qtiles[d];
     }
     const int occ = mode == kUnfused ? unfused_ctas_per_sm() : fused_ctas_per_sm();
-    const int S = forced_splits > 0 ? forced_splits : choose_splits(units, ceil_div(std::max(N, M), kTile), occ);
-    for (int d = 0; d < 2; ++d) {
-        p.ttiles[d] = ceil_div(p.npts[1 - d], kTile);
-        p.splits[d] = std::max(1, std::min(S, p.ttiles[d]));  // <= T: every split non-empty
-        if (p.qtiles[d] == 0) p.splits[d] = 1;
+    if (mode == kUnfused) {
+        const int S = forced_splits > 0 ? forced_splits : choose_splits(units, ceil_div(std::max(N, M), kTile), occ);
+        for (int d = 0; d < 2; ++d) {
+            p.ttiles[d] = ceil_div(p.npts[1 - d], kTile);
+            p.splits[d] = std::max(1, std::min(S, p.ttiles[d]));  // <= T: every split non-empty
+            if (p.qtiles[d] == 0) p.splits[d] = 1;
+        }
+    } else {
+        // the fused kernel splits the targets in 512-target tiles, or in 32-target blocks when even
+        // one tile per CTA cannot fill the GPU (small M, e.g. c2: 4 tiles per batch element)
+        const int tt = ceil_div(M, kTile), nb = ceil_div(M, kBlockK);
+        const bool blocks = forced_splits <= 0 && units * tt < (int64_t)device_sm_count() * occ;
+        p.split_unit = blocks ? kBlockK : kTile;
+        const int nu = blocks ? nb : tt;
+        const int S = forced_splits > 0 ? forced_splits
+                                        : (blocks ? choose_splits_blocks(units, nb, occ) : choose_splits(units, tt, occ));
+        for (int d = 0; d < 2; ++d) {
+            p.ttiles[d] = ceil_div(p.npts[1 - d], kTile);
+            p.splits[d] = std::max(1, std::min(S, nu));   // <= units: every split non-empty
+            if (p.qtiles[d] == 0) p.splits[d] = 1;
+        }
     }
     const int64_t sq = (int64_t)(q1 - q0), sr = (int64_t)(r1 - r0);
     p.slice_off[0] = 0;

@@ -35,6 +35,7 @@ struct FusedArgs {
     int N, M, xpad, ypad;
     int q0, q1;         // X row slice
     int qtiles, splits, ttiles;
+    int split_unit;       // targets per split unit: kTile or kBlockK
     int64_t slice_total;  // B * (q1 - q0)
     long long* rowkey;  // [B*(q1-q0)]: min over splits of (best bits << 32 | block start)
     long long* colkey;  // [B][M], non-negative keys; kColKeyEmpty = none
@@ -43,6 +44,7 @@ struct FusedArgs {
 #ifndef CD_FUSED_MINB
 #define CD_FUSED_MINB 3
 #endif
+template <bool kPartial>   // true: block-granular splits (partial tiles possible)
 __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(FusedArgs a) {
     __shared__ __align__(128) float4 sm[kStages][kTile];
     __shared__ float colv[2][kFwdThreads / 32][kTile];
@@ -54,9 +56,14 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
     const int split = blockIdx.x - tile * a.splits;
     const float4* __restrict__ Q = a.xp + (int64_t)b * a.xpad;
     const float4* __restrict__ T = a.yp + (int64_t)b * a.ypad;
-    const int j0 = (int)((int64_t)split * a.ttiles / a.splits) * kTile;  // tiles [s*T/S, (s+1)*T/S)
-    const int j1 = min((int)((int64_t)(split + 1) * a.ttiles / a.splits) * kTile, a.M);
-    const int ntiles = (j1 - j0 + kTile - 1) / kTile;
+    // split s covers the split units [s*nu/S, (s+1)*nu/S): 512-target tiles normally, 32-target
+    // blocks when there are too few tiles to fill the GPU (small M; plan_forward)
+    const int ulen = a.split_unit;                      // targets per split unit (512 or 32)
+    const int nu = (a.M + ulen - 1) / ulen;
+    const int j0 = (int)((int64_t)split * nu / a.splits) * ulen;
+    const int j1b = (int)((int64_t)(split + 1) * nu / a.splits) * ulen;   // unit-aligned end (<= ppad)
+    const int j1 = min(j1b, a.M);
+    const int ntiles = (j1b - j0 + kTile - 1) / kTile;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
 
@@ -68,8 +75,9 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
     if (threadIdx.x == 0) {
         const int pre = min(kStages, ntiles);
         for (int k = 0; k < pre; ++k) {
-            mbar_arrive_expect_tx(&full_bar[k], kTile * 16);
-            tma_load_1d(sm[k], T + j0 + (int64_t)k * kTile, kTile * 16, &full_bar[k]);
+            const uint32_t bytes = (uint32_t)min(kTile, j1b - (j0 + k * kTile)) * 16;
+            mbar_arrive_expect_tx(&full_bar[k], bytes);
+            tma_load_1d(sm[k], T + j0 + (int64_t)k * kTile, bytes, &full_bar[k]);
         }
     }
 
@@ -100,7 +108,9 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
         float* cv = colv[k & 1][warp];
         unsigned char* cl = coll[k & 1][warp];
         const int jt = j0 + k * kTile;
+        const int kend = min(kTile, j1b - jt);   // this tile's targets (a multiple of 32)
         for (int kb = 0; kb < kTile; kb += kBlockK) {
+            if (kPartial && kb >= kend) break;   // partial last tile of a block-granular split
             static_assert(kBlockK == 32, "one column result per lane per block");
             float old[kR];
 #pragma unroll
@@ -172,9 +182,11 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
         }
         __syncthreads();  // every warp is done with stage s and has written colv[k & 1]
         if (threadIdx.x == 0 && k + kStages < ntiles) {
+            const int jn = jt + kStages * kTile;
+            const uint32_t bytes = (uint32_t)min(kTile, j1b - jn) * 16;
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&full_bar[s], kTile * 16);
-            tma_load_1d(sm[s], T + jt + (int64_t)kStages * kTile, kTile * 16, &full_bar[s]);
+            mbar_arrive_expect_tx(&full_bar[s], bytes);
+            tma_load_1d(sm[s], T + jn, bytes, &full_bar[s]);
         }
         // combine the 4 warps per target and publish one key per (CTA, target)
         for (int t = threadIdx.x; t < kTile; t += kFwdThreads) {
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
 int fused_ctas_per_sm() {
     static thread_local int occ = 0;
     if (occ == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nn_fused_kernel, kFwdThreads, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nn_fused_kernel<false>, kFwdThreads, 0) != cudaSuccess ||
             occ <= 0) {
             cudaGetLastError();
             occ = 3;
@@ -236,13 +248,17 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
     a.qtiles = p.qtiles[0];
     a.splits = p.splits[0];
     a.ttiles = p.ttiles[0];
+    a.split_unit = p.split_unit;
     a.slice_total = p.slice_total;
     a.rowkey = rowkey;
     a.colkey = colkey;
     const int gx = p.qtiles[0] * p.splits[0];
     if (gx > 0) {
         if (g_prof_start) record_profile_event(g_prof_start, st);
-        nn_fused_kernel<<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
+        if (p.split_unit == kTile)
+            nn_fused_kernel<false><<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
+        else
+            nn_fused_kernel<true><<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
         if (g_prof_stop) record_profile_event(g_prof_stop, st);
     }
     return cudaGetLastError();

@@ -305,8 +305,10 @@ def test_errors_raise(cd):
 
 # ------------------------------------------------------------------------------ fused vs per-direction
 @pytest.mark.parametrize("B,N,M", [(1, 1, 1), (2, 3, 7), (2, 1000, 1024), (3, 2049, 4097), (1, 5000, 1),
-                                   (4, 8192, 3000)])
+                                   (4, 8192, 3000), (32, 2048, 2048), (8, 4096, 1000), (2, 300, 70000)])
 def test_fused_equals_unfused_bitwise(cd, B, N, M):
+    """Also covers the fused kernel's block-granular target splits (small M: partial tiles) and the
+    tile-granular ones (large M)."""
     X, Y = synth.shape_pair(B, N, M, config_index=40 + N % 7)
     _, _, fused = _run(cd, X, Y, tau=0.01)
     old = cd.set_forward_mode(1)
