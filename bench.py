@@ -505,6 +505,18 @@ def main():
                     "frac": alg / (bms * 1e-3) / 1e9 / hbm_peak[0], "peak_source": hbm_peak[1],
                     "algorithmic": "28 B per point (clouds 12 + indices 4 + gradients 12); the sort's key/value "
                                    "passes and the partner gathers are extra traffic"}
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tb = json.load(f).get(f"backward/{args.config}")
+        except (OSError, ValueError):
+            tb = None
+        if tb:
+            gbs = tb["dram_bytes_per_call"] / (tb["ms_cold"] * 1e-3) / 1e9
+            bwd_roof["dram_measured"] = {
+                "bytes_per_call": tb["dram_bytes_per_call"], "ms_cold": tb["ms_cold"], "GB_s": gbs,
+                "frac": gbs / hbm_peak[0], "source": "profiles/" + tb["source"],
+                "note": "ncu dram__bytes_read+write summed over the backward's kernels (cold, serialised); "
+                        "all DRAM traffic incl. the sort passes and the random coordinate gathers"}
 
     # ---------------------------------------------------------------- tensor-core forward (mode 3)
     tcf = None
