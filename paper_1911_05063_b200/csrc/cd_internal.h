@@ -142,7 +142,7 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits,
 int radix_digit_bits(int64_t L, int nbits);
 size_t radix_sort_counts_words(int64_t L, int nbits);
 int radix_sort_launches(int64_t L, int nbits);
-constexpr int kSortTotalsWords = 1 << 11;
+constexpr int kSortTotalsWords = 1 << 12;   // >= 2^kMaxDigitBits
 
 // thread-local measurement hook (cd_set_profile_events)
 extern thread_local cudaEvent_t g_prof_start;

@@ -33,7 +33,10 @@ constexpr int kSortWarps = kSortThreads / 32;
 #endif
 constexpr int kSortItems = CD_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;  // elements per tile (kSortItems * 32 per warp)
-constexpr int kMaxDigitBits = 11;                     // digits of up to 11 bits: 2 passes cover 2^22 keys
+#ifndef CD_SORT_MAXBITS
+#define CD_SORT_MAXBITS 11
+#endif
+constexpr int kMaxDigitBits = CD_SORT_MAXBITS;        // digits of up to 11 bits: 2 passes cover 2^22 keys
 
 // Edge keys fused with the first radix pass's per-tile histogram: one CTA per sort
 // tile writes its 4096 (key, value) pairs and counts digit 0 (saves a launch and a read of the keys).
