@@ -8,7 +8,7 @@ torch = pytest.importorskip("torch")
 
 import oracle
 from paper_1911_05063_b200 import synth
-from tests.gpu_helpers import gate_forward_batch, gate_grad, gate_mirror, RTOL
+from tests.gpu_helpers import gate_forward_batch, gate_grad, gate_mirror, GAP, RTOL
 
 pytestmark = pytest.mark.gpu
 
@@ -139,6 +139,29 @@ def test_large_configs_sampled(cd, name, nrows):
                                        h_scalar=np.float32(1.0 / (B * M)))
     np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
     np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_large_configs_all_points_kdtree(cd, name):
+    """Every point of c4 / c5 (not a sample): the GPU minimum equals the exact nearest-neighbour
+    distance from scipy's cKDTree (fp64, k=2) within 1e-5 relative, and the index is exact wherever
+    the top-2 gap exceeds 1e-6 relative (SURVEY §8.c.4 "large configs"; readings R12, R13); the
+    pruned forward reproduces the brute force's d / idx / hit counts on every point."""
+    from scipy.spatial import cKDTree
+    X, Y = synth.config_inputs(name)
+    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
+    # the pruned path on every point of the same problem: bit for bit the brute force's results
+    pr = [t.cpu().numpy() for t in cd.forward(x, y, tau=0.01, algorithm="pruned")]
+    for a, b in zip(pr[:4], (d_xy, i_xy, d_yx, i_yx)):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(pr[4][:, 2:], part[:, 2:])
+    for Q, T, d, i in ((X, Y, d_xy, i_xy), (Y, X, d_yx, i_yx)):
+        for b in range(Q.shape[0]):
+            dist, idx = cKDTree(T[b].astype(np.float64)).query(Q[b].astype(np.float64), k=2, workers=-1)
+            d1, d2 = dist[:, 0] ** 2, dist[:, 1] ** 2
+            np.testing.assert_allclose(d[b].astype(np.float64), d1, rtol=RTOL, atol=0)
+            clear = (d2 - d1) > GAP * d1
+            np.testing.assert_array_equal(i[b][clear], idx[clear, 0])
 
 
 # ------------------------------------------------------------------------------ edge cases
