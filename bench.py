@@ -223,13 +223,19 @@ def _measured_peak(key, fallback):
 
 
 def _traffic(kernel, cfg):
-    """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
+    """dram read+write bytes per launch of `kernel` (and its ncu FMA-pipe utilisation) from the
+    committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
         e = d.get(f"{kernel}/{cfg}")
-        return None if e is None else {"bytes_per_launch": e["dram_bytes_per_launch"], "source": "profiles/" + e["source"]}
+        if e is None:
+            return None
+        out = {"bytes_per_launch": e["dram_bytes_per_launch"], "source": "profiles/" + e["source"]}
+        if "pipe_fma_pct" in e:
+            out["ncu_pipe_fma_cycles_active_pct"] = e["pipe_fma_pct"]
+        return out
     except (OSError, ValueError, KeyError):
         return None
 

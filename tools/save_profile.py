@@ -66,6 +66,10 @@ def full(tag, rnd, cfg):
     tj = os.path.join(P, "traffic.json")
     d = json.load(open(tj)) if os.path.exists(tj) else {}
     d[f"{name}/{cfg}"] = {"dram_bytes_per_launch": traffic, "source": f"{rnd}_ncu_full_{name}_{cfg}.txt"}
+    for key, metric in (("pipe_fma_pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                        ("pipe_alu_pct", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active")):
+        if metric in hdr:
+            d[f"{name}/{cfg}"][key] = float(vals[hdr.index(metric)])
     json.dump(d, open(tj, "w"), indent=1)
     print(txt)
     print("traffic", traffic)
