@@ -147,6 +147,17 @@ def cpu_cores():
 
 
 # ------------------------------------------------------------------------------------------ oracle timing
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(X, Y, budget_s: float, min_rows: int = 8):
     """Time the fp64 oracle brute force on row samples of both directions (bounded, ~budget_s).
     Returns (pairs/s, cores, description).  Rows are spread uniformly over all batch elements."""
@@ -166,13 +177,19 @@ def oracle_sample(X, Y, budget_s: float, min_rows: int = 8):
     rows_x = np.linspace(0, B * N - 1, rx).astype(np.int64)
     rows_y = np.linspace(0, B * M - 1, ry).astype(np.int64)
     t0 = time.perf_counter()
-    oracle.nn(X, Y, rows=rows_x)
-    oracle.nn(Y, X, rows=rows_y)
+    oracle.nn(X, Y, rows=rows_x, nthreads=threads)
+    oracle.nn(Y, X, rows=rows_y, nthreads=threads)
     dt = time.perf_counter() - t0
     pairs = rx * M + ry * N
     desc = (f"fp64 brute-force oracle (oracle/chamfer_oracle.c, OpenMP) on {rx} X rows x {M} targets + {ry} Y rows "
             f"x {N} targets ({pairs:.3g} directed pairs, {dt:.1f} s) of the same workload; backward O(N+M) omitted")
-    return pairs / dt, threads, desc, dt
+    # single-core rate on a short sample (~1/8 of the budget), then the OpenMP default is restored
+    r1 = int(max(min_rows, min(B * N, (budget_s / 8) * (rate / max(threads, 1)) / M)))
+    t0 = time.perf_counter()
+    oracle.nn(X, Y, rows=np.linspace(0, B * N - 1, r1).astype(np.int64), nthreads=1)
+    one = r1 * M / max(time.perf_counter() - t0, 1e-6)
+    oracle.nn(X[:, :1], Y[:, :1], nthreads=threads)
+    return pairs / dt, threads, desc, dt, one
 
 
 def run_reference(args):
@@ -189,7 +206,7 @@ def run_reference(args):
     budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
     vals = []
     for k in range(args.warmup + args.steps):
-        v, cores, desc, dt = oracle_sample(X, Y, budget)
+        v, cores, desc, dt, one = oracle_sample(X, Y, budget)
         if k >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -200,7 +217,8 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": pairs / value * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "desc": c["desc"], "B": B, "N": N, "M": M, "tau": c["tau"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                         "value_1core": one, "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -607,8 +625,9 @@ def main():
     # ---------------------------------------------------------------- cpu baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, desc, dt = oracle_sample(X, Y, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        v, cores, desc, dt, one = oracle_sample(X, Y, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc, "value_1core": one,
+               "cpu_model": _cpu_model()}
 
     launches = cd.launch_count(_lib.CD_OP_STEP, B_local, N, M)
     if rank == 0:
