@@ -402,26 +402,19 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         blk[r] = -1;
         tie[r] = false;
     }
-    // box of this warp's 256 consecutive sorted rows (valid rows only)
-    float wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    // box of this lane's rows (valid rows only): a 32-target block is evaluated only if some lane of
+    // the warp may still improve (or tie) one of its rows
+    float llo[3] = {INFINITY, INFINITY, INFINITY}, lhi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int r = 0; r < kPrR / 2; ++r) {
         float v0, v1;
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             upk2(q == 0 ? qx[r] : (q == 1 ? qy[r] : qz[r]), v0, v1);
-            if (qbase + 2 * r < P) { wlo[q] = fminf(wlo[q], v0); whi[q] = fmaxf(whi[q], v0); }
-            if (qbase + 2 * r + 1 < P) { wlo[q] = fminf(wlo[q], v1); whi[q] = fmaxf(whi[q], v1); }
+            if (qbase + 2 * r < P) { llo[q] = fminf(llo[q], v0); lhi[q] = fmaxf(lhi[q], v0); }
+            if (qbase + 2 * r + 1 < P) { llo[q] = fminf(llo[q], v1); lhi[q] = fmaxf(lhi[q], v1); }
         }
     }
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            wlo[q] = fminf(wlo[q], __shfl_xor_sync(0xffffffffu, wlo[q], o));
-            whi[q] = fmaxf(whi[q], __shfl_xor_sync(0xffffffffu, whi[q], o));
-        }
-    float wmax = INFINITY;      // warp-uniform: max over the warp's rows of their current minimum
     float maxbest = INFINITY;   // CTA-uniform (read from shared memory after a barrier)
     unsigned long long next = cand[0];
     int k = 0;
@@ -437,8 +430,15 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         const float4* bb = smb[s];
         const int jt = t * kTile;
         for (int kb = 0; kb < kTile; kb += kBlockK) {
-            // warp-uniform skip: every pair of this block is farther than every row's minimum
-            if (box_lb(wlo, whi, bb[2 * (kb / kBlockK)], bb[2 * (kb / kBlockK) + 1]) > wmax) continue;
+            // skip unless some lane may improve or tie: LB(lane box, block) <= the lane's largest minimum
+            {
+                float lmax = -1.0f;   // no valid row: never needs a block
+#pragma unroll
+                for (int r = 0; r < kPrR; ++r)
+                    if (qbase + r < P) lmax = fmaxf(lmax, best[r]);
+                const bool need = box_lb(llo, lhi, bb[2 * (kb / kBlockK)], bb[2 * (kb / kBlockK) + 1]) <= lmax;
+                if (!__any_sync(0xffffffffu, need)) continue;
+            }
             float cur[kPrR];   // this block's minimum per row
 #pragma unroll
             for (int r = 0; r < kPrR; ++r) cur[r] = INFINITY;
@@ -484,7 +484,6 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         for (int r = 0; r < kPrR; ++r)
             if (qbase + r < P) m = max(m, __float_as_uint(best[r]));
         m = __reduce_max_sync(0xffffffffu, m);
-        wmax = __uint_as_float(m);
         if (lane == 0) s_wmax[warp] = m;
         __syncthreads();  // stage s consumed by every warp; s_wmax complete
         unsigned mm = s_wmax[0];

@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(256) tc_resolve_kernel(TcResolveArgs a) {
         const bool valid = e < L;
         const int dir = (valid && e >= L0) ? 1 : 0;
         const int64_t g = dir == 0 ? e : e - L0;
-        const int n = a.npts[dir], nT = a.npts[1 - dir];
+        const int n = a.npts[dir];
         const int b = valid ? (int)(g / n) : 0;
         const int i = valid ? (int)(g - (int64_t)b * n) : 0;
         float g1 = INFINITY, g2 = INFINITY, g3 = INFINITY;
