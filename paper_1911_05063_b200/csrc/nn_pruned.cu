@@ -328,6 +328,7 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
 struct PrunedArgs {
     const float4* sorted[2];
     const float4* bbox32[2];
+    const float4* tbox[2];    // 512-point tile boxes
     int npts[2], ppad[2];
     int qtiles[2];
     int64_t cand_off[2];
@@ -344,11 +345,18 @@ __device__ __forceinline__ float box_lb(const float wlo[3], const float whi[3], 
     return (gx * gx + gy * gy + gz * gz) * kLbScale;
 }
 
+#ifdef CD_PR_STATS
+__device__ unsigned long long g_pr_stats[4];
+#endif
 __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) {
     __shared__ __align__(128) float4 sm[kStages][kTile];
     __shared__ __align__(128) float4 smb[kStages][kBlocksPerTile * 2];   // the tile's 32-point block boxes
     __shared__ __align__(8) u64 full_bar[kStages];
     __shared__ unsigned s_wmax[kPrThreads / 32];
+#ifdef CD_PR_STATS
+    __shared__ int s_used;
+    if (threadIdx.x == 0) s_used = 0;
+#endif
 
     int u = blockIdx.x;
     const int b = blockIdx.y;
@@ -368,18 +376,9 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
     const int ncand = a.ccount[(int64_t)(dir == 0 ? 0 : (int64_t)gridDim.y * a.qtiles[0]) + (int64_t)b * a.qtiles[dir] + u];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    int issued = 0;  // thread 0 only
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
         fence_mbar_init();
-        const int pre = min(kStages, ncand);
-        for (int k = 0; k < pre; ++k) {
-            const int t = (int)(cand[k] & 0xffffffffull);
-            mbar_arrive_expect_tx(&full_bar[k], kTile * 16 + kBlocksPerTile * 32);
-            tma_load_1d(sm[k], T + (int64_t)t * kTile, kTile * 16, &full_bar[k]);
-            tma_load_1d(smb[k], TB + (int64_t)t * kBlocksPerTile * 2, kBlocksPerTile * 32, &full_bar[k]);
-        }
-        issued = pre;
     }
     __syncthreads();
 
@@ -402,8 +401,8 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         blk[r] = -1;
         tie[r] = false;
     }
-    // box of this lane's rows (valid rows only): a 32-target block is evaluated only if some lane of
-    // the warp may still improve (or tie) one of its rows
+    // box of this lane's rows (valid rows only): a tile is fetched, and a 32-target block inside it
+    // evaluated, only if some lane may still improve (or tie) one of its rows
     float llo[3] = {INFINITY, INFINITY, INFINITY}, lhi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int r = 0; r < kPrR / 2; ++r) {
@@ -415,17 +414,73 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
             if (qbase + 2 * r + 1 < P) { llo[q] = fminf(llo[q], v1); lhi[q] = fmaxf(lhi[q], v1); }
         }
     }
-    float maxbest = INFINITY;   // CTA-uniform (read from shared memory after a barrier)
-    unsigned long long next = cand[0];
-    int k = 0;
-    for (; k < ncand; ++k) {
-        const unsigned long long cur = next;
-        if (k + 1 < ncand) next = cand[k + 1];   // prefetch the next list entry
-        const float lb = __uint_as_float((unsigned)(cur >> 32));
-        if (lb > maxbest) break;               // every remaining tile is farther: done (uniform)
-        const int t = (int)(cur & 0xffffffffull);
-        const int s = k % kStages;
-        mbar_wait(&full_bar[s], (k / kStages) & 1);
+    auto lane_max = [&]() {
+        float lmax = -1.0f;   // no valid row: never needs anything
+#pragma unroll
+        for (int r = 0; r < kPrR; ++r)
+            if (qbase + r < P) lmax = fmaxf(lmax, best[r]);
+        return lmax;
+    };
+    const float4* __restrict__ TT = a.tbox[tc] + (int64_t)b * tnt * 2;
+    // next candidate tile that some thread still needs (list order = ascending LB of the query tile;
+    // the walk ends at the first LB above every row's minimum).  CTA-uniform; one barrier per
+    // candidate considered.
+    int pos = 0;
+    auto advance = [&]() -> int {
+        unsigned m = 0u;
+#pragma unroll
+        for (int r = 0; r < kPrR; ++r)
+            if (qbase + r < P) m = max(m, __float_as_uint(best[r]));
+        m = __reduce_max_sync(0xffffffffu, m);
+        if (lane == 0) s_wmax[warp] = m;
+        __syncthreads();
+        unsigned mm = s_wmax[0];
+#pragma unroll
+        for (int w = 1; w < kPrThreads / 32; ++w) mm = max(mm, s_wmax[w]);
+        const float maxbest = __uint_as_float(mm);
+        const float lmax = lane_max();
+        int found = -1;
+        while (pos < ncand) {
+            const unsigned long long e = cand[pos];
+            if (__uint_as_float((unsigned)(e >> 32)) > maxbest) {
+                pos = ncand;
+                break;
+            }
+            const int t = (int)(e & 0xffffffffull);
+            ++pos;
+            const bool need = box_lb(llo, lhi, TT[2 * t], TT[2 * t + 1]) <= lmax;
+            if (__syncthreads_or(need)) {
+                found = t;
+                break;
+            }
+        }
+        __syncthreads();   // s_wmax reuse
+        return found;
+    };
+    auto issue = [&](int t, int s) {
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], kTile * 16 + kBlocksPerTile * 32);
+            tma_load_1d(sm[s], T + (int64_t)t * kTile, kTile * 16, &full_bar[s]);
+            tma_load_1d(smb[s], TB + (int64_t)t * kBlocksPerTile * 2, kBlocksPerTile * 32, &full_bar[s]);
+        }
+    };
+    int tiles[kStages];
+    int tail = 0;
+#pragma unroll
+    for (int k = 0; k < kStages; ++k) {
+        const int t = advance();
+        tiles[k] = t;
+        if (t < 0) break;
+        issue(t, k);
+        ++tail;
+    }
+    for (int head = 0; head < tail; ++head) {
+        const int s = head % kStages;
+        int t = tiles[0];
+#pragma unroll
+        for (int q = 1; q < kStages; ++q) t = s == q ? tiles[q] : t;
+        mbar_wait(&full_bar[s], (head / kStages) & 1);
         const float4* tb = sm[s];
         const float4* bb = smb[s];
         const int jt = t * kTile;
@@ -438,6 +493,9 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
                     if (qbase + r < P) lmax = fmaxf(lmax, best[r]);
                 const bool need = box_lb(llo, lhi, bb[2 * (kb / kBlockK)], bb[2 * (kb / kBlockK) + 1]) <= lmax;
                 if (!__any_sync(0xffffffffu, need)) continue;
+#ifdef CD_PR_STATS
+                if (lane == 0) { atomicAdd(&g_pr_stats[1], 1ull); s_used = 1; }
+#endif
             }
             float cur[kPrR];   // this block's minimum per row
 #pragma unroll
@@ -478,34 +536,15 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
                 best[r] = fminf(best[r], cur[r]);
             }
         }
-        // CTA maximum of the rows' current minima (valid rows only; d >= 0 so bits order = float order)
-        unsigned m = 0u;
+        __syncthreads();   // stage s consumed by every warp
+        const int tn = advance();
+        if (tn >= 0) {
 #pragma unroll
-        for (int r = 0; r < kPrR; ++r)
-            if (qbase + r < P) m = max(m, __float_as_uint(best[r]));
-        m = __reduce_max_sync(0xffffffffu, m);
-        if (lane == 0) s_wmax[warp] = m;
-        __syncthreads();  // stage s consumed by every warp; s_wmax complete
-        unsigned mm = s_wmax[0];
-#pragma unroll
-        for (int w = 1; w < kPrThreads / 32; ++w) mm = max(mm, s_wmax[w]);
-        maxbest = __uint_as_float(mm);
-        if (threadIdx.x == 0 && issued == k + kStages && issued < ncand) {
-            const unsigned long long e = cand[issued];
-            if (__uint_as_float((unsigned)(e >> 32)) <= maxbest) {
-                const int tn = (int)(e & 0xffffffffull);
-                fence_proxy_async_smem();
-                mbar_arrive_expect_tx(&full_bar[s], kTile * 16 + kBlocksPerTile * 32);
-                tma_load_1d(sm[s], T + (int64_t)tn * kTile, kTile * 16, &full_bar[s]);
-                tma_load_1d(smb[s], TB + (int64_t)tn * kBlocksPerTile * 2, kBlocksPerTile * 32, &full_bar[s]);
-                ++issued;
-            }
+            for (int q = 0; q < kStages; ++q) tiles[q] = s == q ? tn : tiles[q];
+            issue(tn, s);
+            ++tail;
         }
-        __syncthreads();  // s_wmax may be rewritten by the next tile only after everyone read it
     }
-    // drain copies that were issued but not consumed (no shared-memory writes after exit)
-    if (threadIdx.x == 0)
-        for (int kk = k; kk < issued; ++kk) mbar_wait(&full_bar[kk % kStages], (kk / kStages) & 1);
 
     const int64_t rowbase = (int64_t)b * P;
 #pragma unroll
@@ -834,6 +873,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         for (int c = 0; c < 2; ++c) {
             a.sorted[c] = sorted[c];
             a.bbox32[c] = box32[c];
+            a.tbox[c] = box[c];
             a.npts[c] = p.npts[c];
             a.ppad[c] = p.ppad[c];
             a.qtiles[c] = p.qtiles[c];
@@ -876,6 +916,11 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         cudaStreamSynchronize(st);
         cudaMemcpy(&h, a.fb_count, 4, cudaMemcpyDeviceToHost);
         printf("pruned tie rows: %u of %lld\n", h, (long long)p.L);
+        unsigned long long st3[4];
+        cudaMemcpyFromSymbol(st3, g_pr_stats, sizeof(st3));
+        printf("tiles fetched %llu, tiles with >= 1 evaluated block %llu, warp-blocks evaluated %llu\n", st3[0], st3[2], st3[1]);
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_pr_stats, z, sizeof(z));
 #endif
     }
     if (o.partials) {
