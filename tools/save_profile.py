@@ -49,6 +49,7 @@ def full(tag, rnd, cfg):
     txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep], capture_output=True,
                          text=True).stdout
     name = txt.splitlines()[0].replace("## ", "").split("(")[0] if txt else "kernel"
+    name = name.replace("void ", "").split("<")[0].split("::")[-1]   # template / namespace decorations
     with open(os.path.join(P, f"{rnd}_ncu_full_{name}_{cfg}.txt"), "w") as f:
         f.write(f"# ncu --set full --clock-control none --import-source on -k regex:{name} -s 1 -c 1 (bench.py --config {cfg})\n")
         f.write(txt)
