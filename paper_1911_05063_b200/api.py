@@ -58,7 +58,12 @@ def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=
     """cd_forward: both NN directions.  Returns (d_xy, idx_xy, d_yx, idx_yx, partials[B,4] fp64).
 
     q_slice=(q0,q1) / r_slice=(r0,r1) restrict the query rows (query sharding); outputs are
-    slice-sized.  algorithm="pruned" uses cd_forward_pruned (exact, culled; full problems only)."""
+    slice-sized.  algorithm="pruned" uses cd_forward_pruned (exact, culled; full problems only);
+    "auto" picks it for full problems with at least 8192 points per cloud (its results equal the brute
+    force's bit for bit, R3'), the brute force otherwise."""
+    if algorithm == "auto":
+        full = q_slice is None and r_slice is None
+        algorithm = "pruned" if full and min(x.shape[1], y.shape[1]) >= 8192 else "brute"
     if algorithm == "pruned":
         if q_slice is not None or r_slice is not None:
             raise ValueError("the pruned forward takes the full problem")
@@ -287,8 +292,8 @@ class ChamferFunction(torch.autograd.Function):
     """loss = mean_b [w1 mean_i d_xy + w2 mean_j d_yx] with the argmin held fixed in backward."""
 
     @staticmethod
-    def forward(ctx, x, y, w1, w2):
-        d_xy, i_xy, d_yx, i_yx, part = forward(x, y)
+    def forward(ctx, x, y, w1, w2, algorithm="brute"):
+        d_xy, i_xy, d_yx, i_yx, part = forward(x, y, algorithm=algorithm)
         _, loss, _, _, _ = finalize(part, x.shape[1], y.shape[1], w1, w2)
         ctx.save_for_backward(x, y, i_xy, i_yx)
         ctx.w = (w1, w2)
@@ -304,12 +309,12 @@ class ChamferFunction(torch.autograd.Function):
         g = (go * (w1 / (B * N))).expand(B, N)
         h = (go * (w2 / (B * M))).expand(B, M)
         gx, gy = backward(x, y, i_xy, i_yx, g, h)
-        return gx, gy, None, None
+        return gx, gy, None, None, None
 
 
-def chamfer(x: torch.Tensor, y: torch.Tensor, w1: float = 1.0, w2: float = 1.0) -> torch.Tensor:
+def chamfer(x: torch.Tensor, y: torch.Tensor, w1: float = 1.0, w2: float = 1.0, algorithm: str = "brute") -> torch.Tensor:
     """Differentiable Chamfer loss (R1)."""
-    return ChamferFunction.apply(x, y, w1, w2)
+    return ChamferFunction.apply(x, y, w1, w2, algorithm)
 
 
 def launch_count(op: int, B: int, N: int, M: int) -> int:

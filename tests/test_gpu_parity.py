@@ -451,3 +451,25 @@ def test_step_host_overlapped_equals_step_host(cd):
         torch.cuda.synchronize()
         assert float(loss[0]) == float(ref["loss"][0])
         np.testing.assert_array_equal(fs.numpy(), ref["fscore"].numpy())
+
+
+def test_auto_algorithm_and_pruned_autograd(cd):
+    """algorithm="auto" (pruned for >= 8192-point clouds) and the autograd loss through the pruned
+    forward equal the brute force bit for bit (the pruned results are identical, R3')."""
+    X, Y = synth.shape_pair(2, 9000, 8500, config_index=81)
+    x = torch.from_numpy(X).cuda()
+    y = torch.from_numpy(Y).cuda()
+    a = [t.cpu().numpy() for t in cd.forward(x, y, tau=0.01, algorithm="auto")]
+    b = [t.cpu().numpy() for t in cd.forward(x, y, tau=0.01)]
+    for p, q in zip(a[:4], b[:4]):
+        np.testing.assert_array_equal(p, q)
+    grads = []
+    for algo in ("brute", "pruned"):
+        xg = x.clone().requires_grad_(True)
+        yg = y.clone().requires_grad_(True)
+        loss = cd.chamfer(xg, yg, algorithm=algo)
+        loss.backward()
+        grads.append((loss.item(), xg.grad.cpu().numpy(), yg.grad.cpu().numpy()))
+    assert abs(grads[0][0] - grads[1][0]) <= 1e-12 * abs(grads[0][0])
+    np.testing.assert_array_equal(grads[0][1], grads[1][1])
+    np.testing.assert_array_equal(grads[0][2], grads[1][2])
