@@ -53,7 +53,7 @@ typedef enum {
     CD_OK = 0,
     CD_ERR_INVALID_VALUE = 1,     /* null pointer, B/N/M < 1 (empty cloud), tau < 0, bad slice */
     CD_ERR_MISALIGNED = 2,        /* cloud base pointer not 4-byte aligned / workspace not 256-B aligned */
-    CD_ERR_TOO_LARGE = 3,         /* B*N or B*M or B*(N+M) exceeds 2^31-1, or workspace too small */
+    CD_ERR_TOO_LARGE = 3,         /* B*N or B*M or B*(N+M) exceeds 2^31-1, B > 65535, or workspace too small */
     CD_ERR_UNSUPPORTED_DEVICE = 4,/* current device is not sm_100 */
     CD_ERR_CUDA = 5               /* a CUDA runtime call failed; see cd_last_error_string() */
 } cd_status;

@@ -40,12 +40,15 @@ cd_status cuda_status(cudaError_t e, const char* where) {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+constexpr int kMaxBatch = 65535;   // batch elements map to gridDim.y
+
 cd_status check_sizes(int B, int N, int M) {
     if (B < 1 || N < 1 || M < 1)
         return fail(CD_ERR_INVALID_VALUE, "B, N, M must be >= 1 (empty cloud, SPEC.md:440-442): B=%d N=%d M=%d", B,
                     N, M);
     const long long L = (long long)B * ((long long)N + (long long)M);
     if (L > 0x7fffffffLL) return fail(CD_ERR_TOO_LARGE, "B*(N+M) = %lld exceeds 2^31-1", L);
+    if (B > kMaxBatch) return fail(CD_ERR_TOO_LARGE, "B = %d exceeds %d (one grid row per batch element)", B, kMaxBatch);
     return CD_OK;
 }
 
@@ -314,6 +317,7 @@ cd_status cd_sample_mesh(const float* verts, const int32_t* faces, int B, int Nv
         return fail(CD_ERR_INVALID_VALUE, "need B >= 1, Nv >= 3, Nf >= 1, N >= 1 (got %d %d %d %d)", B, Nv, Nf, N);
     if ((long long)B * N * 3 > 0x7fffffffLL || (long long)B * Nv > 0x7fffffffLL)
         return fail(CD_ERR_TOO_LARGE, "B*N*3 or B*Nv exceeds 2^31-1");
+    if (B > kMaxBatch) return fail(CD_ERR_TOO_LARGE, "B = %d exceeds %d (one grid row per batch element)", B, kMaxBatch);
     if (!verts || !faces || !r_face || !r_bary || !points || !face_idx || !workspace)
         return fail(CD_ERR_INVALID_VALUE, "null pointer argument");
     if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
@@ -365,6 +369,7 @@ static cd_status check_p2s_sizes(int B, int N, int Nv, int Nf) {
         return fail(CD_ERR_INVALID_VALUE, "need B, N, Nf >= 1 and Nv >= 3 (got %d %d %d %d)", B, N, Nv, Nf);
     if ((long long)B * N * 3 > 0x7fffffffLL || (long long)B * Nv > 0x7fffffffLL || (long long)B * Nf * 24 > 0x7fffffffLL)
         return fail(CD_ERR_TOO_LARGE, "problem too large for 32-bit indexing");
+    if (B > kMaxBatch) return fail(CD_ERR_TOO_LARGE, "B = %d exceeds %d (one grid row per batch element)", B, kMaxBatch);
     return CD_OK;
 }
 

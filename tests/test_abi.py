@@ -82,6 +82,8 @@ def test_forward_validation_before_launch(lib):
     assert _forward(lib, ws=255) == 2    # misaligned workspace
     assert _forward(lib, wsb=16) == 3    # workspace too small
     assert _forward(lib, B=1 << 20, N=1 << 12, M=1 << 12, q=(0, 1 << 12), r=(0, 1 << 12)) == 3
+    assert _forward(lib, B=65536, N=4, M=4, q=(0, 4), r=(0, 4)) == 3   # batch elements map to gridDim.y
+    assert b"65535" in lib.cd_last_error_string()
 
 
 def test_backward_and_fscore_validation(lib):
