@@ -1,0 +1,46 @@
+#!/usr/bin/env python
+"""Randomised cross-check of the culled point-to-surface forward against the brute-force kernel:
+the same face (then bit-identical d / closest / bary) or, on exact fp32 ties, a face at the same
+distance to within the R24 band.  python tools/stress_p2s.py [draws] [seed]"""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_1911_05063_b200 import api as cd, synth
+import oracle
+
+draws = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 5)
+bad = 0
+for k in range(draws):
+    B = int(rng.integers(1, 4))
+    sub = int(rng.integers(0, 5))
+    N = int(rng.choice([1, 5, 100, 1000, 4097, 10000]))
+    V, F = synth.mesh_batch(B, subdiv=sub, config_index=3000 + k)
+    kind = rng.choice(["near", "on", "far", "shape", "scaled"])
+    if kind in ("near", "on"):
+        rf, rb = synth.sampling_randoms(B, N, seed=4000 + k)
+        P, _, _, _ = oracle.sample_mesh(V, F, rf, rb)
+        if kind == "near":
+            P = P + rng.normal(scale=10 ** rng.uniform(-4, -1), size=P.shape)
+    elif kind == "far":
+        P = rng.uniform(-3, 3, size=(B, N, 3))
+    else:
+        P = synth.shape_pair(B, N, 8, config_index=5000 + k)[0]
+    P = P.astype(np.float32)
+    if kind == "scaled":
+        s = float(2.0 ** rng.integers(-6, 7))
+        P, V = (P * s + 7.0).astype(np.float32), (V * s + 7.0).astype(np.float32)
+    p, v, f = torch.from_numpy(np.ascontiguousarray(P)).cuda(), torch.from_numpy(V).cuda(), torch.from_numpy(F).cuda()
+    ob = [t.cpu().numpy() for t in cd.p2s_forward(p, v, f)]
+    op = [t.cpu().numpy() for t in cd.p2s_forward(p, v, f, algorithm="pruned")]
+    same = op[1] == ob[1]
+    R = max(np.abs(P).max(), np.abs(V).max())
+    band = 2.0 ** -22 * R * R
+    ok = (np.array_equal(op[0][same], ob[0][same]) and np.array_equal(op[2][same], ob[2][same])
+          and np.all(np.abs(op[0][~same].astype(np.float64) - ob[0][~same]) <= 1e-5 * np.abs(ob[0][~same]) + band))
+    if not ok:
+        bad += 1
+        print(f"MISMATCH draw {k} {kind} B={B} sub={sub} N={N}", flush=True)
+print(f"stress_p2s: {draws} draws, {bad} failures")
