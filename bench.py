@@ -351,9 +351,20 @@ def measure_extras(cd, torch, dev, flush, args, K_extra):
         return cd.sample_mesh_backward(f, fi, ba, Nv, gx)
 
     ms = _timed(torch, pipe_step, flush, K_extra)
+
+    def pipe_step_pruned():
+        pts, fi, ba = cd.sample_mesh(v, f, rft, rbt)
+        d_xy, i_xy, d_yx, i_yx, part = cd.forward(pts, y, tau=0.01, algorithm="pruned")
+        _, loss, F1, _, _ = cd.finalize(part, N, M)
+        gx, _ = cd.backward(pts, y, i_xy, i_yx, g_scalar=1.0 / (B * N), h_scalar=1.0 / (B * M))
+        return cd.sample_mesh_backward(f, fi, ba, Nv, gx)
+
+    ms_pr = _timed(torch, pipe_step_pruned, flush, K_extra)
     out["next4_sample_chamfer"] = {
         "workload": f"B={B} meshes (icosphere-5) -> N={N} samples -> Chamfer + F@0.01 vs M={M} -> grad to vertices",
         "ms_per_step": ms, "directed_pairs_per_s": 2 * B * N * M / (ms * 1e-3),
+        "pruned_forward": {"ms_per_step": ms_pr, "directed_pairs_per_s_effective": 2 * B * N * M / (ms_pr * 1e-3),
+                           "note": "same pipeline through cd_forward_pruned (results identical to the brute force)"},
     }
     return out
 
