@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* _
 // Phase 3: the tile is re-ordered by digit in shared memory, then written out so that consecutive
 // threads write consecutive addresses of each digit's run (coalesced stores).
 // Dynamic shared memory: (kSortWarps + 2) * D + 2 * kSortTile words.
-__global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB) radix_scatter_kernel(
+__global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB : 2) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int D, int ntiles,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout) {
@@ -176,12 +176,19 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB) radix_scatter_kern
     uint32_t kk[kSortItems], vv[kSortItems], rk[kSortItems];
     uint32_t* my = wcnt + warp * D;
     // all 16 loads first (independent: full memory-level parallelism), then the ranking rounds
+    // all loads issued before the ranking rounds, as volatile loads: the compiler would otherwise
+    // re-issue (rematerialise) each read-only load at its first use, exposing one memory latency per round
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
-        const int64_t e = wbase + k * 32 + lane;
-        const bool valid = e < L;
-        kk[k] = valid ? kin[e] : 0u;
-        vv[k] = valid ? vin[e] : 0u;
+        const int64_t e = min(wbase + k * 32 + lane, L - 1);
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(kk[k]) : "l"(kin + e));
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(vv[k]) : "l"(vin + e));
+    }
+    {
+        uint32_t all = 0;
+#pragma unroll
+        for (int k = 0; k < kSortItems; ++k) all ^= kk[k];
+        asm volatile("" ::"r"(all));   // every key has arrived before the first ranking round
     }
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
