@@ -85,10 +85,16 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t
     for (int d = threadIdx.x; d < D; d += kSortThreads) hist[d] = 0;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * kSortTile;
-#pragma unroll 4
+    uint32_t kk[kSortItems];
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {   // all loads in flight before the shared-memory adds
+        const int64_t e = min(base + (int64_t)k * kSortThreads + threadIdx.x, L - 1);
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(kk[k]) : "l"(keys + e));
+    }
+#pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
         const int64_t e = base + (int64_t)k * kSortThreads + threadIdx.x;
-        if (e < L) atomicAdd(&hist[(keys[e] >> shift) & (D - 1)], 1u);  // integer adds: order-free
+        if (e < L) atomicAdd(&hist[(kk[k] >> shift) & (D - 1)], 1u);  // integer adds: order-free
     }
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
