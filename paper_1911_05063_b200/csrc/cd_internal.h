@@ -161,4 +161,22 @@ inline void record_profile_event(cudaEvent_t ev, cudaStream_t st) {
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per (device, kernel) on the
+// calling thread (the attribute is per device: a thread that switches devices sets it again).
+inline void ensure_smem_attr(const void* func, int bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static thread_local const void* done_fn[32];
+    static thread_local int done_dev[32];
+    static thread_local int ndone = 0;
+    for (int i = 0; i < ndone; ++i)
+        if (done_fn[i] == func && done_dev[i] == dev) return;
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (ndone < 32) {
+        done_fn[ndone] = func;
+        done_dev[ndone] = dev;
+        ++ndone;
+    }
+}
+
 }  // namespace cdk

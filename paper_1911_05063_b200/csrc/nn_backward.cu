@@ -375,12 +375,7 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits,
     radix_sort_plan(L, nbits, npasses, digit_bits, ntiles);
     const int D = 1 << digit_bits;
     const size_t scatter_smem = ((size_t)(kSortWarps + 2) * D + 2 * kSortTile) * 4;
-    static thread_local bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile) * 4);
-        attr_set = true;
-    }
+    ensure_smem_attr((const void*)radix_scatter_kernel, ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile) * 4);
     int cur = 0;
     for (int pass = 0; pass < npasses; ++pass) {
         const int shift = pass * digit_bits;

@@ -855,11 +855,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         int npow = 1;
         while (npow < std::max(p.ttiles[0], p.ttiles[1])) npow <<= 1;
         const size_t smem = (size_t)npow * 8;
-        static thread_local bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrMaxTiles * 8);
-            attr = true;
-        }
+        ensure_smem_attr((const void*)candidates_kernel, kPrMaxTiles * 8);
         candidates_kernel<<<p.B * (p.qtiles[0] + p.qtiles[1]), 256, smem, st>>>(a);
     }
     float* best_d[2];

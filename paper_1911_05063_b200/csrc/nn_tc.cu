@@ -839,11 +839,7 @@ cudaError_t launch_tc(const TcPlan& p, const float* x, const float* y, const Fwd
         a.rowsum = rowsum;
         a.colsum = colsum;
         const size_t smem = (size_t)(kTcSub + kTcStages) * kTcTileBytes + 256 + (5 * kTcSub * 2 * kTcRows + 5 * kTcRows) * 4;
-        static thread_local bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(nn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        ensure_smem_attr((const void*)nn_tc_kernel, (int)smem);
         if (g_prof_start) record_profile_event(g_prof_start, st);
         nn_tc_kernel<<<dim3(p.qblocks * p.splits, p.B), kTcThreads, smem, st>>>(a);
         if (g_prof_stop) record_profile_event(g_prof_stop, st);

@@ -701,11 +701,7 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
         PsCandArgs a{qbox, fbox, p.qtiles, p.ftiles, cand};
         int npow = 1;
         while (npow < p.ftiles) npow <<= 1;
-        static thread_local bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(ps_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPsMaxTiles * 8);
-            attr = true;
-        }
+        ensure_smem_attr((const void*)ps_candidates_kernel, kPsMaxTiles * 8);
         ps_candidates_kernel<<<B * p.qtiles, 256, (size_t)npow * 8, st>>>(a);
     }
     {
