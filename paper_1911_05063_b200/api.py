@@ -26,18 +26,24 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def workspace(op: int, B: int, N: int, M: int, device) -> torch.Tensor:
-    """Workspace bytes from cd_workspace_size, cached per (device, op, sizes)."""
-    lib = _lib.load()
-    n = int(lib.cd_workspace_size(op, B, N, M))
-    if n == 0:
-        raise _lib.CdError(1, f"invalid sizes B={B} N={N} M={M}")
-    key = (str(device), op, B, N, M)
+def _cached_ws(kind: str, op: int, n: int, device) -> torch.Tensor:
+    """One workspace per (device, current stream, kind, op), grown to the largest size requested:
+    calls on one stream are ordered, so they may share it; calls on different streams never do."""
+    device = torch.device(device)
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream, kind, op)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < n:
         buf = torch.empty(n, dtype=torch.uint8, device=device)  # caching allocator: >= 512-B aligned
         _ws_cache[key] = buf
     return buf
+
+
+def workspace(op: int, B: int, N: int, M: int, device) -> torch.Tensor:
+    """Workspace bytes from cd_workspace_size (see _cached_ws)."""
+    n = int(_lib.load().cd_workspace_size(op, B, N, M))
+    if n == 0:
+        raise _lib.CdError(1, f"invalid sizes B={B} N={N} M={M}")
+    return _cached_ws("cd", op, n, device)
 
 
 def _check_cloud(t, name):
@@ -252,7 +258,11 @@ class HostStepper:
         self.B, self.N, self.M, self.tau, self.w1, self.w2 = B, N, M, tau, w1, w2
         self.nchunks = nchunks or (4 if B >= 8 else 1)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
-        self.ws = workspace(_lib.CD_OP_STEP, B, N, M, self.device)
+        # a private workspace: its staging area is written by this stepper's copy stream
+        n = int(_lib.load().cd_workspace_size(_lib.CD_OP_STEP, B, N, M))
+        if n == 0:
+            raise _lib.CdError(1, f"invalid sizes B={B} N={N} M={M}")
+        self.ws = torch.empty(n, dtype=torch.uint8, device=self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.events = [torch.cuda.Event() for _ in range(self.nchunks + 1)]
         for ev in self.events:       # materialise the cudaEvent handles
@@ -334,12 +344,7 @@ def _sample_ws(op, B, Nv, Nf, N, device):
     n = int(lib.cd_sample_workspace_size(op, B, Nv, Nf, N))
     if n == 0:
         raise _lib.CdError(1, f"invalid sizes B={B} Nv={Nv} Nf={Nf} N={N}")
-    key = (str(device), op, B, Nv, Nf, N)
-    buf = _ws_cache.get(key)
-    if buf is None or buf.numel() < n:
-        buf = torch.empty(n, dtype=torch.uint8, device=device)
-        _ws_cache[key] = buf
-    return buf
+    return _cached_ws("sample", op, n, device)
 
 
 def sample_mesh(verts: torch.Tensor, faces: torch.Tensor, r_face: torch.Tensor, r_bary: torch.Tensor):
@@ -405,12 +410,7 @@ def _p2s_ws(op, B, N, Nv, Nf, device):
     n = int(_lib.load().cd_p2s_workspace_size(op, B, N, Nv, Nf))
     if n == 0:
         raise _lib.CdError(1, f"invalid sizes B={B} N={N} Nv={Nv} Nf={Nf}")
-    key = (str(device), op, B, N, Nv, Nf)
-    buf = _ws_cache.get(key)
-    if buf is None or buf.numel() < n:
-        buf = torch.empty(n, dtype=torch.uint8, device=device)
-        _ws_cache[key] = buf
-    return buf
+    return _cached_ws("p2s", op, n, device)
 
 
 def p2s_forward(points: torch.Tensor, verts: torch.Tensor, faces: torch.Tensor, algorithm: str = "brute"):
