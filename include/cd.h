@@ -104,9 +104,10 @@ CD_API cd_status cd_forward(const float* x, const float* y, int B, int N, int M,
  * lowest row group.  cd_forward_cols then turns reduced keys into d_yx / idx_yx for Y rows [r0, r1)
  * (re-evaluating the winning group's 16 rows with the same fp32 ops, lowest index).
  *   cd_forward_rows: d_xy, idx_xy [B x (q1-q0)]; colkeys [B x M] (written); partials [B x 4] (may be
- *     NULL): writes columns 0 and 2 only (sum d_xy over the slice, hits_xy).  Requires q0 < q1.
+ *     NULL): writes columns 0 and 2 only (sum d_xy over the slice, hits_xy).  An empty slice
+ *     (q0 == q1, e.g. more ranks than rows) is valid: keys = identity, partials 0.
  *   cd_forward_cols: colkeys [B x M] (read); d_yx, idx_yx [B x (r1-r0)]; partials: writes columns 1
- *     and 3 only.  Requires r0 < r1.
+ *     and 3 only.  An empty slice (r0 == r1) is valid and resolves nothing.
  * Results are bit-identical to cd_forward on the full problem.
  */
 CD_API cd_status cd_forward_rows(const float* x, const float* y, int B, int N, int M, int q0, int q1,

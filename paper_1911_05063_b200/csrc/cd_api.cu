@@ -224,8 +224,8 @@ cd_status cd_forward_rows(const float* x, const float* y, int B, int N, int M, i
     cd_status s = check_sizes(B, N, M);
     if (s != CD_OK) return s;
     if (!x || !y || !workspace || !colkeys) return fail(CD_ERR_INVALID_VALUE, "null x, y, colkeys or workspace");
-    if (q0 < 0 || q1 <= q0 || q1 > N) return fail(CD_ERR_INVALID_VALUE, "bad row slice [%d,%d) of N=%d", q0, q1, N);
-    if (!d_xy || !idx_xy) return fail(CD_ERR_INVALID_VALUE, "null d_xy / idx_xy");
+    if (q0 < 0 || q1 < q0 || q1 > N) return fail(CD_ERR_INVALID_VALUE, "bad row slice [%d,%d) of N=%d", q0, q1, N);
+    if (q1 > q0 && (!d_xy || !idx_xy)) return fail(CD_ERR_INVALID_VALUE, "null d_xy / idx_xy");
     if (tau != tau) return fail(CD_ERR_INVALID_VALUE, "tau is NaN");
     if (!aligned(x, 4) || !aligned(y, 4) || !aligned(colkeys, 8))
         return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte and colkeys 8-byte aligned");
@@ -255,8 +255,8 @@ cd_status cd_forward_cols(const float* x, const float* y, int B, int N, int M, c
     cd_status s = check_sizes(B, N, M);
     if (s != CD_OK) return s;
     if (!x || !y || !workspace || !colkeys) return fail(CD_ERR_INVALID_VALUE, "null x, y, colkeys or workspace");
-    if (r0 < 0 || r1 <= r0 || r1 > M) return fail(CD_ERR_INVALID_VALUE, "bad column slice [%d,%d) of M=%d", r0, r1, M);
-    if (!d_yx || !idx_yx) return fail(CD_ERR_INVALID_VALUE, "null d_yx / idx_yx");
+    if (r0 < 0 || r1 < r0 || r1 > M) return fail(CD_ERR_INVALID_VALUE, "bad column slice [%d,%d) of M=%d", r0, r1, M);
+    if (r1 > r0 && (!d_yx || !idx_yx)) return fail(CD_ERR_INVALID_VALUE, "null d_yx / idx_yx");
     if (tau != tau) return fail(CD_ERR_INVALID_VALUE, "tau is NaN");
     if (!aligned(x, 4) || !aligned(y, 4) || !aligned(colkeys, 8))
         return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte and colkeys 8-byte aligned");

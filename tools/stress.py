@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Randomised cross-check of every forward path on one GPU: fused (default), per-direction, pruned and
-tensor-core forwards must agree bit for bit (d, idx, hit counts) on random shapes / distributions,
-and the backward must be deterministic.  python tools/stress.py [draws] [seed]"""
+"""Randomised cross-check of every forward path on one GPU: fused (default), per-direction, pruned,
+tensor-core and query-sharded (rows / MIN of column keys / columns, emulated) forwards must agree bit
+for bit (d, idx, hit counts) on random shapes / distributions, and the backward must be
+deterministic.  python tools/stress.py [draws] [seed]"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -52,6 +53,27 @@ for k in range(draws):
         if not ok:
             bad += 1
             print(f"MISMATCH draw {k} {kind} B={B} N={N} M={M} tau={tau} path={name}", flush=True)
+    # query sharding emulated on one GPU: rows per "rank", element-wise MIN of the column keys,
+    # columns per "rank" -> the 1-GPU per-point results
+    world = int(rng.integers(2, 9))
+    keys = None
+    drs, irs, dcs, ics = [], [], [], []
+    for r in range(world):
+        q = ((N * r) // world, (N * (r + 1)) // world)
+        d_, i_, kk, _ = cd.forward_rows(x, y, q, tau=tau)
+        drs.append(d_)
+        irs.append(i_)
+        keys = kk if keys is None else torch.minimum(keys, kk)
+    for r in range(world):
+        rr = ((M * r) // world, (M * (r + 1)) // world)
+        d_, i_, _ = cd.forward_cols(x, y, keys, rr, tau=tau)
+        dcs.append(d_)
+        ics.append(i_)
+    sh = [torch.cat(t, 1).cpu().numpy() for t in (drs, irs, dcs, ics)]
+    if not all(np.array_equal(a.view(np.uint32) if a.dtype == np.float32 else a,
+                              b.view(np.uint32) if b.dtype == np.float32 else b) for a, b in zip(sh, ref[:4])):
+        bad += 1
+        print(f"MISMATCH draw {k} query-sharded x{world}", flush=True)
     g1 = cd.backward(x, y, torch.from_numpy(ref[1]).cuda(), torch.from_numpy(ref[3]).cuda(), g_scalar=0.5, h_scalar=0.25)
     g2 = cd.backward(x, y, torch.from_numpy(ref[1]).cuda(), torch.from_numpy(ref[3]).cuda(), g_scalar=0.5, h_scalar=0.25)
     if not all(torch.equal(a, b) for a, b in zip(g1, g2)):
