@@ -214,3 +214,18 @@ def test_p2s_pruned_autograd(cd):
     gp, gb = p.grad.cpu().numpy(), p2.grad.cpu().numpy()
     assert np.quantile(np.abs(gp - gb) / (np.abs(gb) + 1e-9), 0.99) < 1e-6
     assert np.linalg.norm(v.grad.cpu().numpy() - v2.grad.cpu().numpy()) <= 1e-4 * np.linalg.norm(v2.grad.cpu().numpy())
+
+
+def test_p2s_degenerate_faces(cd):
+    """Zero-area faces (a repeated vertex): the brute-force and culled kernels still pass the oracle
+    gate (a degenerate face is a segment; its 'inside' test never fires, R24)."""
+    B, N = 2, 3000
+    V, F = synth.mesh_batch(B, subdiv=3, config_index=137)
+    F = F.copy()
+    sel = np.random.default_rng(14).choice(len(F), size=len(F) // 8, replace=False)
+    F[sel, 2] = F[sel, 1]
+    P = synth.shape_pair(B, N, 8, config_index=138)[0]
+    for algo in ("brute", "pruned"):
+        out = cd.p2s_forward(_t(P), _t(V), _t(F), algorithm=algo)
+        torch.cuda.synchronize()
+        _gate(P, V, F, out)

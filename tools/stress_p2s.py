@@ -18,6 +18,10 @@ for k in range(draws):
     sub = int(rng.integers(0, 5))
     N = int(rng.choice([1, 5, 100, 1000, 4097, 10000]))
     V, F = synth.mesh_batch(B, subdiv=sub, config_index=3000 + k)
+    if rng.random() < 0.3:   # some degenerate faces: a repeated vertex (zero area) or collinear corners
+        F = F.copy()
+        bad_f = rng.choice(len(F), size=max(1, len(F) // 10), replace=False)
+        F[bad_f, 2] = F[bad_f, 1]
     kind = rng.choice(["near", "on", "far", "shape", "scaled"])
     if kind in ("near", "on"):
         rf, rb = synth.sampling_randoms(B, N, seed=4000 + k)
