@@ -9,8 +9,8 @@
 //                      radix_hist_kernel   per-tile digit histograms (shared-memory integer adds)
 //                      radix_rowscan_kernel exclusive scan of each digit's row of tile counts (the
 //                                          digit bases are scanned inside the scatter kernel)
-//                      radix_scatter_kernel stable in-tile ranks (warp match + per-warp counts in
-//                                          element order) -> scatter.  Stability keeps ascending
+//                      radix_scatter_kernel stable in-tile ranks (warp ballot multisplit + per-warp
+//                                          counts in element order) -> scatter.  Stability keeps ascending
 //                                          source rows inside every key segment.
 //   offsets_kernel   segment offsets from the sorted keys (disjoint gap fills, no atomics).
 //   grad_kernel      one thread per output point: own term 2 g (p - partner) then the segment's
@@ -33,6 +33,9 @@ constexpr int kSortWarps = kSortThreads / 32;
 #endif
 constexpr int kSortItems = CD_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;  // elements per tile (kSortItems * 32 per warp)
+#ifndef CD_SORT_BALLOT
+#define CD_SORT_BALLOT 1
+#endif
 #ifndef CD_SORT_MAXBITS
 #define CD_SORT_MAXBITS 11
 #endif
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* _
 
 // Stable scatter of one tile.  Warp w owns elements [w*512, (w+1)*512) of the tile (16 rounds of
 // 32), so tile order = (warp, round, lane).  Phase 1: per-warp digit counters in shared memory give
-// every element its rank among equal digits of its warp (warp match; only the warp's own counter row
+// every element its rank among equal digits of its warp (warp ballot multisplit; only the warp's own counter row
 // is touched, no block barrier per round).  Phase 2: per digit, the tile-local start (exclusive scan
 // of the tile's digit counts) plus the prefix over the warps; delta[d] = global base - local start.
 // Phase 3: the tile is re-ordered by digit in shared memory, then written out so that consecutive
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
     __shared__ uint32_t warp_tot[kSortWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    const int dbits = __ffs(D) - 1;
     const int per = (D + kSortThreads - 1) / kSortThreads;   // digits owned by this thread in the scans
     const int d0 = threadIdx.x * per;
     for (int i = threadIdx.x; i < kSortWarps * D; i += kSortThreads) wcnt[i] = 0;
@@ -201,7 +205,21 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
         const int64_t e = wbase + k * 32 + lane;
         const bool valid = e < L;
         const int digit = valid ? (int)((kk[k] >> shift) & (D - 1)) : D;  // D: sentinel group
+#if CD_SORT_BALLOT
+        // warp multisplit: the lanes with an equal digit = AND over the digit bits (and validity) of
+        // the matching ballot or its complement.  VOTE issues at ALU rate; MATCH.ANY is a slow,
+        // long-latency op (ncu: the match results were the top short-scoreboard stall, c5 scatter
+        // 117 -> 100 us with ballots)
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+        if (!valid) peers = ~peers;
+        for (int b = 0; b < dbits; ++b) {
+            const bool bit = (digit >> b) & 1;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
+#else
         const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+#endif
         const uint32_t before = valid ? my[digit] : 0u;
         rk[k] = before + __popc(peers & lt_mask);
         __syncwarp();
