@@ -128,6 +128,7 @@ struct BwdPlan {
     int64_t L;          // B*(N+M) key/value pairs
     int64_t kmax;       // number of distinct keys B*(M+N)
     int nbits, npasses, digit_bits, ntiles;
+    bool segsort;       // max(N, M) <= 24576: one CTA per (direction, batch) segment sorts on chip
     size_t off_keys[2], off_vals[2], off_counts, off_totals, off_offsets, bytes;
 };
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1);

@@ -273,6 +273,165 @@ __global__ void __launch_bounds__(256) offsets_kernel(const uint32_t* __restrict
     }
 }
 
+// Segment-local sort (small clouds: max(N, M) <= kSegMax).  The edges of one (direction, batch
+// element) segment have keys in one range of T = M (xy) or N (yx) consecutive keys and land in one
+// contiguous range of the sorted order, so each segment sorts on its own: one CTA per segment, a
+// stable LSD radix sort entirely in shared memory (digits of <= 7 bits; warp w owns a contiguous
+// range of the segment and places it in order with warp ballot multisplit ranks; the per-warp digit
+// counts of a pass are integer shared-memory adds made while loading / while placing the previous
+// pass), then the sorted sources and the segment's key offsets (gap fill) go to global memory.
+// Replaces keys_hist + the global passes + offsets_kernel: 2 launches per backward, not 3 passes + 2.
+constexpr int kSegThreads = 512;
+constexpr int kSegWarps = kSegThreads / 32;
+constexpr int kSegMax = 24576;   // 8 B per edge + 32 KB of counters <= 227 KB of shared memory
+constexpr int kSegDigitBits = 7;
+constexpr int kSegD = 1 << kSegDigitBits;
+
+size_t seg_sort_smem(int nmax) { return (size_t)nmax * 8 + 2 * (size_t)kSegWarps * kSegD * 4 + 1024; }
+
+// One placement sweep of seg_sort_kernel with DB-bit digits (compile-time: unrolled ballots).
+template <int DB>
+__device__ __forceinline__ void seg_place(const uint16_t* kA, const uint16_t* vA, uint16_t* kB, uint16_t* vB,
+                                          uint32_t* wcur, uint32_t* wnext, int n, int R, int lspan, int shift,
+                                          bool last) {
+    constexpr uint32_t D = 1u << DB;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t* my = wcur + warp * D;
+    for (int t = 0; t < R; ++t) {
+        const int e0 = (warp * R + t) * 32;
+        if (e0 >= n) break;   // warp-uniform
+        const int e = e0 + lane;
+        const bool valid = e < n;
+        const uint16_t key = valid ? kA[e] : (uint16_t)0;
+        const uint32_t digit = ((uint32_t)key >> shift) & (D - 1);
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+        if (!valid) peers = ~peers;
+#pragma unroll
+        for (int bt = 0; bt < DB; ++bt) {
+            const bool bit = (digit >> bt) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
+        const uint32_t before = valid ? my[digit] : 0u;
+        if (valid) {
+            const uint32_t pos = before + __popc(peers & lt_mask);
+            kB[pos] = key;
+            vB[pos] = vA[e];
+            if (!last) atomicAdd(&wnext[(pos >> lspan) * D + (((uint32_t)key >> (shift + DB)) & (D - 1))], 1u);
+        }
+        __syncwarp();
+        if (valid && (peers & lt_mask) == 0u) my[digit] = before + __popc(peers);
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __restrict__ idx_xy,
+                                                               const int32_t* __restrict__ idx_yx, int B, int N,
+                                                               int M, int nmax, uint32_t* __restrict__ vals_out,
+                                                               uint32_t* __restrict__ off) {
+    extern __shared__ __align__(16) uint32_t smem_seg[];
+    uint32_t* wcur = smem_seg;                   // [kSegWarps][D] this pass's per-warp digit counts
+    uint32_t* wnext = wcur + kSegWarps * kSegD;  // next pass's, counted while placing
+    uint16_t* kA = reinterpret_cast<uint16_t*>(wnext + kSegWarps * kSegD);   // keys
+    uint16_t* kB = kA + nmax;
+    uint16_t* vA = kB + nmax;                    // values: the source's index in the segment
+    uint16_t* vB = vA + nmax;
+    __shared__ uint32_t dstart[kSegD];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int dir = blockIdx.x / B, b = blockIdx.x - dir * B;
+    const int n = dir == 0 ? N : M;          // edges (sources) of the segment
+    const int T = dir == 0 ? M : N;          // keys (targets) of the segment
+    const int32_t* idx = dir == 0 ? idx_xy + (int64_t)b * N : idx_yx + (int64_t)b * M;
+    const uint32_t vbase = (uint32_t)((int64_t)b * n);                          // source rows b*n + i
+    const int64_t pbase = dir == 0 ? (int64_t)b * N : (int64_t)B * N + (int64_t)b * M;   // sorted positions
+    const int64_t kbase = dir == 0 ? (int64_t)b * M : (int64_t)B * M + (int64_t)b * N;   // keys
+    int nb = 1;
+    while ((1 << nb) < T) ++nb;
+    const int passes = (nb + kSegDigitBits - 1) / kSegDigitBits;
+    const int db = (nb + passes - 1) / passes;
+    const int D = 1 << db;
+    int lspan = 5;   // rounds per warp R = span / 32, a power of two: warp w owns [w*span, (w+1)*span)
+    while (kSegWarps << lspan < n) ++lspan;
+    const int R = 1 << (lspan - 5);
+    for (int i = threadIdx.x; i < 2 * kSegWarps * kSegD; i += kSegThreads) wcur[i] = 0;
+    __syncthreads();
+    // load + the first pass's per-warp digit counts (integer shared-memory adds: order-free)
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n; i += kSegThreads) {
+        const uint16_t k = (uint16_t)min(max(idx[i], 0), T - 1);
+        kA[i] = k;
+        vA[i] = (uint16_t)i;
+        atomicAdd(&wcur[(i >> lspan) * D + (k & (D - 1))], 1u);
+    }
+    for (int pass = 0; pass < passes; ++pass) {
+        const int shift = pass * db;
+        const bool last = pass + 1 == passes;
+        __syncthreads();
+        // digit starts, then per-warp starts inside each digit run
+        if (threadIdx.x < D) {
+            uint32_t tot = 0;
+            for (int w = 0; w < kSegWarps; ++w) tot += wcur[w * D + threadIdx.x];
+            dstart[threadIdx.x] = tot;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t c[kSegD / 32], loc = 0;
+#pragma unroll
+            for (int r = 0; r < kSegD / 32; ++r) {
+                const int d = lane * (kSegD / 32) + r;
+                c[r] = d < D ? dstart[d] : 0u;
+                loc += c[r];
+            }
+            uint32_t incl = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            uint32_t run = incl - loc;
+#pragma unroll
+            for (int r = 0; r < kSegD / 32; ++r) {
+                const int d = lane * (kSegD / 32) + r;
+                if (d < D) dstart[d] = run;
+                run += c[r];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < D) {
+            uint32_t run = dstart[threadIdx.x];
+            for (int w = 0; w < kSegWarps; ++w) {
+                const uint32_t c = wcur[w * D + threadIdx.x];
+                wcur[w * D + threadIdx.x] = run;
+                run += c;
+            }
+        }
+        for (int i = threadIdx.x; i < kSegWarps * kSegD; i += kSegThreads) wnext[i] = 0;
+        __syncthreads();
+        // stable placement: each warp walks its range in order; ranks from a ballot multisplit
+        switch (db) {
+            case 1: seg_place<1>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
+            case 2: seg_place<2>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
+            case 3: seg_place<3>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
+            case 4: seg_place<4>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
+            case 5: seg_place<5>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
+            case 6: seg_place<6>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
+            default: seg_place<7>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
+        }
+        uint16_t* tv = vA; vA = vB; vB = tv;
+        uint16_t* tk = kA; kA = kB; kB = tk;
+        uint32_t* tw = wcur; wcur = wnext; wnext = tw;
+    }
+    __syncthreads();
+    // sorted sources and key offsets (off[k] = first position with key >= k; gaps filled)
+    for (int p = threadIdx.x; p <= n; p += kSegThreads) {
+        if (p < n) vals_out[pbase + p] = vbase + vA[p];
+        const int lo = p == 0 ? 0 : (int)kA[p - 1] + 1;
+        const int hi = p == n ? T : (int)kA[p];
+        for (int k = lo; k <= hi; ++k) off[kbase + k] = (uint32_t)(pbase + p);
+    }
+}
+
 struct GradArgs {
     const float* x;
     const float* y;
@@ -419,6 +578,10 @@ int radix_digit_bits(int64_t L, int nbits) {
     return db;
 }
 
+#ifndef CD_SEGSORT
+#define CD_SEGSORT 1
+#endif
+
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1) {
     p.B = B;
     p.N = N;
@@ -433,6 +596,7 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
     while (bits < 32 && ((int64_t)1 << bits) < p.kmax) ++bits;
     p.nbits = std::max(bits, 1);
     radix_sort_plan(p.L, p.nbits, p.npasses, p.digit_bits, p.ntiles);
+    p.segsort = CD_SEGSORT != 0 && std::max(N, M) <= kSegMax;
     size_t off = 0;
     for (int i = 0; i < 2; ++i) {
         p.off_keys[i] = off;
@@ -449,7 +613,9 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
     p.bytes = off;
 }
 
-int backward_launches(const BwdPlan& p) { return 3 * p.npasses + 2; }  // keys fused with pass-0 hist
+int backward_launches(const BwdPlan& p) {
+    return p.segsort ? 2 : 3 * p.npasses + 2;   // keys fused with the pass-0 histogram
+}
 
 cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, const int32_t* idx_xy,
                             const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar,
@@ -460,14 +626,20 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     uint32_t* counts = reinterpret_cast<uint32_t*>(w + p.off_counts);
     uint32_t* totals = reinterpret_cast<uint32_t*>(w + p.off_totals);
     uint32_t* off = reinterpret_cast<uint32_t*>(w + p.off_offsets);
-    {
+    int cur = 0;
+    if (p.segsort) {
+        const int nmax = std::max(p.N, p.M);
+        const size_t smem = seg_sort_smem(nmax);
+        ensure_smem_attr((const void*)seg_sort_kernel, (int)seg_sort_smem(kSegMax));
+        seg_sort_kernel<<<2 * p.B, kSegThreads, smem, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, nmax, vals[0], off);
+    } else {
         const int D = 1 << p.digit_bits;
         keys_hist_kernel<<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles,
                                                                         keys[0], vals[0], counts);
+        cur = radix_sort_pairs(keys, vals, p.L, p.nbits, counts, totals, st, /*first_hist_done=*/true);
+        const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);
+        offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], p.L, p.kmax, off);
     }
-    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, counts, totals, st, /*first_hist_done=*/true);
-    const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);
-    offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], p.L, p.kmax, off);
     GradArgs a;
     a.x = x;
     a.y = y;
