@@ -55,9 +55,12 @@ def test_workspace_sizes(lib):
 def test_launch_counts(lib):
     # fused forward: pack + fused + epilogue (row merge | column resolve) + partials
     assert lib.cd_launch_count(0, 32, 16384, 16384) == 4
-    # backward: keys+hist, 2 radix passes (11-bit digits cover 2^20 keys) x 3 kernels - 1 hist, offsets, grad
-    assert lib.cd_launch_count(2, 32, 16384, 16384) == 2 * 3 + 2
-    assert lib.cd_launch_count(3, 32, 16384, 16384) == 4 + 1 + 8
+    # backward, clouds of <= 24576 points: segment sort on chip + grad
+    assert lib.cd_launch_count(2, 32, 16384, 16384) == 2
+    assert lib.cd_launch_count(3, 32, 16384, 16384) == 4 + 1 + 2
+    assert lib.cd_launch_count(2, 8, 24577, 100) == 2 * 3 + 2   # 2^18 keys: 2 global radix passes
+    # backward, larger clouds: keys+hist, radix passes x 3 kernels - 1 hist, offsets, grad
+    assert lib.cd_launch_count(2, 8, 100000, 100000) == 2 * 3 + 2   # 1.6e6 keys: 2 passes of 11 bits
     # c5: 2^23 keys -> 3 passes
     assert lib.cd_launch_count(2, 4, 1 << 20, 1 << 20) == 3 * 3 + 2
 

@@ -266,6 +266,28 @@ def test_backward_slices_match_full(cd):
     np.testing.assert_array_equal(sy.cpu().numpy(), gy.cpu().numpy()[:, 7:2500])
 
 
+@pytest.mark.parametrize("N,M", [(24576, 700), (24577, 700), (3, 24576), (5000, 24577)])
+def test_backward_segment_sort_boundary(cd, N, M):
+    """max(N, M) <= 24576 sorts each (direction, batch) segment on chip (seg_sort_kernel), larger
+    clouds take the global radix passes: both against the oracle bit for bit, with skewed in-degree
+    (many sources on few targets) and a single-target segment."""
+    rng = np.random.default_rng(N + 7 * M)
+    B = 2
+    X = rng.normal(size=(B, N, 3)).astype(np.float32)
+    Y = rng.normal(size=(B, M, 3)).astype(np.float32)
+    ixy = (M * rng.random(size=(B, N)) ** 4).astype(np.int32)
+    iyx = (N * rng.random(size=(B, M)) ** 4).astype(np.int32)
+    ixy[1] = M - 1                                   # batch 1: every x on one y
+    g = rng.normal(size=(B, N)).astype(np.float32)
+    h = rng.normal(size=(B, M)).astype(np.float32)
+    gx, gy = cd.backward(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), torch.from_numpy(ixy).cuda(),
+                         torch.from_numpy(iyx).cuda(), torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda())
+    torch.cuda.synchronize()
+    gxr, gyr, _, _ = oracle.backward(X, Y, ixy, iyx, g, h)
+    np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
+    np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+
+
 def test_vjp_linearity_bit_exact(cd):
     X, Y = synth.shape_pair(1, 4000, 3000, config_index=25)
     x, y, (d_xy, i_xy, d_yx, i_yx, _) = _run(cd, X, Y)
