@@ -254,9 +254,11 @@ CD_API int cd_p2s_launch_count(int op, int B, int N, int Nv, int Nf);
  * of a box lower bound and stop once the bound exceeds every point's current minimum; tiles and
  * 32-face blocks no lane can improve on are skipped.  Boxes are widened by 2^-14 max|coord| so that the bound also
  * holds for the fp32-evaluated distances of the hot loop (R26): the minimum is the brute force's.
- * Same arguments and outputs as cd_p2s_forward except the tie rule: among faces with EXACTLY equal
- * fp32 minima one is returned deterministically, not necessarily the lowest index (any of them is a
- * closest face; R26).  Workspace: cd_p2s_workspace_size(CD_OP_P2S_PRUNED, ...); 0 = unsupported
+ * Same arguments, outputs and tie rule as cd_p2s_forward (the lowest face index among EXACTLY equal
+ * fp32 minima): a block whose minimum equals the current one flags the point (also across the
+ * culling's chunks, through the value atomicMin returns), and flagged points re-walk their
+ * candidate tiles for the lowest original index at the minimum (R3').  Outputs are bit-identical to
+ * cd_p2s_forward's.  Workspace: cd_p2s_workspace_size(CD_OP_P2S_PRUNED, ...); 0 = unsupported
  * size (Nf > 524288, B*(N+Nf) >= 2^31, or per-query-tile candidate lists B*ceil(N/64)*ceil(Nf/64)*8
  * bytes > 4 GiB) and the call returns CD_ERR_TOO_LARGE.
  */

@@ -133,6 +133,77 @@ __device__ __forceinline__ void face_dist2(const float* f, u64 qx, u64 qy, u64 q
     d1 = fmin3(ab1, ac1, fminf(bc1, in1 ? p1 : INFINITY));
 }
 
+// A 24-float face record (96 B, 16-B aligned) as six 16-byte loads.
+__device__ __forceinline__ void load_face_record(const float* src, float* dst) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+#pragma unroll
+    for (int k = 0; k < kFaceFloats / 4; ++k) {
+        const float4 v = __ldg(s4 + k);
+        dst[4 * k] = v.x;
+        dst[4 * k + 1] = v.y;
+        dst[4 * k + 2] = v.z;
+        dst[4 * k + 3] = v.w;
+    }
+}
+
+// The same per-lane arithmetic as face_dist2 with the lanes swapped round: ONE point (px, py, pz)
+// against TWO face records (fa in the low lane, fb in the high lane).  Every lane executes the
+// identical op sequence, so the distances are bit-identical to face_dist2's for the same (point,
+// face); used where one point meets many faces (the exact-face re-scans).
+__device__ __forceinline__ void face_dist2_2f(const float* fa, const float* fb, float px, float py, float pz,
+                                              float& da, float& db) {
+    auto F = [&](int k) { return pk2(fa[k], fb[k]); };
+    const u64 ax = sub2(bc2(px), F(0)), ay = sub2(bc2(py), F(1)), az = sub2(bc2(pz), F(2));
+    u64 s = mul2(ax, F(3));
+    s = fma2(ay, F(4), s);
+    s = fma2(az, F(5), s);
+    u64 t = mul2(ax, F(6));
+    t = fma2(ay, F(7), t);
+    t = fma2(az, F(8), t);
+    u64 u = fma2(s, F(18), F(21));
+    u = fma2(t, F(19), u);
+    u64 v = fma2(s, F(19), F(21));
+    v = fma2(t, F(20), v);
+    u64 h = mul2(ax, F(12));
+    h = fma2(ay, F(13), h);
+    h = fma2(az, F(14), h);
+    const u64 pl = mul2(h, h);
+    const u64 t0 = sat_mul2(s, F(15));
+    u64 dx = fma2(t0, F(3), ax), dy = fma2(t0, F(4), ay), dz = fma2(t0, F(5), az);
+    u64 dab = mul2(dx, dx);
+    dab = fma2(dy, dy, dab);
+    dab = fma2(dz, dz, dab);
+    const u64 t1 = sat_mul2(t, F(16));
+    dx = fma2(t1, F(6), ax);
+    dy = fma2(t1, F(7), ay);
+    dz = fma2(t1, F(8), az);
+    u64 dac = mul2(dx, dx);
+    dac = fma2(dy, dy, dac);
+    dac = fma2(dz, dz, dac);
+    const u64 bx = add2(ax, F(3)), by = add2(ay, F(4)), bz = add2(az, F(5));
+    u64 s2 = mul2(bx, F(9));
+    s2 = fma2(by, F(10), s2);
+    s2 = fma2(bz, F(11), s2);
+    const u64 t2 = sat_mul2(s2, F(17));
+    dx = fma2(t2, F(9), bx);
+    dy = fma2(t2, F(10), by);
+    dz = fma2(t2, F(11), bz);
+    u64 dbc = mul2(dx, dx);
+    dbc = fma2(dy, dy, dbc);
+    dbc = fma2(dz, dz, dbc);
+    float u0, u1, v0, v1, p0, p1, ab0, ab1, ac0, ac1, bc0, bc1;
+    upk2(u, u0, u1);
+    upk2(v, v0, v1);
+    upk2(pl, p0, p1);
+    upk2(dab, ab0, ab1);
+    upk2(dac, ac0, ac1);
+    upk2(dbc, bc0, bc1);
+    const float w0 = __fsub_rn(__fsub_rn(1.0f, u0), v0), w1 = __fsub_rn(__fsub_rn(1.0f, u1), v1);
+    const bool in0 = fmin3(u0, v0, w0) >= 0.0f, in1 = fmin3(u1, v1, w1) >= 0.0f;
+    da = fmin3(ab0, ac0, fminf(bc0, in0 ? p0 : INFINITY));
+    db = fmin3(ab1, ac1, fminf(bc1, in1 ? p1 : INFINITY));
+}
+
 // fp64 closest point on triangle (region decomposition; the same case order as the definition)
 __device__ __forceinline__ void closest64(const double p[3], const double A[3], const double Bv[3], const double C[3], double out[3],
                           double lam[3]) {

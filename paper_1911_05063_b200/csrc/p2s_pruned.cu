@@ -279,12 +279,14 @@ struct PsCandArgs {
     const float4* fbox;
     int qtiles, ftiles;
     unsigned long long* cand;   // [B][qtiles][ftiles]: (LB bits << 32) | face tile, ascending
+    unsigned* tiecount;         // zeroed here (the tie queue of this call is filled by the NN kernel)
 };
 
 __global__ void __launch_bounds__(256) ps_candidates_kernel(PsCandArgs a) {
     extern __shared__ unsigned long long keys[];
     const int u = blockIdx.x;
     const int b = u / a.qtiles;
+    if (u == 0 && threadIdx.x == 0) *a.tiecount = 0u;
     const float4 ql = a.qbox[(int64_t)u * 2], qh = a.qbox[(int64_t)u * 2 + 1];
     const float qlo[3] = {ql.x, ql.y, ql.z}, qhi[3] = {qh.x, qh.y, qh.z};
     int npow = 1;
@@ -332,6 +334,9 @@ struct PsArgs {
     int k0, klen, nchunk;   // candidate range of chunk c: [k0 + c klen, k0 + (c+1) klen)
     int phase;              // 0: first tiles, plain store of the row keys; 1: refine from the row keys
     long long* rowkey;      // [B][N] sorted order: (best bits << 32) | sorted block position
+    int* tieflag;           // [B][N] sorted order: 1 if a block other than the key's may hold the minimum
+    int* tiequeue;          // flagged sorted rows, each once (the 0 -> 1 transition of its flag appends it)
+    unsigned* tiecount;
 };
 
 // Per-lane lower bound: the lane's two points (widened box) against a face box; a tile or block is
@@ -378,6 +383,7 @@ __global__ void __launch_bounds__(kPsThreads, CD_PS_MINB) p2s_pruned_kernel(PsAr
     if (qbase + 1 >= P) best1 = -1.0f;
     const float init0 = best0, init1 = best1;
     int blk0 = -1, blk1 = -1;
+    bool tie0 = false, tie1 = false;
     // widened box of the lane's (valid) points
     float llo[3] = {INFINITY, INFINITY, INFINITY}, lhi[3] = {-INFINITY, -INFINITY, -INFINITY};
     if (qbase < P) {
@@ -461,16 +467,22 @@ __global__ void __launch_bounds__(kPsThreads, CD_PS_MINB) p2s_pruned_kernel(PsAr
             if (lane == 0) atomicAdd(&g_ps_stats[1], 1ull);
             ++nblk_stat;
 #endif
-            const float o0 = best0, o1 = best1;
+            float m0 = INFINITY, m1 = INFINITY;   // block minima
 #pragma unroll 2
             for (int j = 0; j < kBlockK; ++j) {
                 float d0, d1;
                 face_dist2(tb + (kb * kBlockK + j) * kFaceFloats, qx, qy, qz, d0, d1);
-                best0 = fminf(best0, d0);
-                best1 = fminf(best1, d1);
+                m0 = fminf(m0, d0);
+                m1 = fminf(m1, d1);
             }
-            blk0 = best0 < o0 ? ft + kb * kBlockK : blk0;
-            blk1 = best1 < o1 ? ft + kb * kBlockK : blk1;
+            // a block whose minimum equals the current one: an exact tie across blocks (R3'); the
+            // flag is reset whenever the minimum strictly improves
+            tie0 = m0 < best0 ? false : (m0 == best0 && m0 < INFINITY ? true : tie0);
+            tie1 = m1 < best1 ? false : (m1 == best1 && m1 < INFINITY ? true : tie1);
+            blk0 = m0 < best0 ? ft + kb * kBlockK : blk0;
+            blk1 = m1 < best1 ? ft + kb * kBlockK : blk1;
+            best0 = fminf(best0, m0);
+            best1 = fminf(best1, m1);
         }
         __syncthreads();   // stage s consumed by every warp
         const int tn = advance();
@@ -492,13 +504,132 @@ __global__ void __launch_bounds__(kPsThreads, CD_PS_MINB) p2s_pruned_kernel(PsAr
 #endif
 
     if (a.phase == 0) {
-        if (qbase < P) a.rowkey[rowbase + qbase] = row_key(best0, blk0);
-        if (qbase + 1 < P) a.rowkey[rowbase + qbase + 1] = row_key(best1, blk1);
+        if (qbase < P) {
+            a.rowkey[rowbase + qbase] = row_key(best0, blk0);
+            a.tieflag[rowbase + qbase] = tie0;
+            if (tie0) a.tiequeue[atomicAdd(a.tiecount, 1u)] = (int)(rowbase + qbase);
+        }
+        if (qbase + 1 < P) {
+            a.rowkey[rowbase + qbase + 1] = row_key(best1, blk1);
+            a.tieflag[rowbase + qbase + 1] = tie1;
+            if (tie1) a.tiequeue[atomicAdd(a.tiecount, 1u)] = (int)(rowbase + qbase + 1);
+        }
     } else {
-        // strictly improved rows only; the 64-bit minimum over chunks is order-independent
-        if (qbase < P && best0 < init0) atomicMin(a.rowkey + rowbase + qbase, row_key(best0, blk0));
-        if (qbase + 1 < P && best1 < init1) atomicMin(a.rowkey + rowbase + qbase + 1, row_key(best1, blk1));
+        // strictly improved rows only; the 64-bit minimum over chunks is order-independent.  A tie
+        // between chunks shows in the value atomicMin returns (equal distance, other block): the
+        // second of the two writers sees it.  Flags are only ever set here (a flag that a later,
+        // strictly smaller minimum makes moot costs a re-scan, never a wrong face).
+        if (qbase < P) {
+            bool t = tie0;
+            if (best0 < init0) {
+                const long long k = row_key(best0, blk0);
+                const long long old = atomicMin(a.rowkey + rowbase + qbase, k);
+                t |= (old >> 32) == (k >> 32) && old != k;
+            }
+            if (t && atomicExch(a.tieflag + rowbase + qbase, 1) == 0)
+                a.tiequeue[atomicAdd(a.tiecount, 1u)] = (int)(rowbase + qbase);
+        }
+        if (qbase + 1 < P) {
+            bool t = tie1;
+            if (best1 < init1) {
+                const long long k = row_key(best1, blk1);
+                const long long old = atomicMin(a.rowkey + rowbase + qbase + 1, k);
+                t |= (old >> 32) == (k >> 32) && old != k;
+            }
+            if (t && atomicExch(a.tieflag + rowbase + qbase + 1, 1) == 0)
+                a.tiequeue[atomicAdd(a.tiecount, 1u)] = (int)(rowbase + qbase + 1);
+        }
     }
+}
+
+// Rows flagged with a possible cross-block tie: one warp re-walks the row's query-tile candidate list
+// (tiles in LB order while LB <= the row's minimum: every face whose fp32 distance equals the minimum
+// has LB <= it, R26) and returns the lowest ORIGINAL face index among the faces at the minimum — the
+// brute force's choice (R3').
+struct PsTieArgs {
+    const float4* spts;
+    const float* fd;
+    const float4* fbox32;
+    const unsigned long long* cand;
+    const int* perm_f;
+    int B, N, Nf, Fpad, qtiles, ftiles;
+    const long long* rowkey;
+    const int* tiequeue;
+    const unsigned* tiecount;
+    int* tieface;           // [B][N] sorted order: original face index (flagged rows)
+};
+
+// Persistent warps over the queue of flagged rows (a few % of the rows; the order of the queue does
+// not matter: every row's result is its own).
+__device__ __forceinline__ void ps_tie_row(const PsTieArgs& a, int64_t srow, int lane) {
+    const int b = (int)(srow / a.N);
+    const int pr = (int)(srow - (int64_t)b * a.N);
+    const int u = pr / kPsQ;
+    const float best = __uint_as_float((unsigned)((unsigned long long)a.rowkey[srow] >> 32));
+    const float4 pp = a.spts[srow];
+    float llo[3] = {pp.x, pp.y, pp.z}, lhi[3] = {pp.x, pp.y, pp.z};
+    widen(llo, lhi);
+    const int nt = a.ftiles;
+    const unsigned long long* cand = a.cand + ((int64_t)b * a.qtiles + u) * nt;
+    const float* FD = a.fd + (int64_t)b * a.Fpad * kFaceFloats;
+    const float4* FB = a.fbox32 + (int64_t)b * nt * kPsBlocks * 2;
+    const int* PF = a.perm_f + (int64_t)b * a.Nf;
+    int low = 0x7fffffff;
+#ifdef CD_PS_STATS
+    int nblk_row = 0;
+#endif
+    // 32 candidates per step, one per lane: the tile LB (sorted) and the point's block LBs decide
+    // which 32-face blocks hold a face that can equal the minimum; each such block is then evaluated
+    // lane-parallel (two faces per lane: block halves)
+    for (int k0 = 0; k0 < nt; k0 += 32) {
+        const int k = k0 + lane;
+        const unsigned long long e = k < nt ? cand[k] : ~0ull;
+        const bool live = k < nt && __uint_as_float((unsigned)(e >> 32)) <= best;
+        const int t = (int)(e & 0xffffffffull);
+        static_assert(kPsBlocks == 2, "two 32-face blocks per face tile");
+        const bool n0 = live && lane_lb(llo, lhi, FB[(t * 2) * 2], FB[(t * 2) * 2 + 1]) <= best;
+        const bool n1 = live && lane_lb(llo, lhi, FB[(t * 2 + 1) * 2], FB[(t * 2 + 1) * 2 + 1]) <= best;
+        // needed blocks as bits (kb * 32 + lane), two per step: half-warp h takes the h-th
+        unsigned long long mm = ((unsigned long long)__ballot_sync(0xffffffffu, n1) << 32) | __ballot_sync(0xffffffffu, n0);
+        while (mm) {
+            const int i0 = __ffsll((long long)mm) - 1;
+            mm &= mm - 1;
+            const int i1 = mm ? __ffsll((long long)mm) - 1 : -1;
+            if (mm) mm &= mm - 1;
+            const int t0 = __shfl_sync(0xffffffffu, t, i0 & 31), t1 = __shfl_sync(0xffffffffu, t, i1 & 31);
+            const int mine = lane < 16 ? i0 : i1;
+            const int tm = lane < 16 ? t0 : t1;
+#ifdef CD_PS_STATS
+            if (lane == 0) atomicAdd(&g_ps_stats[1], i1 >= 0 ? 2ull : 1ull);
+            nblk_row += i1 >= 0 ? 2 : 1;
+#endif
+            if (mine >= 0) {
+                const int f = tm * kPsTile + (mine >> 5) * kBlockK + (lane & 15) * 2;   // faces f, f + 1
+                float fa[kFaceFloats], fb[kFaceFloats];
+                load_face_record(FD + (int64_t)f * kFaceFloats, fa);
+                load_face_record(FD + (int64_t)(f + 1) * kFaceFloats, fb);
+                float d0, d1;
+                face_dist2_2f(fa, fb, pp.x, pp.y, pp.z, d0, d1);
+                if (d0 == best) low = min(low, PF[min(f, a.Nf - 1)]);
+                if (d1 == best) low = min(low, PF[min(f + 1, a.Nf - 1)]);
+            }
+        }
+        if (__ballot_sync(0xffffffffu, live) != 0xffffffffu) break;   // sorted: the rest are above the minimum
+    }
+    low = __reduce_min_sync(0xffffffffu, low);
+    if (lane == 0) a.tieface[srow] = low;
+#ifdef CD_PS_STATS
+    if (lane == 0) atomicAdd(&g_ps_stats[0], 1ull);
+    if (lane == 0) atomicMax(&g_ps_stats[2], (unsigned long long)(nblk_row));
+    if (lane == 0) atomicMax(&g_ps_stats[3], (unsigned long long)__float_as_uint(best));
+#endif
+}
+
+__global__ void __launch_bounds__(256) ps_tie_kernel(PsTieArgs a) {
+    const int lane = threadIdx.x & 31;
+    const unsigned count = *a.tiecount;
+    for (unsigned qi = blockIdx.x * 8 + (threadIdx.x >> 5); qi < count; qi += gridDim.x * 8)
+        ps_tie_row(a, a.tiequeue[qi], lane);
 }
 
 // ------------------------------------------------------------------------------------------ resolve
@@ -511,6 +642,8 @@ struct PsResolveArgs {
     const int* faces;
     int B, N, Nv, Nf, Fpad, nchunks;
     const long long* rowkey;
+    const int* tieflag;
+    const int* tieface;
     float* d_out;
     int* face_out;
     float* closest;
@@ -530,20 +663,24 @@ __global__ void __launch_bounds__(kMergeThreads) ps_resolve_kernel(PsResolveArgs
         const int bb = (int)(unsigned)(key & 0xffffffffull);   // 0xffffffff -> -1
         const float4 pp = a.spts[srow];
         int face = a.perm_f[(int64_t)b * a.Nf];
-        if (bb >= 0) {
-            const u64 qx = pk2(pp.x, pp.x), qy = pk2(pp.y, pp.y), qz = pk2(pp.z, pp.z);
+        if (bb >= 0 && a.tieflag[srow] && a.tieface[srow] != 0x7fffffff) {
+            face = a.tieface[srow];   // cross-block tie: lowest original index over all faces at the minimum
+        } else if (bb >= 0) {
+            // lowest original index among the winning block's faces at the minimum (R3')
             const float* FD = a.fd + (int64_t)b * a.Fpad * kFaceFloats;
             const int fend = min(bb + kBlockK, a.Nf);
-            int pos = bb;
-            for (int f = bb; f < fend; ++f) {
+            int low = 0x7fffffff;
+            for (int f = bb; f < fend; f += 2) {   // two faces per packed evaluation
+                const int g = min(f + 1, fend - 1);
+                float fa[kFaceFloats], fb[kFaceFloats];
+                load_face_record(FD + (int64_t)f * kFaceFloats, fa);
+                load_face_record(FD + (int64_t)g * kFaceFloats, fb);
                 float d0, d1;
-                face_dist2(FD + (int64_t)f * kFaceFloats, qx, qy, qz, d0, d1);
-                if (d0 == best) {
-                    pos = f;
-                    break;
-                }
+                face_dist2_2f(fa, fb, pp.x, pp.y, pp.z, d0, d1);
+                if (d0 == best) low = min(low, a.perm_f[(int64_t)b * a.Nf + f]);
+                if (d1 == best) low = min(low, a.perm_f[(int64_t)b * a.Nf + g]);
             }
-            face = a.perm_f[(int64_t)b * a.Nf + min(pos, a.Nf - 1)];
+            face = low != 0x7fffffff ? low : a.perm_f[(int64_t)b * a.Nf + min(bb, a.Nf - 1)];
         }
         const float* vv = a.verts + (int64_t)b * a.Nv * 3;
         double A[3], Bv[3], C[3], q[3] = {pp.x, pp.y, pp.z}, c[3], lam[3];
@@ -584,7 +721,7 @@ struct PsPlan {
     int B, N, Nv, Nf, Fpad, qtiles, ftiles, nchunks, bbits, kbits, nbits;
     int64_t L;
     size_t off_bbox, off_keys[2], off_vals[2], off_counts, off_totals, off_spts, off_perm_p, off_perm_f, off_fd,
-        off_qbox, off_fbox, off_fbox32, off_cand, off_rowkey, off_chunk, bytes;
+        off_qbox, off_fbox, off_fbox32, off_cand, off_rowkey, off_tieflag, off_tieface, off_tiequeue, off_tiecount, off_chunk, bytes;
     int k_first, klen, nchunk;   // phase 0: candidates [0, k_first); phase 1: nchunk chunks of klen
     bool supported;
 };
@@ -626,6 +763,10 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
     p.off_fbox32 = take((size_t)B * p.ftiles * kPsBlocks * 32);
     p.off_cand = take((size_t)B * p.qtiles * p.ftiles * 8);
     p.off_rowkey = take((size_t)B * N * 8);
+    p.off_tieflag = take((size_t)B * N * 4);
+    p.off_tieface = take((size_t)B * N * 4);
+    p.off_tiequeue = take((size_t)B * N * 4);
+    p.off_tiecount = take(256);
     p.off_chunk = take((size_t)B * p.nchunks * 8);
     p.bytes = off;
     // phase 0 visits each query tile's nearest kPsFirst face tiles (tight upper bounds for most rows);
@@ -647,7 +788,7 @@ size_t p2s_pruned_workspace(int B, int N, int Nv, int Nf) {
 int p2s_pruned_launches(int B, int N, int Nv, int Nf) {
     PsPlan p;
     plan_ps(p, B, N, Nv, Nf);
-    return 2 + radix_sort_launches(p.L, p.nbits) + 6 + (p.nchunk > 0 ? 1 : 0) + 1;   // + finalize
+    return 2 + radix_sort_launches(p.L, p.nbits) + 7 + (p.nchunk > 0 ? 1 : 0) + 1;   // + ties + finalize
 }
 
 cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int* faces, int B, int N, int Nv, int Nf,
@@ -683,6 +824,10 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
     float4* fbox32 = reinterpret_cast<float4*>(w + p.off_fbox32);
     unsigned long long* cand = reinterpret_cast<unsigned long long*>(w + p.off_cand);
     long long* rowkey = reinterpret_cast<long long*>(w + p.off_rowkey);
+    int* tieflag = reinterpret_cast<int*>(w + p.off_tieflag);
+    int* tieface = reinterpret_cast<int*>(w + p.off_tieface);
+    int* tiequeue = reinterpret_cast<int*>(w + p.off_tiequeue);
+    unsigned* tiecount = reinterpret_cast<unsigned*>(w + p.off_tiecount);
     double* chunk = reinterpret_cast<double*>(w + p.off_chunk);
     {
         PsGatherArgs a{points, B, N, Nf, vals[cur], spts, perm_p, perm_f};
@@ -698,14 +843,14 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
         ps_aabb_kernel<<<ps_cdiv(tasks * 32, 256), 256, 0, st>>>(a);
     }
     {
-        PsCandArgs a{qbox, fbox, p.qtiles, p.ftiles, cand};
+        PsCandArgs a{qbox, fbox, p.qtiles, p.ftiles, cand, tiecount};
         int npow = 1;
         while (npow < p.ftiles) npow <<= 1;
         ensure_smem_attr((const void*)ps_candidates_kernel, kPsMaxTiles * 8);
         ps_candidates_kernel<<<B * p.qtiles, 256, (size_t)npow * 8, st>>>(a);
     }
     {
-        PsArgs a{spts, fd, fbox, fbox32, cand, N, p.Fpad, p.qtiles, p.ftiles, 0, p.k_first, 1, 0, rowkey};
+        PsArgs a{spts, fd, fbox, fbox32, cand, N, p.Fpad, p.qtiles, p.ftiles, 0, p.k_first, 1, 0, rowkey, tieflag, tiequeue, tiecount};
         if (g_prof_start) record_profile_event(g_prof_start, st);
         p2s_pruned_kernel<<<dim3(p.qtiles, B), kPsThreads, 0, st>>>(a);
         if (p.nchunk > 0) {
@@ -727,8 +872,22 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
 #endif
     }
     {
+        PsTieArgs a{spts, fd, fbox32, cand, perm_f, B, N, Nf, p.Fpad, p.qtiles, p.ftiles, rowkey, tiequeue, tiecount,
+                    tieface};
+        ps_tie_kernel<<<std::min(ps_cdiv((int64_t)B * N, 8), sms * 8), 256, 0, st>>>(a);
+#ifdef CD_PS_STATS
+        unsigned long long h[4];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_ps_stats, sizeof(h));
+        printf("ps_tie_stats flagged_rows=%llu blocks=%llu of rows=%d maxblocks=%llu maxbest=%g\n", h[0], h[1], B * N, h[2],
+               (double)__builtin_bit_cast(float, (unsigned)h[3]));
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_ps_stats, z, sizeof(z));
+#endif
+    }
+    {
         PsResolveArgs a{spts, perm_p, perm_f, fd, verts, faces, B, N, Nv, Nf, p.Fpad, p.nchunks,
-                        rowkey, d, face, closest, bary, chunk};
+                        rowkey, tieflag, tieface, d, face, closest, bary, chunk};
         ps_resolve_kernel<<<B * p.nchunks, kMergeThreads, 0, st>>>(a);
     }
     launch_p2s_finalize(chunk, B, N, p.nchunks, per_batch, loss, st);

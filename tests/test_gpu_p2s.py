@@ -133,26 +133,21 @@ def test_p2s_autograd(cd):
 
 
 # ---------------------------------------------------------------------------------- culled path (R26)
-def _pruned_vs_brute(cd, P, V, F, rows=None, min_clear=0.3, min_same=0.5):
+def _pruned_vs_brute(cd, P, V, F, rows=None, min_clear=0.3):
     """The culled forward against the oracle (same gate) and against the brute-force kernel: the
-    same face wherever the brute force's choice is unique up to fp32 ties, and then bit-identical
-    d / closest / bary (both evaluate the chosen face with the same fp64 code)."""
+    same face for every point — the lowest original face index among the faces at the exact fp32
+    minimum, ties included (R3') — and then bit-identical d / closest / bary (both evaluate the
+    chosen face with the same fp64 code)."""
     outp = cd.p2s_forward(_t(P), _t(V), _t(F), algorithm="pruned")
     outb = cd.p2s_forward(_t(P), _t(V), _t(F))
     torch.cuda.synchronize()
     d1, f1, clear = _gate(P, V, F, outp, rows=rows, min_clear=min_clear)
     dp, fp, cp, bp = (o.cpu().numpy() for o in outp[:4])
     db, fb, cb, bb = (o.cpu().numpy() for o in outb[:4])
-    # exact fp32 ties are common (a shared closest vertex evaluated through two faces with the same
-    # corner role): there the culled path keeps the first face in its visiting order (R26)
-    same = fp == fb
-    assert same.mean() >= min_same
-    np.testing.assert_array_equal(dp[same], db[same])
-    np.testing.assert_array_equal(cp[same], cb[same])
-    np.testing.assert_array_equal(bp[same], bb[same])
-    # a different face only on (near-)ties: the two fp64 distances agree to the fp32 band
-    R = max(np.abs(P).max(), np.abs(V).max())
-    np.testing.assert_allclose(dp[~same], db[~same], rtol=1e-5, atol=2.0 ** -22 * R * R)
+    np.testing.assert_array_equal(fp, fb)
+    np.testing.assert_array_equal(dp, db)
+    np.testing.assert_array_equal(cp, cb)
+    np.testing.assert_array_equal(bp, bb)
     # loss: fp64 sums of the per-point d (summation order differs from the brute force)
     assert abs(outp[5].item() - dp.astype(np.float64).mean()) <= 1e-6 * dp.mean() + 1e-30
     np.testing.assert_allclose(outp[4].cpu().numpy(), dp.astype(np.float64).mean(1), rtol=1e-6)
@@ -179,7 +174,7 @@ def test_p2s_pruned_far_and_exact_surface(cd):
     B, N = 2, 3000
     V, F = synth.mesh_batch(B, subdiv=3, config_index=132)
     Pfar = (synth.shape_pair(B, N, 8, config_index=133)[0] * 5.0 + 3.0).astype(np.float32)
-    _pruned_vs_brute(cd, Pfar, V, F, min_clear=0.0, min_same=0.0)   # mostly vertex-closest: ties
+    _pruned_vs_brute(cd, Pfar, V, F, min_clear=0.0)   # mostly vertex-closest: exact ties between blocks
     rf, rb = synth.sampling_randoms(B, N, seed=12)
     Pon, _, _, _ = oracle.sample_mesh(V, F, rf, rb)
     _pruned_vs_brute(cd, Pon.astype(np.float32), V, F, min_clear=0.0)

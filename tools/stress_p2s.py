@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Randomised cross-check of the culled point-to-surface forward against the brute-force kernel:
-the same face (then bit-identical d / closest / bary) or, on exact fp32 ties, a face at the same
-distance to within the R24 band.  python tools/stress_p2s.py [draws] [seed]"""
+the same face for every point (lowest original index among exact fp32 ties, R3') and bit-identical
+d / closest / bary.  python tools/stress_p2s.py [draws] [seed]"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -39,11 +39,7 @@ for k in range(draws):
     p, v, f = torch.from_numpy(np.ascontiguousarray(P)).cuda(), torch.from_numpy(V).cuda(), torch.from_numpy(F).cuda()
     ob = [t.cpu().numpy() for t in cd.p2s_forward(p, v, f)]
     op = [t.cpu().numpy() for t in cd.p2s_forward(p, v, f, algorithm="pruned")]
-    same = op[1] == ob[1]
-    R = max(np.abs(P).max(), np.abs(V).max())
-    band = 2.0 ** -22 * R * R
-    ok = (np.array_equal(op[0][same], ob[0][same]) and np.array_equal(op[2][same], ob[2][same])
-          and np.all(np.abs(op[0][~same].astype(np.float64) - ob[0][~same]) <= 1e-5 * np.abs(ob[0][~same]) + band))
+    ok = all(np.array_equal(a, b) for a, b in zip(op[:4], ob[:4]))
     if not ok:
         bad += 1
         print(f"MISMATCH draw {k} {kind} B={B} sub={sub} N={N}", flush=True)
