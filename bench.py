@@ -534,12 +534,14 @@ def main():
         pts = B_local * (N + M)
         alg = 28 * pts   # read both clouds (12 B) + both index arrays (4 B) + write both gradients (12 B)
         hbm_peak = _measured_peak("hbm_gbs", 7700.0)
-        bwd_roof = {"bound": "hbm", "kernel": "cd_backward (keys+hist, radix passes, offsets, grad: "
-                    f"{cd.launch_count(_lib.CD_OP_BACKWARD, B_local, N, M)} launches)", "ms": bms,
+        nbl = cd.launch_count(_lib.CD_OP_BACKWARD, B_local, N, M)
+        bwd_kern = ("cd_backward (seg_sort: one CTA per (direction, batch) segment sorts on chip; grad: "
+                    if max(N, M) <= 24576 else "cd_backward (keys+hist, radix passes, offsets, grad: ")
+        bwd_roof = {"bound": "hbm", "kernel": f"{bwd_kern}{nbl} launches)", "ms": bms,
                     "achieved": alg / (bms * 1e-3) / 1e9, "peak": hbm_peak[0], "unit": "GB/s",
                     "frac": alg / (bms * 1e-3) / 1e9 / hbm_peak[0], "peak_source": hbm_peak[1],
-                    "algorithmic": "28 B per point (clouds 12 + indices 4 + gradients 12); the sort's key/value "
-                                   "passes and the partner gathers are extra traffic"}
+                    "algorithmic": "28 B per point (clouds 12 + indices 4 + gradients 12); the sort (global key/value "
+                                   "passes or the on-chip segment sort) and the partner gathers are extra traffic"}
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
                 tb = json.load(f).get(f"backward/{args.config}")
