@@ -313,7 +313,10 @@ CD_API void cd_set_profile_events(void* start, void* stop);
  * fused bidirectional kernel for full problems, the per-direction kernel for query slices),
  * 1 = always the per-direction kernel, 2 = the fused kernel (full problems), 3 = the tensor-core
  * filter + exact re-scan forward (nn_tc.cu, R27; full problems).  Returns the
- * previous value.  All produce bit-identical outputs.
+ * previous value.  All produce bit-identical outputs.  Mode 3's workspace
+ * (per-(128-row query block, column) summaries: ~N*M/8 bytes per batch element) is part of
+ * cd_workspace_size(CD_OP_FORWARD / CD_OP_STEP) only while mode 3 is selected; a mode-3 call with a
+ * smaller workspace returns CD_ERR_TOO_LARGE before any launch.
  */
 CD_API int cd_set_forward_mode(int mode);
 

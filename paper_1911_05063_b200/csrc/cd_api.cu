@@ -65,12 +65,15 @@ cd_status check_device() {
 }
 
 size_t forward_ws(int B, int N, int M, int q0, int q1, int r0, int r1) {
-    // large enough for either forward kernel (the mode is chosen per call)
+    // large enough for either FP32-pipe forward kernel (the mode is chosen per call); the tensor-core
+    // filter's per-(query block, column) summaries grow as N*M/128, so its workspace is only
+    // included while forward mode 3 is selected on this thread (a call in mode 3 with a smaller
+    // workspace fails with CD_ERR_TOO_LARGE before any launch)
     cdk::FwdPlan p, u;
     cdk::plan_forward(p, cdk::kFusedFull, B, N, M, q0, q1, r0, r1, g_forced_splits);
     cdk::plan_forward(u, cdk::kUnfused, B, N, M, q0, q1, r0, r1, g_forced_splits);
     size_t bytes = std::max(p.bytes, u.bytes);
-    if (q0 == 0 && q1 == N && r0 == 0 && r1 == M) {
+    if (g_forward_mode == 3 && q0 == 0 && q1 == N && r0 == 0 && r1 == M) {
         cdk::FwdPlan t;
         cdk::plan_forward(t, cdk::kTensor, B, N, M, q0, q1, r0, r1, g_forced_splits);
         bytes = std::max(bytes, t.bytes);
