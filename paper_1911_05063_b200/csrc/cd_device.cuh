@@ -15,6 +15,7 @@ typedef unsigned long long u64;
 // ---------------------------------------------------------------- tiling constants
 constexpr int kFwdThreads = 128;                 // 4 warps per CTA
 constexpr int kR = 16;                           // queries per thread (8 packed f32x2 pairs)
+constexpr int kRSmall = 8;                       // fused kernel on small clouds: 1024-row query tiles
 constexpr int kQTile = kFwdThreads * kR;         // 2048 queries per CTA
 constexpr int kTile = 512;                       // targets per shared-memory stage (8 KB)
 constexpr int kStages = 3;                       // TMA ring depth

@@ -31,6 +31,7 @@ struct FwdPlan {
     size_t off_pack[2], off_rowkey, off_chunk_sum, off_chunk_hits, off_colkey, bytes;
     int forced_splits;   // 0: automatic
     int split_unit;      // fused kernel: targets per split unit (kTile, or kBlockK for small M)
+    int fused_rows;      // fused kernel: rows per thread (kR = 16, or kRSmall = 8 for small clouds)
 };
 
 struct FwdOutputs {
@@ -56,7 +57,7 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
 cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
                            cudaStream_t st);
 int forward_launches(const FwdPlan& p);
-int fused_ctas_per_sm();
+int fused_ctas_per_sm(int rows);
 int unfused_ctas_per_sm();
 // fused kernels (nn_fused.cu)
 cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey,

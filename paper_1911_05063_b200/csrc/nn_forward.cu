@@ -547,6 +547,10 @@ static int choose_splits_blocks(int64_t units, int nb, int ctas_per_sm) {
     return best_s;
 }
 
+#ifndef CD_FUSED_SMALL
+#define CD_FUSED_SMALL 1
+#endif
+
 void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits) {
     if (mode == kTensor) {   // full problems only (q = [0,N), r = [0,M)); the tensor plan carves its own workspace
         plan_forward(p, kFusedFull, B, N, M, q0, q1, r0, r1, forced_splits);
@@ -575,7 +579,16 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
         if (mode != kUnfused && d == 1) p.qtiles[d] = 0;  // dir 1 comes from the column keys
         units += (int64_t)B * p.qtiles[d];
     }
-    const int occ = mode == kUnfused ? unfused_ctas_per_sm() : fused_ctas_per_sm();
+    p.fused_rows = kR;
+    if (CD_FUSED_SMALL && mode != kUnfused && p.qtiles[0] > 0 && (int64_t)B * p.qtiles[0] < device_sm_count()) {
+        // fewer 2048-row units than SMs: 1024-row query tiles (the per-CTA fixed cost — query load,
+        // per-tile column combine, row keys — over half the rows, twice the units to spread)
+        p.fused_rows = kRSmall;
+        units -= (int64_t)B * p.qtiles[0];
+        p.qtiles[0] = ceil_div(p.qhi[0] - p.qlo[0], kFwdThreads * kRSmall);
+        units += (int64_t)B * p.qtiles[0];
+    }
+    const int occ = mode == kUnfused ? unfused_ctas_per_sm() : fused_ctas_per_sm(p.fused_rows);
     if (mode == kUnfused) {
         const int S = forced_splits > 0 ? forced_splits : choose_splits(units, ceil_div(std::max(N, M), kTile), occ);
         for (int d = 0; d < 2; ++d) {

@@ -1,7 +1,8 @@
 // nn_fused.cu — fused bidirectional forward (built into the hot path):
 // every distance d(x_i, y_j) is evaluated ONCE and feeds both nearest-neighbour directions.
 //
-//   nn_fused_kernel   CTA = 2048 X rows (kR = 16 per thread, packed f32x2) x one split of Y
+//   nn_fused_kernel   CTA = 2048 X rows (kR = 16 per thread, packed f32x2; 1024 rows / kRSmall = 8
+//                     when the clouds are too small to fill the GPU with 2048-row tiles) x one split of Y
 //                     (3-stage TMA bulk ring).  Row direction (x -> nearest y): value-only running
 //                     min folded two targets per FMNMX3, argmin block tracked per kBlockK targets
 //                     (as nn_fwd_kernel).  Column direction (y -> nearest x): per target, min over
@@ -44,7 +45,7 @@ struct FusedArgs {
 #ifndef CD_FUSED_MINB
 #define CD_FUSED_MINB 3
 #endif
-template <bool kPartial>   // true: block-granular splits (partial tiles possible)
+template <bool kPartial, int R>   // kPartial: block-granular splits (partial tiles); R: rows per thread
 __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(FusedArgs a) {
     __shared__ __align__(128) float4 sm[kStages][kTile];
     __shared__ float colv[2][kFwdThreads / 32][kTile];
@@ -81,10 +82,10 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
         }
     }
 
-    const int qbase = a.q0 + tile * kQTile + threadIdx.x * kR;  // first row of this thread's group
-    u64 qx[kR / 2], qy[kR / 2], qz[kR / 2];
+    const int qbase = a.q0 + tile * (kFwdThreads * R) + threadIdx.x * R;  // first row of this thread's group
+    u64 qx[R / 2], qy[R / 2], qz[R / 2];
 #pragma unroll
-    for (int r = 0; r < kR / 2; ++r) {
+    for (int r = 0; r < R / 2; ++r) {
         // rows past the slice end duplicate the last row of the slice: same values, higher index,
         // so they never win a column and their row results are never stored
         const float4 p0 = Q[min(qbase + 2 * r, a.q1 - 1)];
@@ -93,10 +94,10 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
         qy[r] = pk2(p0.y, p1.y);
         qz[r] = pk2(p0.z, p1.z);
     }
-    float best[kR];
-    int blk[kR];
+    float best[R];
+    int blk[R];
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
+    for (int r = 0; r < R; ++r) {
         best[r] = INFINITY;
         blk[r] = -1;
     }
@@ -112,9 +113,9 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
         for (int kb = 0; kb < kTile; kb += kBlockK) {
             if (kPartial && kb >= kend) break;   // partial last tile of a block-granular split
             static_assert(kBlockK == 32, "one column result per lane per block");
-            float old[kR];
+            float old[R];
 #pragma unroll
-            for (int r = 0; r < kR; ++r) old[r] = best[r];
+            for (int r = 0; r < R; ++r) old[r] = best[r];
             unsigned keep_m = 0x7f800000u, keep_e = 0u;  // this lane's target (kb + lane) results
 #pragma unroll kFusedUnroll
             for (int jj = 0; jj < kBlockK; jj += 2) {
@@ -125,10 +126,10 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
 #ifndef CD_COLMIN_TREE
                 float ca[2], cb[2];   // column partials: two FMNMX3 accumulators per target (depth 4)
 #else
-                float ca[kR / 2], cb[kR / 2];
+                float ca[R / 2], cb[R / 2];
 #endif
 #pragma unroll
-                for (int r = 0; r < kR / 2; ++r) {
+                for (int r = 0; r < R / 2; ++r) {
                     u64 dx = sub2(qx[r], t0x), dy = sub2(qy[r], t0y), dz = sub2(qz[r], t0z);
                     u64 s0 = mul2(dx, dx);
                     s0 = fma2(dy, dy, s0);
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
             cv[kb + lane] = __uint_as_float(keep_m);
             cl[kb + lane] = (unsigned char)(__ffs(keep_e) - 1);  // lowest lane; 255 if none (NaN)
 #pragma unroll
-            for (int r = 0; r < kR; ++r) blk[r] = best[r] < old[r] ? jt + kb : blk[r];
+            for (int r = 0; r < R; ++r) blk[r] = best[r] < old[r] ? jt + kb : blk[r];
         }
         __syncthreads();  // every warp is done with stage s and has written colv[k & 1]
         if (threadIdx.x == 0 && k + kStages < ntiles) {
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
             }
             const unsigned l = coll[k & 1][w][t];
             if (l < 32u) {
-                const unsigned row0 = (unsigned)(a.q0 + tile * kQTile + (w * 32 + (int)l) * kR);
+                const unsigned row0 = (unsigned)(a.q0 + tile * (kFwdThreads * R) + (w * 32 + (int)l) * R);
                 const long long key = (long long)(((unsigned long long)__float_as_uint(m) << 32) | row0);
                 atomicMin(&a.colkey[(int64_t)b * a.M + j], key);  // keys >= 0: signed min == lexicographic
             }
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
     const int slen = a.q1 - a.q0;
     const int64_t rowbase = (int64_t)b * slen;
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
+    for (int r = 0; r < R; ++r) {
         const int q = qbase + r;
         if (q < a.q1) atomicMin(&a.rowkey[rowbase + (q - a.q0)], row_key(best[r], blk[r]));
     }
@@ -222,16 +223,20 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
 
 // ------------------------------------------------------------------------------------------------
 // ------------------------------------------------------------------------------------------------
-int fused_ctas_per_sm() {
-    static thread_local int occ = 0;
-    if (occ == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nn_fused_kernel<false>, kFwdThreads, 0) != cudaSuccess ||
-            occ <= 0) {
+int fused_ctas_per_sm(int rows) {
+    static thread_local int occ[2] = {0, 0};
+    int& o = occ[rows == kR ? 0 : 1];
+    if (o == 0) {
+        const cudaError_t e = rows == kR
+                                  ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, nn_fused_kernel<false, kR>, kFwdThreads, 0)
+                                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, nn_fused_kernel<false, kRSmall>,
+                                                                                  kFwdThreads, 0);
+        if (e != cudaSuccess || o <= 0) {
             cudaGetLastError();
-            occ = 3;
+            o = 3;
         }
     }
-    return occ;
+    return o;
 }
 
 cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey,
@@ -255,10 +260,18 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
     const int gx = p.qtiles[0] * p.splits[0];
     if (gx > 0) {
         if (g_prof_start) record_profile_event(g_prof_start, st);
-        if (p.split_unit == kTile)
-            nn_fused_kernel<false><<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
-        else
-            nn_fused_kernel<true><<<dim3(gx, p.B), kFwdThreads, 0, st>>>(a);
+        const dim3 grid(gx, p.B);
+        if (p.fused_rows == kR) {
+            if (p.split_unit == kTile)
+                nn_fused_kernel<false, kR><<<grid, kFwdThreads, 0, st>>>(a);
+            else
+                nn_fused_kernel<true, kR><<<grid, kFwdThreads, 0, st>>>(a);
+        } else {   // small clouds: 1024-row query tiles (twice the CTAs per batch element)
+            if (p.split_unit == kTile)
+                nn_fused_kernel<false, kRSmall><<<grid, kFwdThreads, 0, st>>>(a);
+            else
+                nn_fused_kernel<true, kRSmall><<<grid, kFwdThreads, 0, st>>>(a);
+        }
         if (g_prof_stop) record_profile_event(g_prof_stop, st);
     }
     return cudaGetLastError();
