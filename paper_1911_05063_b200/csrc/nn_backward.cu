@@ -328,7 +328,8 @@ __device__ __forceinline__ void seg_place(const uint16_t* kA, const uint16_t* vA
 
 __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __restrict__ idx_xy,
                                                                const int32_t* __restrict__ idx_yx, int B, int N,
-                                                               int M, int nmax, uint32_t* __restrict__ vals_out,
+                                                               int M, int nmax, int lparts,
+                                                               uint32_t* __restrict__ vals_out,
                                                                uint32_t* __restrict__ off) {
     extern __shared__ __align__(16) uint32_t smem_seg[];
     uint32_t* wcur = smem_seg;                   // [kSegWarps][D] this pass's per-warp digit counts
@@ -338,31 +339,89 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
     uint16_t* vA = kB + nmax;                    // values: the source's index in the segment
     uint16_t* vB = vA + nmax;
     __shared__ uint32_t dstart[kSegD];
+    __shared__ uint32_t wsum[2][kSegWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int dir = blockIdx.x / B, b = blockIdx.x - dir * B;
-    const int n = dir == 0 ? N : M;          // edges (sources) of the segment
+    const int seg = blockIdx.x >> lparts, part = blockIdx.x & ((1 << lparts) - 1);
+    const int dir = seg / B, b = seg - dir * B;
+    const int nseg = dir == 0 ? N : M;       // edges (sources) of the segment
     const int T = dir == 0 ? M : N;          // keys (targets) of the segment
     const int32_t* idx = dir == 0 ? idx_xy + (int64_t)b * N : idx_yx + (int64_t)b * M;
-    const uint32_t vbase = (uint32_t)((int64_t)b * n);                          // source rows b*n + i
+    const uint32_t vbase = (uint32_t)((int64_t)b * nseg);                       // source rows b*n + i
     const int64_t pbase = dir == 0 ? (int64_t)b * N : (int64_t)B * N + (int64_t)b * M;   // sorted positions
     const int64_t kbase = dir == 0 ? (int64_t)b * M : (int64_t)B * M + (int64_t)b * N;   // keys
     int nb = 1;
     while ((1 << nb) < T) ++nb;
-    const int passes = (nb + kSegDigitBits - 1) / kSegDigitBits;
-    const int db = (nb + passes - 1) / passes;
+    // part h of the segment's 2^lparts CTAs owns the keys whose top lparts bits are h: [K0, K1)
+    const int lp = min(lparts, nb);
+    const int kb_low = nb - lp;              // key bits sorted on chip
+    const int K0 = min(part << kb_low, T), K1 = min((part + 1) << kb_low, T);
+    // phase A: per-warp counts of this part's edges and of the edges of lower parts (the part's
+    // global base); warp w scans a contiguous range of the segment in order
+    const int lspan_l = max(5, 31 - __clz(max((nseg + kSegWarps - 1) / kSegWarps, 1) - 1) + 1);
+    const int spanl = 1 << lspan_l;
+    const int wend = min((warp + 1) * spanl, nseg);
+    {
+        uint32_t mine = 0, lower = 0;
+        for (int e0 = warp * spanl; e0 < wend; e0 += 8 * 32) {   // 8 index loads in flight per lane
+            int k[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * 32 + lane;
+                k[u] = e < wend ? min(max(__ldg(idx + e), 0), T - 1) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                mine += __popc(__ballot_sync(0xffffffffu, k[u] >= K0 && k[u] < K1));
+                lower += __popc(__ballot_sync(0xffffffffu, k[u] >= 0 && k[u] < K0));
+            }
+        }
+        if (lane == 0) {
+            wsum[0][warp] = mine;
+            wsum[1][warp] = lower;
+        }
+    }
+    for (int i = threadIdx.x; i < 2 * kSegWarps * kSegD; i += kSegThreads) wcur[i] = 0;
+    __syncthreads();
+    uint32_t wbase = 0, n_u = 0, base_u = 0;
+    for (int w = 0; w < kSegWarps; ++w) {
+        const uint32_t c = wsum[0][w];
+        wbase += w < warp ? c : 0u;
+        n_u += c;
+        base_u += wsum[1][w];
+    }
+    const int n = (int)n_u;                  // edges of this part
+    const int64_t obase = pbase + base_u;    // sorted positions of this part
+    const int passes = kb_low > 0 ? (kb_low + kSegDigitBits - 1) / kSegDigitBits : 0;
+    const int db = passes > 0 ? (kb_low + passes - 1) / passes : 1;
     const int D = 1 << db;
     int lspan = 5;   // rounds per warp R = span / 32, a power of two: warp w owns [w*span, (w+1)*span)
     while (kSegWarps << lspan < n) ++lspan;
     const int R = 1 << (lspan - 5);
-    for (int i = threadIdx.x; i < 2 * kSegWarps * kSegD; i += kSegThreads) wcur[i] = 0;
-    __syncthreads();
-    // load + the first pass's per-warp digit counts (integer shared-memory adds: order-free)
-#pragma unroll 4
-    for (int i = threadIdx.x; i < n; i += kSegThreads) {
-        const uint16_t k = (uint16_t)min(max(idx[i], 0), T - 1);
-        kA[i] = k;
-        vA[i] = (uint16_t)i;
-        atomicAdd(&wcur[(i >> lspan) * D + (k & (D - 1))], 1u);
+    // phase B: ordered compaction of the part's edges + the first pass's per-warp digit counts
+    // (integer shared-memory adds: order-free)
+    {
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        uint32_t run = wbase;
+        for (int e0 = warp * spanl; e0 < wend; e0 += 8 * 32) {
+            int k[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * 32 + lane;
+                k[u] = e < wend ? min(max(__ldg(idx + e), 0), T - 1) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const bool in = k[u] >= K0 && k[u] < K1;
+                const uint32_t m = __ballot_sync(0xffffffffu, in);
+                if (in) {
+                    const uint32_t pos = run + __popc(m & lt_mask);
+                    kA[pos] = (uint16_t)k[u];
+                    vA[pos] = (uint16_t)(e0 + u * 32 + lane);
+                    if (passes > 0) atomicAdd(&wcur[(pos >> lspan) * D + (k[u] & (D - 1))], 1u);
+                }
+                run += __popc(m);
+            }
+        }
     }
     for (int pass = 0; pass < passes; ++pass) {
         const int shift = pass * db;
@@ -423,12 +482,13 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
         uint32_t* tw = wcur; wcur = wnext; wnext = tw;
     }
     __syncthreads();
-    // sorted sources and key offsets (off[k] = first position with key >= k; gaps filled)
+    // sorted sources and key offsets over [K0, K1] (off[k] = first position with key >= k; gaps
+    // filled; off[K1] is written by both neighbouring parts with the same value)
     for (int p = threadIdx.x; p <= n; p += kSegThreads) {
-        if (p < n) vals_out[pbase + p] = vbase + vA[p];
-        const int lo = p == 0 ? 0 : (int)kA[p - 1] + 1;
-        const int hi = p == n ? T : (int)kA[p];
-        for (int k = lo; k <= hi; ++k) off[kbase + k] = (uint32_t)(pbase + p);
+        if (p < n) vals_out[obase + p] = vbase + vA[p];
+        const int lo = p == 0 ? K0 : (int)kA[p - 1] + 1;
+        const int hi = p == n ? K1 : (int)kA[p];
+        for (int k = lo; k <= hi; ++k) off[kbase + k] = (uint32_t)(obase + p);
     }
 }
 
@@ -631,7 +691,11 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
         const int nmax = std::max(p.N, p.M);
         const size_t smem = seg_sort_smem(nmax);
         ensure_smem_attr((const void*)seg_sort_kernel, (int)seg_sort_smem(kSegMax));
-        seg_sort_kernel<<<2 * p.B, kSegThreads, smem, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, nmax, vals[0], off);
+        // 2^lparts CTAs per segment (split by the keys' top bits) while the segments alone leave SMs idle
+        int lparts = 0;
+        while (lparts < 3 && (int64_t)2 * p.B << (lparts + 1) <= sm_count()) ++lparts;
+        seg_sort_kernel<<<(unsigned)((int64_t)2 * p.B << lparts), kSegThreads, smem, st>>>(
+            idx_xy, idx_yx, p.B, p.N, p.M, nmax, lparts, vals[0], off);
     } else {
         const int D = 1 << p.digit_bits;
         keys_hist_kernel<<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles,
