@@ -26,5 +26,15 @@ pts, fi, ba = cd.sample_mesh(v, f, torch.from_numpy(rf).cuda(), torch.from_numpy
 cd.sample_mesh_backward(f, fi, ba, V.shape[1], torch.ones_like(pts))
 d, fi2, cl, ba2, pb, loss = cd.p2s_forward(pts.contiguous(), v, f)
 cd.p2s_backward(pts, cl, fi2, ba2, f, V.shape[1], g_scalar=1.0)
+cd.p2s_forward(pts.contiguous(), v, f, algorithm="pruned")                       # incl. the tie re-walk
+far = (pts * 4.0 + 2.0).contiguous()
+cd.p2s_forward(far, v, f, algorithm="pruned")
+# backward both ways round the segment-sort limit, with a single-target segment
+for (B, N, M) in [(3, 24576, 5), (1, 24577, 40)]:
+    X, Y = synth.uniform_pair(B, N, M, seed=3)
+    x, y = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    ixy = torch.zeros((B, N), dtype=torch.int32, device="cuda")
+    iyx = torch.randint(0, N, (B, M), dtype=torch.int32, device="cuda")
+    cd.backward(x, y, ixy, iyx, g_scalar=1.0, h_scalar=1.0)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
