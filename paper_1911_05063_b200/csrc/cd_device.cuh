@@ -1,6 +1,7 @@
 // cd_device.cuh — device-side helpers for libcd (sm_100a only).
 // Packed-FP32 (f32x2) arithmetic, mbarrier + 1-D TMA bulk copies, and the fixed distance formula.
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -9,6 +10,24 @@
 #endif
 
 namespace cdk {
+
+// Device bounds checks for debug builds (-DCD_DEBUG_CHECKS=1, tools/build_variant.py): a failed check
+// traps the kernel (cudaErrorLaunchFailure / assert) instead of corrupting memory.
+#if CD_DEBUG_CHECKS
+#define CD_CHECK(cond)                                                                          \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("CD_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define CD_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 
 typedef unsigned long long u64;
 

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
     for (int i = threadIdx.x; i < nvalid; i += kSortThreads) {
         const uint32_t key = skey[i];
         const uint32_t pos = (uint32_t)i + delta[(key >> shift) & (D - 1)];
+        CD_CHECK(pos < (uint64_t)L);
         kout[pos] = key;
         vout[pos] = sval[i];
     }
@@ -316,6 +317,7 @@ __device__ __forceinline__ void seg_place(const uint16_t* kA, const uint16_t* vA
         const uint32_t before = valid ? my[digit] : 0u;
         if (valid) {
             const uint32_t pos = before + __popc(peers & lt_mask);
+            CD_CHECK(pos < (uint32_t)n);
             kB[pos] = key;
             vB[pos] = vA[e];
             if (!last) atomicAdd(&wnext[(pos >> lspan) * D + (((uint32_t)key >> (shift + DB)) & (D - 1))], 1u);
@@ -390,6 +392,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
         base_u += wsum[1][w];
     }
     const int n = (int)n_u;                  // edges of this part
+    CD_CHECK(n <= nmax && (int64_t)base_u + n <= nseg);
     const int64_t obase = pbase + base_u;    // sorted positions of this part
     const int passes = kb_low > 0 ? (kb_low + kSegDigitBits - 1) / kSegDigitBits : 0;
     const int db = passes > 0 ? (kb_low + passes - 1) / passes : 1;
@@ -415,6 +418,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
                 const uint32_t m = __ballot_sync(0xffffffffu, in);
                 if (in) {
                     const uint32_t pos = run + __popc(m & lt_mask);
+                    CD_CHECK(pos < (uint32_t)n && (pos >> lspan) < (uint32_t)kSegWarps);
                     kA[pos] = (uint16_t)k[u];
                     vA[pos] = (uint16_t)(e0 + u * 32 + lane);
                     if (passes > 0) atomicAdd(&wcur[(pos >> lspan) * D + (k[u] & (D - 1))], 1u);
@@ -488,6 +492,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
         if (p < n) vals_out[obase + p] = vbase + vA[p];
         const int lo = p == 0 ? K0 : (int)kA[p - 1] + 1;
         const int hi = p == n ? K1 : (int)kA[p];
+        CD_CHECK(lo >= K0 && hi <= K1);
         for (int k = lo; k <= hi; ++k) off[kbase + k] = (uint32_t)(obase + p);
     }
 }

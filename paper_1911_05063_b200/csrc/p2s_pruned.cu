@@ -605,6 +605,7 @@ __device__ __forceinline__ void ps_tie_row(const PsTieArgs& a, int64_t srow, int
 #endif
             if (mine >= 0) {
                 const int f = tm * kPsTile + (mine >> 5) * kBlockK + (lane & 15) * 2;   // faces f, f + 1
+                CD_CHECK(tm >= 0 && tm < nt && f + 1 < a.Fpad);
                 float fa[kFaceFloats], fb[kFaceFloats];
                 load_face_record(FD + (int64_t)f * kFaceFloats, fa);
                 load_face_record(FD + (int64_t)(f + 1) * kFaceFloats, fb);
@@ -628,6 +629,7 @@ __device__ __forceinline__ void ps_tie_row(const PsTieArgs& a, int64_t srow, int
 __global__ void __launch_bounds__(256) ps_tie_kernel(PsTieArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned count = *a.tiecount;
+    CD_CHECK(count <= (unsigned)((int64_t)a.B * a.N));
     for (unsigned qi = blockIdx.x * 8 + (threadIdx.x >> 5); qi < count; qi += gridDim.x * 8)
         ps_tie_row(a, a.tiequeue[qi], lane);
 }
