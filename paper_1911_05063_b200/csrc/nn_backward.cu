@@ -545,8 +545,10 @@ __global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
             }
             const int64_t key = (int64_t)a.B * a.M + b * a.N + i;
             const uint32_t e0 = a.off[key], e1 = a.off[key + 1];
+            CD_CHECK(e0 <= e1 && e1 <= (uint32_t)((int64_t)a.B * (a.N + a.M)));
             for (uint32_t e = e0; e < e1; ++e) {
                 const uint32_t src = a.vals[e];  // y row b*M + j
+                CD_CHECK(src < (uint32_t)((int64_t)a.B * a.M));
                 const double hj = a.h ? (double)a.h[src] : (double)a.h_scalar;
                 acc_term(acc, p, a.y + (int64_t)src * 3, hj);
             }
@@ -570,8 +572,10 @@ __global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
             }
             const int64_t key = b * a.M + j;
             const uint32_t e0 = a.off[key], e1 = a.off[key + 1];
+            CD_CHECK(e0 <= e1 && e1 <= (uint32_t)((int64_t)a.B * (a.N + a.M)));
             for (uint32_t e = e0; e < e1; ++e) {
                 const uint32_t src = a.vals[e];  // x row b*N + i
+                CD_CHECK(src < (uint32_t)((int64_t)a.B * a.N));
                 const double gi = a.g ? (double)a.g[src] : (double)a.g_scalar;
                 acc_term(acc, p, a.x + (int64_t)src * 3, gi);
             }

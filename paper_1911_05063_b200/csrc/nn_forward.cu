@@ -263,6 +263,7 @@ __device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
             const float4 qp = a.pack[dir][(int64_t)b * a.ppad[dir] + a.qlo[dir] + sq];
             const float4* T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
             const int jend = min(bb + kBlockK, a.npts[tdir]);
+            CD_CHECK(bb < a.npts[tdir] && bb % kBlockK == 0);
             // chunks of 8 independent loads (memory-level parallelism), first match wins
             for (int c = bb; c < jend && idx < 0; c += 8) {
                 float d[8];
@@ -324,6 +325,7 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
         if ((long long)key != kColKeyEmpty && __uint_as_float((unsigned)(key >> 32)) < INFINITY) {
             m = __uint_as_float((unsigned)(key >> 32));
             const int i0 = (int)(unsigned)(key & 0xffffffffull);
+            CD_CHECK(i0 >= a.q0 && i0 < a.q1);
             const float4 t = a.yp[(int64_t)b * a.ypad + j];
             const float4* X = a.xp + (int64_t)b * a.xpad;
             const int iend = min(i0 + kR, a.q1);

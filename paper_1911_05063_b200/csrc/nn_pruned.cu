@@ -595,6 +595,7 @@ __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolve
         const int bbt = a.best_blk[dir][(int64_t)b * P + p];
         const bool tie = bbt != -1 && (bbt & (int)0x80000000) != 0;
         const int bb = bbt == -1 ? -1 : (bbt & 0x7fffffff);
+        CD_CHECK(bb < a.ppad[tc]);
         int idx = -1;
         if (bb >= 0) {
             // the lowest ORIGINAL index among the block's targets at the minimum distance

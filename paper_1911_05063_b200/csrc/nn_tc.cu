@@ -635,6 +635,7 @@ __global__ void __launch_bounds__(256) tc_fallback_kernel(TcResolveArgs a) {
         const int n = a.npts[dir], nT = a.npts[1 - dir];
         const int b = (int)(g / n);
         const int i = (int)(g - (int64_t)b * n);
+        CD_CHECK(b < a.B && i < n);
         const float4 q = a.pack[dir][(int64_t)b * a.ppad[dir] + i];
         const float4* T = a.pack[1 - dir] + (int64_t)b * a.ppad[1 - dir];
         float bd = INFINITY;
