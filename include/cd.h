@@ -269,9 +269,10 @@ CD_API cd_status cd_p2s_forward_pruned(const float* points, const float* verts, 
 
 /*
  * cd_step_host_overlapped — cd_step_host with the host->device copies overlapped with the compute:
- * the clouds are copied in `nchunks` batch ranges on `copy_stream`; the forward of range c runs on
- * `stream` as soon as range c has landed (cudaStreamWaitEvent), while later ranges are still in
- * flight; finalize, backward and the D2H copies follow on `stream`.  Results are identical to
+ * the clouds are copied in `nchunks` batch ranges on `copy_stream` (the first range half an equal
+ * share, max(1, B / (2 nchunks)) elements, since only its copy is exposed; the rest split equally);
+ * the forward of range c runs on `stream` as soon as range c has landed (cudaStreamWaitEvent), while
+ * later ranges are still in flight; finalize, backward and the D2H copies follow on `stream`.  Results are identical to
  * cd_step_host (per-batch outputs do not depend on the chunking).  events: nchunks + 1 cudaEvent_t
  * created by the caller (disable-timing events are fine); events[nchunks] is recorded at the end of
  * the step, and the next call's copies wait on it before overwriting the staging buffers.

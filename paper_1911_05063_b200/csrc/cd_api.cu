@@ -556,6 +556,9 @@ cd_status cd_step_host(const float* x_host, const float* y_host, int B, int N, i
     return cuda_status(e, "cd_step_host D2H");
 }
 
+#ifndef CD_STEP_FIRST_DIV
+#define CD_STEP_FIRST_DIV 2
+#endif
 cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int B, int N, int M, float tau, float w1,
                                   float w2, float* loss_host, float* fscore_host, float* grad_x_host,
                                   float* grad_y_host, int nchunks, void* workspace, size_t workspace_bytes,
@@ -590,10 +593,18 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
     float* gy = reinterpret_cast<float*>(w + L.gy);
     void* inner = w + L.inner;
     cudaEvent_t done = static_cast<cudaEvent_t>(events[nchunks]);
+    // batch ranges: the first range is 1/CD_STEP_FIRST_DIV of an equal share (its copy is the only
+    // exposed one), the rest split equally
+    auto bound = [&](int c) -> int {
+        if (c <= 0) return 0;
+        if (c >= nchunks) return B;
+        const int first = std::max(1, (int)((int64_t)B / ((int64_t)nchunks * CD_STEP_FIRST_DIV)));
+        return first + (int)((int64_t)(B - first) * (c - 1) / (nchunks - 1));
+    };
     // the staging buffers are free once the previous step on `stream` is done (never-recorded: no-op)
     cudaError_t e = cudaStreamWaitEvent(cs, done, 0);
     for (int c = 0; c < nchunks && e == cudaSuccess; ++c) {
-        const int b0 = (int)((int64_t)B * c / nchunks), b1 = (int)((int64_t)B * (c + 1) / nchunks);
+        const int b0 = bound(c), b1 = bound(c + 1);
         e = cudaMemcpyAsync(x + (size_t)b0 * N * 3, x_host + (size_t)b0 * N * 3, (size_t)(b1 - b0) * N * 12,
                             cudaMemcpyHostToDevice, cs);
         if (e == cudaSuccess)
@@ -604,7 +615,7 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
     if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped H2D");
     // chunk c's forward starts as soon as its clouds have landed; later chunks copy meanwhile
     for (int c = 0; c < nchunks; ++c) {
-        const int b0 = (int)((int64_t)B * c / nchunks), b1 = (int)((int64_t)B * (c + 1) / nchunks);
+        const int b0 = bound(c), b1 = bound(c + 1);
         e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(events[c]), 0);
         if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped wait");
         s = cd_forward(x + (size_t)b0 * N * 3, y + (size_t)b0 * M * 3, b1 - b0, N, M, 0, N, 0, M,

@@ -466,7 +466,7 @@ def test_step_host_overlapped_equals_step_host(cd):
     X, Y = synth.shape_pair(8, 3000, 2500, config_index=29)
     xh, yh = cd.pinned_copy(X), cd.pinned_copy(Y)
     ref = cd.step_host(xh.numpy(), yh.numpy(), tau=0.01, want_grads=False)
-    for nchunks in (1, 3, 8):
+    for nchunks in (1, 2, 3, 8, None):          # None: the default (2 ranges, the first short)
         st = cd.HostStepper(8, 3000, 2500, tau=0.01, nchunks=nchunks)
         for _ in range(2):                      # back-to-back steps reuse the staging buffers
             loss, fs = st.step(xh, yh)
