@@ -11,6 +11,19 @@
 
 namespace cdk {
 
+// Programmatic dependent launch (CD_PDL): kernels of the step are launched with programmatic stream
+// serialisation so that a kernel's launch and CTA rasterisation overlap its predecessor's tail; every
+// such kernel calls pdl_wait() before touching memory its predecessors wrote or read (it returns once
+// the predecessor grid has completed and its writes are visible; a no-op without a programmatic edge).
+#ifndef CD_PDL
+#define CD_PDL 0
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if CD_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // Device bounds checks for debug builds (-DCD_DEBUG_CHECKS=1, tools/build_variant.py): a failed check
 // traps the kernel (cudaErrorLaunchFailure / assert) instead of corrupting memory.
 #if CD_DEBUG_CHECKS

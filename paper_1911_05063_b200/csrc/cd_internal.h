@@ -1,5 +1,6 @@
 // cd_internal.h — host-side launch plumbing shared by the libcd translation units (not public).
 #pragma once
+#include <utility>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -181,4 +182,26 @@ inline void ensure_smem_attr(const void* func, int bytes) {
     }
 }
 
+
+// Launch with programmatic stream serialisation when CD_PDL (see pdl_wait in cd_device.cuh).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+#if defined(CD_PDL) && CD_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+#else
+    kernel<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+    return cudaSuccess;
+#endif
+}
 }  // namespace cdk

@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
                                                                int M, int nmax, int lparts,
                                                                uint32_t* __restrict__ vals_out,
                                                                uint32_t* __restrict__ off) {
+    pdl_wait();
     extern __shared__ __align__(16) uint32_t smem_seg[];
     uint32_t* wcur = smem_seg;                   // [kSegWarps][D] this pass's per-warp digit counts
     uint32_t* wnext = wcur + kSegWarps * kSegD;  // next pass's, counted while placing
@@ -520,6 +521,7 @@ __device__ __forceinline__ void acc_term(double acc[3], const float* p, const fl
 }
 
 __global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
+    pdl_wait();
     const int sq = a.q1 - a.q0, sr = a.r1 - a.r0;
     const int64_t nx = (int64_t)a.B * sq;
     const int64_t total = nx + (int64_t)a.B * sr;
@@ -703,8 +705,8 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
         // 2^lparts CTAs per segment (split by the keys' top bits) while the segments alone leave SMs idle
         int lparts = 0;
         while (lparts < 3 && (int64_t)2 * p.B << (lparts + 1) <= sm_count()) ++lparts;
-        seg_sort_kernel<<<(unsigned)((int64_t)2 * p.B << lparts), kSegThreads, smem, st>>>(
-            idx_xy, idx_yx, p.B, p.N, p.M, nmax, lparts, vals[0], off);
+        launch_pdl(seg_sort_kernel, dim3((unsigned)((int64_t)2 * p.B << lparts)), dim3(kSegThreads), smem, st,
+                   idx_xy, idx_yx, p.B, p.N, p.M, nmax, lparts, vals[0], off);
     } else {
         const int D = 1 << p.digit_bits;
         keys_hist_kernel<<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles,
@@ -736,7 +738,7 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     const int64_t total = (int64_t)p.B * ((p.q1 - p.q0) + (p.r1 - p.r0));
     if (total > 0) {
         const int grid_g = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32);
-        grad_kernel<<<grid_g, 256, 0, st>>>(a);
+        launch_pdl(grad_kernel, dim3(grid_g), dim3(256), 0, st, a);
     }
     return cudaGetLastError();
 }

@@ -44,6 +44,7 @@ struct PackArgs {
 };
 
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
+    pdl_wait();
     const int64_t n0 = (int64_t)a.B * a.ppad[0];
     const int64_t total = n0 + (int64_t)a.B * a.ppad[1];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -359,6 +360,7 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
 // a.4 epilogue of the forward in ONE launch: blocks [0, merge_blocks) merge the row splits, the rest
 // resolve the fused kernel's column keys (independent work, so the two overlap on the GPU).
 __global__ void __launch_bounds__(kMergeThreads) nn_epilogue_kernel(MergeArgs m, ResolveArgs r, int merge_blocks) {
+    pdl_wait();
     if ((int)blockIdx.x < merge_blocks)
         row_merge_block(m, blockIdx.x);
     else
@@ -415,6 +417,7 @@ struct PartialsArgs {
 };
 
 __global__ void __launch_bounds__(256) partials_kernel(PartialsArgs a) {
+    pdl_wait();
     __shared__ double ssum[256];
     __shared__ long long shit[256];
     const int b = blockIdx.x;
@@ -454,6 +457,7 @@ struct FinalizeArgs {
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs a) {
+    pdl_wait();
     __shared__ double sl[256];
     double acc = 0.0;
     for (int b = threadIdx.x; b < a.B; b += 256) {
@@ -670,7 +674,7 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
         a.nrowkey = p.mode == kFusedCols ? 0 : p.slice_total;
         const int64_t total = (int64_t)p.B * (p.ppad[0] + p.ppad[1]);
         const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)device_sm_count() * 16);
-        pack_kernel<<<grid, 256, 0, st>>>(a);
+        launch_pdl(pack_kernel, dim3(grid), dim3(256), 0, st, a);
     }
     if (p.mode == kUnfused) {
         const int gx = p.qtiles[0] * p.splits[0] + p.qtiles[1] * p.splits[1];
@@ -748,8 +752,8 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
         resolve_chunks = (int64_t)p.B * p.nchunks[1];
     }
     if (merge_chunks + resolve_chunks > 0)
-        nn_epilogue_kernel<<<(unsigned)(merge_chunks + resolve_chunks), kMergeThreads, 0, st>>>(ma, ra,
-                                                                                                (int)merge_chunks);
+        launch_pdl(nn_epilogue_kernel, dim3((unsigned)(merge_chunks + resolve_chunks)), dim3(kMergeThreads), 0, st, ma,
+                   ra, (int)merge_chunks);
     if (o.partials) {
         PartialsArgs a;
         a.chunk_sum = chunk_sum;
@@ -760,7 +764,7 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
         }
         a.partials = o.partials;
         a.dirmask = p.mode == kFusedRows ? 1 : (p.mode == kFusedCols ? 2 : 3);
-        partials_kernel<<<p.B, 256, 0, st>>>(a);
+        launch_pdl(partials_kernel, dim3(p.B), dim3(256), 0, st, a);
     }
     return cudaGetLastError();
 }
@@ -841,7 +845,7 @@ cudaError_t launch_fscore(const float* d_xy, const float* d_yx, int B, int N, in
     f.fscore = fscore;
     f.precision = precision;
     f.recall = recall;
-    finalize_kernel<<<1, 256, 0, st>>>(f);
+    launch_pdl(finalize_kernel, dim3(1), dim3(256), 0, st, f);
     return cudaGetLastError();
 }
 
@@ -859,7 +863,7 @@ cudaError_t launch_finalize(const double* partials, int B, int N, int M, float w
     f.fscore = fscore;
     f.precision = precision;
     f.recall = recall;
-    finalize_kernel<<<1, 256, 0, st>>>(f);
+    launch_pdl(finalize_kernel, dim3(1), dim3(256), 0, st, f);
     return cudaGetLastError();
 }
 

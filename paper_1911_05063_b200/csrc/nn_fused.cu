@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
     __shared__ unsigned char coll[2][kFwdThreads / 32][kTile];
     __shared__ __align__(8) u64 full_bar[kStages];
 
+    pdl_wait();
     const int b = blockIdx.y;
     const int tile = blockIdx.x / a.splits;
     const int split = blockIdx.x - tile * a.splits;
@@ -263,14 +264,14 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
         const dim3 grid(gx, p.B);
         if (p.fused_rows == kR) {
             if (p.split_unit == kTile)
-                nn_fused_kernel<false, kR><<<grid, kFwdThreads, 0, st>>>(a);
+                launch_pdl(nn_fused_kernel<false, kR>, grid, dim3(kFwdThreads), 0, st, a);
             else
-                nn_fused_kernel<true, kR><<<grid, kFwdThreads, 0, st>>>(a);
+                launch_pdl(nn_fused_kernel<true, kR>, grid, dim3(kFwdThreads), 0, st, a);
         } else {   // small clouds: 1024-row query tiles (twice the CTAs per batch element)
             if (p.split_unit == kTile)
-                nn_fused_kernel<false, kRSmall><<<grid, kFwdThreads, 0, st>>>(a);
+                launch_pdl(nn_fused_kernel<false, kRSmall>, grid, dim3(kFwdThreads), 0, st, a);
             else
-                nn_fused_kernel<true, kRSmall><<<grid, kFwdThreads, 0, st>>>(a);
+                launch_pdl(nn_fused_kernel<true, kRSmall>, grid, dim3(kFwdThreads), 0, st, a);
         }
         if (g_prof_stop) record_profile_event(g_prof_stop, st);
     }
