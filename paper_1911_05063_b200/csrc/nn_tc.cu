@@ -622,11 +622,20 @@ __global__ void __launch_bounds__(256) tc_resolve_kernel(TcResolveArgs a) {
     }
 }
 
-// exact brute force for the queued rows: one CTA (256 threads) per row, 8 loads in flight per thread
+// Exact re-scan of the queued rows (the band could not be settled from the merged summaries): one CTA
+// (256 threads) per row.  It re-reads the row's per-CTA summaries and scans only what can hold a
+// target inside the band: the identified chunks whose minimum is inside it, and the WHOLE target
+// range of every CTA whose third chunk minimum is inside it (that CTA's untracked chunks may be
+// too); with thousands of such ranges (never seen) the whole cloud.  Targets are compared
+// lexicographically on (distance, index), so the range order does not matter.
+constexpr int kTcFbRanges = 2048;
 __global__ void __launch_bounds__(256) tc_fallback_kernel(TcResolveArgs a) {
     const unsigned count = *a.fb_count;
     __shared__ float sd[8];
     __shared__ int si[8];
+    __shared__ float s_g1[8];
+    __shared__ int2 s_rng[kTcFbRanges];
+    __shared__ unsigned s_nr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned w = blockIdx.x; w < count; w += gridDim.x) {
         const unsigned item = a.fb_list[w];
@@ -638,19 +647,65 @@ __global__ void __launch_bounds__(256) tc_fallback_kernel(TcResolveArgs a) {
         CD_CHECK(b < a.B && i < n);
         const float4 q = a.pack[dir][(int64_t)b * a.ppad[dir] + i];
         const float4* T = a.pack[1 - dir] + (int64_t)b * a.ppad[1 - dir];
+        const int64_t stride = (int64_t)a.B * n;
+        const int nsum = dir == 0 ? a.splits : a.qblocks;
+        // the band threshold from the smallest approximate minimum (as tc_resolve_kernel)
+        float m = INFINITY;
+        for (int k = threadIdx.x; k < nsum; k += 256) m = fminf(m, a.sums[dir][(int64_t)k * stride + g].x);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) s_g1[warp] = m;
+        if (threadIdx.x == 0) s_nr = 0u;
+        __syncthreads();
+        float g1 = s_g1[0];
+        for (int k = 1; k < 8; ++k) g1 = fminf(g1, s_g1[k]);
+        float cc[3], sc, U;
+        tc_scale(a.box + b * 6, cc, sc, U);
+        const float E = kTcErel * U * U;
+        const float thr = g1 + (2.f * E + (fabsf(g1) + E) * (1.0f / 262144.0f));
+        // ranges to scan
+        for (int k = threadIdx.x; k < nsum; k += 256) {
+            const float4 v = a.sums[dir][(int64_t)k * stride + g];
+            const int cb = dir == 0 ? (int)((int64_t)k * a.ttiles / a.splits) * kTcRows : k * kTcQB;
+            const int ce = dir == 0 ? (int)((int64_t)(k + 1) * a.ttiles / a.splits) * kTcRows : (k + 1) * kTcQB;
+            const unsigned bb = __float_as_uint(v.w);
+            if (v.z <= thr) {
+                const unsigned r = atomicAdd(&s_nr, 1u);
+                if (r < kTcFbRanges) s_rng[r] = make_int2(cb, min(ce, nT));
+            } else {
+                if (v.x <= thr) {
+                    const unsigned r = atomicAdd(&s_nr, 1u);
+                    const int c0 = cb + kTcChunk * (int)(bb & 0xffffu);
+                    if (r < kTcFbRanges) s_rng[r] = make_int2(c0, min(c0 + kTcChunk, nT));
+                }
+                if (v.y <= thr) {
+                    const unsigned r = atomicAdd(&s_nr, 1u);
+                    const int c0 = cb + kTcChunk * (int)(bb >> 16);
+                    if (r < kTcFbRanges) s_rng[r] = make_int2(c0, min(c0 + kTcChunk, nT));
+                }
+            }
+        }
+        __syncthreads();
+        const unsigned nr = s_nr;
+        const bool whole = nr > (unsigned)kTcFbRanges;
         float bd = INFINITY;
         int bi = 0x7fffffff;
-        for (int j0 = 0; j0 < nT; j0 += 256 * 8) {
-            float4 t[8];
+        const unsigned nscan = whole ? 1u : nr;
+        for (unsigned r = 0; r < nscan; ++r) {
+            const int2 rg = whole ? make_int2(0, nT) : s_rng[r];
+            CD_CHECK(rg.x >= 0 && rg.y <= nT);
+            for (int j0 = rg.x; j0 < rg.y; j0 += 256 * 4) {
+                float4 t[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) t[u] = T[min(j0 + 256 * u + (int)threadIdx.x, nT - 1)];
+                for (int u = 0; u < 4; ++u) t[u] = T[min(j0 + 256 * u + (int)threadIdx.x, rg.y - 1)];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {   // j ascending per thread: strict < keeps the lowest index
-                const int j = j0 + 256 * u + (int)threadIdx.x;
-                const float d = dist_rn(q.x, q.y, q.z, t[u].x, t[u].y, t[u].z);
-                if (j < nT && d < bd) {
-                    bd = d;
-                    bi = j;
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 256 * u + (int)threadIdx.x;
+                    const float d = dist_rn(q.x, q.y, q.z, t[u].x, t[u].y, t[u].z);
+                    if (j < rg.y && (d < bd || (d == bd && j < bi))) {
+                        bd = d;
+                        bi = j;
+                    }
                 }
             }
         }
