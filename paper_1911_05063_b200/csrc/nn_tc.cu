@@ -564,28 +564,44 @@ __global__ void __launch_bounds__(256) tc_resolve_kernel(TcResolveArgs a) {
         float my_d = INFINITY;
         int my_i = 0x7fffffff;
         unsigned todo = __ballot_sync(0xffffffffu, nblk > 0);
+        // four rows per step: lane group grp (8 lanes) re-scans the grp-th pending row; its 8 lanes
+        // take interleaved targets of each 64-target chunk (every load instruction covers one
+        // contiguous 128-byte line per row), then an 8-lane (distance, index) reduction
+        const int grp = lane >> 3, gl = lane & 7;
         while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int sdir = __shfl_sync(0xffffffffu, dir, src);
-            const int sb = __shfl_sync(0xffffffffu, b, src);
-            const int snb = __shfl_sync(0xffffffffu, nblk, src);
-            const int s1 = __shfl_sync(0xffffffffu, gb1, src), s2 = __shfl_sync(0xffffffffu, gb2, src);
-            const float qx = __shfl_sync(0xffffffffu, q.x, src), qy = __shfl_sync(0xffffffffu, q.y, src),
-                        qz = __shfl_sync(0xffffffffu, q.z, src);
-            const int snT = a.npts[1 - sdir];
-            const float4* T = a.pack[1 - sdir] + (int64_t)sb * a.ppad[1 - sdir];
+            int src = -1;
+            {
+                unsigned t = todo;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int f = t ? __ffs(t) - 1 : -1;
+                    if (t) t &= t - 1;
+                    if (k == grp) src = f;
+                }
+                todo = t;
+            }
+            const int srcc = src < 0 ? 0 : src;
+            const int sdir = __shfl_sync(0xffffffffu, dir, srcc);
+            const int sb = __shfl_sync(0xffffffffu, b, srcc);
+            const int snb = __shfl_sync(0xffffffffu, nblk, srcc);
+            const int s1 = __shfl_sync(0xffffffffu, gb1, srcc), s2 = __shfl_sync(0xffffffffu, gb2, srcc);
+            const float qx = __shfl_sync(0xffffffffu, q.x, srcc), qy = __shfl_sync(0xffffffffu, q.y, srcc),
+                        qz = __shfl_sync(0xffffffffu, q.z, srcc);
             float bd = INFINITY;
             int bi = 0x7fffffff;
-            for (int h = 0; h < snb; ++h) {
-                const int start = h == 0 ? s1 : s2;
+            if (src >= 0) {
+                const int snT = a.npts[1 - sdir];
+                const float4* T = a.pack[1 - sdir] + (int64_t)sb * a.ppad[1 - sdir];
+                for (int h = 0; h < snb; ++h) {
+                    const int start = h == 0 ? s1 : s2;
+                    float4 t[kTcChunk / 8];
 #pragma unroll
-                for (int u = 0; u < kTcChunk / 32; ++u) {
-                    const int j = start + 32 * u + lane;
-                    if (j < snT) {
-                        const float4 t = T[j];
-                        const float d = dist_rn(qx, qy, qz, t.x, t.y, t.z);
-                        if (d < bd || (d == bd && j < bi)) {
+                    for (int u = 0; u < kTcChunk / 8; ++u) t[u] = T[min(start + 8 * u + gl, snT - 1)];
+#pragma unroll
+                    for (int u = 0; u < kTcChunk / 8; ++u) {   // j ascending per lane
+                        const int j = start + 8 * u + gl;
+                        const float d = dist_rn(qx, qy, qz, t[u].x, t[u].y, t[u].z);
+                        if (j < snT && (d < bd || (d == bd && j < bi))) {
                             bd = d;
                             bi = j;
                         }
@@ -593,7 +609,7 @@ __global__ void __launch_bounds__(256) tc_resolve_kernel(TcResolveArgs a) {
                 }
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
+            for (int o = 4; o > 0; o >>= 1) {
                 const float od = __shfl_xor_sync(0xffffffffu, bd, o);
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (od < bd || (od == bd && oi < bi)) {
@@ -601,9 +617,15 @@ __global__ void __launch_bounds__(256) tc_resolve_kernel(TcResolveArgs a) {
                     bi = oi;
                 }
             }
-            if (lane == src) {
-                my_d = bd;
-                my_i = bi;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {   // hand each group's result to the row's own lane
+                const int ks = __shfl_sync(0xffffffffu, src, 8 * k);
+                const float kd = __shfl_sync(0xffffffffu, bd, 8 * k);
+                const int ki = __shfl_sync(0xffffffffu, bi, 8 * k);
+                if (lane == ks) {
+                    my_d = kd;
+                    my_i = ki;
+                }
             }
         }
         if (valid) {
