@@ -1,5 +1,9 @@
 // nn_backward.cu — backward of the Chamfer per-point distances, argmin held fixed
-// (SURVEY.md §8.a.6-a.8).  Deterministic and free of floating-point atomics:
+// (SURVEY.md §8.a.6-a.8).  Deterministic and free of floating-point atomics.
+//
+// Clouds of <= kSegMax points (c1-c3): seg_sort_kernel (one or 2^p CTAs per (direction, batch)
+// segment; on-chip stable LSD sort of the segment's edges, see below) writes the sorted sources and
+// the key offsets directly, then grad_kernel: 2 launches.  Larger clouds (c4, c5):
 //
 //   keys_hist_kernel one (key, value) pair per NN edge: xy edge i -> a_i gets key b*M + a_i,
 //                    yx edge j -> b_j gets key B*M + b*N + b_j; value = the source row.  Built in
