@@ -24,9 +24,16 @@
 //                        chunks, one CTA each, that start from those bounds, stop once the list's LB
 //                        exceeds every row's bound and merge improvements with atomicMin on the keys
 //                        (order-independent: deterministic).
-//   ps_resolve_kernel    exact face inside the winning block (same fp32 ops; first in sorted order),
-//                        fp64 closest point / barycentrics / distance on that face, outputs in the
-//                        original point order, fp64 chunk sums; then p2s_finalize (p2s.cu).
+//                        Exact ties between blocks (a block minimum EQUAL to the current one, or an
+//                        equal key from another chunk, seen in atomicMin's return value) flag the
+//                        point and queue it once.
+//   ps_tie_kernel        flagged points: re-walk the LB-sorted candidate tiles while LB <= the minimum
+//                        and keep the lowest ORIGINAL face index at the minimum (R3', the brute
+//                        force's rule; persistent warps over the queue).
+//   ps_resolve_kernel    the face: the tie result, else the lowest original index at the minimum inside
+//                        the winning block (same fp32 ops); fp64 closest point / barycentrics /
+//                        distance on that face, outputs in the original point order, fp64 chunk
+//                        sums; then p2s_finalize (p2s.cu).  Outputs are bit-identical to p2s.cu's.
 #include "cd_internal.h"
 #include "p2s_common.cuh"
 
