@@ -35,8 +35,12 @@ constexpr int kSortWarps = kSortThreads / 32;
 #ifndef CD_SORT_MINB
 #define CD_SORT_MINB 1
 #endif
-constexpr int kSortItems = CD_SORT_ITEMS;
-constexpr int kSortTile = kSortThreads * kSortItems;  // elements per tile (kSortItems * 32 per warp)
+constexpr int kSortItems = CD_SORT_ITEMS;           // elements per thread per tile (digits <= 9 bits)
+constexpr int kSortItemsWide = 24;                   // ... for 10-11-bit digits: the per-tile digit scans
+                                                     // (8 warps x D counters) amortised over 1.5x the tile
+// elements per thread of a sort whose digits have `digit_bits` bits (measured: c4 backward, two
+// 11-bit passes, 0.187 -> 0.164 ms with 24; 8-bit digits gain nothing)
+inline int sort_items(int digit_bits) { return digit_bits >= 10 ? kSortItemsWide : kSortItems; }
 #ifndef CD_SORT_BALLOT
 #define CD_SORT_BALLOT 1
 #endif
@@ -47,6 +51,7 @@ constexpr int kMaxDigitBits = CD_SORT_MAXBITS;        // digits of up to 11 bits
 
 // Edge keys fused with the first radix pass's per-tile histogram: one CTA per sort
 // tile writes its 4096 (key, value) pairs and counts digit 0 (saves a launch and a read of the keys).
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(const int32_t* __restrict__ idx_xy,
                                                                  const int32_t* __restrict__ idx_yx, int B, int N,
                                                                  int M, int D, int ntiles, uint32_t* __restrict__ keys,
@@ -57,9 +62,9 @@ __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(const int32_t* 
     __syncthreads();
     const int64_t L0 = (int64_t)B * N;
     const int64_t L = L0 + (int64_t)B * M;
-    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    const int64_t base = (int64_t)blockIdx.x * (kSortThreads * ITEMS);
 #pragma unroll 4
-    for (int k = 0; k < kSortItems; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {
         const int64_t p = base + (int64_t)k * kSortThreads + threadIdx.x;
         if (p < L) {
             uint32_t key, val;
@@ -85,21 +90,22 @@ __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(const int32_t* 
 }
 
 // counts[digit * ntiles + tile]; D = 1 << digit bits (dynamic shared memory: D words)
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t L,
                                                                   int shift, int D, int ntiles,
                                                                   uint32_t* __restrict__ counts) {
     extern __shared__ uint32_t hist[];
     for (int d = threadIdx.x; d < D; d += kSortThreads) hist[d] = 0;
     __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kSortTile;
-    uint32_t kk[kSortItems];
+    const int64_t base = (int64_t)blockIdx.x * (kSortThreads * ITEMS);
+    uint32_t kk[ITEMS];
 #pragma unroll
-    for (int k = 0; k < kSortItems; ++k) {   // all loads in flight before the shared-memory adds
+    for (int k = 0; k < ITEMS; ++k) {   // all loads in flight before the shared-memory adds
         const int64_t e = min(base + (int64_t)k * kSortThreads + threadIdx.x, L - 1);
         asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(kk[k]) : "l"(keys + e));
     }
 #pragma unroll
-    for (int k = 0; k < kSortItems; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {
         const int64_t e = base + (int64_t)k * kSortThreads + threadIdx.x;
         if (e < L) atomicAdd(&hist[(kk[k] >> shift) & (D - 1)], 1u);  // integer adds: order-free
     }
@@ -154,7 +160,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* _
 // of the tile's digit counts) plus the prefix over the warps; delta[d] = global base - local start.
 // Phase 3: the tile is re-ordered by digit in shared memory, then written out so that consecutive
 // threads write consecutive addresses of each digit's run (coalesced stores).
-// Dynamic shared memory: (kSortWarps + 2) * D + 2 * kSortTile words.
+// Dynamic shared memory: (kSortWarps + 2) * D + 2 * tile words (tile = kSortThreads * ITEMS).
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB : 2) radix_scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int D, int ntiles,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals, uint32_t* __restrict__ kout,
@@ -163,8 +170,8 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
     uint32_t* wcnt = smem;                       // [kSortWarps][D]
     uint32_t* dbase = smem + kSortWarps * D;     // [D] global base of digit d for this tile
     uint32_t* delta = dbase + D;                 // [D] global base - tile-local start
-    uint32_t* skey = delta + D;                  // [kSortTile] tile re-ordered by digit
-    uint32_t* sval = skey + kSortTile;
+    uint32_t* skey = delta + D;                  // [(kSortThreads * ITEMS)] tile re-ordered by digit
+    uint32_t* sval = skey + (kSortThreads * ITEMS);
     __shared__ uint32_t warp_tot[kSortWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -185,15 +192,15 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
     }
     __syncthreads();
     const uint32_t lt_mask = (1u << lane) - 1u;
-    const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
-    const int64_t wbase = tbase + (int64_t)warp * (kSortItems * 32);
-    uint32_t kk[kSortItems], vv[kSortItems], rk[kSortItems];
+    const int64_t tbase = (int64_t)blockIdx.x * (kSortThreads * ITEMS);
+    const int64_t wbase = tbase + (int64_t)warp * (ITEMS * 32);
+    uint32_t kk[ITEMS], vv[ITEMS], rk[ITEMS];
     uint32_t* my = wcnt + warp * D;
     // all 16 loads first (independent: full memory-level parallelism), then the ranking rounds
     // all loads issued before the ranking rounds, as volatile loads: the compiler would otherwise
     // re-issue (rematerialise) each read-only load at its first use, exposing one memory latency per round
 #pragma unroll
-    for (int k = 0; k < kSortItems; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {
         const int64_t e = min(wbase + k * 32 + lane, L - 1);
         asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(kk[k]) : "l"(kin + e));
         asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(vv[k]) : "l"(vin + e));
@@ -201,11 +208,11 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
     {
         uint32_t all = 0;
 #pragma unroll
-        for (int k = 0; k < kSortItems; ++k) all ^= kk[k];
+        for (int k = 0; k < ITEMS; ++k) all ^= kk[k];
         asm volatile("" ::"r"(all));   // every key has arrived before the first ranking round
     }
 #pragma unroll
-    for (int k = 0; k < kSortItems; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {
         const int64_t e = wbase + k * 32 + lane;
         const bool valid = e < L;
         const int digit = valid ? (int)((kk[k] >> shift) & (D - 1)) : D;  // D: sentinel group
@@ -248,9 +255,9 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
         }
     }
     __syncthreads();
-    const int nvalid = (int)min((int64_t)kSortTile, L - tbase);
+    const int nvalid = (int)min((int64_t)(kSortThreads * ITEMS), L - tbase);
 #pragma unroll
-    for (int k = 0; k < kSortItems; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {
         const int64_t e = wbase + k * 32 + lane;
         if (e < L) {
             const uint32_t lp = my[(kk[k] >> shift) & (D - 1)] + rk[k];
@@ -609,7 +616,8 @@ void radix_sort_plan(int64_t L, int nbits, int& npasses, int& digit_bits, int& n
     nbits = std::max(nbits, 1);
     npasses = (nbits + kMaxDigitBits - 1) / kMaxDigitBits;
     digit_bits = (nbits + npasses - 1) / npasses;
-    ntiles = (int)((L + kSortTile - 1) / kSortTile);
+    const int tile = kSortThreads * sort_items(digit_bits);
+    ntiles = (int)((L + tile - 1) / tile);
 }
 
 size_t radix_sort_counts_words(int64_t L, int nbits) {
@@ -626,16 +634,30 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits,
     int npasses, digit_bits, ntiles;
     radix_sort_plan(L, nbits, npasses, digit_bits, ntiles);
     const int D = 1 << digit_bits;
-    const size_t scatter_smem = ((size_t)(kSortWarps + 2) * D + 2 * kSortTile) * 4;
-    ensure_smem_attr((const void*)radix_scatter_kernel, ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile) * 4);
+    const int items = sort_items(digit_bits);
+    const size_t scatter_smem = ((size_t)(kSortWarps + 2) * D + 2 * kSortThreads * items) * 4;
+    ensure_smem_attr((const void*)radix_scatter_kernel<kSortItems>,
+                     ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortThreads * kSortItems) * 4);
+    ensure_smem_attr((const void*)radix_scatter_kernel<kSortItemsWide>,
+                     ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortThreads * kSortItemsWide) * 4);
     int cur = 0;
     for (int pass = 0; pass < npasses; ++pass) {
         const int shift = pass * digit_bits;
-        if (!(pass == 0 && first_hist_done))
-            radix_hist_kernel<<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D, ntiles, counts);
+        if (!(pass == 0 && first_hist_done)) {
+            if (items == kSortItemsWide)
+                radix_hist_kernel<kSortItemsWide><<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D,
+                                                                                              ntiles, counts);
+            else
+                radix_hist_kernel<kSortItems><<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D, ntiles,
+                                                                                          counts);
+        }
         radix_rowscan_kernel<<<D, kSortThreads, 0, st>>>(counts, ntiles, totals);
-        radix_scatter_kernel<<<ntiles, kSortThreads, scatter_smem, st>>>(keys[cur], vals[cur], L, shift, D, ntiles,
-                                                                         counts, totals, keys[1 - cur], vals[1 - cur]);
+        if (items == kSortItemsWide)
+            radix_scatter_kernel<kSortItemsWide><<<ntiles, kSortThreads, scatter_smem, st>>>(
+                keys[cur], vals[cur], L, shift, D, ntiles, counts, totals, keys[1 - cur], vals[1 - cur]);
+        else
+            radix_scatter_kernel<kSortItems><<<ntiles, kSortThreads, scatter_smem, st>>>(
+                keys[cur], vals[cur], L, shift, D, ntiles, counts, totals, keys[1 - cur], vals[1 - cur]);
         cur = 1 - cur;
     }
     return cur;
@@ -713,8 +735,12 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
                    idx_xy, idx_yx, p.B, p.N, p.M, nmax, lparts, vals[0], off);
     } else {
         const int D = 1 << p.digit_bits;
-        keys_hist_kernel<<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles,
-                                                                        keys[0], vals[0], counts);
+        if (sort_items(p.digit_bits) == kSortItemsWide)
+            keys_hist_kernel<kSortItemsWide><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
+                idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles, keys[0], vals[0], counts);
+        else
+            keys_hist_kernel<kSortItems><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
+                idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles, keys[0], vals[0], counts);
         cur = radix_sort_pairs(keys, vals, p.L, p.nbits, counts, totals, st, /*first_hist_done=*/true);
         const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);
         offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], p.L, p.kmax, off);
