@@ -22,6 +22,7 @@
 //                    .rn ops (no contraction), one fp32 store.
 #include "cd_device.cuh"
 #include "cd_internal.h"
+#include "seg_sort.cuh"
 
 #include <algorithm>
 
@@ -293,52 +294,6 @@ __global__ void __launch_bounds__(256) offsets_kernel(const uint32_t* __restrict
 // counts of a pass are integer shared-memory adds made while loading / while placing the previous
 // pass), then the sorted sources and the segment's key offsets (gap fill) go to global memory.
 // Replaces keys_hist + the global passes + offsets_kernel: 2 launches per backward, not 3 passes + 2.
-constexpr int kSegThreads = 512;
-constexpr int kSegWarps = kSegThreads / 32;
-constexpr int kSegMax = 24576;   // 8 B per edge + 32 KB of counters <= 227 KB of shared memory
-constexpr int kSegDigitBits = 7;
-constexpr int kSegD = 1 << kSegDigitBits;
-
-size_t seg_sort_smem(int nmax) { return (size_t)nmax * 8 + 2 * (size_t)kSegWarps * kSegD * 4 + 1024; }
-
-// One placement sweep of seg_sort_kernel with DB-bit digits (compile-time: unrolled ballots).
-template <int DB>
-__device__ __forceinline__ void seg_place(const uint16_t* kA, const uint16_t* vA, uint16_t* kB, uint16_t* vB,
-                                          uint32_t* wcur, uint32_t* wnext, int n, int R, int lspan, int shift,
-                                          bool last) {
-    constexpr uint32_t D = 1u << DB;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    uint32_t* my = wcur + warp * D;
-    for (int t = 0; t < R; ++t) {
-        const int e0 = (warp * R + t) * 32;
-        if (e0 >= n) break;   // warp-uniform
-        const int e = e0 + lane;
-        const bool valid = e < n;
-        const uint16_t key = valid ? kA[e] : (uint16_t)0;
-        const uint32_t digit = ((uint32_t)key >> shift) & (D - 1);
-        uint32_t peers = __ballot_sync(0xffffffffu, valid);
-        if (!valid) peers = ~peers;
-#pragma unroll
-        for (int bt = 0; bt < DB; ++bt) {
-            const bool bit = (digit >> bt) & 1u;
-            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-            peers &= bit ? bal : ~bal;
-        }
-        const uint32_t before = valid ? my[digit] : 0u;
-        if (valid) {
-            const uint32_t pos = before + __popc(peers & lt_mask);
-            CD_CHECK(pos < (uint32_t)n);
-            kB[pos] = key;
-            vB[pos] = vA[e];
-            if (!last) atomicAdd(&wnext[(pos >> lspan) * D + (((uint32_t)key >> (shift + DB)) & (D - 1))], 1u);
-        }
-        __syncwarp();
-        if (valid && (peers & lt_mask) == 0u) my[digit] = before + __popc(peers);
-        __syncwarp();
-    }
-}
-
 __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __restrict__ idx_xy,
                                                                const int32_t* __restrict__ idx_yx, int B, int N,
                                                                int M, int nmax, int lparts,
@@ -439,64 +394,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
             }
         }
     }
-    for (int pass = 0; pass < passes; ++pass) {
-        const int shift = pass * db;
-        const bool last = pass + 1 == passes;
-        __syncthreads();
-        // digit starts, then per-warp starts inside each digit run
-        if (threadIdx.x < D) {
-            uint32_t tot = 0;
-            for (int w = 0; w < kSegWarps; ++w) tot += wcur[w * D + threadIdx.x];
-            dstart[threadIdx.x] = tot;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t c[kSegD / 32], loc = 0;
-#pragma unroll
-            for (int r = 0; r < kSegD / 32; ++r) {
-                const int d = lane * (kSegD / 32) + r;
-                c[r] = d < D ? dstart[d] : 0u;
-                loc += c[r];
-            }
-            uint32_t incl = loc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            uint32_t run = incl - loc;
-#pragma unroll
-            for (int r = 0; r < kSegD / 32; ++r) {
-                const int d = lane * (kSegD / 32) + r;
-                if (d < D) dstart[d] = run;
-                run += c[r];
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < D) {
-            uint32_t run = dstart[threadIdx.x];
-            for (int w = 0; w < kSegWarps; ++w) {
-                const uint32_t c = wcur[w * D + threadIdx.x];
-                wcur[w * D + threadIdx.x] = run;
-                run += c;
-            }
-        }
-        for (int i = threadIdx.x; i < kSegWarps * kSegD; i += kSegThreads) wnext[i] = 0;
-        __syncthreads();
-        // stable placement: each warp walks its range in order; ranks from a ballot multisplit
-        switch (db) {
-            case 1: seg_place<1>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
-            case 2: seg_place<2>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
-            case 3: seg_place<3>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
-            case 4: seg_place<4>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
-            case 5: seg_place<5>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
-            case 6: seg_place<6>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
-            default: seg_place<7>(kA, vA, kB, vB, wcur, wnext, n, R, lspan, shift, last); break;
-        }
-        uint16_t* tv = vA; vA = vB; vB = tv;
-        uint16_t* tk = kA; kA = kB; kB = tk;
-        uint32_t* tw = wcur; wcur = wnext; wnext = tw;
-    }
+    seg_lsd_passes(kA, vA, kB, vB, wcur, wnext, dstart, n, passes, db, lspan, R);
     __syncthreads();
     // sorted sources and key offsets over [K0, K1] (off[k] = first position with key >= k; gaps
     // filled; off[K1] is written by both neighbouring parts with the same value)

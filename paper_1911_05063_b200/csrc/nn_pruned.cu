@@ -21,6 +21,7 @@
 // force returns the lowest index); any such index is an exact nearest neighbour (R3').
 #include "cd_device.cuh"
 #include "cd_internal.h"
+#include "seg_sort.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -159,6 +160,81 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
         const int b = (int)(f / w);
         const int p = a.npts[c] + (int)(f - (int64_t)b * w);
         a.sorted[c][(int64_t)b * a.ppad[c] + p] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+    }
+}
+
+
+// ------------------------------------------------------------------------------ on-chip Hilbert sort
+// Clouds of <= kSegMax points: one CTA per (cloud, batch element) computes 14-bit Hilbert keys (a 32^3
+// grid over the element's box, top 14 of 15 bits), sorts them stably on chip (seg_sort.cuh: two 7-bit
+// passes) and writes the sorted packed points, the permutation and the +inf padding directly —
+// replacing hilbert_kernel + the global radix passes + gather_kernel.  Any order is correct (the
+// culling is exact for every permutation); the order only sets how tight the tile boxes are.
+constexpr int kPrSegKeyBits = 14;
+
+struct PrSegArgs {
+    const float* src[2];
+    int npts[2], ppad[2];
+    int B, nmax;
+    const float* bbox;
+    float4* sorted[2];
+    int* perm[2];
+    unsigned* fb_count;   // tie queue of the resolve, reset here
+};
+
+__global__ void __launch_bounds__(kSegThreads) pr_segsort_kernel(PrSegArgs a) {
+    extern __shared__ __align__(16) uint32_t smem_pr[];
+    uint32_t* wcur = smem_pr;
+    uint32_t* wnext = wcur + kSegWarps * kSegD;
+    uint16_t* kA = reinterpret_cast<uint16_t*>(wnext + kSegWarps * kSegD);
+    uint16_t* kB = kA + a.nmax;
+    uint16_t* vA = kB + a.nmax;
+    uint16_t* vB = vA + a.nmax;
+    __shared__ uint32_t dstart[kSegD];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.fb_count) *a.fb_count = 0u;
+    const int c = blockIdx.x / a.B, b = blockIdx.x - c * a.B;
+    const int n = a.npts[c];
+    const float* P = a.src[c] + (int64_t)b * n * 3;
+    const float* bb = a.bbox + ((int64_t)c * a.B + b) * 6;
+    const int passes = 2, db = kPrSegKeyBits / 2, D = 1 << db;
+    int lspan = 5;   // warp w owns [w*span, (w+1)*span), span a power of two
+    while (kSegWarps << lspan < n) ++lspan;
+    const int R = 1 << (lspan - 5);
+    for (int i = threadIdx.x; i < 2 * kSegWarps * kSegD; i += kSegThreads) wcur[i] = 0;
+    float lo[3], sc[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float ext = bb[3 + k] - bb[k];
+        lo[k] = bb[k];
+        sc[k] = ext > 0.f ? 31.f / ext : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n; i += kSegThreads) {
+        uint32_t q[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float t = fminf(fmaxf((__ldg(P + (int64_t)i * 3 + k) - lo[k]) * sc[k], 0.f), 31.f);   // NaN -> 0
+            q[k] = (uint32_t)(t + 0.5f);
+        }
+        const uint16_t key = (uint16_t)(hilbert3(q[0], q[1], q[2], 5) >> (15 - kPrSegKeyBits));
+        kA[i] = key;
+        vA[i] = (uint16_t)i;
+        atomicAdd(&wcur[(i >> lspan) * D + (key & (D - 1))], 1u);
+    }
+    seg_lsd_passes(kA, vA, kB, vB, wcur, wnext, dstart, n, passes, db, lspan, R);
+    __syncthreads();
+    float4* S = a.sorted[c] + (int64_t)b * a.ppad[c];
+    int* PM = a.perm[c] + (int64_t)b * n;
+    for (int pos = threadIdx.x; pos < a.ppad[c]; pos += kSegThreads) {
+        if (pos < n) {
+            const int i = vA[pos];
+            const float* q = P + (int64_t)i * 3;
+            S[pos] = make_float4(__ldg(q), __ldg(q + 1), __ldg(q + 2), 0.f);
+            PM[pos] = i;
+        } else {
+            S[pos] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);   // padding: never a neighbour
+        }
     }
 }
 
@@ -770,7 +846,17 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
     p.supported = p.ttiles[0] <= kPrMaxTiles && p.ttiles[1] <= kPrMaxTiles;
 }
 
-int pruned_launches(const PrunedPlan& p) { return 2 + radix_sort_launches(p.L, p.nbits) + 7; }
+#ifndef CD_PR_SEGSORT
+#define CD_PR_SEGSORT 1
+#endif
+// clouds of <= kSegMax points: the on-chip Hilbert sort (pr_segsort_kernel)
+static bool pruned_segsort(const PrunedPlan& p) {
+    return CD_PR_SEGSORT && std::max(p.npts[0], p.npts[1]) <= kSegMax;
+}
+
+int pruned_launches(const PrunedPlan& p) {
+    return pruned_segsort(p) ? 2 + 6 : 2 + radix_sort_launches(p.L, p.nbits) + 7;
+}
 
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
                           cudaStream_t st) {
@@ -786,6 +872,34 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
     uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);
+    float4* sorted[2];
+    int* perm[2];
+    float4* box[2];
+    float4* box32[2];
+    for (int c = 0; c < 2; ++c) {
+        sorted[c] = reinterpret_cast<float4*>(w + p.off_sorted[c]);
+        perm[c] = reinterpret_cast<int*>(w + p.off_perm[c]);
+        box[c] = reinterpret_cast<float4*>(w + p.off_box[c]);
+        box32[c] = reinterpret_cast<float4*>(w + p.off_box32[c]);
+    }
+    if (pruned_segsort(p)) {
+        PrSegArgs a;
+        a.src[0] = x;
+        a.src[1] = y;
+        a.B = p.B;
+        a.nmax = std::max(p.npts[0], p.npts[1]);
+        a.bbox = bbox;
+        a.fb_count = reinterpret_cast<unsigned*>(w + p.off_fb);
+        for (int c = 0; c < 2; ++c) {
+            a.npts[c] = p.npts[c];
+            a.ppad[c] = p.ppad[c];
+            a.sorted[c] = sorted[c];
+            a.perm[c] = perm[c];
+        }
+        const size_t smem = seg_sort_smem(a.nmax);
+        ensure_smem_attr((const void*)pr_segsort_kernel, (int)seg_sort_smem(kSegMax));
+        pr_segsort_kernel<<<2 * p.B, kSegThreads, smem, st>>>(a);
+    } else {
     {
         HilbertArgs a;
         a.src[0] = x;
@@ -803,16 +917,6 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
     }
     const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
                                      reinterpret_cast<uint32_t*>(w + p.off_totals), st);
-    float4* sorted[2];
-    int* perm[2];
-    float4* box[2];
-    float4* box32[2];
-    for (int c = 0; c < 2; ++c) {
-        sorted[c] = reinterpret_cast<float4*>(w + p.off_sorted[c]);
-        perm[c] = reinterpret_cast<int*>(w + p.off_perm[c]);
-        box[c] = reinterpret_cast<float4*>(w + p.off_box[c]);
-        box32[c] = reinterpret_cast<float4*>(w + p.off_box32[c]);
-    }
     {
         GatherArgs a;
         a.src[0] = x;
@@ -826,6 +930,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
             a.perm[c] = perm[c];
         }
         gather_kernel<<<grid_l, 256, 0, st>>>(a);
+    }
     }
     {
         AabbArgs a;
