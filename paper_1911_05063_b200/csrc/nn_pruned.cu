@@ -176,9 +176,10 @@ struct PrSegArgs {
     const float* src[2];
     int npts[2], ppad[2];
     int B, nmax;
-    const float* bbox;
     float4* sorted[2];
     int* perm[2];
+    float4* box[2];       // [B][ppad/kTile][2] tile boxes (as aabb_kernel)
+    float4* bbox32[2];    // [B][ppad/kBlockK][2] 32-point block boxes
     unsigned* fb_count;   // tie queue of the resolve, reset here
 };
 
@@ -192,10 +193,36 @@ __global__ void __launch_bounds__(kSegThreads) pr_segsort_kernel(PrSegArgs a) {
     uint16_t* vB = vA + a.nmax;
     __shared__ uint32_t dstart[kSegD];
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.fb_count) *a.fb_count = 0u;
+    __shared__ float s_box[kSegWarps][6];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = blockIdx.x / a.B, b = blockIdx.x - c * a.B;
     const int n = a.npts[c];
     const float* P = a.src[c] + (int64_t)b * n * 3;
-    const float* bb = a.bbox + ((int64_t)c * a.B + b) * 6;
+    // the element's box (it only sets the quantisation; NaN coordinates are ignored by fminf/fmaxf)
+    float bb[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n; i += kSegThreads)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float v = __ldg(P + (int64_t)i * 3 + k);
+            bb[k] = fminf(bb[k], v);
+            bb[3 + k] = fmaxf(bb[3 + k], v);
+        }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            bb[k] = fminf(bb[k], __shfl_xor_sync(0xffffffffu, bb[k], o));
+            bb[3 + k] = fmaxf(bb[3 + k], __shfl_xor_sync(0xffffffffu, bb[3 + k], o));
+        }
+    if (lane == 0)
+        for (int k = 0; k < 6; ++k) s_box[warp][k] = bb[k];
+    __syncthreads();
+    for (int w = 0; w < kSegWarps; ++w)
+        for (int k = 0; k < 3; ++k) {
+            bb[k] = fminf(bb[k], s_box[w][k]);
+            bb[3 + k] = fmaxf(bb[3 + k], s_box[w][3 + k]);
+        }
     const int passes = 2, db = kPrSegKeyBits / 2, D = 1 << db;
     int lspan = 5;   // warp w owns [w*span, (w+1)*span), span a power of two
     while (kSegWarps << lspan < n) ++lspan;
@@ -206,7 +233,7 @@ __global__ void __launch_bounds__(kSegThreads) pr_segsort_kernel(PrSegArgs a) {
     for (int k = 0; k < 3; ++k) {
         const float ext = bb[3 + k] - bb[k];
         lo[k] = bb[k];
-        sc[k] = ext > 0.f ? 31.f / ext : 0.f;
+        sc[k] = ext > 0.f ? 31.f / ext : 0.f;   // (no finite point: ext is NaN or -inf -> 0)
     }
     __syncthreads();
 #pragma unroll 4
@@ -234,6 +261,42 @@ __global__ void __launch_bounds__(kSegThreads) pr_segsort_kernel(PrSegArgs a) {
             PM[pos] = i;
         } else {
             S[pos] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);   // padding: never a neighbour
+        }
+    }
+    // block and tile boxes of the sorted element (one warp per 512-point tile, as aabb_kernel)
+    const int nt = a.ppad[c] / kTile;
+    for (int t = warp; t < nt; t += kSegWarps) {
+        float tlo[3] = {INFINITY, INFINITY, INFINITY}, thi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int k = 0; k < (kTile / kBlockK); ++k) {
+            const int pos = t * kTile + k * kBlockK + lane;
+            float lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+            if (pos < n) {
+                const float* q = P + (int64_t)vA[pos] * 3;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) lo3[d] = hi3[d] = __ldg(q + d);
+            }
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo3[d] = fminf(lo3[d], __shfl_xor_sync(0xffffffffu, lo3[d], o));
+                    hi3[d] = fmaxf(hi3[d], __shfl_xor_sync(0xffffffffu, hi3[d], o));
+                }
+            if (lane == 0) {
+                float4* o = a.bbox32[c] + (((int64_t)b * nt + t) * (kTile / kBlockK) + k) * 2;
+                o[0] = make_float4(lo3[0], lo3[1], lo3[2], 0.f);
+                o[1] = make_float4(hi3[0], hi3[1], hi3[2], 0.f);
+            }
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                tlo[d] = fminf(tlo[d], lo3[d]);
+                thi[d] = fmaxf(thi[d], hi3[d]);
+            }
+        }
+        if (lane == 0) {
+            float4* o = a.box[c] + ((int64_t)b * nt + t) * 2;
+            o[0] = make_float4(tlo[0], tlo[1], tlo[2], 0.f);
+            o[1] = make_float4(thi[0], thi[1], thi[2], 0.f);
         }
     }
 }
@@ -855,7 +918,8 @@ static bool pruned_segsort(const PrunedPlan& p) {
 }
 
 int pruned_launches(const PrunedPlan& p) {
-    return pruned_segsort(p) ? 2 + 6 : 2 + radix_sort_launches(p.L, p.nbits) + 7;
+    // segment sort: sort+boxes, candidates, kernel, resolve, tie, partials
+    return pruned_segsort(p) ? 6 : 2 + radix_sort_launches(p.L, p.nbits) + 7;
 }
 
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
@@ -868,7 +932,8 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     float* bbox = reinterpret_cast<float*>(w + p.off_bbox);
-    launch_bbox(x, p.npts[0], y, p.npts[1], p.B, bbox, st);
+    const bool segsort = pruned_segsort(p);
+    if (!segsort) launch_bbox(x, p.npts[0], y, p.npts[1], p.B, bbox, st);
     uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);
@@ -882,19 +947,20 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         box[c] = reinterpret_cast<float4*>(w + p.off_box[c]);
         box32[c] = reinterpret_cast<float4*>(w + p.off_box32[c]);
     }
-    if (pruned_segsort(p)) {
+    if (segsort) {   // sort + element boxes + tile / block boxes in one launch
         PrSegArgs a;
         a.src[0] = x;
         a.src[1] = y;
         a.B = p.B;
         a.nmax = std::max(p.npts[0], p.npts[1]);
-        a.bbox = bbox;
         a.fb_count = reinterpret_cast<unsigned*>(w + p.off_fb);
         for (int c = 0; c < 2; ++c) {
             a.npts[c] = p.npts[c];
             a.ppad[c] = p.ppad[c];
             a.sorted[c] = sorted[c];
             a.perm[c] = perm[c];
+            a.box[c] = box[c];
+            a.bbox32[c] = box32[c];
         }
         const size_t smem = seg_sort_smem(a.nmax);
         ensure_smem_attr((const void*)pr_segsort_kernel, (int)seg_sort_smem(kSegMax));
@@ -932,7 +998,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         gather_kernel<<<grid_l, 256, 0, st>>>(a);
     }
     }
-    {
+    if (!segsort) {
         AabbArgs a;
         a.B = p.B;
         for (int c = 0; c < 2; ++c) {
