@@ -532,6 +532,26 @@ static int choose_splits(int64_t units, int ttiles, int ctas_per_sm) {
     return best_s;
 }
 
+// Fused kernel, whole 512-target tiles per split: t(S) = U (T + S c0) / slots + (ceil(T/S) + c0) / 2 —
+// the work spread over all CTA slots plus half a CTA of tail — with c0 = 0.1 tile of per-CTA cost.
+// Fitted to forced-split sweeps (tools/sweep_splits.py): c3 best S = 16 (1.897 ms vs 1.903 at S = 8,
+// the ceil-wave model's choice), c4 best S = 32 (17.47 vs 17.60 ms).
+static int choose_splits_fused(int64_t units, int ttiles, int ctas_per_sm) {
+    const double slots = (double)device_sm_count() * ctas_per_sm;
+    const double c0 = 0.1;
+    const int smax = std::max(1, std::min(64, ttiles));
+    int best_s = 1;
+    double best_t = 1e300;
+    for (int s = 1; s <= smax; ++s) {
+        const double t = (double)units * (ttiles + s * c0) / slots + 0.5 * ((double)ceil_div(ttiles, s) + c0);
+        if (t < best_t * 0.999) {
+            best_t = t;
+            best_s = s;
+        }
+    }
+    return best_s;
+}
+
 // Block-granular version for the fused kernel: a CTA's work is ceil(nb/S) 32-target blocks (plus a
 // fixed overhead of ~4 tiles' worth: the 2048-row load, the per-tile column combine, the row keys).
 static int choose_splits_blocks(int64_t units, int nb, int ctas_per_sm) {
@@ -555,6 +575,9 @@ static int choose_splits_blocks(int64_t units, int nb, int ctas_per_sm) {
 
 #ifndef CD_FUSED_SMALL
 #define CD_FUSED_SMALL 1
+#endif
+#ifndef CD_SPLITS_FUSED_MODEL
+#define CD_SPLITS_FUSED_MODEL 1
 #endif
 
 void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int r0, int r1, int forced_splits) {
@@ -610,7 +633,9 @@ void plan_forward(FwdPlan& p, int mode, int B, int N, int M, int q0, int q1, int
         p.split_unit = blocks ? kBlockK : kTile;
         const int nu = blocks ? nb : tt;
         const int S = forced_splits > 0 ? forced_splits
-                                        : (blocks ? choose_splits_blocks(units, nb, occ) : choose_splits(units, tt, occ));
+                                        : (blocks ? choose_splits_blocks(units, nb, occ)
+                                                  : CD_SPLITS_FUSED_MODEL ? choose_splits_fused(units, tt, occ)
+                                                                          : choose_splits(units, tt, occ));
         for (int d = 0; d < 2; ++d) {
             p.ttiles[d] = ceil_div(p.npts[1 - d], kTile);
             p.splits[d] = std::max(1, std::min(S, nu));   // <= units: every split non-empty
