@@ -147,6 +147,7 @@ void cd_set_profile_events(void* start, void* stop) {
 int cd_set_forward_splits(int splits) {
     int old = g_forced_splits;
     g_forced_splits = splits > 0 ? splits : 0;
+    cdk::set_p2s_forced_splits(g_forced_splits);
     return old;
 }
 

@@ -204,4 +204,6 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     return cudaSuccess;
 #endif
 }
+void set_p2s_forced_splits(int s);   // p2s.cu (cd_set_forward_splits)
+
 }  // namespace cdk

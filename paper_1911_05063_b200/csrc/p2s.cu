@@ -275,6 +275,10 @@ struct P2sPlan {
     size_t off_pts, off_fd, off_best_d, off_best_blk, off_chunk, bytes;
 };
 
+// cd_set_forward_splits also forces the point-to-surface split count (design sweeps)
+static thread_local int g_p2s_forced_splits = 0;
+void set_p2s_forced_splits(int s) { g_p2s_forced_splits = s > 0 ? s : 0; }
+
 static void plan_p2s(P2sPlan& p, int B, int N, int Nv, int Nf) {
     p.B = B;
     p.N = N;
@@ -286,17 +290,19 @@ static void plan_p2s(P2sPlan& p, int B, int N, int Nv, int Nf) {
     p.ftiles = p.Nfpad / kFaceTile;
     int sms = 148;
     const int64_t units = (int64_t)B * p.qtiles, slots = (int64_t)sms * 3;
+    // t(S) = U (T + S c0) / slots + (ceil(T/S) + c0) / 2, c0 = 0.1 face tile: the fused kernel's fitted
+    // split model (nn_forward.cu); sweep (tools/sweep_p2s_splits.py, NEXT-3 workload): S = 32-40
+    // 4.37-4.39 ms vs 4.54 ms at the ceil-wave model's choice
     int best = 1;
     double bt = 1e300;
     for (int s = 1; s <= std::min(64, p.ftiles); ++s) {
-        const double t = (double)cdiv(units * s, slots) * ((double)cdiv(p.ftiles, s) + 0.25) *
-                         ((units * s < slots && s < std::min(64, p.ftiles)) ? 1.15 : 1.0);
+        const double t = (double)units * (p.ftiles + 0.1 * s) / (double)slots + 0.5 * ((double)cdiv(p.ftiles, s) + 0.1);
         if (t < bt * 0.999) {
             bt = t;
             best = s;
         }
     }
-    p.splits = best;
+    p.splits = g_p2s_forced_splits > 0 ? std::min(g_p2s_forced_splits, p.ftiles) : best;
     p.nchunks = cdiv(N, kMergeThreads);
     size_t off = 0;
     auto take = [&](size_t bytes) {
