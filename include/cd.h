@@ -295,9 +295,11 @@ CD_API const char* cd_last_error_string(void);   /* thread-local; "" when no err
 CD_API int cd_abi_version(void);                 /* == CD_ABI_VERSION */
 
 /*
- * Tuning / test hooks (not needed for normal use).  cd_set_forward_config forces the forward's
- * target-split count (0 = automatic) for the calling thread, so tests can check that results are
- * independent of the tiling.  Returns the previous value.
+ * Tuning / test hooks (not needed for normal use).  cd_set_forward_splits forces the target-split
+ * count (0 = automatic) of the forward kernels and of the brute-force point-to-surface kernel for
+ * the calling thread, so tests can check that results are independent of the tiling (DESIGN.md
+ * §4.4) and sweeps can fit the split model (§4.3).  Workspace sizes queried afterwards follow the
+ * forced count.  Returns the previous value.
  */
 CD_API int cd_set_forward_splits(int splits);
 
