@@ -8,7 +8,10 @@
 
 namespace cdk {
 
-constexpr int kSegThreads = 512;
+#ifndef CD_SEG_THREADS
+#define CD_SEG_THREADS 1024
+#endif
+constexpr int kSegThreads = CD_SEG_THREADS;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr int kSegMax = 24576;   // 8 B per edge + 32 KB of counters <= 227 KB of shared memory
 constexpr int kSegDigitBits = 7;
