@@ -407,6 +407,9 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
     }
 }
 
+#ifndef CD_SEG_MAXPARTS
+#define CD_SEG_MAXPARTS 3   // log2 of the most CTAs per segment
+#endif
 #ifndef CD_GRAD_CTAS_PER_SM
 #define CD_GRAD_CTAS_PER_SM 0   // 0: the occupancy (one resident wave)
 #endif
@@ -631,7 +634,7 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
         ensure_smem_attr((const void*)seg_sort_kernel, (int)seg_sort_smem(kSegMax));
         // 2^lparts CTAs per segment (split by the keys' top bits) while the segments alone leave SMs idle
         int lparts = 0;
-        while (lparts < 3 && (int64_t)2 * p.B << (lparts + 1) <= sm_count()) ++lparts;
+        while (lparts < CD_SEG_MAXPARTS && (int64_t)2 * p.B << (lparts + 1) <= sm_count()) ++lparts;
         launch_pdl(seg_sort_kernel, dim3((unsigned)((int64_t)2 * p.B << lparts)), dim3(kSegThreads), smem, st,
                    idx_xy, idx_yx, p.B, p.N, p.M, nmax, lparts, vals[0], off);
     } else {
