@@ -7,11 +7,15 @@ cd_finalize (CD_b, loss, F) -> cd_backward of the loss (argmin fixed), all throu
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
-Default workload: config c3 (B=32, N=M=16,384, F-score at tau=0.01) — the smallest BASELINE.json
-config that exercises every §8.a row (c2 has no F-score) and one the forward roofline is judged on
-(BASELINE.md §3).  --gpus N > 1 (under torchrun) shards batches (weak scaling: each rank runs the
-full c3 batch of 32 on its own batch elements; the loss is combined by one NCCL all-reduce); with
---config c5 it shards query rows (strong scaling, target broadcast).  Inputs are seeded synthetic
+Default workload on 1 GPU: config c3 (B=32, N=M=16,384, F-score at tau=0.01) — the largest
+BASELINE.json config without a multi-GPU designation and the one naming F@0.01.  --gpus N > 1
+(under torchrun) defaults to c5 (B=4, N=M=2^20) query-sharded across the ranks: STRONG scaling of
+the north star's largest config (clouds broadcast from rank 0, X rows split, one MIN all-reduce of
+the column keys, one partials all-reduce, all-gather of the index slices for the backward).
+--config c4 splits its B=8 batch elements over the ranks (strong); other configs run their full
+batch on every rank (weak).  For N > 1 the line also carries the same config on ONE GPU (rank 0
+alone: the scaling fraction value_N / (N value_1)), the time inside collectives (max over ranks),
+and c3 weak scaling (multi_gpu.c3_weak).  Inputs are seeded synthetic
 ShapeNet-like clouds.  Timing: W untimed warm-up steps; K timed steps, each
 bracketed by CUDA events on the launching stream with an L2 flush (256 MiB write) between steps
 outside the events; barrier + synchronize on both sides; max over ranks.
@@ -49,7 +53,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None, help="timed steps (default: ~1 s of work per config)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(synth.CONFIGS),
+                    help="default: c3 on 1 GPU; c5 (query-sharded strong scaling) on N > 1 GPUs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline oracle sample")
     ap.add_argument("--no-e2e", action="store_true")
@@ -61,6 +66,7 @@ def parse():
     ap.add_argument("--no-tc", action="store_true", help="skip the tensor-core forward (mode 3) comparison")
     ap.add_argument("--no-bwd-roofline", action="store_true", help="skip the separate backward timing")
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-3 / NEXT-4 workload lines")
+    ap.add_argument("--no-extra-lines", action="store_true", help="N > 1: skip the 1-GPU reference and c3 weak runs")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise the multi-rank "
                     "logic when several ranks share one GPU")
     return ap.parse_args()
@@ -258,6 +264,87 @@ def _traffic(kernel, cfg):
         return None
 
 
+COLL_NAMES = ("broadcast_clouds", "all_reduce_min_colkeys", "all_reduce_partials", "all_gather_idx")
+
+
+def _mean_ms(torch, fn, flush, K, warmup=1):
+    """Mean device ms of K eager calls of fn (CUDA events on the launching stream, L2 flushed between)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record()
+        fn()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev) / K
+
+
+def multi_gpu_extras(cd, pdist, torch, dist, dev, flush, args, rank, world, value, X, Y, query_sharded,
+                     strong_batch, loss_N):
+    """N > 1 only: (a) the same config's full problem on ONE GPU (rank 0 alone, no collectives) and
+    the scaling fraction value_N / (N x value_1); (b) c3 weak scaling (every rank its own batch of
+    32, one partials all-reduce) with its own 1-GPU value — the two scaling regimes of SURVEY §8.e."""
+    c = synth.CONFIGS[args.config]
+    B, N, M, tau = c["B"], c["N"], c["M"], c["tau"]
+    out = {}
+    t = torch.zeros(2, dtype=torch.float64, device=dev)
+    if rank == 0:
+        if query_sharded:
+            x1, y1 = torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev)
+        else:
+            X1, Y1 = synth.config_inputs(args.config)
+            x1, y1 = torch.from_numpy(X1).to(dev), torch.from_numpy(Y1).to(dev)
+
+        loss1 = []
+
+        def one():
+            d_xy, i_xy, d_yx, i_yx, part = cd.forward(x1, y1, tau=tau)
+            _, l1, _, _, _ = cd.finalize(part, N, M)
+            cd.loss_backward(x1, y1, i_xy, i_yx, one_t)
+            loss1[:] = [l1]
+        one_t = torch.ones(1, dtype=torch.float32, device=dev)
+        K1 = 2 if args.config == "c5" else max(3, min(args.steps, 20))
+        t[0] = _mean_ms(torch, one, flush, K1)
+        t[1] = float(loss1[0].item())
+        del x1, y1
+    dist.barrier()
+    dist.broadcast(t, src=0)
+    v1 = 2 * B * N * M / (t[0].item() * 1e-3)
+    out["same_config_1gpu"] = {"value": v1, "ms_per_step": t[0].item(), "scaling_fraction": value / (world * v1),
+                               "loss_1gpu": t[1].item(), "loss_bit_identical": t[1].item() == loss_N,
+                               "note": "rank 0 alone, full problem, no collectives; fraction = value / (N x value_1gpu)"}
+    if args.config != "c3":
+        c3 = synth.CONFIGS["c3"]
+        X3, Y3 = synth.config_inputs("c3", b0=rank * c3["B"], B=c3["B"])
+        x3, y3 = torch.from_numpy(X3).to(dev), torch.from_numpy(Y3).to(dev)
+        K3 = 50
+        step3 = lambda: pdist.batch_sharded_step(cd, x3, y3, c3["B"] * world, rank * c3["B"], tau=c3["tau"])
+        tt = torch.tensor([_mean_ms(torch, step3, flush, K3, warmup=3)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t1 = torch.zeros(1, dtype=torch.float64, device=dev)
+        if rank == 0:
+            t1[0] = _mean_ms(torch, lambda: _c3_single(cd, x3, y3, c3), flush, K3, warmup=3)
+        dist.barrier()
+        dist.broadcast(t1, src=0)
+        pairs3 = 2 * c3["B"] * world * c3["N"] * c3["M"]
+        v3 = pairs3 / (tt.item() * 1e-3)
+        v31 = 2 * c3["B"] * c3["N"] * c3["M"] / (t1.item() * 1e-3)
+        out["c3_weak"] = {"value": v3, "unit": UNIT, "ms_per_step": tt.item(), "global_batch": c3["B"] * world,
+                          "scaling": "weak", "value_1gpu": v31, "scaling_fraction": v3 / (world * v31),
+                          "note": "each rank: the full c3 batch of 32 on its own batch elements; one B x 4 "
+                                  "partials all-reduce; eager launches (no CUDA graph)"}
+    return out
+
+
+def _c3_single(cd, x, y, c3):
+    d_xy, i_xy, d_yx, i_yx, part = cd.forward(x, y, tau=c3["tau"])
+    cd.finalize(part, c3["N"], c3["M"])
+    return cd.backward(x, y, i_xy, i_yx, g_scalar=1.0 / (c3["B"] * c3["N"]), h_scalar=1.0 / (c3["B"] * c3["M"]))
+
+
 P2S_OPS_PER_PAIR = 44   # FP32-pipe lane ops per (point, face) of the p2s hot loop (DESIGN.md §11)
 
 
@@ -372,6 +459,8 @@ def measure_extras(cd, torch, dev, flush, args, K_extra):
 # ------------------------------------------------------------------------------------------ ours
 def main():
     args = parse()
+    if args.config is None:
+        args.config = "c3" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "c5"
     if args.steps is None:
         args.steps = DEFAULT_STEPS[args.config]
     if args.impl == "reference":
@@ -397,11 +486,22 @@ def main():
             dist.init_process_group(args.dist_backend, init_method="env://")
     c = synth.CONFIGS[args.config]
     B, N, M, tau = c["B"], c["N"], c["M"], c["tau"]
+    # partitioning per BASELINE.json configs: c5 query-sharded and c4 batch-sharded
+    # (B = 8 split over the ranks) are STRONG scaling of the named problem; any other config under
+    # N > 1 runs its full batch on every rank (weak scaling)
     query_sharded = args.config == "c5" and world > 1
+    strong_batch = args.config == "c4" and world > 1
     if query_sharded:
         B_local, b0, B_global = B, 0, B
         X, Y = synth.config_inputs(args.config) if rank == 0 else (np.empty((B, N, 3), np.float32),
                                                                     np.empty((B, M, 3), np.float32))
+        scaling = "strong"
+    elif strong_batch:
+        b0, b1 = pdist.shard_range(B, rank, world)
+        B_local, B_global = b1 - b0, B
+        if B_local < 1:
+            raise SystemExit(f"c4 strong scaling needs at most B={B} ranks")
+        X, Y = synth.config_inputs(args.config, b0=b0, B=B_local)
         scaling = "strong"
     else:
         B_local, b0, B_global = B, rank * B, B * world
@@ -412,18 +512,21 @@ def main():
     w1 = w2 = 1.0
     pairs_total = 2 * B_global * N * M           # directed pairs of the whole job per step
     # the fused kernel evaluates each distance once for both directions: B*N*M evaluations per launch
-    evals_fwd_launch = (B * N * M) // (world if query_sharded else 1)
+    evals_fwd_launch = (B * N * M) // world if query_sharded else B_local * N * M
+    prof = pdist.CollectiveTimer() if world > 1 else None
 
     def step():
         if query_sharded:
-            pdist.broadcast_clouds(x, y, src=0)
-            return pdist.query_sharded_step(cd, x, y, tau=tau, w1=w1, w2=w2)
-        return pdist.batch_sharded_step(cd, x, y, B_global, b0, tau=tau, w1=w1, w2=w2)
+            pdist.broadcast_clouds(x, y, src=0, prof=prof)
+            return pdist.query_sharded_step(cd, x, y, tau=tau, w1=w1, w2=w2, prof=prof)
+        return pdist.batch_sharded_step(cd, x, y, B_global, b0, tau=tau, w1=w1, w2=w2, prof=prof)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         out = step()
     torch.cuda.synchronize()
+    if prof is not None:
+        prof.reset()
 
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -482,6 +585,22 @@ def main():
     ms_per_step = tot[0].item() / K
     fwd_kernel_ms = tot[1].item() / K
     value = pairs_total / (ms_per_step * 1e-3)
+    multi = None
+    if world > 1:
+        coll = prof.by_name_ms()
+        ct = torch.tensor([sum(coll.values())] + [coll.get(n, 0.0) for n in COLL_NAMES], dtype=torch.float64,
+                          device=dev)
+        dist.all_reduce(ct, op=dist.ReduceOp.MAX)
+        multi = {"ranks": dist.get_world_size(), "backend": dist.get_backend(),
+                 "collective_ms_per_step_max_rank": ct[0].item() / K,
+                 "collective_share_of_step": ct[0].item() / K / ms_per_step,
+                 "collectives_ms_per_step": {n: ct[i + 1].item() / K for i, n in enumerate(COLL_NAMES)
+                                             if ct[i + 1].item() > 0},
+                 "work_per_rank": ("B*N*M/world distance evaluations (X rows split; the fused kernel serves both "
+                                   "directions)" if query_sharded else f"B_local={B_local} of B={B_global}")}
+        if not args.no_extra_lines:
+            multi.update(multi_gpu_extras(cd, pdist, torch, dist, dev, flush, args, rank, world, value, X, Y,
+                                          query_sharded, strong_batch, float(out["loss"].item())))
     loss = float(out["loss"].item())
 
     # ---------------------------------------------------------------- exact pruned algorithm (NEXT-2)
@@ -582,39 +701,65 @@ def main():
     # ---------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
-        if query_sharded:
-            e2e = {"value": None, "unit": UNIT, "note": "query-sharded e2e not measured (clouds originate on rank 0)"}
-        else:
-            xh = cd.pinned_copy(X)
-            yh = cd.pinned_copy(Y)
+        xh = cd.pinned_copy(X)
+        yh = cd.pinned_copy(Y)
+        if world == 1:
             stepper = cd.HostStepper(B_local, N, M, tau=tau, w1=w1, w2=w2, device=dev)
 
             def e2e_step():
                 stepper.step(xh, yh)
-            for _ in range(max(1, args.warmup)):
-                e2e_step()
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-            for k in range(K):
-                flush.fill_(k & 0xFF)
-                eev[k][0].record()
-                e2e_step()
-                eev[k][1].record()
-            torch.cuda.synchronize()
-            et = torch.tensor([sum(a.elapsed_time(b) for a, b in eev)], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.barrier()
-                dist.all_reduce(et, op=dist.ReduceOp.MAX)
-            e2e_ms = et.item() / K
-            e2e = {"value": pairs_total / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-                   "h2d_bytes_per_step": int(X.nbytes + Y.nbytes),
-                   "d2h_bytes_per_step": int(4 + (4 * B_local if tau is not None else 0)),
-                   "api": (f"cd_step_host_overlapped via api.HostStepper (pinned host clouds -> H2D in "
-                           f"{stepper.nchunks} batch ranges on a copy stream, each range's forward starting as "
-                           "it lands -> finalize -> backward -> D2H loss, F; every step copies its inputs)"),
-                   "loss_e2e": float(stepper.loss[0])}
+            api_desc = (f"cd_step_host_overlapped via api.HostStepper (pinned host clouds -> H2D in {stepper.nchunks} "
+                        "batch ranges on a copy stream, each range's forward starting as it lands -> finalize -> "
+                        "backward -> D2H of loss, F and both gradients; every step copies its inputs and results)")
+            h2d, d2h = int(X.nbytes + Y.nbytes), stepper.d2h_bytes()
+        else:
+            # the public API under torch.distributed: the clouds land from pinned host memory (rank 0 only
+            # when query-sharded: the broadcast inside the step replicates them), the sharded step runs,
+            # and loss + this rank's gradient rows return to pinned host memory
+            own = rank == 0 or not query_sharded
+            lh = cd.pinned_empty((1,))
+            gxh = cd.pinned_empty((B_local, out["grad_x"].shape[1], 3))
+            gyh = cd.pinned_empty((B_local, out["grad_y"].shape[1], 3))
+
+            def e2e_step():
+                if own:
+                    x.copy_(xh, non_blocking=True)
+                    y.copy_(yh, non_blocking=True)
+                o = step()
+                lh.copy_(o["loss"], non_blocking=True)
+                gxh.copy_(o["grad_x"], non_blocking=True)
+                gyh.copy_(o["grad_y"], non_blocking=True)
+                stepper_loss[0] = lh
+            stepper_loss = [None]
+            api_desc = ("api + distributed.{} (pinned host clouds -> H2D{} -> sharded step with its collectives -> "
+                        "D2H of loss and this rank's gradient rows)".format(
+                            "query_sharded_step" if query_sharded else "batch_sharded_step",
+                            " on rank 0, broadcast" if query_sharded else ""))
+            h2d = int(X.nbytes + Y.nbytes) if own else 0
+            d2h = 4 + 4 * (gxh.numel() + gyh.numel())
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            eev[k][0].record()
+            e2e_step()
+            eev[k][1].record()
+        torch.cuda.synchronize()
+        et = torch.tensor([sum(a.elapsed_time(b) for a, b in eev)], dtype=torch.float64, device=dev)
+        hd = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.barrier()
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            dist.all_reduce(hd, op=dist.ReduceOp.SUM)
+        e2e_ms = et.item() / K
+        e2e = {"value": pairs_total / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(hd[0].item()), "d2h_bytes_per_step": int(hd[1].item()),
+               "api": api_desc,
+               "loss_e2e": float(stepper.loss[0]) if world == 1 else float(stepper_loss[0][0])}
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -664,6 +809,7 @@ def main():
             "pruned": pruned,
             "tensor_core_forward": tcf,
             "next_rows": extras,
+            "multi_gpu": multi,
             "gpu_launches": launches * K,
             "gpu_launches_per_step": launches,
             "clocks": clocks,

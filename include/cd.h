@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define CD_ABI_VERSION 3
+#define CD_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define CD_API __attribute__((visibility("default")))
@@ -181,6 +181,25 @@ CD_API cd_status cd_backward(const float* x, const float* y, int B, int N, int M
                       void* workspace, size_t workspace_bytes, cd_stream_t stream);
 
 /*
+ * cd_loss_backward — gradient of the batch loss that cd_finalize returns,
+ *     L = (1/B) sum_b [ w1 (1/N) sum_i d_xy[b,i] + w2 (1/M) sum_j d_yx[b,j] ]   (R1)
+ * times a DEVICE-resident upstream scalar u = grad_loss[0] (autograd's dL_total/dL), with the
+ * argmin held fixed ("VJP holds the argmin fixed"; R8).  Equivalent to cd_backward with
+ * the per-point upstreams filled with
+ *     g = RN32(u * RN32(w1 / (B N))),   h = RN32(u * RN32(w2 / (B M)))
+ * (RN32(w/(B P)) computed in fp64 and rounded once; the product rounded once in fp32), evaluated
+ * inside the kernels: no B x N / B x M upstream array is materialised and u is read on the device,
+ * so the call is asynchronous and graph-capturable.  Arguments, slices, outputs, workspace
+ * (CD_OP_BACKWARD) and errors as cd_backward; grad_loss == NULL -> CD_ERR_INVALID_VALUE.
+ */
+CD_API cd_status cd_loss_backward(const float* x, const float* y, int B, int N, int M,
+                      const int32_t* idx_xy, const int32_t* idx_yx,
+                      const float* grad_loss, float w1, float w2,
+                      int q0, int q1, int r0, int r1,
+                      float* grad_x, float* grad_y,
+                      void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
  * cd_step_host — one whole training/evaluation step through HOST buffers (the end-to-end entry
  * point): copies x_host, y_host (pinned host memory recommended) into device staging inside the
  * workspace, runs cd_forward (full slices, tau) + cd_finalize + cd_backward of loss = mean_b CD_b
@@ -244,6 +263,17 @@ CD_API cd_status cd_p2s_forward(const float* points, const float* verts, const i
 CD_API cd_status cd_p2s_backward(const float* points, const float* closest, const int32_t* face,
                          const float* bary, const int32_t* faces, int B, int N, int Nv, int Nf,
                          const float* g, float g_scalar, float* grad_points, float* grad_verts,
+                         void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_p2s_loss_backward — gradient of the point-to-surface loss cd_p2s_forward returns,
+ * L = (1/B) sum_b (1/N) sum_i d[b,i] (R23), times the DEVICE-resident upstream scalar
+ * u = grad_loss[0]: cd_p2s_backward with g = RN32(u * RN32(1 / (B N))) for every point, formed in the
+ * kernel (no B x N upstream array).  Other arguments, workspace and errors as cd_p2s_backward.
+ */
+CD_API cd_status cd_p2s_loss_backward(const float* points, const float* closest, const int32_t* face,
+                         const float* bary, const int32_t* faces, int B, int N, int Nv, int Nf,
+                         const float* grad_loss, float* grad_points, float* grad_verts,
                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
 CD_API size_t cd_p2s_workspace_size(int op, int B, int N, int Nv, int Nf);
 CD_API int cd_p2s_launch_count(int op, int B, int N, int Nv, int Nf);

@@ -18,6 +18,7 @@ if os.environ.get("CD_LIB_VARIANT"):
 HEADER = os.path.join(os.path.dirname(HERE), "include", "cd.h")
 
 CD_OK = 0
+ABI_VERSION = 4
 CD_OP_FORWARD, CD_OP_FSCORE, CD_OP_BACKWARD, CD_OP_STEP, CD_OP_FORWARD_PRUNED = 0, 1, 2, 3, 4
 CD_OP_SAMPLE, CD_OP_SAMPLE_BACKWARD, CD_OP_P2S, CD_OP_P2S_BACKWARD, CD_OP_P2S_PRUNED = 5, 6, 7, 8, 9
 STATUS_NAMES = {0: "CD_OK", 1: "CD_ERR_INVALID_VALUE", 2: "CD_ERR_MISALIGNED", 3: "CD_ERR_TOO_LARGE",
@@ -36,6 +37,7 @@ _SIGS = {
     "cd_finalize": ([vp, i32, i32, i32, f32, f32, vp, vp, vp, vp, vp, vp], i32),
     "cd_fscore": ([vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, sz, vp], i32),
     "cd_backward": ([vp, vp, i32, i32, i32, vp, vp, vp, vp, f32, f32, i32, i32, i32, i32, vp, vp, vp, sz, vp], i32),
+    "cd_loss_backward": ([vp, vp, i32, i32, i32, vp, vp, vp, f32, f32, i32, i32, i32, i32, vp, vp, vp, sz, vp], i32),
     "cd_step_host": ([vp, vp, i32, i32, i32, f32, f32, f32, vp, vp, vp, vp, vp, sz, vp], i32),
     "cd_step_host_overlapped": ([vp, vp, i32, i32, i32, f32, f32, f32, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp],
                                 i32),
@@ -54,6 +56,7 @@ _SIGS = {
     "cd_sample_launch_count": ([i32, i32, i32, i32, i32], i32),
     "cd_p2s_forward": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "cd_p2s_backward": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, f32, vp, vp, vp, sz, vp], i32),
+    "cd_p2s_loss_backward": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, sz, vp], i32),
     "cd_p2s_workspace_size": ([i32, i32, i32, i32, i32], sz),
     "cd_p2s_launch_count": ([i32, i32, i32, i32, i32], i32),
     "cd_p2s_forward_pruned": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
@@ -88,7 +91,7 @@ def load():
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res
-            if lib.cd_abi_version() != 3:
+            if lib.cd_abi_version() != ABI_VERSION:
                 raise RuntimeError("libcd ABI version mismatch")
             _lib = lib
     return _lib

@@ -8,6 +8,7 @@ nearest-neighbour indices of X in Y, d_yx / idx_yx the reverse dir
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 import torch
@@ -24,6 +25,22 @@ def _ptr(t):
 
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _device_guard(fn):
+    """Run a wrapper with the CUDA device of its tensor arguments current, so libcd's device checks,
+    launches and the current stream all refer to the GPU the data lives on; tensors on two different
+    GPUs are rejected before any call."""
+    @functools.wraps(fn)
+    def wrapped(*args, **kw):
+        devs = {a.device for a in (*args, *kw.values()) if isinstance(a, torch.Tensor) and a.is_cuda}
+        if len(devs) > 1:
+            raise ValueError(f"{fn.__name__}: tensors on several devices {sorted(map(str, devs))}")
+        if not devs:
+            return fn(*args, **kw)
+        with torch.cuda.device(devs.pop()):
+            return fn(*args, **kw)
+    return wrapped
 
 
 def _cached_ws(kind: str, op: int, n: int, device) -> torch.Tensor:
@@ -59,6 +76,7 @@ def set_forward_splits(s: int) -> int:
     return int(_lib.load().cd_set_forward_splits(int(s)))
 
 
+@_device_guard
 def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=None, r_slice=None,
             want_partials: bool = True, algorithm: str = "brute"):
     """cd_forward: both NN directions.  Returns (d_xy, idx_xy, d_yx, idx_yx, partials[B,4] fp64).
@@ -97,6 +115,7 @@ def forward(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, q_slice=
     return d_xy, i_xy, d_yx, i_yx, part
 
 
+@_device_guard
 def forward_pruned(x: torch.Tensor, y: torch.Tensor, tau: float | None = None, want_partials: bool = True):
     """cd_forward_pruned: exact nearest neighbours with Hilbert-ordered tiles and lower-bound culling (same results as the brute force)."""
     x = _check_cloud(x, "x")
@@ -126,6 +145,7 @@ def set_forward_mode(mode: int) -> int:
 COLKEY_EMPTY = (1 << 63) - 1
 
 
+@_device_guard
 def forward_rows(x: torch.Tensor, y: torch.Tensor, q_slice, tau: float | None = None, partials=None):
     """cd_forward_rows: X rows q_slice fully + column keys for every Y point (query sharding).
 
@@ -148,6 +168,7 @@ def forward_rows(x: torch.Tensor, y: torch.Tensor, q_slice, tau: float | None = 
     return d_xy, i_xy, keys, partials
 
 
+@_device_guard
 def forward_cols(x: torch.Tensor, y: torch.Tensor, colkeys: torch.Tensor, r_slice, tau: float | None = None,
                  partials=None):
     """cd_forward_cols: resolve Y rows r_slice from (reduced) column keys.  Returns (d_yx, idx_yx,
@@ -169,6 +190,7 @@ def forward_cols(x: torch.Tensor, y: torch.Tensor, colkeys: torch.Tensor, r_slic
     return d_yx, i_yx, partials
 
 
+@_device_guard
 def finalize(partials: torch.Tensor, N: int, M: int, w1: float = 1.0, w2: float = 1.0):
     """cd_finalize: returns (cd_per_batch[B], loss[1], fscore[B], precision[B], recall[B])."""
     B = partials.shape[0]
@@ -183,6 +205,7 @@ def finalize(partials: torch.Tensor, N: int, M: int, w1: float = 1.0, w2: float 
     return cd, loss, F, P, R
 
 
+@_device_guard
 def fscore_from_distances(d_xy: torch.Tensor, d_yx: torch.Tensor, tau: float):
     """cd_fscore: (F, P, R) per batch element from per-point squared distances."""
     B, N = d_xy.shape
@@ -197,6 +220,7 @@ def fscore_from_distances(d_xy: torch.Tensor, d_yx: torch.Tensor, tau: float):
     return F, P, R
 
 
+@_device_guard
 def fscore(x: torch.Tensor, y: torch.Tensor, tau: float):
     """F-score at radius tau built on the same NN pass (forward with hit counting + finalize)."""
     _, _, _, _, part = forward(x, y, tau=tau)
@@ -204,6 +228,7 @@ def fscore(x: torch.Tensor, y: torch.Tensor, tau: float):
     return F, P, R
 
 
+@_device_guard
 def backward(x: torch.Tensor, y: torch.Tensor, idx_xy: torch.Tensor, idx_yx: torch.Tensor, g=None, h=None,
              g_scalar: float = 0.0, h_scalar: float = 0.0, q_slice=None, r_slice=None):
     """cd_backward: gradients of sum(g*d_xy) + sum(h*d_yx) wrt x (rows q_slice) and y (rows r_slice)."""
@@ -222,6 +247,29 @@ def backward(x: torch.Tensor, y: torch.Tensor, idx_xy: torch.Tensor, idx_yx: tor
     check(_lib.load().cd_backward(_ptr(x), _ptr(y), B, N, M, _ptr(idx_xy.contiguous()), _ptr(idx_yx.contiguous()),
                                   _ptr(g), _ptr(h), float(g_scalar), float(h_scalar), q0, q1, r0, r1, _ptr(gx),
                                   _ptr(gy), _ptr(ws), ws.numel(), _stream()))
+    return gx, gy
+
+
+@_device_guard
+def loss_backward(x: torch.Tensor, y: torch.Tensor, idx_xy: torch.Tensor, idx_yx: torch.Tensor,
+                  grad_loss: torch.Tensor, w1: float = 1.0, w2: float = 1.0, q_slice=None, r_slice=None):
+    """cd_loss_backward: gradients of grad_loss[0] * loss (cd_finalize's loss with weights w1, w2) wrt
+    x (rows q_slice) and y (rows r_slice); grad_loss is a 1-element fp32 CUDA tensor read on the device."""
+    x = _check_cloud(x, "x")
+    y = _check_cloud(y, "y")
+    B, N, _ = x.shape
+    M = y.shape[1]
+    q0, q1 = q_slice if q_slice is not None else (0, N)
+    r0, r1 = r_slice if r_slice is not None else (0, M)
+    if grad_loss.numel() != 1 or grad_loss.dtype != torch.float32 or not grad_loss.is_cuda:
+        raise TypeError("grad_loss must be a 1-element fp32 CUDA tensor")
+    dev = x.device
+    gx = torch.empty((B, q1 - q0, 3), dtype=torch.float32, device=dev)
+    gy = torch.empty((B, r1 - r0, 3), dtype=torch.float32, device=dev)
+    ws = workspace(_lib.CD_OP_BACKWARD, B, N, M, dev)
+    check(_lib.load().cd_loss_backward(_ptr(x), _ptr(y), B, N, M, _ptr(idx_xy.contiguous()),
+                                       _ptr(idx_yx.contiguous()), _ptr(grad_loss.contiguous()), float(w1), float(w2),
+                                       q0, q1, r0, r1, _ptr(gx), _ptr(gy), _ptr(ws), ws.numel(), _stream()))
     return gx, gy
 
 
@@ -254,7 +302,7 @@ class HostStepper:
     host tensors.  step() is asynchronous: call synchronize() (or read after the stream syncs)."""
 
     def __init__(self, B: int, N: int, M: int, tau: float | None = None, w1: float = 1.0, w2: float = 1.0,
-                 nchunks: int | None = None, device=None):
+                 nchunks: int | None = None, device=None, want_grads: bool = True):
         self.B, self.N, self.M, self.tau, self.w1, self.w2 = B, N, M, tau, w1, w2
         self.nchunks = nchunks or (2 if B >= 2 else 1)   # measured (tools/time_e2e.py c3): 2 ranges (first 1/4 of B) 2.18 ms, 4 equal: 2.28
         self.device = device or torch.device("cuda", torch.cuda.current_device())
@@ -271,15 +319,22 @@ class HostStepper:
         self._evp = (ctypes.c_void_p * (self.nchunks + 1))(*[ev.cuda_event for ev in self.events])
         self.loss = pinned_empty((1,))
         self.fscore = pinned_empty((B,))
+        self.grad_x = pinned_empty((B, N, 3)) if want_grads else None
+        self.grad_y = pinned_empty((B, M, 3)) if want_grads else None
+
+    def d2h_bytes(self) -> int:
+        """Bytes copied device -> host per step (loss, F-score, gradients)."""
+        return 4 + (4 * self.B if self.tau is not None else 0) + \
+            (12 * self.B * (self.N + self.M) if self.grad_x is not None else 0)
 
     def step(self, x_host: torch.Tensor, y_host: torch.Tensor):
         check(_lib.load().cd_step_host_overlapped(
             _host_ptr(x_host), _host_ptr(y_host), self.B, self.N, self.M,
             float(-1.0 if self.tau is None else self.tau), float(self.w1), float(self.w2),
-            _host_ptr(self.loss), _host_ptr(self.fscore) if self.tau is not None else None, None, None,
-            self.nchunks, _ptr(self.ws), self.ws.numel(), _stream(),
+            _host_ptr(self.loss), _host_ptr(self.fscore) if self.tau is not None else None,
+            _host_ptr(self.grad_x), _host_ptr(self.grad_y), self.nchunks, _ptr(self.ws), self.ws.numel(), _stream(),
             ctypes.c_void_p(self.copy_stream.cuda_stream), self._evp))
-        return self.loss, self.fscore
+        return self.loss, self.fscore, self.grad_x, self.grad_y
 
 
 def _host_ptr(t):
@@ -313,12 +368,8 @@ class ChamferFunction(torch.autograd.Function):
     def backward(ctx, grad_out):
         x, y, i_xy, i_yx = ctx.saved_tensors
         w1, w2 = ctx.w
-        B, N, M = x.shape[0], x.shape[1], y.shape[1]
         # g = dL/dd_xy = grad_out * w1 / (B N): the upstream scalar multiplies a uniform fill
-        go = grad_out.reshape(1).float()
-        g = (go * (w1 / (B * N))).expand(B, N)
-        h = (go * (w2 / (B * M))).expand(B, M)
-        gx, gy = backward(x, y, i_xy, i_yx, g, h)
+        gx, gy = loss_backward(x, y, i_xy, i_yx, grad_out.reshape(1), w1, w2)
         return gx, gy, None, None, None
 
 
@@ -347,6 +398,7 @@ def _sample_ws(op, B, Nv, Nf, N, device):
     return _cached_ws("sample", op, n, device)
 
 
+@_device_guard
 def sample_mesh(verts: torch.Tensor, faces: torch.Tensor, r_face: torch.Tensor, r_bary: torch.Tensor):
     """cd_sample_mesh: (points [B,N,3], face_idx [B,N], bary [B,N,3]) for B meshes sharing `faces`."""
     if not verts.is_cuda or verts.dtype != torch.float32 or verts.dim() != 3:
@@ -367,6 +419,7 @@ def sample_mesh(verts: torch.Tensor, faces: torch.Tensor, r_face: torch.Tensor, 
     return pts, fi, ba
 
 
+@_device_guard
 def sample_mesh_backward(faces: torch.Tensor, face_idx: torch.Tensor, bary: torch.Tensor, Nv: int,
                          grad_points: torch.Tensor):
     """cd_sample_mesh_backward: gradient w.r.t. the vertices (choices fixed)."""
@@ -413,6 +466,7 @@ def _p2s_ws(op, B, N, Nv, Nf, device):
     return _cached_ws("p2s", op, n, device)
 
 
+@_device_guard
 def p2s_forward(points: torch.Tensor, verts: torch.Tensor, faces: torch.Tensor, algorithm: str = "brute"):
     """cd_p2s_forward (algorithm="brute") or cd_p2s_forward_pruned (algorithm="pruned", R26):
     (d [B,N], face [B,N], closest [B,N,3], bary [B,N,3], per_batch [B], loss [1])."""
@@ -439,6 +493,7 @@ def p2s_forward(points: torch.Tensor, verts: torch.Tensor, faces: torch.Tensor, 
     return d, fi, cl, ba, pb, loss
 
 
+@_device_guard
 def p2s_backward(points, closest, face, bary, faces, Nv: int, g=None, g_scalar: float = 0.0,
                  want_points: bool = True, want_verts: bool = True):
     """cd_p2s_backward: (grad_points or None, grad_verts or None)."""
@@ -456,6 +511,26 @@ def p2s_backward(points, closest, face, bary, faces, Nv: int, g=None, g_scalar: 
     return gp, gv
 
 
+@_device_guard
+def p2s_loss_backward(points, closest, face, bary, faces, Nv: int, grad_loss: torch.Tensor,
+                      want_points: bool = True, want_verts: bool = True):
+    """cd_p2s_loss_backward: gradients of grad_loss[0] * (mean point-to-surface loss)."""
+    faces = faces.to(torch.int32).contiguous()
+    B, N, _ = points.shape
+    Nf = faces.shape[0]
+    if grad_loss.numel() != 1 or grad_loss.dtype != torch.float32 or not grad_loss.is_cuda:
+        raise TypeError("grad_loss must be a 1-element fp32 CUDA tensor")
+    dev = points.device
+    gp = torch.empty((B, N, 3), dtype=torch.float32, device=dev) if want_points else None
+    gv = torch.empty((B, Nv, 3), dtype=torch.float32, device=dev) if want_verts else None
+    ws = _p2s_ws(_lib.CD_OP_P2S_BACKWARD, B, N, Nv, Nf, dev)
+    check(_lib.load().cd_p2s_loss_backward(_ptr(points.contiguous()), _ptr(closest.contiguous()),
+                                           _ptr(face.contiguous()), _ptr(bary.contiguous()), _ptr(faces), B, N, Nv,
+                                           Nf, _ptr(grad_loss.contiguous()), _ptr(gp), _ptr(gv), _ptr(ws),
+                                           ws.numel(), _stream()))
+    return gp, gv
+
+
 class PointToSurfaceFunction(torch.autograd.Function):
     """loss = mean_b mean_i min_f dist^2(p_i, face f); gradients to points and mesh vertices."""
 
@@ -469,10 +544,8 @@ class PointToSurfaceFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, grad_out):
         points, cl, fi, ba, faces = ctx.saved_tensors
-        B, N = fi.shape
-        g = (grad_out.reshape(1).float() / (B * N)).expand(B, N)
-        gp, gv = p2s_backward(points, cl, fi, ba, faces, ctx.Nv, g=g, want_points=ctx.needs_input_grad[0],
-                              want_verts=ctx.needs_input_grad[1])
+        gp, gv = p2s_loss_backward(points, cl, fi, ba, faces, ctx.Nv, grad_out.reshape(1),
+                                   want_points=ctx.needs_input_grad[0], want_verts=ctx.needs_input_grad[1])
         return gp, gv, None, None
 
 

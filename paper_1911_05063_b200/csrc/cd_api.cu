@@ -137,6 +137,9 @@ const char* cd_status_string(cd_status s) {
     return "CD_ERR_UNKNOWN";
 }
 
+// The loss's fills (R8): RN32(w / (B P)) in fp64 then rounded once.
+static float loss_fill(float w, int B, int P) { return (float)((double)w / ((double)B * P)); }
+
 const char* cd_last_error_string(void) { return g_err.c_str(); }
 
 void cd_set_profile_events(void* start, void* stop) {
@@ -394,10 +397,11 @@ cd_status cd_p2s_forward(const float* points, const float* verts, const int32_t*
                        "cd_p2s_forward");
 }
 
-cd_status cd_p2s_backward(const float* points, const float* closest, const int32_t* face, const float* bary,
-                          const int32_t* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
-                          float* grad_points, float* grad_verts, void* workspace, size_t workspace_bytes,
-                          cd_stream_t stream) {
+static cd_status p2s_backward_common(const char* who, const float* points, const float* closest,
+                                     const int32_t* face, const float* bary, const int32_t* faces, int B, int N,
+                                     int Nv, int Nf, const float* g, float g_scalar, const float* upstream,
+                                     float* grad_points, float* grad_verts, void* workspace, size_t workspace_bytes,
+                                     cd_stream_t stream) {
     g_err.clear();
     cd_status s = check_p2s_sizes(B, N, Nv, Nf);
     if (s != CD_OK) return s;
@@ -408,9 +412,30 @@ cd_status cd_p2s_backward(const float* points, const float* closest, const int32
     if (workspace_bytes < need) return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu", workspace_bytes, need);
     s = check_device();
     if (s != CD_OK) return s;
-    return cuda_status(cdk::launch_p2s_backward(points, closest, face, bary, faces, B, N, Nv, Nf, g, g_scalar,
+    return cuda_status(cdk::launch_p2s_backward(points, closest, face, bary, faces, B, N, Nv, Nf, g, g_scalar, upstream,
                                                 grad_points, grad_verts, workspace, static_cast<cudaStream_t>(stream)),
-                       "cd_p2s_backward");
+                       who);
+}
+
+cd_status cd_p2s_backward(const float* points, const float* closest, const int32_t* face, const float* bary,
+                          const int32_t* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
+                          float* grad_points, float* grad_verts, void* workspace, size_t workspace_bytes,
+                          cd_stream_t stream) {
+    return p2s_backward_common("cd_p2s_backward", points, closest, face, bary, faces, B, N, Nv, Nf, g, g_scalar,
+                               nullptr, grad_points, grad_verts, workspace, workspace_bytes, stream);
+}
+
+cd_status cd_p2s_loss_backward(const float* points, const float* closest, const int32_t* face, const float* bary,
+                               const int32_t* faces, int B, int N, int Nv, int Nf, const float* grad_loss,
+                               float* grad_points, float* grad_verts, void* workspace, size_t workspace_bytes,
+                               cd_stream_t stream) {
+    if (!grad_loss || B < 1 || N < 1) {
+        g_err.clear();
+        return fail(CD_ERR_INVALID_VALUE, "null grad_loss or empty point set");
+    }
+    return p2s_backward_common("cd_p2s_loss_backward", points, closest, face, bary, faces, B, N, Nv, Nf, nullptr,
+                               loss_fill(1.0f, B, N), grad_loss, grad_points, grad_verts, workspace, workspace_bytes,
+                               stream);
 }
 
 size_t cd_p2s_workspace_size(int op, int B, int N, int Nv, int Nf) {
@@ -483,10 +508,11 @@ cd_status cd_fscore(const float* d_xy, const float* d_yx, int B, int N, int M, f
                        "cd_fscore");
 }
 
-cd_status cd_backward(const float* x, const float* y, int B, int N, int M, const int32_t* idx_xy,
-                      const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar, int q0,
-                      int q1, int r0, int r1, float* grad_x, float* grad_y, void* workspace, size_t workspace_bytes,
-                      cd_stream_t stream) {
+static cd_status backward_common(const char* who, const float* x, const float* y, int B, int N, int M,
+                                 const int32_t* idx_xy, const int32_t* idx_yx, const float* g, const float* h,
+                                 float g_scalar, float h_scalar, const float* upstream, int q0, int q1, int r0, int r1,
+                                 float* grad_x, float* grad_y, void* workspace, size_t workspace_bytes,
+                                 cd_stream_t stream) {
     g_err.clear();
     cd_status s = check_sizes(B, N, M);
     if (s != CD_OK) return s;
@@ -503,9 +529,34 @@ cd_status cd_backward(const float* x, const float* y, int B, int N, int M, const
         return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
     s = check_device();
     if (s != CD_OK) return s;
-    return cuda_status(cdk::launch_backward(p, x, y, idx_xy, idx_yx, g, h, g_scalar, h_scalar, grad_x, grad_y,
-                                            workspace, static_cast<cudaStream_t>(stream)),
-                       "cd_backward");
+    return cuda_status(cdk::launch_backward(p, x, y, idx_xy, idx_yx, g, h, g_scalar, h_scalar, upstream, grad_x,
+                                            grad_y, workspace, static_cast<cudaStream_t>(stream)),
+                       who);
+}
+
+cd_status cd_backward(const float* x, const float* y, int B, int N, int M, const int32_t* idx_xy,
+                      const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar, int q0,
+                      int q1, int r0, int r1, float* grad_x, float* grad_y, void* workspace, size_t workspace_bytes,
+                      cd_stream_t stream) {
+    return backward_common("cd_backward", x, y, B, N, M, idx_xy, idx_yx, g, h, g_scalar, h_scalar, nullptr, q0, q1,
+                           r0, r1, grad_x, grad_y, workspace, workspace_bytes, stream);
+}
+
+cd_status cd_loss_backward(const float* x, const float* y, int B, int N, int M, const int32_t* idx_xy,
+                           const int32_t* idx_yx, const float* grad_loss, float w1, float w2, int q0, int q1, int r0,
+                           int r1, float* grad_x, float* grad_y, void* workspace, size_t workspace_bytes,
+                           cd_stream_t stream) {
+    if (!grad_loss) {
+        g_err.clear();
+        return fail(CD_ERR_INVALID_VALUE, "null grad_loss");
+    }
+    if (B < 1 || N < 1 || M < 1) {
+        g_err.clear();
+        return fail(CD_ERR_INVALID_VALUE, "empty cloud: B=%d N=%d M=%d", B, N, M);
+    }
+    return backward_common("cd_loss_backward", x, y, B, N, M, idx_xy, idx_yx, nullptr, nullptr, loss_fill(w1, B, N),
+                           loss_fill(w2, B, M), grad_loss, q0, q1, r0, r1, grad_x, grad_y, workspace, workspace_bytes,
+                           stream);
 }
 
 cd_status cd_step_host(const float* x_host, const float* y_host, int B, int N, int M, float tau, float w1, float w2,
@@ -542,8 +593,8 @@ cd_status cd_step_host(const float* x_host, const float* y_host, int B, int N, i
     if (s != CD_OK) return s;
     s = cd_finalize(part, B, N, M, w1, w2, nullptr, loss, tau >= 0.f ? fs : nullptr, nullptr, nullptr, stream);
     if (s != CD_OK) return s;
-    const float gs = (float)((double)w1 / ((double)B * N));
-    const float hs = (float)((double)w2 / ((double)B * M));
+    const float gs = loss_fill(w1, B, N);
+    const float hs = loss_fill(w2, B, M);
     s = cd_backward(x, y, B, N, M, ixy, iyx, nullptr, nullptr, gs, hs, 0, N, 0, M, gx, gy, inner, L.inner_bytes,
                     stream);
     if (s != CD_OK) return s;
@@ -626,8 +677,8 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
     }
     s = cd_finalize(part, B, N, M, w1, w2, nullptr, loss, tau >= 0.f ? fs : nullptr, nullptr, nullptr, stream);
     if (s != CD_OK) return s;
-    const float gs = (float)((double)w1 / ((double)B * N));
-    const float hs = (float)((double)w2 / ((double)B * M));
+    const float gs = loss_fill(w1, B, N);
+    const float hs = loss_fill(w2, B, M);
     s = cd_backward(x, y, B, N, M, ixy, iyx, nullptr, nullptr, gs, hs, 0, N, 0, M, gx, gy, inner, L.inner_bytes,
                     stream);
     if (s != CD_OK) return s;

@@ -100,7 +100,7 @@ cudaError_t launch_p2s(const float* points, const float* verts, const int* faces
                        cudaStream_t st);
 cudaError_t launch_p2s_backward(const float* points, const float* closest, const int* face, const float* bary,
                                 const int* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
-                                float* grad_points, float* grad_verts, void* ws, cudaStream_t st);
+                                const float* upstream, float* grad_points, float* grad_verts, void* ws, cudaStream_t st);
 int p2s_launches();
 void launch_p2s_finalize(const double* chunk_sum, int B, int N, int nchunks, float* per_batch, float* loss,
                          cudaStream_t st);
@@ -136,7 +136,7 @@ struct BwdPlan {
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1);
 cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, const int32_t* idx_xy,
                             const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar,
-                            float* grad_x, float* grad_y, void* ws, cudaStream_t st);
+                            const float* upstream, float* grad_x, float* grad_y, void* ws, cudaStream_t st);
 int backward_launches(const BwdPlan& p);
 
 // Reusable stable LSD radix sort of u32 (key, value) pairs (nn_backward.cu).

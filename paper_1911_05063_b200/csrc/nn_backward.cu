@@ -422,6 +422,7 @@ struct GradArgs {
     const float* g;
     const float* h;
     float g_scalar, h_scalar;
+    const float* upstream;   // optional device scalar u: the fills become RN(u * g_scalar), RN(u * h_scalar)
     const uint32_t* vals;
     const uint32_t* off;
     float* grad_x;
@@ -437,6 +438,11 @@ __device__ __forceinline__ void acc_term(double acc[3], const float* p, const fl
 
 __global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
     pdl_wait();
+    if (a.upstream) {
+        const float u = *a.upstream;
+        a.g_scalar = __fmul_rn(u, a.g_scalar);
+        a.h_scalar = __fmul_rn(u, a.h_scalar);
+    }
     const int sq = a.q1 - a.q0, sr = a.r1 - a.r0;
     const int64_t nx = (int64_t)a.B * sq;
     const int64_t total = nx + (int64_t)a.B * sr;
@@ -620,7 +626,7 @@ int backward_launches(const BwdPlan& p) {
 
 cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, const int32_t* idx_xy,
                             const int32_t* idx_yx, const float* g, const float* h, float g_scalar, float h_scalar,
-                            float* grad_x, float* grad_y, void* ws, cudaStream_t st) {
+                            const float* upstream, float* grad_x, float* grad_y, void* ws, cudaStream_t st) {
     char* w = static_cast<char*>(ws);
     uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
@@ -665,6 +671,7 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     a.h = h;
     a.g_scalar = g_scalar;
     a.h_scalar = h_scalar;
+    a.upstream = upstream;
     a.vals = vals[cur];
     a.off = off;
     a.grad_x = grad_x;

@@ -238,6 +238,10 @@ struct MergeArgs {
     double tau2;  // < 0: no hits
 };
 
+// Row direction: per query row, unpack the merged key and find the lowest index inside the winning
+// 32-target block with d == min (same .rn ops as the kernel).  Warp-cooperative: the warp walks its
+// rows four at a time; for each, the 32 lanes load the block's 32 targets (one coalesced 512-B
+// read) and a ballot picks the first match.
 __device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
     int u = blk;
     int dir = 0;
@@ -249,35 +253,53 @@ __device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
     const int chunk = u - b * a.nchunks[dir];
     const int slen = a.qhi[dir] - a.qlo[dir];
     const int sq = chunk * kMergeThreads + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     const bool valid = sq < slen;
+    float best = INFINITY;
+    int bb = -1;
+    float4 qp = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+        // the atomicMin over splits kept the smallest distance, then the lowest block start
+        const unsigned long long key = (unsigned long long)a.rowkey[a.slice_off[dir] + (int64_t)b * slen + sq];
+        best = __uint_as_float((unsigned)(key >> 32));
+        bb = (int)(unsigned)(key & 0xffffffffull);   // 0xffffffff -> -1: no finite distance
+        if (bb >= 0) qp = a.pack[dir][(int64_t)b * a.ppad[dir] + a.qlo[dir] + sq];
+    }
+    const int tdir = 1 - dir;
+    const float4* T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
+    const int ntgt = a.npts[tdir];
+    CD_CHECK(bb < 0 || (bb < ntgt && bb % kBlockK == 0));
+    int idx = -1;
+    unsigned todo = __ballot_sync(0xffffffffu, bb >= 0);
+    while (todo) {
+        int r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            r[k] = todo ? __ffs(todo) - 1 : -1;
+            todo &= todo - 1;
+        }
+        float4 t[4];
+        int base[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            base[k] = __shfl_sync(0xffffffffu, bb, r[k] & 31);
+            const int j = base[k] + lane;
+            t[k] = (r[k] >= 0 && j < ntgt) ? T[j] : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int src = r[k] & 31;
+            const float qx = __shfl_sync(0xffffffffu, qp.x, src), qy = __shfl_sync(0xffffffffu, qp.y, src),
+                        qz = __shfl_sync(0xffffffffu, qp.z, src);
+            const float m = __shfl_sync(0xffffffffu, best, src);
+            const float d = dist_rn(qx, qy, qz, t[k].x, t[k].y, t[k].z);
+            const unsigned hit = __ballot_sync(0xffffffffu, r[k] >= 0 && base[k] + lane < ntgt && d == m);
+            if (lane == r[k] && hit) idx = base[k] + __ffs(hit) - 1;
+        }
+    }
     double v = 0.0;
     int h = 0;
     if (valid) {
-        const int64_t row = a.slice_off[dir] + (int64_t)b * slen + sq;
-        // the atomicMin over splits kept the smallest distance, then the lowest block start
-        const unsigned long long key = (unsigned long long)a.rowkey[row];
-        const float best = __uint_as_float((unsigned)(key >> 32));
-        const int bb = (int)(unsigned)(key & 0xffffffffull);   // 0xffffffff -> -1: no finite distance
-        int idx = -1;
-        if (bb >= 0) {
-            const int tdir = 1 - dir;
-            const float4 qp = a.pack[dir][(int64_t)b * a.ppad[dir] + a.qlo[dir] + sq];
-            const float4* T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
-            const int jend = min(bb + kBlockK, a.npts[tdir]);
-            CD_CHECK(bb < a.npts[tdir] && bb % kBlockK == 0);
-            // chunks of 8 independent loads (memory-level parallelism), first match wins
-            for (int c = bb; c < jend && idx < 0; c += 8) {
-                float d[8];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const float4 t = T[min(c + r, jend - 1)];
-                    d[r] = dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z);
-                }
-#pragma unroll
-                for (int r = 7; r >= 0; --r)
-                    if (c + r < jend && d[r] == best) idx = c + r;
-            }
-        }
         a.d_out[dir][(int64_t)b * slen + sq] = best;
         a.idx_out[dir][(int64_t)b * slen + sq] = idx;
         v = (double)best;
@@ -310,48 +332,76 @@ struct ResolveArgs {
 
 // column direction of the fused forward: per Y row, unpack the key and re-evaluate the winning
 // thread's 16 rows with the same .rn ops (lowest index with d == min); `blk` = this CTA's chunk.
+// Warp-cooperative: two columns per step, each half-warp loading one column's 16 rows (coalesced).
 __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk) {
     const int b = blk / a.nchunks;
     const int chunk = blk - b * a.nchunks;
     const int slen = a.r1 - a.r0;
     const int sj = chunk * kMergeThreads + threadIdx.x;
-    double v = 0.0;
-    int h = 0;
+    const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+    float m = INFINITY;
+    int i0 = -1;
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sj < slen) {
         const int j = a.r0 + sj;
         const unsigned long long key = (unsigned long long)a.colkey[(int64_t)b * a.M + j];
-        float m = INFINITY;
-        int idx = -1;
         // a +inf minimum is no finite candidate (R6): (+inf, -1) like the row direction
         if ((long long)key != kColKeyEmpty && __uint_as_float((unsigned)(key >> 32)) < INFINITY) {
             m = __uint_as_float((unsigned)(key >> 32));
-            const int i0 = (int)(unsigned)(key & 0xffffffffull);
+            i0 = (int)(unsigned)(key & 0xffffffffull);
             CD_CHECK(i0 >= a.q0 && i0 < a.q1);
-            const float4 t = a.yp[(int64_t)b * a.ypad + j];
-            const float4* X = a.xp + (int64_t)b * a.xpad;
-            const int iend = min(i0 + kR, a.q1);
-            float d[kR];
-#pragma unroll
-            for (int r = 0; r < kR; ++r) {
-                const float4 q = X[min(i0 + r, a.q1 - 1)];
-                d[r] = dist_rn(q.x, q.y, q.z, t.x, t.y, t.z);  // same operand order as the kernel
-            }
-#pragma unroll
-            for (int r = kR - 1; r >= 0; --r)
-                if (i0 + r < iend && d[r] == m) idx = i0 + r;
-            if (idx < 0) m = INFINITY;  // only when every distance was NaN
+            t = a.yp[(int64_t)b * a.ypad + j];
         }
+    }
+    const float4* X = a.xp + (int64_t)b * a.xpad;
+    static_assert(kR == 16, "the column resolve re-scans 16-row groups with half-warps");
+    int idx = -1;
+    unsigned todo = __ballot_sync(0xffffffffu, i0 >= 0);
+    while (todo) {
+        int r[2][2];   // [step][half]
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            r[k >> 1][k & 1] = todo ? __ffs(todo) - 1 : -1;
+            todo &= todo - 1;
+        }
+        float4 q[2];
+        int g0[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int mine = r[k][half];
+            g0[k] = __shfl_sync(0xffffffffu, i0, mine & 31);
+            const int i = g0[k] + hl;
+            q[k] = (mine >= 0 && i < a.q1) ? X[i] : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int mine = r[k][half], src = mine & 31;
+            const float tx = __shfl_sync(0xffffffffu, t.x, src), ty = __shfl_sync(0xffffffffu, t.y, src),
+                        tz = __shfl_sync(0xffffffffu, t.z, src);
+            const float mm = __shfl_sync(0xffffffffu, m, src);
+            const float d = dist_rn(q[k].x, q[k].y, q[k].z, tx, ty, tz);  // same operand order as the kernel
+            const unsigned hit = __ballot_sync(0xffffffffu, mine >= 0 && g0[k] + hl < a.q1 && d == mm);
+            const unsigned h0 = hit & 0xffffu, h1 = hit >> 16;
+            const int gA = __shfl_sync(0xffffffffu, g0[k], 0), gB = __shfl_sync(0xffffffffu, g0[k], 16);
+            if (lane == r[k][0] && h0) idx = gA + __ffs(h0) - 1;
+            if (lane == r[k][1] && h1) idx = gB + __ffs(h1) - 1;
+        }
+    }
+    if (idx < 0) m = INFINITY;  // no finite candidate, or every distance was NaN
+    double v = 0.0;
+    int h = 0;
+    if (sj < slen) {
         a.d_out[(int64_t)b * slen + sj] = m;
         a.idx_out[(int64_t)b * slen + sj] = idx;
         v = (double)m;
         h = (a.tau2 >= 0.0 && (double)m <= a.tau2) ? 1 : 0;
     }
     double s;
-    int t;
-    block_sum_hits(v, h, &s, &t);
+    int hs;
+    block_sum_hits(v, h, &s, &hs);
     if (threadIdx.x == 0) {
         a.chunk_sum[(int64_t)b * a.nchunks + chunk] = s;
-        a.chunk_hits[(int64_t)b * a.nchunks + chunk] = t;
+        a.chunk_hits[(int64_t)b * a.nchunks + chunk] = hs;
     }
 }
 

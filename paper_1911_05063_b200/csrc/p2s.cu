@@ -190,8 +190,7 @@ __global__ void __launch_bounds__(kMergeThreads) p2s_merge_kernel(P2sMergeArgs a
             Bv[k] = vv[3 * ib + k];
             C[k] = vv[3 * ic + k];
         }
-        closest64(p, A, Bv, C, c, lam);
-        const double dd = (p[0] - c[0]) * (p[0] - c[0]) + (p[1] - c[1]) * (p[1] - c[1]) + (p[2] - c[2]) * (p[2] - c[2]);
+        const double dd = face_foot64(p, A, Bv, C, c, lam);
         a.d_out[row] = (float)dd;
         a.face_out[row] = face;
         if (a.closest)
@@ -255,8 +254,9 @@ __global__ void __launch_bounds__(256) p2s_pack_kernel(P2sPackArgs a) {
 }
 
 __global__ void __launch_bounds__(256) p2s_grad_points_kernel(const float* pts, const float* closest, const float* g,
-                                                              float g_scalar, int64_t total, float* grad_points,
-                                                              float* upstream_verts) {
+                                                              float g_scalar, const float* upstream, int64_t total,
+                                                              float* grad_points, float* upstream_verts) {
+    if (upstream) g_scalar = __fmul_rn(*upstream, g_scalar);   // loss backward: the fill RN(u * 1/(B N))
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const double gi = g ? (double)g[e] : (double)g_scalar;
         for (int k = 0; k < 3; ++k) {
@@ -395,12 +395,12 @@ cudaError_t launch_p2s(const float* points, const float* verts, const int* faces
 
 cudaError_t launch_p2s_backward(const float* points, const float* closest, const int* face, const float* bary,
                                 const int* faces, int B, int N, int Nv, int Nf, const float* g, float g_scalar,
-                                float* grad_points, float* grad_verts, void* ws, cudaStream_t st) {
+                                const float* upstream, float* grad_points, float* grad_verts, void* ws, cudaStream_t st) {
     char* w = static_cast<char*>(ws);
     float* up = reinterpret_cast<float*>(w);
     const int64_t total = (int64_t)B * N;
-    p2s_grad_points_kernel<<<std::min(cdiv(total, 256), 148 * 16), 256, 0, st>>>(points, closest, g, g_scalar, total,
-                                                                                 grad_points, up);
+    p2s_grad_points_kernel<<<std::min(cdiv(total, 256), 148 * 16), 256, 0, st>>>(points, closest, g, g_scalar, upstream,
+                                                                                 total, grad_points, up);
     if (grad_verts)
         return launch_sample_backward(faces, face, bary, B, Nv, Nf, N, up, grad_verts,
                                       w + align_up((size_t)B * N * 12, 256), st);

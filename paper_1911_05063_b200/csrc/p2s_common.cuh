@@ -1,6 +1,7 @@
 // p2s_common.cuh — shared device code of the point-to-surface kernels (p2s.cu, p2s_pruned.cu):
 // the packed face record (R24), the packed-FP32 point-to-triangle squared distance, and the fp64
-// closest point on a triangle (the region decomposition of the oracle's definition).
+// closest point on the chosen face (R24's plane-or-edges formulation in fp64; the oracle uses the
+// region decomposition instead and shares no code with this file).
 #pragma once
 #include "cd_device.cuh"
 
@@ -74,105 +75,36 @@ __device__ __forceinline__ u64 add2(u64 a, u64 b) {
     return r;
 }
 
-// Packed squared distance of two points (qx, qy, qz lanes) to one face record (R24, fixed op order).
-// With ne = -e: s' = ap.ne0 = -ap.e0, t0 = sat(s' * (-1/|e0|^2)), x - t0 e0 = fma(t0, ne0, ap).
-__device__ __forceinline__ void face_dist2(const float* f, u64 qx, u64 qy, u64 qz, float& d0, float& d1) {
-    const u64 ax = sub2(qx, bc2(f[0])), ay = sub2(qy, bc2(f[1])), az = sub2(qz, bc2(f[2]));
-    u64 s = mul2(ax, bc2(f[3]));
-    s = fma2(ay, bc2(f[4]), s);
-    s = fma2(az, bc2(f[5]), s);
-    u64 t = mul2(ax, bc2(f[6]));
-    t = fma2(ay, bc2(f[7]), t);
-    t = fma2(az, bc2(f[8]), t);
-    // in-plane coordinates of the projection
-    u64 u = fma2(s, bc2(f[18]), bc2(f[21]));
-    u = fma2(t, bc2(f[19]), u);
-    u64 v = fma2(s, bc2(f[19]), bc2(f[21]));
-    v = fma2(t, bc2(f[20]), v);
-    // plane distance
-    u64 h = mul2(ax, bc2(f[12]));
-    h = fma2(ay, bc2(f[13]), h);
-    h = fma2(az, bc2(f[14]), h);
-    const u64 pl = mul2(h, h);
-    // edge a-b
-    const u64 t0 = sat_mul2(s, bc2(f[15]));
-    u64 dx = fma2(t0, bc2(f[3]), ax), dy = fma2(t0, bc2(f[4]), ay), dz = fma2(t0, bc2(f[5]), az);
-    u64 dab = mul2(dx, dx);
-    dab = fma2(dy, dy, dab);
-    dab = fma2(dz, dz, dab);
-    // edge a-c
-    const u64 t1 = sat_mul2(t, bc2(f[16]));
-    dx = fma2(t1, bc2(f[6]), ax);
-    dy = fma2(t1, bc2(f[7]), ay);
-    dz = fma2(t1, bc2(f[8]), az);
-    u64 dac = mul2(dx, dx);
-    dac = fma2(dy, dy, dac);
-    dac = fma2(dz, dz, dac);
-    // edge b-c: bp = ap - e0 = ap + ne0
-    const u64 bx = add2(ax, bc2(f[3])), by = add2(ay, bc2(f[4])), bz = add2(az, bc2(f[5]));
-    u64 s2 = mul2(bx, bc2(f[9]));
-    s2 = fma2(by, bc2(f[10]), s2);
-    s2 = fma2(bz, bc2(f[11]), s2);
-    const u64 t2 = sat_mul2(s2, bc2(f[17]));
-    dx = fma2(t2, bc2(f[9]), bx);
-    dy = fma2(t2, bc2(f[10]), by);
-    dz = fma2(t2, bc2(f[11]), bz);
-    u64 dbc = mul2(dx, dx);
-    dbc = fma2(dy, dy, dbc);
-    dbc = fma2(dz, dz, dbc);
-    float u0, u1, v0, v1, p0, p1, ab0, ab1, ac0, ac1, bc0, bc1;
-    upk2(u, u0, u1);
-    upk2(v, v0, v1);
-    upk2(pl, p0, p1);
-    upk2(dab, ab0, ab1);
-    upk2(dac, ac0, ac1);
-    upk2(dbc, bc0, bc1);
-    const float w0 = __fsub_rn(__fsub_rn(1.0f, u0), v0), w1 = __fsub_rn(__fsub_rn(1.0f, u1), v1);
-    const bool in0 = fmin3(u0, v0, w0) >= 0.0f, in1 = fmin3(u1, v1, w1) >= 0.0f;
-    d0 = fmin3(ab0, ac0, fminf(bc0, in0 ? p0 : INFINITY));
-    d1 = fmin3(ab1, ac1, fminf(bc1, in1 ? p1 : INFINITY));
-}
-
-// A 24-float face record (96 B, 16-B aligned) as six 16-byte loads.
-__device__ __forceinline__ void load_face_record(const float* src, float* dst) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-#pragma unroll
-    for (int k = 0; k < kFaceFloats / 4; ++k) {
-        const float4 v = __ldg(s4 + k);
-        dst[4 * k] = v.x;
-        dst[4 * k + 1] = v.y;
-        dst[4 * k + 2] = v.z;
-        dst[4 * k + 3] = v.w;
-    }
-}
-
-// The same per-lane arithmetic as face_dist2 with the lanes swapped round: ONE point (px, py, pz)
-// against TWO face records (fa in the low lane, fb in the high lane).  Every lane executes the
-// identical op sequence, so the distances are bit-identical to face_dist2's for the same (point,
-// face); used where one point meets many faces (the exact-face re-scans).
-__device__ __forceinline__ void face_dist2_2f(const float* fa, const float* fb, float px, float py, float pz,
-                                              float& da, float& db) {
-    auto F = [&](int k) { return pk2(fa[k], fb[k]); };
-    const u64 ax = sub2(bc2(px), F(0)), ay = sub2(bc2(py), F(1)), az = sub2(bc2(pz), F(2));
+// Packed squared distance, per lane, of a point (qx, qy, qz) to a face record (R24, fixed op
+// order); F(k) gives face float k as a packed pair.  With ne = -e: s' = ap.ne0 = -ap.e0,
+// t0 = sat(s' * (-1/|e0|^2)), x - t0 e0 = fma(t0, ne0, ap).  Both callers below run this one op
+// sequence, so a (point, face) pair gets the same bits whichever lane layout evaluates it.
+template <class FaceK>
+__device__ __forceinline__ void face_dist2_lanes(FaceK F, u64 qx, u64 qy, u64 qz, float& d0, float& d1) {
+    const u64 ax = sub2(qx, F(0)), ay = sub2(qy, F(1)), az = sub2(qz, F(2));
     u64 s = mul2(ax, F(3));
     s = fma2(ay, F(4), s);
     s = fma2(az, F(5), s);
     u64 t = mul2(ax, F(6));
     t = fma2(ay, F(7), t);
     t = fma2(az, F(8), t);
+    // in-plane coordinates of the projection
     u64 u = fma2(s, F(18), F(21));
     u = fma2(t, F(19), u);
     u64 v = fma2(s, F(19), F(21));
     v = fma2(t, F(20), v);
+    // plane distance
     u64 h = mul2(ax, F(12));
     h = fma2(ay, F(13), h);
     h = fma2(az, F(14), h);
     const u64 pl = mul2(h, h);
+    // edge a-b
     const u64 t0 = sat_mul2(s, F(15));
     u64 dx = fma2(t0, F(3), ax), dy = fma2(t0, F(4), ay), dz = fma2(t0, F(5), az);
     u64 dab = mul2(dx, dx);
     dab = fma2(dy, dy, dab);
     dab = fma2(dz, dz, dab);
+    // edge a-c
     const u64 t1 = sat_mul2(t, F(16));
     dx = fma2(t1, F(6), ax);
     dy = fma2(t1, F(7), ay);
@@ -180,6 +112,7 @@ __device__ __forceinline__ void face_dist2_2f(const float* fa, const float* fb, 
     u64 dac = mul2(dx, dx);
     dac = fma2(dy, dy, dac);
     dac = fma2(dz, dz, dac);
+    // edge b-c: bp = ap - e0 = ap + ne0
     const u64 bx = add2(ax, F(3)), by = add2(ay, F(4)), bz = add2(az, F(5));
     u64 s2 = mul2(bx, F(9));
     s2 = fma2(by, F(10), s2);
@@ -200,51 +133,86 @@ __device__ __forceinline__ void face_dist2_2f(const float* fa, const float* fb, 
     upk2(dbc, bc0, bc1);
     const float w0 = __fsub_rn(__fsub_rn(1.0f, u0), v0), w1 = __fsub_rn(__fsub_rn(1.0f, u1), v1);
     const bool in0 = fmin3(u0, v0, w0) >= 0.0f, in1 = fmin3(u1, v1, w1) >= 0.0f;
-    da = fmin3(ab0, ac0, fminf(bc0, in0 ? p0 : INFINITY));
-    db = fmin3(ab1, ac1, fminf(bc1, in1 ? p1 : INFINITY));
+    d0 = fmin3(ab0, ac0, fminf(bc0, in0 ? p0 : INFINITY));
+    d1 = fmin3(ab1, ac1, fminf(bc1, in1 ? p1 : INFINITY));
 }
 
-// fp64 closest point on triangle (region decomposition; the same case order as the definition)
-__device__ __forceinline__ void closest64(const double p[3], const double A[3], const double Bv[3], const double C[3], double out[3],
-                          double lam[3]) {
-    double ab[3], ac[3], ap[3], bp[3], cp[3];
+// Two points (qx, qy, qz lanes) against one face record (face floats broadcast to both lanes).
+__device__ __forceinline__ void face_dist2(const float* f, u64 qx, u64 qy, u64 qz, float& d0, float& d1) {
+    face_dist2_lanes([&](int k) { return bc2(f[k]); }, qx, qy, qz, d0, d1);
+}
+
+// A 24-float face record (96 B, 16-B aligned) as six 16-byte loads.
+__device__ __forceinline__ void load_face_record(const float* src, float* dst) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+#pragma unroll
+    for (int k = 0; k < kFaceFloats / 4; ++k) {
+        const float4 v = __ldg(s4 + k);
+        dst[4 * k] = v.x;
+        dst[4 * k + 1] = v.y;
+        dst[4 * k + 2] = v.z;
+        dst[4 * k + 3] = v.w;
+    }
+}
+
+// ONE point (px, py, pz) against TWO face records (fa in the low lane, fb in the high lane): used
+// where one point meets many faces (the exact-face re-scans).
+__device__ __forceinline__ void face_dist2_2f(const float* fa, const float* fb, float px, float py, float pz,
+                                              float& da, float& db) {
+    face_dist2_lanes([&](int k) { return pk2(fa[k], fb[k]); }, bc2(px), bc2(py), bc2(pz), da, db);
+}
+
+// fp64 closest point of p on the triangle (A, B, C) and its squared distance: R24's formulation
+// carried out in fp64 for the one face the hot loop chose.  Candidates, in this
+// order: the foot of the perpendicular on the face's plane, taken only when its barycentrics
+// (solved with the inverse Gram matrix of e0 = B - A, e1 = C - A) are all >= 0; then the nearest
+// point of each edge AB, AC, BC (parameter clamped to [0, 1]).  The first candidate at the
+// smallest squared distance wins.  A face with zero Gram determinant (a segment or a point) has
+// no plane candidate.  lam = barycentric coordinates of the returned point on (A, B, C).
+__device__ __forceinline__ double face_foot64(const double p[3], const double A[3], const double Bv[3], const double C[3],
+                                              double out[3], double lam[3]) {
+    double e0[3], e1[3], e2[3], ap[3], bp[3];
     for (int k = 0; k < 3; ++k) {
-        ab[k] = Bv[k] - A[k];
-        ac[k] = C[k] - A[k];
+        e0[k] = Bv[k] - A[k];
+        e1[k] = C[k] - A[k];
+        e2[k] = C[k] - Bv[k];
         ap[k] = p[k] - A[k];
         bp[k] = p[k] - Bv[k];
-        cp[k] = p[k] - C[k];
     }
-    auto dot = [](const double* x, const double* y) { return x[0] * y[0] + x[1] * y[1] + x[2] * y[2]; };
-    const double d1 = dot(ab, ap), d2 = dot(ac, ap), d3 = dot(ab, bp), d4 = dot(ac, bp), d5 = dot(ab, cp),
-                 d6 = dot(ac, cp);
-    const double vc = d1 * d4 - d3 * d2, vb = d5 * d2 - d1 * d6, va = d3 * d6 - d5 * d4;
-    double l0, l1, l2;
-    if (d1 <= 0.0 && d2 <= 0.0) {
-        l0 = 1; l1 = 0; l2 = 0;
-    } else if (d3 >= 0.0 && d4 <= d3) {
-        l0 = 0; l1 = 1; l2 = 0;
-    } else if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
-        const double v = d1 / (d1 - d3);
-        l0 = 1 - v; l1 = v; l2 = 0;
-    } else if (d6 >= 0.0 && d5 <= d6) {
-        l0 = 0; l1 = 0; l2 = 1;
-    } else if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
-        const double w = d2 / (d2 - d6);
-        l0 = 1 - w; l1 = 0; l2 = w;
-    } else if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
-        const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
-        l0 = 0; l1 = 1 - w; l2 = w;
-    } else {
-        const double den = va + vb + vc;
-        const double v = vb / den, w = vc / den;
-        l0 = 1 - v - w; l1 = v; l2 = w;
+    const double g00 = e0[0] * e0[0] + e0[1] * e0[1] + e0[2] * e0[2];
+    const double g01 = e0[0] * e1[0] + e0[1] * e1[1] + e0[2] * e1[2];
+    const double g11 = e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2];
+    const double g22 = e2[0] * e2[0] + e2[1] * e2[1] + e2[2] * e2[2];
+    const double s = ap[0] * e0[0] + ap[1] * e0[1] + ap[2] * e0[2];
+    const double t = ap[0] * e1[0] + ap[1] * e1[1] + ap[2] * e1[2];
+    const double s2 = bp[0] * e2[0] + bp[1] * e2[1] + bp[2] * e2[2];
+    double best = INFINITY;
+    auto take = [&](double l0, double l1, double l2) {
+        double q[3], dd = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            q[k] = l0 * A[k] + l1 * Bv[k] + l2 * C[k];
+            dd += (p[k] - q[k]) * (p[k] - q[k]);
+        }
+        if (dd < best) {
+            best = dd;
+            for (int k = 0; k < 3; ++k) out[k] = q[k];
+            lam[0] = l0;
+            lam[1] = l1;
+            lam[2] = l2;
+        }
+    };
+    const double det = g00 * g11 - g01 * g01;
+    if (det > 0.0) {
+        const double v = (g11 * s - g01 * t) / det, w = (g00 * t - g01 * s) / det, u = 1.0 - v - w;
+        if (u >= 0.0 && v >= 0.0 && w >= 0.0) take(u, v, w);
     }
-    for (int k = 0; k < 3; ++k) out[k] = l0 * A[k] + l1 * Bv[k] + l2 * C[k];
-    lam[0] = l0;
-    lam[1] = l1;
-    lam[2] = l2;
+    const double tab = g00 > 0.0 ? fmin(fmax(s / g00, 0.0), 1.0) : 0.0;
+    const double tac = g11 > 0.0 ? fmin(fmax(t / g11, 0.0), 1.0) : 0.0;
+    const double tbc = g22 > 0.0 ? fmin(fmax(s2 / g22, 0.0), 1.0) : 0.0;
+    take(1.0 - tab, tab, 0.0);
+    take(1.0 - tac, 0.0, tac);
+    take(0.0, 1.0 - tbc, tbc);
+    return best;
 }
-
 
 }  // namespace cdk

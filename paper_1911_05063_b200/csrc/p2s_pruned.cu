@@ -700,8 +700,7 @@ __global__ void __launch_bounds__(kMergeThreads) ps_resolve_kernel(PsResolveArgs
             Bv[k] = vv[3 * ib + k];
             C[k] = vv[3 * ic + k];
         }
-        closest64(q, A, Bv, C, c, lam);
-        const double dd = (q[0] - c[0]) * (q[0] - c[0]) + (q[1] - c[1]) * (q[1] - c[1]) + (q[2] - c[2]) * (q[2] - c[2]);
+        const double dd = face_foot64(q, A, Bv, C, c, lam);
         const int64_t row = (int64_t)b * a.N + a.perm_p[srow];
         a.d_out[row] = (float)dd;
         a.face_out[row] = face;

@@ -23,6 +23,41 @@ import torch
 import torch.distributed as dist
 
 
+class CollectiveTimer:
+    """Optional CUDA-event brackets around every collective of a step (name -> list of (start, end)
+    events on the current stream), so a caller can report the time a step spends in collectives.
+    The events measure how long the launching stream waits for the collective."""
+
+    def __init__(self):
+        self.spans = []
+
+    def __call__(self, name, fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn()
+        b.record()
+        self.spans.append((name, a, b))
+        return r
+
+    def total_ms(self):
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for _, a, b in self.spans)
+
+    def by_name_ms(self):
+        torch.cuda.synchronize()
+        out = {}
+        for n, a, b in self.spans:
+            out[n] = out.get(n, 0.0) + a.elapsed_time(b)
+        return out
+
+    def reset(self):
+        self.spans = []
+
+
+def _coll(prof, name, fn):
+    return prof(name, fn) if prof is not None else fn()
+
+
 def shard_range(n: int, rank: int, world: int):
     """Balanced contiguous [lo, hi) slice of n items for `rank` of `world`."""
     return (n * rank) // world, (n * (rank + 1)) // world
@@ -34,7 +69,7 @@ def _world(group=None):
     return 0, 1
 
 
-def allreduce_partials(part_local: torch.Tensor, B_global: int, b0: int, group=None) -> torch.Tensor:
+def allreduce_partials(part_local: torch.Tensor, B_global: int, b0: int, group=None, prof=None) -> torch.Tensor:
     """Place the local B_l x 4 partials at rows [b0, b0+B_l) of a zero B_global x 4 tensor and
     all-reduce (sum).  With B_global == B_l and b0 == 0 this is the query-sharded sum."""
     rank, world = _world(group)
@@ -43,11 +78,11 @@ def allreduce_partials(part_local: torch.Tensor, B_global: int, b0: int, group=N
     full = torch.zeros((B_global, 4), dtype=torch.float64, device=part_local.device)
     full[b0:b0 + part_local.shape[0]] = part_local
     if world > 1:
-        dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+        _coll(prof, "all_reduce_partials", lambda: dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group))
     return full
 
 
-def all_gather_rows(local: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
+def all_gather_rows(local: torch.Tensor, n_total: int, group=None, prof=None) -> torch.Tensor:
     """Gather (B, n_r, ...) row slices produced by shard_range into (B, n_total, ...)."""
     rank, world = _world(group)
     if world == 1:
@@ -57,7 +92,7 @@ def all_gather_rows(local: torch.Tensor, n_total: int, group=None) -> torch.Tens
     pad = torch.zeros((B, width) + tuple(local.shape[2:]), dtype=local.dtype, device=local.device)
     pad[:, :local.shape[1]] = local
     bufs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
+    _coll(prof, "all_gather_idx", lambda: dist.all_gather(bufs, pad, group=group))
     parts = []
     for r in range(world):
         lo, hi = shard_range(n_total, r, world)
@@ -65,22 +100,22 @@ def all_gather_rows(local: torch.Tensor, n_total: int, group=None) -> torch.Tens
     return torch.cat(parts, dim=1).contiguous()
 
 
-def broadcast_clouds(x: torch.Tensor, y: torch.Tensor, src: int = 0, group=None):
+def broadcast_clouds(x: torch.Tensor, y: torch.Tensor, src: int = 0, group=None, prof=None):
     """Replicate the clouds from `src` (the "target broadcast over NVLink" of config c5)."""
     _, world = _world(group)
     if world > 1:
-        dist.broadcast(x, src=src, group=group)
-        dist.broadcast(y, src=src, group=group)
+        _coll(prof, "broadcast_clouds", lambda: (dist.broadcast(x, src=src, group=group),
+                                                 dist.broadcast(y, src=src, group=group)))
     return x, y
 
 
 def batch_sharded_step(engine, x_local, y_local, B_global: int, b0: int, tau=None, w1: float = 1.0,
-                       w2: float = 1.0, group=None, backward: bool = True):
+                       w2: float = 1.0, group=None, backward: bool = True, prof=None):
     """One fwd(+F)+loss+bwd step on this rank's batch block.  Returns a dict with the global loss,
     per-batch CD / F (global), and this rank's per-point outputs and gradients."""
     N, M = x_local.shape[1], y_local.shape[1]
     d_xy, i_xy, d_yx, i_yx, part = engine.forward(x_local, y_local, tau=tau)
-    part = allreduce_partials(part, B_global, b0, group)
+    part = allreduce_partials(part, B_global, b0, group, prof)
     cd, loss, F, P, R = engine.finalize(part, N, M, w1, w2)
     out = dict(d_xy=d_xy, idx_xy=i_xy, d_yx=d_yx, idx_yx=i_yx, partials=part, cd=cd, loss=loss, fscore=F,
                precision=P, recall=R)
@@ -91,17 +126,17 @@ def batch_sharded_step(engine, x_local, y_local, B_global: int, b0: int, tau=Non
     return out
 
 
-def allreduce_colkeys(keys: torch.Tensor, group=None) -> torch.Tensor:
+def allreduce_colkeys(keys: torch.Tensor, group=None, prof=None) -> torch.Tensor:
     """Element-wise MIN of the int64 column keys across ranks (keys are >= 0, so signed MIN is the
     lexicographic (distance, row group) minimum)."""
     _, world = _world(group)
     if world > 1:
-        dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
+        _coll(prof, "all_reduce_min_colkeys", lambda: dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group))
     return keys
 
 
 def query_sharded_step(engine, x, y, tau=None, w1: float = 1.0, w2: float = 1.0, group=None,
-                       backward: bool = True):
+                       backward: bool = True, prof=None):
     """One step with query rows split across ranks; x, y are full replicas on every rank.
 
     Rank r evaluates X rows q_r against all of Y ONCE (fused kernel): its d_xy rows are final and
@@ -113,17 +148,17 @@ def query_sharded_step(engine, x, y, tau=None, w1: float = 1.0, w2: float = 1.0,
     r = shard_range(M, rank, world)
     if hasattr(engine, "forward_rows"):
         d_xy, i_xy, keys, part = engine.forward_rows(x, y, q, tau=tau)
-        keys = allreduce_colkeys(keys, group)
+        keys = allreduce_colkeys(keys, group, prof)
         d_yx, i_yx, part = engine.forward_cols(x, y, keys, r, tau=tau, partials=part)
     else:
         d_xy, i_xy, d_yx, i_yx, part = engine.forward(x, y, tau=tau, q_slice=q, r_slice=r)
-    part = allreduce_partials(part, B, 0, group)
+    part = allreduce_partials(part, B, 0, group, prof)
     cd, loss, F, P, R = engine.finalize(part, N, M, w1, w2)
     out = dict(d_xy=d_xy, idx_xy=i_xy, d_yx=d_yx, idx_yx=i_yx, partials=part, cd=cd, loss=loss, fscore=F,
                precision=P, recall=R, q_slice=q, r_slice=r)
     if backward:
-        i_xy_full = all_gather_rows(i_xy, N, group)
-        i_yx_full = all_gather_rows(i_yx, M, group)
+        i_xy_full = all_gather_rows(i_xy, N, group, prof)
+        i_yx_full = all_gather_rows(i_yx, M, group, prof)
         gx, gy = engine.backward(x, y, i_xy_full, i_yx_full, g_scalar=w1 / (B * N), h_scalar=w2 / (B * M),
                                  q_slice=q, r_slice=r)
         out.update(grad_x=gx, grad_y=gy)

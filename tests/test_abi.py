@@ -37,7 +37,7 @@ def test_only_cd_symbols_exported():
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.cd_abi_version() == 3
+    assert lib.cd_abi_version() == 4
     assert lib.cd_status_string(0) == b"CD_OK"
     assert lib.cd_status_string(1) == b"CD_ERR_INVALID_VALUE"
     assert lib.cd_status_string(5) == b"CD_ERR_CUDA"
@@ -97,6 +97,16 @@ def test_backward_and_fscore_validation(lib):
                            1 << 30, None) == 1
     assert lib.cd_fscore(v(4), v(4), 1, 4, 4, -0.5, v(4), None, None, v(256), 1 << 20, None) == 1
     assert lib.cd_finalize(None, 1, 4, 4, 1.0, 1.0, None, v(4), None, None, None, None) == 1
+    # the loss backward: null upstream scalar, empty cloud, bad slice -> invalid value before any launch
+    assert lib.cd_loss_backward(v(4), v(4), 1, 4, 4, v(4), v(4), None, 1.0, 1.0, 0, 4, 0, 4, v(4), v(4), v(256),
+                                1 << 30, None) == 1
+    assert b"grad_loss" in lib.cd_last_error_string()
+    assert lib.cd_loss_backward(v(4), v(4), 1, 0, 4, v(4), v(4), v(4), 1.0, 1.0, 0, 0, 0, 4, v(4), v(4), v(256),
+                                1 << 30, None) == 1
+    assert lib.cd_loss_backward(v(4), v(4), 1, 4, 4, v(4), v(4), v(4), 1.0, 1.0, 0, 4, 0, 5, v(4), v(4), v(256),
+                                1 << 30, None) == 1
+    assert lib.cd_p2s_loss_backward(v(4), v(4), v(4), v(4), v(4), 1, 4, 3, 1, None, v(4), v(4), v(256), 1 << 30,
+                                    None) == 1
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) not in (None, "") and False, reason="")

@@ -94,25 +94,23 @@ def test_c2_full_per_direction_kernel(cd):
         cd.set_forward_mode(old)
 
 
-def test_c3_sampled_forward_full_backward(cd):
+def test_c3_full(cd):
+    """The headline config (the one naming F@0.01) on EVERY row of both directions: distances and
+    indices vs the fp64 oracle (R12/R13), distance bits and indices vs the fp32 mirror, partials,
+    CD_b and loss within 1e-5, hit counts inside the R16 band, F at the GPU's counts, and the
+    backward (random upstream) bit-identical to the oracle's; then the loss gradient."""
     X, Y = synth.config_inputs("c3")
-    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
+    d_xy, i_xy, d_yx, i_yx, part = _full_check(cd, X, Y, tau=0.01)
     B, N, M = X.shape[0], X.shape[1], Y.shape[1]
-    rng = np.random.default_rng(3)
-    rows_x = np.sort(rng.choice(B * N, 20000, replace=False))
-    rows_y = np.sort(rng.choice(B * M, 20000, replace=False))
-    rows_x[:3] = [0, N - 1, B * N - 1]     # tile edges and the ragged tail
-    gate_forward_batch(X, Y, d_xy, i_xy, d_yx, i_yx, rows_x=np.unique(rows_x), rows_y=np.unique(rows_y))
-    gate_mirror(X, Y, d_xy, i_xy, rows=np.unique(rows_x))
-    # sums: partials equal fp64 sums of the per-point outputs; loss within 1e-5 of the oracle's loss
-    np.testing.assert_allclose(part[:, 0], d_xy.astype(np.float64).sum(1), rtol=1e-12)
-    g = np.full((B, N), 1.0 / (B * N), np.float32)
-    h = np.full((B, M), 1.0 / (B * M), np.float32)
+    x = torch.from_numpy(X).cuda()
+    y = torch.from_numpy(Y).cuda()
     gx, gy = cd.backward(x, y, torch.from_numpy(i_xy).cuda(), torch.from_numpy(i_yx).cuda(),
-                         torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda())
-    gxr, gyr, sx, sy = oracle.backward(X, Y, i_xy, i_yx, g, h)
+                         g_scalar=1.0 / (B * N), h_scalar=1.0 / (B * M))
+    gxr, gyr, sx, sy = oracle.backward(X, Y, i_xy, i_yx, g_scalar=np.float32(1.0 / (B * N)),
+                                       h_scalar=np.float32(1.0 / (B * M)))
     np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
     np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+    gate_grad(gx.cpu().numpy(), gxr, sx)
     gate_grad(gy.cpu().numpy(), gyr, sy)
 
 
@@ -146,7 +144,8 @@ def test_large_configs_all_points_kdtree(cd, name):
     """Every point of c4 / c5 (not a sample): the GPU minimum equals the exact nearest-neighbour
     distance from scipy's cKDTree (fp64, k=2) within 1e-5 relative, and the index is exact wherever
     the top-2 gap exceeds 1e-6 relative (SURVEY §8.c.4 "large configs"; readings R12, R13); the
-    pruned forward reproduces the brute force's d / idx / hit counts on every point."""
+    pruned forward reproduces the brute force's d / idx / hit counts on every point; loss, CD_b and the hit counts
+    (R16 band) / F from the exact distances."""
     from scipy.spatial import cKDTree
     X, Y = synth.config_inputs(name)
     x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
@@ -155,13 +154,30 @@ def test_large_configs_all_points_kdtree(cd, name):
     for a, b in zip(pr[:4], (d_xy, i_xy, d_yx, i_yx)):
         np.testing.assert_array_equal(a, b)
     np.testing.assert_array_equal(pr[4][:, 2:], part[:, 2:])
+    refs = []
     for Q, T, d, i in ((X, Y, d_xy, i_xy), (Y, X, d_yx, i_yx)):
+        ref_d = []
         for b in range(Q.shape[0]):
             dist, idx = cKDTree(T[b].astype(np.float64)).query(Q[b].astype(np.float64), k=2, workers=-1)
             d1, d2 = dist[:, 0] ** 2, dist[:, 1] ** 2
             np.testing.assert_allclose(d[b].astype(np.float64), d1, rtol=RTOL, atol=0)
             clear = (d2 - d1) > GAP * d1
             np.testing.assert_array_equal(i[b][clear], idx[clear, 0])
+            ref_d.append(d1)
+        refs.append(np.stack(ref_d))
+    # loss, hit counts inside the R16 band and F at the GPU's counts, from the exact distances
+    B, N, M = X.shape[0], X.shape[1], Y.shape[1]
+    cdb, loss, F, P, R = cd.finalize(torch.from_numpy(part).cuda(), N, M)
+    cd_ref, loss_ref = oracle.chamfer_loss(refs[0], refs[1])
+    assert abs(loss.item() - loss_ref) <= RTOL * loss_ref
+    np.testing.assert_allclose(cdb.cpu().numpy(), cd_ref, rtol=RTOL)
+    t2 = oracle.tau_sq(0.01)
+    for dist, hits in ((refs[0], part[:, 2]), (refs[1], part[:, 3])):
+        lo = (dist < t2 * (1 - GAP)).sum(1)
+        hi = (dist <= t2 * (1 + GAP)).sum(1)
+        assert np.all((hits >= lo) & (hits <= hi))
+    np.testing.assert_allclose(F.cpu().numpy(), oracle.fscore_from_hits(part[:, 2], part[:, 3], N, M),
+                               rtol=RTOL, atol=1e-7)
 
 
 # ------------------------------------------------------------------------------ edge cases
@@ -465,14 +481,47 @@ def test_pruned_large_sampled(cd):
 def test_step_host_overlapped_equals_step_host(cd):
     X, Y = synth.shape_pair(8, 3000, 2500, config_index=29)
     xh, yh = cd.pinned_copy(X), cd.pinned_copy(Y)
-    ref = cd.step_host(xh.numpy(), yh.numpy(), tau=0.01, want_grads=False)
+    ref = cd.step_host(xh.numpy(), yh.numpy(), tau=0.01, want_grads=True)
     for nchunks in (1, 2, 3, 8, None):          # None: the default (2 ranges, the first short)
         st = cd.HostStepper(8, 3000, 2500, tau=0.01, nchunks=nchunks)
         for _ in range(2):                      # back-to-back steps reuse the staging buffers
-            loss, fs = st.step(xh, yh)
+            loss, fs, gx, gy = st.step(xh, yh)
         torch.cuda.synchronize()
         assert float(loss[0]) == float(ref["loss"][0])
         np.testing.assert_array_equal(fs.numpy(), ref["fscore"].numpy())
+        np.testing.assert_array_equal(gx.numpy(), ref["grad_x"].numpy())
+        np.testing.assert_array_equal(gy.numpy(), ref["grad_y"].numpy())
+        assert st.d2h_bytes() == 4 + 4 * 8 + 12 * 8 * (3000 + 2500)
+    # the end-to-end gradients are the loss backward of the oracle (g = w1/(B N) fill, R8)
+    _, i_xy, _, i_yx = (t.cpu().numpy() for t in cd.forward(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda())[:4])
+    gxr, gyr, sx, sy = oracle.backward(X, Y, i_xy, i_yx, g_scalar=np.float32(1.0 / (8 * 3000)),
+                                       h_scalar=np.float32(1.0 / (8 * 2500)))
+    np.testing.assert_array_equal(ref["grad_x"].numpy(), gxr.astype(np.float32))
+    np.testing.assert_array_equal(ref["grad_y"].numpy(), gyr.astype(np.float32))
+
+
+def test_loss_backward_device_upstream(cd):
+    """cd_loss_backward (the autograd path): the upstream scalar u is read on the device and the fills
+    are g = RN32(u * RN32(w1/(B N))), h = RN32(u * RN32(w2/(B M))) (include/cd.h); gradients equal the
+    oracle's backward with those fills bit for bit, for u != 1 and unequal weights."""
+    X, Y = synth.shape_pair(3, 2100, 1700, config_index=31)
+    x, y = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    _, i_xy, _, i_yx, _ = cd.forward(x, y)
+    B, N, M = 3, 2100, 1700
+    for u, w1, w2 in ((1.0, 1.0, 1.0), (-2.75, 0.3, 1.7)):
+        gl = torch.tensor([u], dtype=torch.float32, device="cuda")
+        gx, gy = cd.loss_backward(x, y, i_xy, i_yx, gl, w1, w2)
+        # w1, w2 cross the C ABI as fp32; the fill is RN32(w / (B P)) of that value (include/cd.h)
+        g = np.float32(u) * np.float32(float(np.float32(w1)) / (B * N))
+        h = np.float32(u) * np.float32(float(np.float32(w2)) / (B * M))
+        gxr, gyr, sx, sy = oracle.backward(X, Y, i_xy.cpu().numpy(), i_yx.cpu().numpy(), g_scalar=g, h_scalar=h)
+        np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
+        np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+    # autograd with a non-unit upstream goes through the same entry point
+    xg, yg = x.clone().requires_grad_(True), y.clone().requires_grad_(True)
+    (cd.chamfer(xg, yg, 0.3, 1.7) * -2.75).backward()
+    np.testing.assert_array_equal(xg.grad.cpu().numpy(), gx.cpu().numpy())
+    np.testing.assert_array_equal(yg.grad.cpu().numpy(), gy.cpu().numpy())
 
 
 def test_auto_algorithm_and_pruned_autograd(cd):

@@ -52,6 +52,33 @@ def test_golden_fscore():
     np.testing.assert_allclose(out["fscore"], e["fscore"], rtol=1e-15)
 
 
+def test_fscore_from_hits_pins():
+    """oracle.fscore_from_hits (it evaluates the oracle F at the GPU's hit counts, R16) against the
+    golden example's counts, exact rationals F = 2 hx hy / (hx M + hy N) (R15 written over the
+    integers), the degenerate P + R = 0 case, and oracle.fscore on random distances."""
+    from fractions import Fraction
+    g = _golden("fscore_example.json")
+    N, M = len(g["x"][0]), len(g["y"][0])
+    e = g["expect"]
+    np.testing.assert_allclose(oracle.fscore_from_hits(e["hits_xy"], e["hits_yx"], N, M), e["fscore"], rtol=1e-15)
+    # roles: hits_xy / N is the precision, hits_yx / M the recall; with N != M a swap changes F
+    assert abs(oracle.fscore_from_hits([1], [3], 2, 4)[0] - 0.6) < 1e-15
+    assert abs(oracle.fscore_from_hits([3], [1], 2, 4)[0] - 0.6) > 0.1
+    assert oracle.fscore_from_hits([0], [0], 5, 7)[0] == 0.0
+    assert oracle.fscore_from_hits([0], [7], 5, 7)[0] == 0.0          # P = 0, R = 1 -> F = 0
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        N, M = (int(v) for v in rng.integers(1, 10 ** 6, size=2))
+        hx, hy = int(rng.integers(0, N + 1)), int(rng.integers(0, M + 1))
+        exact = Fraction(0) if hx == 0 or hy == 0 else Fraction(2 * hx * hy, hx * M + hy * N)
+        got = oracle.fscore_from_hits([hx], [hy], N, M)[0]
+        assert abs(Fraction(got) - exact) <= Fraction(4, 2 ** 53) * exact
+    d_xy = rng.uniform(0, 4e-4, size=(3, 500))
+    d_yx = rng.uniform(0, 4e-4, size=(3, 700))
+    ref = oracle.fscore(d_xy, d_yx, 0.01)
+    np.testing.assert_array_equal(oracle.fscore_from_hits(ref["hits_xy"], ref["hits_yx"], 500, 700), ref["fscore"])
+
+
 def test_golden_same_cloud_prints_zero():
     g = _golden("spec_s613_same_cloud.json")
     x = np.array(g["x"], np.float32)
