@@ -298,15 +298,19 @@ CD_API cd_status cd_p2s_forward_pruned(const float* points, const float* verts, 
                          void* workspace, size_t workspace_bytes, cd_stream_t stream);
 
 /*
- * cd_step_host_overlapped — cd_step_host with the host->device copies overlapped with the compute:
+ * cd_step_host_overlapped — cd_step_host with the host<->device copies overlapped with the compute:
  * the clouds are copied in `nchunks` batch ranges on `copy_stream` (the first range half an equal
- * share, max(1, B / (2 nchunks)) elements, since only its copy is exposed; the rest split equally);
- * the forward of range c runs on `stream` as soon as range c has landed (cudaStreamWaitEvent), while
- * later ranges are still in flight; finalize, backward and the D2H copies follow on `stream`.  Results are identical to
- * cd_step_host (per-batch outputs do not depend on the chunking).  events: nchunks + 1 cudaEvent_t
- * created by the caller (disable-timing events are fine); events[nchunks] is recorded at the end of
- * the step, and the next call's copies wait on it before overwriting the staging buffers.
- * nchunks in [1, B].  Workspace: cd_workspace_size(CD_OP_STEP).
+ * share, max(1, B / (2 nchunks)) elements, since only its copy is exposed; with nchunks >= 3 the
+ * last range is as short, since only its backward and gradient copy are exposed; the rest split
+ * equally).  On `stream`, range c's forward starts as soon as range c has landed
+ * (cudaStreamWaitEvent) and range c's loss backward follows at once (the fills w/(B P) use the whole
+ * batch's B and do not depend on the loss value; each batch element's gradients depend only on its
+ * own clouds and indices), and range c's gradients go back on `copy_stream` while later ranges
+ * compute; finalize and the loss / F-score copies follow on `stream`, which finally waits for the
+ * gradient copies.  Results are identical to cd_step_host (per-batch outputs do not depend on the
+ * chunking).  events: nchunks + 1 cudaEvent_t created by the caller (disable-timing events are
+ * fine); events[nchunks] is recorded at the end of the step, and the next call's copies wait on it
+ * before overwriting the staging buffers.  nchunks in [1, B].  Workspace: cd_workspace_size(CD_OP_STEP).
  */
 CD_API cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int B, int N, int M,
                        float tau, float w1, float w2,

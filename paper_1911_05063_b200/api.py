@@ -304,7 +304,8 @@ class HostStepper:
     def __init__(self, B: int, N: int, M: int, tau: float | None = None, w1: float = 1.0, w2: float = 1.0,
                  nchunks: int | None = None, device=None, want_grads: bool = True):
         self.B, self.N, self.M, self.tau, self.w1, self.w2 = B, N, M, tau, w1, w2
-        self.nchunks = nchunks or (2 if B >= 2 else 1)   # measured (tools/time_e2e.py c3): 2 ranges (first 1/4 of B) 2.18 ms, 4 equal: 2.28
+        # measured (tools/time_e2e.py c3, gradients copied back): 1 range 2.52 ms, 2: 2.36, 3: 2.29, 4: 2.26, 6: 2.35
+        self.nchunks = nchunks or min(4, B)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         # a private workspace: its staging area is written by this stepper's copy stream
         n = int(_lib.load().cd_workspace_size(_lib.CD_OP_STEP, B, N, M))

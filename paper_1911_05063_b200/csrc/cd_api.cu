@@ -647,11 +647,16 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
     cudaEvent_t done = static_cast<cudaEvent_t>(events[nchunks]);
     // batch ranges: the first range is 1/CD_STEP_FIRST_DIV of an equal share (its copy is the only
     // exposed one), the rest split equally
+    // with 3 or more ranges the last one is as short as the first (only its backward and gradient
+    // copy are exposed)
     auto bound = [&](int c) -> int {
         if (c <= 0) return 0;
         if (c >= nchunks) return B;
         const int first = std::max(1, (int)((int64_t)B / ((int64_t)nchunks * CD_STEP_FIRST_DIV)));
-        return first + (int)((int64_t)(B - first) * (c - 1) / (nchunks - 1));
+        const int last = nchunks >= 3 ? first : 0;
+        const int mid = nchunks - 1 - (last > 0 ? 1 : 0);
+        if (c == nchunks - 1 && last > 0) return B - last;
+        return first + (int)((int64_t)(B - first - last) * (c - 1) / mid);
     };
     // the staging buffers are free once the previous step on `stream` is done (never-recorded: no-op)
     cudaError_t e = cudaStreamWaitEvent(cs, done, 0);
@@ -665,30 +670,49 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
         if (e == cudaSuccess) e = cudaEventRecord(static_cast<cudaEvent_t>(events[c]), cs);
     }
     if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped H2D");
-    // chunk c's forward starts as soon as its clouds have landed; later chunks copy meanwhile
-    for (int c = 0; c < nchunks; ++c) {
-        const int b0 = bound(c), b1 = bound(c + 1);
-        e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(events[c]), 0);
-        if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped wait");
-        s = cd_forward(x + (size_t)b0 * N * 3, y + (size_t)b0 * M * 3, b1 - b0, N, M, 0, N, 0, M,
-                       dxy + (size_t)b0 * N, ixy + (size_t)b0 * N, dyx + (size_t)b0 * M, iyx + (size_t)b0 * M,
-                       part + 4 * (size_t)b0, tau, inner, L.inner_bytes, stream);
-        if (s != CD_OK) return s;
-    }
-    s = cd_finalize(part, B, N, M, w1, w2, nullptr, loss, tau >= 0.f ? fs : nullptr, nullptr, nullptr, stream);
-    if (s != CD_OK) return s;
+    // range c's forward starts as soon as its clouds have landed (later ranges copy meanwhile), and its
+    // backward follows at once: the loss gradient's fills w/(B P) do not depend on the loss value, and
+    // every batch element's gradient depends only on its own clouds and indices.  Range c's gradients
+    // then return on the copy stream while the next range computes.
     const float gs = loss_fill(w1, B, N);
     const float hs = loss_fill(w2, B, M);
-    s = cd_backward(x, y, B, N, M, ixy, iyx, nullptr, nullptr, gs, hs, 0, N, 0, M, gx, gy, inner, L.inner_bytes,
-                    stream);
+    for (int c = 0; c < nchunks; ++c) {
+        const int b0 = bound(c), b1 = bound(c + 1);
+        cudaEvent_t ev = static_cast<cudaEvent_t>(events[c]);
+        e = cudaStreamWaitEvent(st, ev, 0);
+        if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped wait");
+        float* xr = x + (size_t)b0 * N * 3;
+        float* yr = y + (size_t)b0 * M * 3;
+        s = cd_forward(xr, yr, b1 - b0, N, M, 0, N, 0, M, dxy + (size_t)b0 * N, ixy + (size_t)b0 * N,
+                       dyx + (size_t)b0 * M, iyx + (size_t)b0 * M, part + 4 * (size_t)b0, tau, inner, L.inner_bytes,
+                       stream);
+        if (s != CD_OK) return s;
+        s = cd_backward(xr, yr, b1 - b0, N, M, ixy + (size_t)b0 * N, iyx + (size_t)b0 * M, nullptr, nullptr, gs, hs,
+                        0, N, 0, M, gx + (size_t)b0 * N * 3, gy + (size_t)b0 * M * 3, inner, L.inner_bytes, stream);
+        if (s != CD_OK) return s;
+        if (grad_x_host || grad_y_host) {
+            // the wait above already captured ev's H2D record, so it can be re-recorded here
+            e = cudaEventRecord(ev, st);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev, 0);
+            if (e == cudaSuccess && grad_x_host)
+                e = cudaMemcpyAsync(grad_x_host + (size_t)b0 * N * 3, gx + (size_t)b0 * N * 3,
+                                    (size_t)(b1 - b0) * N * 12, cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess && grad_y_host)
+                e = cudaMemcpyAsync(grad_y_host + (size_t)b0 * M * 3, gy + (size_t)b0 * M * 3,
+                                    (size_t)(b1 - b0) * M * 12, cudaMemcpyDeviceToHost, cs);
+            if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped gradient D2H");
+        }
+    }
+    s = cd_finalize(part, B, N, M, w1, w2, nullptr, loss, tau >= 0.f ? fs : nullptr, nullptr, nullptr, stream);
     if (s != CD_OK) return s;
     e = cudaMemcpyAsync(loss_host, loss, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess && fscore_host && tau >= 0.f)
         e = cudaMemcpyAsync(fscore_host, fs, (size_t)B * 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && grad_x_host)
-        e = cudaMemcpyAsync(grad_x_host, gx, (size_t)B * N * 12, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && grad_y_host)
-        e = cudaMemcpyAsync(grad_y_host, gy, (size_t)B * M * 12, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && (grad_x_host || grad_y_host)) {
+        // `stream` completes only after the gradient copies (the caller synchronises `stream`)
+        e = cudaEventRecord(static_cast<cudaEvent_t>(events[0]), cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(events[0]), 0);
+    }
     if (e == cudaSuccess) e = cudaEventRecord(done, st);
     return cuda_status(e, "cd_step_host_overlapped D2H");
 }

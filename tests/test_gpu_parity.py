@@ -304,6 +304,29 @@ def test_backward_segment_sort_boundary(cd, N, M):
     np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
 
 
+@pytest.mark.parametrize("B", [5, 12, 32, 40])
+def test_backward_segment_sort_parts(cd, B):
+    """The on-chip segment sort splits each (direction, batch) segment over 2^lparts CTAs while the
+    2B segments alone leave SMs idle (nn_backward.cu): on 148 SMs B = 5 -> 3 (the cap), 12 -> 2,
+    32 -> 1, 40 -> 0.  Every split against the oracle bit for bit, near the on-chip limit (24576)
+    with skewed in-degree and one batch element whose sources all land on one target."""
+    rng = np.random.default_rng(100 + B)
+    N, M = 24000, 23001
+    X = rng.normal(size=(B, N, 3)).astype(np.float32)
+    Y = rng.normal(size=(B, M, 3)).astype(np.float32)
+    ixy = (M * rng.random(size=(B, N)) ** 3).astype(np.int32)
+    iyx = (N * rng.random(size=(B, M)) ** 5).astype(np.int32)
+    ixy[B // 2] = 17
+    g = rng.normal(size=(B, N)).astype(np.float32)
+    h = rng.normal(size=(B, M)).astype(np.float32)
+    gx, gy = cd.backward(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), torch.from_numpy(ixy).cuda(),
+                         torch.from_numpy(iyx).cuda(), torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda())
+    torch.cuda.synchronize()
+    gxr, gyr, _, _ = oracle.backward(X, Y, ixy, iyx, g, h)
+    np.testing.assert_array_equal(gx.cpu().numpy(), gxr.astype(np.float32))
+    np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
+
+
 def test_vjp_linearity_bit_exact(cd):
     X, Y = synth.shape_pair(1, 4000, 3000, config_index=25)
     x, y, (d_xy, i_xy, d_yx, i_yx, _) = _run(cd, X, Y)

@@ -19,6 +19,9 @@ for (B, N, M) in [(1, 1, 1), (2, 3, 7), (2, 1000, 1030), (1, 2049, 513)]:
     keys = cd.forward_rows(x, y, (0, N), tau=0.1)[2]
     cd.forward_cols(x, y, keys, (0, M), tau=0.1)
     cd.step_host(cd.pinned_copy(X).numpy(), cd.pinned_copy(Y).numpy(), tau=0.1)
+    cd.loss_backward(x, y, i_xy, i_yx, torch.full((1,), 0.5, device="cuda"), 0.3, 1.7)
+    st = cd.HostStepper(B, N, M, tau=0.1)
+    st.step(cd.pinned_copy(X), cd.pinned_copy(Y))
 V, F = synth.mesh_batch(2, subdiv=2)
 rf, rb = synth.sampling_randoms(2, 777, seed=1)
 v, f = torch.from_numpy(V).cuda(), torch.from_numpy(F).cuda()
@@ -26,6 +29,7 @@ pts, fi, ba = cd.sample_mesh(v, f, torch.from_numpy(rf).cuda(), torch.from_numpy
 cd.sample_mesh_backward(f, fi, ba, V.shape[1], torch.ones_like(pts))
 d, fi2, cl, ba2, pb, loss = cd.p2s_forward(pts.contiguous(), v, f)
 cd.p2s_backward(pts, cl, fi2, ba2, f, V.shape[1], g_scalar=1.0)
+cd.p2s_loss_backward(pts, cl, fi2, ba2, f, V.shape[1], torch.ones(1, device="cuda"))
 cd.p2s_forward(pts.contiguous(), v, f, algorithm="pruned")                       # incl. the tie re-walk
 far = (pts * 4.0 + 2.0).contiguous()
 cd.p2s_forward(far, v, f, algorithm="pruned")
