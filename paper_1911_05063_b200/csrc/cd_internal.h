@@ -123,6 +123,14 @@ constexpr int kFscoreLaunches = 3;
 cudaError_t launch_finalize(const double* partials, int B, int N, int M, float w1, float w2, float* cd,
                             float* loss, float* fscore, float* precision, float* recall, cudaStream_t st);
 
+// A sequence sorted as independent segments: nA segments of szA elements, then nB of szB.
+struct SegSpec {
+    int nA;
+    int64_t szA;
+    int nB;
+    int64_t szB;
+};
+
 // Backward.
 struct BwdPlan {
     int B, N, M;
@@ -131,6 +139,7 @@ struct BwdPlan {
     int64_t kmax;       // number of distinct keys B*(M+N)
     int nbits, npasses, digit_bits, ntiles;
     bool segsort;       // max(N, M) <= 24576: one CTA per (direction, batch) segment sorts on chip
+    SegSpec segs;       // else: the global radix passes sort the 2B (direction, batch) segments on their own
     size_t off_keys[2], off_vals[2], off_counts, off_totals, off_offsets, bytes;
 };
 void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int r1);

@@ -50,68 +50,112 @@ inline int sort_items(int digit_bits) { return digit_bits >= 10 ? kSortItemsWide
 #endif
 constexpr int kMaxDigitBits = CD_SORT_MAXBITS;        // digits of up to 11 bits: 2 passes cover 2^22 keys
 
-// Edge keys fused with the first radix pass's per-tile histogram: one CTA per sort
-// tile writes its 4096 (key, value) pairs and counts digit 0 (saves a launch and a read of the keys).
+// Segmented sorts: the sequence is nA segments of szA elements followed by nB segments of szB, each
+// sorted on its own (a plain sort is one segment).  Every tile lies inside one segment; the digit-
+// major counts table holds one row of per-tile counts per (segment, digit); a segment's sorted
+// output occupies its input range.  The backward's edges form 2B such segments (B of N xy edges keyed
+// by a target in [0, M), B of M yx edges keyed in [0, N)), so the keys are segment-LOCAL and need
+// ceil(log2(max(N, M))) bits instead of log2(B(N + M)): c5 sorts 20-bit keys in 2 passes, not 23 in 3.
+struct SortSegs {
+    int nA, nB;
+    int64_t szA, szB;
+    int ntA, ntB;   // tiles per segment for the pass's tile size
+    __host__ __device__ int64_t seg_start(int s) const { return s < nA ? s * szA : nA * szA + (s - nA) * szB; }
+    __host__ __device__ int64_t seg_size(int s) const { return s < nA ? szA : szB; }
+    __host__ __device__ int seg_tiles(int s) const { return s < nA ? ntA : ntB; }
+    __host__ __device__ int ntiles() const { return nA * ntA + nB * ntB; }
+    __host__ __device__ int nsegs() const { return nA + nB; }
+    __host__ __device__ void locate(int t, int& s, int& lt) const {
+        if (t < nA * ntA) {
+            s = t / ntA;
+            lt = t - s * ntA;
+        } else {
+            const int u = t - nA * ntA, q = u / ntB;
+            s = nA + q;
+            lt = u - q * ntB;
+        }
+    }
+    // element range [start, end) of tile t (tile size T)
+    __host__ __device__ void range(int t, int T, int& s, int& lt, int64_t& start, int64_t& end) const {
+        locate(t, s, lt);
+        const int64_t s0 = seg_start(s);
+        start = s0 + (int64_t)lt * T;
+        end = s0 + seg_size(s);
+        if (start + T < end) end = start + T;
+    }
+    // first word of the (segment, digit) row of per-tile counts
+    __host__ __device__ int64_t row(int s, int d, int D) const {
+        return s < nA ? ((int64_t)s * D + d) * ntA : (int64_t)nA * D * ntA + ((int64_t)(s - nA) * D + d) * ntB;
+    }
+};
+
+static SortSegs make_segs(const SegSpec& sp, int tile) {
+    SortSegs g;
+    g.nA = sp.nA;
+    g.nB = sp.nB;
+    g.szA = sp.szA;
+    g.szB = sp.szB;
+    g.ntA = (int)((sp.szA + tile - 1) / tile);
+    g.ntB = (int)((sp.szB + tile - 1) / tile);
+    return g;
+}
+
+// Edge keys fused with the first radix pass's per-tile histogram: one CTA per sort tile writes its
+// (key, value) pairs and counts digit 0 (saves a launch and a read of the keys).  Segment s < B holds
+// batch s's xy edges (key a_i, value the global x row), s >= B batch (s - B)'s yx edges.
 template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads) keys_hist_kernel(const int32_t* __restrict__ idx_xy,
                                                                  const int32_t* __restrict__ idx_yx, int B, int N,
-                                                                 int M, int D, int ntiles, uint32_t* __restrict__ keys,
+                                                                 int M, int D, SortSegs g, uint32_t* __restrict__ keys,
                                                                  uint32_t* __restrict__ vals,
                                                                  uint32_t* __restrict__ counts) {
     extern __shared__ uint32_t hist[];
     for (int d = threadIdx.x; d < D; d += kSortThreads) hist[d] = 0;
     __syncthreads();
+    int sg, lt;
+    int64_t start, end;
+    g.range(blockIdx.x, kSortThreads * ITEMS, sg, lt, start, end);
     const int64_t L0 = (int64_t)B * N;
-    const int64_t L = L0 + (int64_t)B * M;
-    const int64_t base = (int64_t)blockIdx.x * (kSortThreads * ITEMS);
+    const bool xy = sg < B;
+    const int kmaxl = xy ? M - 1 : N - 1;
+    const int32_t* idx = xy ? idx_xy : idx_yx - L0;   // idx[p] for p in this segment's range
 #pragma unroll 4
     for (int k = 0; k < ITEMS; ++k) {
-        const int64_t p = base + (int64_t)k * kSortThreads + threadIdx.x;
-        if (p < L) {
-            uint32_t key, val;
-            if (p < L0) {
-                const int64_t b = p / N;
-                const int a = min(max(idx_xy[p], 0), M - 1);
-                key = (uint32_t)(b * M + a);
-                val = (uint32_t)p;
-            } else {
-                const int64_t q = p - L0;
-                const int64_t b = q / M;
-                const int a = min(max(idx_yx[q], 0), N - 1);
-                key = (uint32_t)((int64_t)B * M + b * N + a);
-                val = (uint32_t)q;
-            }
+        const int64_t p = start + (int64_t)k * kSortThreads + threadIdx.x;
+        if (p < end) {
+            const uint32_t key = (uint32_t)min(max(idx[p], 0), kmaxl);
             keys[p] = key;
-            vals[p] = val;
+            vals[p] = (uint32_t)(xy ? p : p - L0);
             atomicAdd(&hist[key & (D - 1)], 1u);  // integer adds: order-free
         }
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < D; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
+    for (int d = threadIdx.x; d < D; d += kSortThreads) counts[g.row(sg, d, D) + lt] = hist[d];
 }
 
-// counts[digit * ntiles + tile]; D = 1 << digit bits (dynamic shared memory: D words)
+// per-tile digit counts into the (segment, digit) rows; D = 1 << digit bits (dynamic smem: D words)
 template <int ITEMS>
-__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t L,
-                                                                  int shift, int D, int ntiles,
-                                                                  uint32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, SortSegs g,
+                                                                  int shift, int D, uint32_t* __restrict__ counts) {
     extern __shared__ uint32_t hist[];
     for (int d = threadIdx.x; d < D; d += kSortThreads) hist[d] = 0;
     __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * (kSortThreads * ITEMS);
+    int sg, lt;
+    int64_t start, end;
+    g.range(blockIdx.x, kSortThreads * ITEMS, sg, lt, start, end);
     uint32_t kk[ITEMS];
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {   // all loads in flight before the shared-memory adds
-        const int64_t e = min(base + (int64_t)k * kSortThreads + threadIdx.x, L - 1);
+        const int64_t e = min(start + (int64_t)k * kSortThreads + threadIdx.x, end - 1);
         asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(kk[k]) : "l"(keys + e));
     }
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
-        const int64_t e = base + (int64_t)k * kSortThreads + threadIdx.x;
-        if (e < L) atomicAdd(&hist[(kk[k] >> shift) & (D - 1)], 1u);  // integer adds: order-free
+        const int64_t e = start + (int64_t)k * kSortThreads + threadIdx.x;
+        if (e < end) atomicAdd(&hist[(kk[k] >> shift) & (D - 1)], 1u);  // integer adds: order-free
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < D; d += kSortThreads) counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
+    for (int d = threadIdx.x; d < D; d += kSortThreads) counts[g.row(sg, d, D) + lt] = hist[d];
 }
 
 // Block-wide exclusive scan of one value per thread (kSortThreads threads); returns the block total.
@@ -136,22 +180,31 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
     return before + incl - v;
 }
 
-// Row-wise exclusive scan of the digit-major histogram table: block d scans counts[d][0..ntiles)
-// in place and writes the row total to totals[d] (coalesced, one CTA per digit).
-__global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* __restrict__ counts, int ntiles,
+// Row-wise exclusive scan of the counts table, one warp per (segment s, digit d) row: scans the row
+// of s's tile counts for d in place (32 tiles per step, shuffle scan) and writes the row total to
+// totals[s * D + d].  8 rows per CTA: short rows (many small segments) cost a warp, not a CTA.
+__global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* __restrict__ counts, SortSegs g, int D,
                                                                      uint32_t* __restrict__ totals) {
-    __shared__ uint32_t warp_tot[kSortWarps];
-    uint32_t* row = counts + (int64_t)blockIdx.x * ntiles;
+    const int lane = threadIdx.x & 31;
+    const int64_t rowid = (int64_t)blockIdx.x * kSortWarps + (threadIdx.x >> 5);
+    if (rowid >= (int64_t)g.nsegs() * D) return;   // warp-uniform
+    const int sg = (int)(rowid / D), d = (int)(rowid - (int64_t)sg * D);
+    const int ntiles = g.seg_tiles(sg);
+    uint32_t* row = counts + g.row(sg, d, D);
     uint32_t carry = 0;
-    for (int base = 0; base < ntiles; base += kSortThreads) {
-        const int i = base + threadIdx.x;
+    for (int base = 0; base < ntiles; base += 32) {
+        const int i = base + lane;
         const uint32_t v = i < ntiles ? row[i] : 0u;
-        uint32_t tot;
-        const uint32_t ex = block_exclusive_scan(v, warp_tot, tot);
-        if (i < ntiles) row[i] = carry + ex;
-        carry += tot;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (i < ntiles) row[i] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+    if (lane == 0) totals[rowid] = carry;
 }
 
 // Stable scatter of one tile.  Warp w owns elements [w*512, (w+1)*512) of the tile (16 rounds of
@@ -164,7 +217,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_rowscan_kernel(uint32_t* _
 // Dynamic shared memory: (kSortWarps + 2) * D + 2 * tile words (tile = kSortThreads * ITEMS).
 template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB : 2) radix_scatter_kernel(
-    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t L, int shift, int D, int ntiles,
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, SortSegs g, int shift, int D,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout) {
     extern __shared__ uint32_t smem[];
@@ -180,20 +233,24 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
     const int per = (D + kSortThreads - 1) / kSortThreads;   // digits owned by this thread in the scans
     const int d0 = threadIdx.x * per;
     for (int i = threadIdx.x; i < kSortWarps * D; i += kSortThreads) wcnt[i] = 0;
-    // global digit bases: exclusive scan of totals[0..D), plus this tile's row-scan offset
+    int sg, lt;
+    int64_t tbase, L;   // this tile's elements [tbase, L): L is the tile's end, inside its segment
+    g.range(blockIdx.x, kSortThreads * ITEMS, sg, lt, tbase, L);
+    // digit bases: the segment's start + exclusive scan of its digit totals, plus this tile's
+    // row-scan offset
     {
+        const uint32_t* tseg = totals + (int64_t)sg * D;
         uint32_t loc = 0;
-        for (int d = d0; d < min(d0 + per, D); ++d) loc += totals[d];
+        for (int d = d0; d < min(d0 + per, D); ++d) loc += tseg[d];
         uint32_t tot;
-        uint32_t run = block_exclusive_scan(loc, warp_tot, tot);
+        uint32_t run = (uint32_t)g.seg_start(sg) + block_exclusive_scan(loc, warp_tot, tot);
         for (int d = d0; d < min(d0 + per, D); ++d) {
-            dbase[d] = run + offsets[(int64_t)d * ntiles + blockIdx.x];
-            run += totals[d];
+            dbase[d] = run + offsets[g.row(sg, d, D) + lt];
+            run += tseg[d];
         }
     }
     __syncthreads();
     const uint32_t lt_mask = (1u << lane) - 1u;
-    const int64_t tbase = (int64_t)blockIdx.x * (kSortThreads * ITEMS);
     const int64_t wbase = tbase + (int64_t)warp * (ITEMS * 32);
     uint32_t kk[ITEMS], vv[ITEMS], rk[ITEMS];
     uint32_t* my = wcnt + warp * D;
@@ -270,19 +327,54 @@ __global__ void __launch_bounds__(kSortThreads, CD_SORT_MINB > 1 ? CD_SORT_MINB 
     for (int i = threadIdx.x; i < nvalid; i += kSortThreads) {
         const uint32_t key = skey[i];
         const uint32_t pos = (uint32_t)i + delta[(key >> shift) & (D - 1)];
-        CD_CHECK(pos < (uint64_t)L);
+        CD_CHECK(pos >= (uint64_t)g.seg_start(sg) && pos < (uint64_t)(g.seg_start(sg) + g.seg_size(sg)));
         kout[pos] = key;
         vout[pos] = sval[i];
     }
 }
 
-// off[k] = first sorted position with key >= k, for k in [0, kmax]; off[kmax] = L.
-__global__ void __launch_bounds__(256) offsets_kernel(const uint32_t* __restrict__ keys, int64_t L, int64_t kmax,
-                                                      uint32_t* __restrict__ off) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= L; p += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t lo = p == 0 ? 0 : (int64_t)keys[p - 1] + 1;
-        const int64_t hi = p == L ? kmax : (int64_t)keys[p];
-        for (int64_t k = lo; k <= hi; ++k) off[k] = (uint32_t)p;
+// off[k] = first sorted position with GLOBAL key >= k, for k in [0, kmax]; off[kmax] = L.  The
+// sorted keys are segment-local: position p of segment s carries global key kbase(s) + key[p], with
+// kbase(s) = s KA (s < nA) or nA KA + (s - nA) KB, and the global keys ascend over all positions.
+// Each thread fills the gaps before kOffRun consecutive positions (one segment division per run, the
+// run's keys loaded together); the writes of different threads are disjoint (no atomics).
+constexpr int kOffRun = 8;
+__global__ void __launch_bounds__(256) offsets_kernel(const uint32_t* __restrict__ keys, SortSegs g, int64_t KA,
+                                                      int64_t KB, int64_t kmax, uint32_t* __restrict__ off) {
+    const int L = (int)g.seg_start(g.nsegs());   // < 2^31 (cd_backward's size limit)
+    const int LA = (int)((int64_t)g.nA * g.szA);
+    const int szA = (int)g.szA, szB = (int)max(g.szB, (int64_t)1);
+    const int nruns = L / kOffRun + 1;            // positions [0, L] inclusive
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += gridDim.x * blockDim.x) {
+        const int p0 = r * kOffRun;
+        // segment of position p0 - 1 (the run's left neighbour) and where it ends
+        const int q = max(p0 - 1, 0);
+        int s = q < LA ? q / szA : g.nA + (q - LA) / szB;
+        int send = (int)g.seg_start(s + 1);
+        int64_t kb = s < g.nA ? (int64_t)s * KA : (int64_t)g.nA * KA + (int64_t)(s - g.nA) * KB;
+        uint32_t kk[kOffRun + 1];
+#pragma unroll
+        for (int u = 0; u <= kOffRun; ++u) kk[u] = (p0 - 1 + u >= 0 && p0 - 1 + u < L) ? keys[p0 - 1 + u] : 0u;
+        int64_t prev = p0 == 0 ? -1 : kb + kk[0];   // global key at p0 - 1
+#pragma unroll
+        for (int u = 0; u < kOffRun; ++u) {
+            const int p = p0 + u;
+            if (p > L) break;
+            int64_t hi;
+            if (p == L) {
+                hi = kmax;
+            } else {
+                while (p >= send) {   // next segment
+                    ++s;
+                    send = (int)g.seg_start(s + 1);
+                    kb = s < g.nA ? (int64_t)s * KA : (int64_t)g.nA * KA + (int64_t)(s - g.nA) * KB;
+                }
+                hi = kb + kk[u + 1];
+            }
+            CD_CHECK(prev + 1 <= hi + 1 && hi <= kmax);
+            for (int64_t k = prev + 1; k <= hi; ++k) off[k] = (uint32_t)p;
+            prev = hi;
+        }
     }
 }
 
@@ -410,6 +502,9 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
 #ifndef CD_SEG_MAXPARTS
 #define CD_SEG_MAXPARTS 3   // log2 of the most CTAs per segment
 #endif
+#ifndef CD_GRAD_MINB
+#define CD_GRAD_MINB 1   // min resident CTAs per SM requested from ptxas (register cap)
+#endif
 #ifndef CD_GRAD_CTAS_PER_SM
 #define CD_GRAD_CTAS_PER_SM 0   // 0: the occupancy (one resident wave)
 #endif
@@ -436,7 +531,7 @@ __device__ __forceinline__ void acc_term(double acc[3], const float* p, const fl
     for (int c = 0; c < 3; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c])));
 }
 
-__global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
+__global__ void __launch_bounds__(256, CD_GRAD_MINB) grad_kernel(GradArgs a) {
     pdl_wait();
     if (a.upstream) {
         const float u = *a.upstream;
@@ -444,13 +539,18 @@ __global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
         a.h_scalar = __fmul_rn(u, a.h_scalar);
     }
     const int sq = a.q1 - a.q0, sr = a.r1 - a.r0;
-    const int64_t nx = (int64_t)a.B * sq;
-    const int64_t total = nx + (int64_t)a.B * sr;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int per_b = sq + sr;
+    const int64_t total = (int64_t)a.B * per_b;
+    // batch-major order: batch b's X outputs, then its Y outputs, so the one resident wave works on
+    // one batch element's two clouds at a time and the second direction's reads (the clouds the
+    // first direction gathered or streamed) hit L2 (c5: DRAM reads ~300 -> ~200 MB)
+    // total = B (|q| + |r|) < 2^31 (cd_backward's size limit): 32-bit index arithmetic
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < (int)total; t += gridDim.x * blockDim.x) {
         double acc[3] = {0.0, 0.0, 0.0};
-        if (t < nx) {
-            const int64_t b = t / sq;
-            const int i = a.q0 + (int)(t - b * sq);
+        const int64_t b = t / per_b;
+        const int u = t - (int)b * per_b;
+        if (u < sq) {
+            const int i = a.q0 + u;
             const int64_t xi = b * a.N + i;
             const float* p = a.x + xi * 3;
             const int part = min(max(a.idx_xy[xi], 0), a.M - 1);
@@ -480,9 +580,7 @@ __global__ void __launch_bounds__(256) grad_kernel(GradArgs a) {
             o[1] = (float)acc[1];
             o[2] = (float)acc[2];
         } else {
-            const int64_t u = t - nx;
-            const int64_t b = u / sr;
-            const int j = a.r0 + (int)(u - b * sr);
+            const int j = a.r0 + (u - sq);
             const int64_t yj = b * a.M + j;
             const float* p = a.y + yj * 3;
             const int part = min(max(a.idx_yx[yj], 0), a.N - 1);
@@ -522,68 +620,95 @@ static int sm_count() {
     return sms;
 }
 
-void radix_sort_plan(int64_t L, int nbits, int& npasses, int& digit_bits, int& ntiles) {
+struct RadixPlan {
+    int npasses, digit_bits, items;
+    SortSegs g;
+};
+
+// Digits per pass: the fewest passes of <= 11-bit digits, or (narrow = true, the backward) the pass
+// count minimising passes x relative pass cost, measured per digit width on the c5 / c4 backward
+// (one 8.4M-element pass: 8-bit digits ~98 us, 10-bit ~170 us, the ballot multisplit and the
+// per-warp counter tables growing with the digit): <= 8 bits 1.0, 9 bits 1.3, 10-11 bits 1.75.
+static RadixPlan radix_plan(const SegSpec& sp, int nbits, bool narrow = false) {
+    RadixPlan r;
     nbits = std::max(nbits, 1);
-    npasses = (nbits + kMaxDigitBits - 1) / kMaxDigitBits;
-    digit_bits = (nbits + npasses - 1) / npasses;
-    const int tile = kSortThreads * sort_items(digit_bits);
-    ntiles = (int)((L + tile - 1) / tile);
+    r.npasses = (nbits + kMaxDigitBits - 1) / kMaxDigitBits;
+    if (narrow) {
+        auto cost = [](int db) { return db <= 8 ? 1.0 : db == 9 ? 1.3 : 1.75; };
+        double best = 1e30;
+        for (int np = r.npasses; np <= r.npasses + 2; ++np) {
+            const int db = (nbits + np - 1) / np;
+            const double c = np * cost(db);
+            if (c < best - 1e-9) {
+                best = c;
+                r.npasses = np;
+            }
+        }
+    }
+    r.digit_bits = (nbits + r.npasses - 1) / r.npasses;
+    r.items = sort_items(r.digit_bits);
+    r.g = make_segs(sp, kSortThreads * r.items);
+    return r;
 }
 
-size_t radix_sort_counts_words(int64_t L, int nbits) {
-    int np, db, nt;
-    radix_sort_plan(L, nbits, np, db, nt);
-    return (size_t)(1 << db) * nt;
-}
+static SegSpec one_segment(int64_t L) { return SegSpec{1, L, 0, 0}; }
 
-// Stable LSD radix sort of (key, value) u32 pairs by the low `nbits` key bits.  keys[0]/vals[0]
-// hold the input; returns the index (0 or 1) of the buffers holding the sorted output.
-// counts: radix_sort_counts_words(L, nbits) words; totals: 2^11 words.
-int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits, uint32_t* counts, uint32_t* totals,
-                     cudaStream_t st, bool first_hist_done) {
-    int npasses, digit_bits, ntiles;
-    radix_sort_plan(L, nbits, npasses, digit_bits, ntiles);
-    const int D = 1 << digit_bits;
-    const int items = sort_items(digit_bits);
-    const size_t scatter_smem = ((size_t)(kSortWarps + 2) * D + 2 * kSortThreads * items) * 4;
+size_t radix_sort_counts_words(const SegSpec& sp, int nbits, bool narrow) {
+    const RadixPlan r = radix_plan(sp, nbits, narrow);
+    return (size_t)(1 << r.digit_bits) * r.g.ntiles();
+}
+size_t radix_sort_totals_words(const SegSpec& sp, int nbits, bool narrow) {
+    const RadixPlan r = radix_plan(sp, nbits, narrow);
+    return (size_t)(1 << r.digit_bits) * r.g.nsegs();
+}
+size_t radix_sort_counts_words(int64_t L, int nbits) { return radix_sort_counts_words(one_segment(L), nbits, false); }
+
+// Stable LSD radix sort of (key, value) u32 pairs by the low `nbits` key bits, every segment of `sp`
+// on its own.  keys[0]/vals[0] hold the input; returns the index (0 or 1) of the buffers holding the
+// sorted output.  counts: radix_sort_counts_words words; totals: radix_sort_totals_words words.
+int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], const SegSpec& sp, int nbits, uint32_t* counts,
+                     uint32_t* totals, cudaStream_t st, bool first_hist_done, bool narrow) {
+    const RadixPlan r = radix_plan(sp, nbits, narrow);
+    const int D = 1 << r.digit_bits;
+    const int ntiles = r.g.ntiles();
+    const size_t scatter_smem = ((size_t)(kSortWarps + 2) * D + 2 * kSortThreads * r.items) * 4;
     ensure_smem_attr((const void*)radix_scatter_kernel<kSortItems>,
                      ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortThreads * kSortItems) * 4);
     ensure_smem_attr((const void*)radix_scatter_kernel<kSortItemsWide>,
                      ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortThreads * kSortItemsWide) * 4);
     int cur = 0;
-    for (int pass = 0; pass < npasses; ++pass) {
-        const int shift = pass * digit_bits;
+    if (ntiles == 0) return cur;
+    for (int pass = 0; pass < r.npasses; ++pass) {
+        const int shift = pass * r.digit_bits;
         if (!(pass == 0 && first_hist_done)) {
-            if (items == kSortItemsWide)
-                radix_hist_kernel<kSortItemsWide><<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D,
-                                                                                              ntiles, counts);
+            if (r.items == kSortItemsWide)
+                radix_hist_kernel<kSortItemsWide><<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], r.g, shift, D,
+                                                                                              counts);
             else
-                radix_hist_kernel<kSortItems><<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], L, shift, D, ntiles,
+                radix_hist_kernel<kSortItems><<<ntiles, kSortThreads, (size_t)D * 4, st>>>(keys[cur], r.g, shift, D,
                                                                                           counts);
         }
-        radix_rowscan_kernel<<<D, kSortThreads, 0, st>>>(counts, ntiles, totals);
-        if (items == kSortItemsWide)
+        radix_rowscan_kernel<<<(unsigned)(((int64_t)r.g.nsegs() * D + kSortWarps - 1) / kSortWarps), kSortThreads, 0,
+                               st>>>(counts, r.g, D, totals);
+        if (r.items == kSortItemsWide)
             radix_scatter_kernel<kSortItemsWide><<<ntiles, kSortThreads, scatter_smem, st>>>(
-                keys[cur], vals[cur], L, shift, D, ntiles, counts, totals, keys[1 - cur], vals[1 - cur]);
+                keys[cur], vals[cur], r.g, shift, D, counts, totals, keys[1 - cur], vals[1 - cur]);
         else
             radix_scatter_kernel<kSortItems><<<ntiles, kSortThreads, scatter_smem, st>>>(
-                keys[cur], vals[cur], L, shift, D, ntiles, counts, totals, keys[1 - cur], vals[1 - cur]);
+                keys[cur], vals[cur], r.g, shift, D, counts, totals, keys[1 - cur], vals[1 - cur]);
         cur = 1 - cur;
     }
     return cur;
 }
 
-int radix_sort_launches(int64_t L, int nbits) {
-    int np, db, nt;
-    radix_sort_plan(L, nbits, np, db, nt);
-    return 3 * np;
+int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits, uint32_t* counts, uint32_t* totals,
+                     cudaStream_t st, bool first_hist_done) {
+    return radix_sort_pairs(keys, vals, one_segment(L), nbits, counts, totals, st, first_hist_done, false);
 }
 
-int radix_digit_bits(int64_t L, int nbits) {
-    int np, db, nt;
-    radix_sort_plan(L, nbits, np, db, nt);
-    return db;
-}
+int radix_sort_launches(int64_t L, int nbits) { return 3 * radix_plan(one_segment(L), nbits).npasses; }
+
+int radix_digit_bits(int64_t L, int nbits) { return radix_plan(one_segment(L), nbits).digit_bits; }
 
 #ifndef CD_SEGSORT
 #define CD_SEGSORT 1
@@ -599,10 +724,15 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
     p.r1 = r1;
     p.L = (int64_t)B * (N + M);
     p.kmax = p.L;  // B*M keys for the xy edges + B*N keys for the yx edges
+    // 2B segments sorted on their own: B of N xy edges keyed in [0, M), B of M yx edges keyed in [0, N)
+    p.segs = SegSpec{B, N, B, M};
     int bits = 0;
-    while (bits < 32 && ((int64_t)1 << bits) < p.kmax) ++bits;
+    while (bits < 31 && (1 << bits) < std::max(N, M)) ++bits;
     p.nbits = std::max(bits, 1);
-    radix_sort_plan(p.L, p.nbits, p.npasses, p.digit_bits, p.ntiles);
+    const RadixPlan r = radix_plan(p.segs, p.nbits, true);
+    p.npasses = r.npasses;
+    p.digit_bits = r.digit_bits;
+    p.ntiles = r.g.ntiles();
     p.segsort = CD_SEGSORT != 0 && std::max(N, M) <= kSegMax;
     size_t off = 0;
     for (int i = 0; i < 2; ++i) {
@@ -612,9 +742,9 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
         off = align_up(off + (size_t)p.L * 4, 256);
     }
     p.off_counts = off;
-    off = align_up(off + radix_sort_counts_words(p.L, p.nbits) * 4, 256);
+    off = align_up(off + radix_sort_counts_words(p.segs, p.nbits, true) * 4, 256);
     p.off_totals = off;
-    off = align_up(off + (size_t)(1 << kMaxDigitBits) * 4, 256);
+    off = align_up(off + radix_sort_totals_words(p.segs, p.nbits, true) * 4, 256);
     p.off_offsets = off;
     off = align_up(off + (size_t)(p.kmax + 1) * 4, 256);
     p.bytes = off;
@@ -644,16 +774,18 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
         launch_pdl(seg_sort_kernel, dim3((unsigned)((int64_t)2 * p.B << lparts)), dim3(kSegThreads), smem, st,
                    idx_xy, idx_yx, p.B, p.N, p.M, nmax, lparts, vals[0], off);
     } else {
-        const int D = 1 << p.digit_bits;
-        if (sort_items(p.digit_bits) == kSortItemsWide)
+        const RadixPlan r = radix_plan(p.segs, p.nbits, true);
+        const int D = 1 << r.digit_bits;
+        if (r.items == kSortItemsWide)
             keys_hist_kernel<kSortItemsWide><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
-                idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles, keys[0], vals[0], counts);
+                idx_xy, idx_yx, p.B, p.N, p.M, D, r.g, keys[0], vals[0], counts);
         else
             keys_hist_kernel<kSortItems><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
-                idx_xy, idx_yx, p.B, p.N, p.M, D, p.ntiles, keys[0], vals[0], counts);
-        cur = radix_sort_pairs(keys, vals, p.L, p.nbits, counts, totals, st, /*first_hist_done=*/true);
-        const int grid_o = (int)std::min<int64_t>((p.L + 1 + 255) / 256, (int64_t)sm_count() * 16);
-        offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], p.L, p.kmax, off);
+                idx_xy, idx_yx, p.B, p.N, p.M, D, r.g, keys[0], vals[0], counts);
+        cur = radix_sort_pairs(keys, vals, p.segs, p.nbits, counts, totals, st, /*first_hist_done=*/true,
+                               /*narrow=*/true);
+        const int grid_o = (int)std::min<int64_t>((p.L / kOffRun + 1 + 255) / 256, (int64_t)sm_count() * 16);
+        offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], r.g, p.M, p.N, p.kmax, off);
     }
     GradArgs a;
     a.x = x;

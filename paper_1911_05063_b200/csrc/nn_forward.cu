@@ -267,36 +267,35 @@ __device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
     }
     const int tdir = 1 - dir;
     const float4* T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
-    const int ntgt = a.npts[tdir];
-    CD_CHECK(bb < 0 || (bb < ntgt && bb % kBlockK == 0));
-    int idx = -1;
-    unsigned todo = __ballot_sync(0xffffffffu, bb >= 0);
-    while (todo) {
-        int r[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            r[k] = todo ? __ffs(todo) - 1 : -1;
-            todo &= todo - 1;
-        }
-        float4 t[4];
+    CD_CHECK(bb < 0 || (bb < a.npts[tdir] && bb % kBlockK == 0));
+    // the warp's 32 rows staged in shared memory: (query, minimum) and block start, read back as
+    // warp-wide broadcasts; targets past the cloud are the +inf padding (bb + 31 < ppad)
+    __shared__ float4 s_q[kMergeThreads];
+    __shared__ int s_b[kMergeThreads];
+    s_q[threadIdx.x] = make_float4(qp.x, qp.y, qp.z, best);
+    s_b[threadIdx.x] = bb;
+    __syncwarp();
+    const int wb = threadIdx.x & ~31;
+    const float4* Tl = T + lane;
+    for (int r0 = 0; r0 < 32; r0 += 4) {
         int base[4];
+        float4 t[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            base[k] = __shfl_sync(0xffffffffu, bb, r[k] & 31);
-            const int j = base[k] + lane;
-            t[k] = (r[k] >= 0 && j < ntgt) ? T[j] : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+            base[k] = s_b[wb + r0 + k];
+            t[k] = Tl[max(base[k], 0)];
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int src = r[k] & 31;
-            const float qx = __shfl_sync(0xffffffffu, qp.x, src), qy = __shfl_sync(0xffffffffu, qp.y, src),
-                        qz = __shfl_sync(0xffffffffu, qp.z, src);
-            const float m = __shfl_sync(0xffffffffu, best, src);
-            const float d = dist_rn(qx, qy, qz, t[k].x, t[k].y, t[k].z);
-            const unsigned hit = __ballot_sync(0xffffffffu, r[k] >= 0 && base[k] + lane < ntgt && d == m);
-            if (lane == r[k] && hit) idx = base[k] + __ffs(hit) - 1;
+            const float4 q = s_q[wb + r0 + k];
+            const float d = dist_rn(q.x, q.y, q.z, t[k].x, t[k].y, t[k].z);
+            const unsigned c = __reduce_min_sync(0xffffffffu, d == q.w ? (unsigned)lane : 32u);
+            // the row's index goes back through its staging slot (a uniform value: one store)
+            if (lane == 0) s_b[wb + r0 + k] = (base[k] >= 0 && c < 32u) ? base[k] + (int)c : -1;
         }
     }
+    __syncwarp();
+    const int idx = s_b[threadIdx.x];
     double v = 0.0;
     int h = 0;
     if (valid) {
@@ -355,38 +354,35 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
     }
     const float4* X = a.xp + (int64_t)b * a.xpad;
     static_assert(kR == 16, "the column resolve re-scans 16-row groups with half-warps");
-    int idx = -1;
-    unsigned todo = __ballot_sync(0xffffffffu, i0 >= 0);
-    while (todo) {
-        int r[2][2];   // [step][half]
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            r[k >> 1][k & 1] = todo ? __ffs(todo) - 1 : -1;
-            todo &= todo - 1;
-        }
+    // the warp's 32 columns staged in shared memory: (target, minimum) and group start
+    __shared__ float4 sc[kMergeThreads];
+    __shared__ int si[kMergeThreads];
+    sc[threadIdx.x] = make_float4(t.x, t.y, t.z, m);
+    si[threadIdx.x] = i0;
+    __syncwarp();
+    const int wb = threadIdx.x & ~31;
+    for (int r0 = 0; r0 < 32; r0 += 4) {   // two steps of two columns (one per half-warp) in flight
+        int g[2];
         float4 q[2];
-        int g0[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int mine = r[k][half];
-            g0[k] = __shfl_sync(0xffffffffu, i0, mine & 31);
-            const int i = g0[k] + hl;
-            q[k] = (mine >= 0 && i < a.q1) ? X[i] : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+            g[k] = si[wb + r0 + 2 * k + half];
+            q[k] = X[min(max(g[k], 0) + hl, a.q1 - 1)];   // a partial last group re-reads row q1 - 1
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int mine = r[k][half], src = mine & 31;
-            const float tx = __shfl_sync(0xffffffffu, t.x, src), ty = __shfl_sync(0xffffffffu, t.y, src),
-                        tz = __shfl_sync(0xffffffffu, t.z, src);
-            const float mm = __shfl_sync(0xffffffffu, m, src);
-            const float d = dist_rn(q[k].x, q[k].y, q[k].z, tx, ty, tz);  // same operand order as the kernel
-            const unsigned hit = __ballot_sync(0xffffffffu, mine >= 0 && g0[k] + hl < a.q1 && d == mm);
-            const unsigned h0 = hit & 0xffffu, h1 = hit >> 16;
-            const int gA = __shfl_sync(0xffffffffu, g0[k], 0), gB = __shfl_sync(0xffffffffu, g0[k], 16);
-            if (lane == r[k][0] && h0) idx = gA + __ffs(h0) - 1;
-            if (lane == r[k][1] && h1) idx = gB + __ffs(h1) - 1;
+            const float4 c = sc[wb + r0 + 2 * k + half];
+            const float d = dist_rn(q[k].x, q[k].y, q[k].z, c.x, c.y, c.z);  // same operand order as the kernel
+            const unsigned v = (g[k] >= 0 && g[k] + hl < a.q1 && d == c.w) ? (unsigned)hl : 16u;
+            const unsigned c0 = __reduce_min_sync(0xffffffffu, half == 0 ? v : 16u);
+            const unsigned c1 = __reduce_min_sync(0xffffffffu, half == 1 ? v : 16u);
+            // results back through the staging slots (lane 0 / lane 16 own the two columns' slots)
+            const unsigned cm = half == 0 ? c0 : c1;
+            if (hl == 0) si[wb + r0 + 2 * k + half] = cm < 16u ? g[k] + (int)cm : -1;
         }
     }
+    __syncwarp();
+    int idx = si[threadIdx.x];
     if (idx < 0) m = INFINITY;  // no finite candidate, or every distance was NaN
     double v = 0.0;
     int h = 0;

@@ -58,10 +58,10 @@ def test_launch_counts(lib):
     # backward, clouds of <= 24576 points: segment sort on chip + grad
     assert lib.cd_launch_count(2, 32, 16384, 16384) == 2
     assert lib.cd_launch_count(3, 32, 16384, 16384) == 4 + 1 + 2
-    assert lib.cd_launch_count(2, 8, 24577, 100) == 2 * 3 + 2   # 2^18 keys: 2 global radix passes
+    assert lib.cd_launch_count(2, 8, 24577, 100) == 2 * 3 + 2   # 15-bit segment-local keys: 2 passes of 8 bits
     # backward, larger clouds: keys+hist, radix passes x 3 kernels - 1 hist, offsets, grad
-    assert lib.cd_launch_count(2, 8, 100000, 100000) == 2 * 3 + 2   # 1.6e6 keys: 2 passes of 11 bits
-    # c5: 2^23 keys -> 3 passes
+    assert lib.cd_launch_count(2, 8, 100000, 100000) == 2 * 3 + 2   # 17-bit local keys: 2 passes of 9 bits
+    # c5: 20-bit local keys -> 3 passes of 7 bits (2 of 10 cost more)
     assert lib.cd_launch_count(2, 4, 1 << 20, 1 << 20) == 3 * 3 + 2
 
 
