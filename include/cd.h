@@ -27,7 +27,9 @@
  *   - Preconditions: B, N, M >= 1 (empty cloud -> domain error =
  *     CD_ERR_INVALID_VALUE); finite coordinates.  Non-finite input does not crash: a
  *     query whose every distance is NaN/+inf gets d = +inf, idx = -1 (R6).
- *   - Thread safety: re-entrant; no mutable global state besides the thread-local error string.
+ *   - Thread safety: re-entrant.  Mutable state: the thread-local error string and test-hook settings
+ *     (cd_set_forward_splits / _mode / _profile_events, per thread), and process-wide per-DEVICE caches
+ *     of the SM count and kernel occupancies (filled once per device ordinal, idempotent atomics).
  */
 #ifndef CD_H_
 #define CD_H_

@@ -1,5 +1,6 @@
 // cd_internal.h — host-side launch plumbing shared by the libcd translation units (not public).
 #pragma once
+#include <atomic>
 #include <utility>
 #include <cstddef>
 #include <cstdint>
@@ -172,6 +173,53 @@ inline void record_profile_event(cudaEvent_t ev, cudaStream_t st) {
 }
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Process-wide per-device caches of device attributes / occupancies: one slot per device ordinal,
+// filled on first use by `f` (idempotent: racing threads store the same value), read by every
+// thread — the library's only mutable global state besides the thread-local error string.
+constexpr int kMaxDevices = 64;
+template <class F>
+inline int per_device_cached(std::atomic<int>* table, F f) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+        cudaGetLastError();
+        return f();
+    }
+    int v = table[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        v = f();
+        table[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+// SMs of the current device (148 on B200; the fallback if the query fails).
+inline int current_sm_count() {
+    static std::atomic<int> table[kMaxDevices];
+    return per_device_cached(table, [] {
+        int dev = 0, s = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || s <= 0) {
+            cudaGetLastError();
+            s = 148;
+        }
+        return s;
+    });
+}
+
+// Resident CTAs per SM of `kernel` with `threads` threads and `smem` dynamic bytes on the current
+// device (`fallback` if the query fails).
+template <class K>
+inline int occupancy_of(std::atomic<int>* table, K kernel, int threads, size_t smem, int fallback) {
+    return per_device_cached(table, [&] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, smem) != cudaSuccess || o <= 0) {
+            cudaGetLastError();
+            o = fallback;
+        }
+        return o;
+    });
+}
 
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per (device, kernel) on the
 // calling thread (the attribute is per device: a thread that switches devices sets it again).

@@ -253,7 +253,7 @@ cudaError_t launch_sample(const float* verts, const int* faces, int B, int Nv, i
     s.face_idx = face_idx;
     s.bary = bary;
     const int64_t total = (int64_t)B * N;
-    mesh_sample_kernel<<<std::min(ceil_div64(total, 256), 148 * 16), 256, 0, st>>>(s);
+    mesh_sample_kernel<<<std::min(ceil_div64(total, 256), current_sm_count() * 16), 256, 0, st>>>(s);
     return cudaGetLastError();
 }
 
@@ -293,11 +293,11 @@ cudaError_t launch_sample_backward(const int* faces, const int* face_idx, const 
     uint32_t* totals = reinterpret_cast<uint32_t*>(w + off);
     off = align_up(off + (size_t)kSortTotalsWords * 4, 256);
     uint32_t* voff = reinterpret_cast<uint32_t*>(w + off);
-    const int grid = std::min(ceil_div64(L, 256), 148 * 16);
+    const int grid = std::min(ceil_div64(L, 256), current_sm_count() * 16);
     sample_keys_kernel<<<grid, 256, 0, st>>>(faces, face_idx, B, Nv, Nf, N, keys[0], vals[0]);
     const int cur = radix_sort_pairs(keys, vals, L, key_bits(kmax), counts, totals, st);
-    vertex_offsets_kernel<<<std::min(ceil_div64(L + 1, 256), 148 * 16), 256, 0, st>>>(keys[cur], L, kmax, voff);
-    vertex_grad_kernel<<<std::min(ceil_div64(kmax, 256), 148 * 16), 256, 0, st>>>(vals[cur], voff, bary, grad_points,
+    vertex_offsets_kernel<<<std::min(ceil_div64(L + 1, 256), current_sm_count() * 16), 256, 0, st>>>(keys[cur], L, kmax, voff);
+    vertex_grad_kernel<<<std::min(ceil_div64(kmax, 256), current_sm_count() * 16), 256, 0, st>>>(vals[cur], voff, bary, grad_points,
                                                                                   kmax, grad_verts);
     return cudaGetLastError();
 }

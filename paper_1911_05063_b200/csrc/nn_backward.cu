@@ -609,16 +609,7 @@ __global__ void __launch_bounds__(256, CD_GRAD_MINB) grad_kernel(GradArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------------
-static int sm_count() {
-    static thread_local int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+static int sm_count() { return current_sm_count(); }
 
 struct RadixPlan {
     int npasses, digit_bits, items;
@@ -812,12 +803,8 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     if (total > 0) {
         // exactly one wave of resident CTAs striding over the points (measured: c5 backward 0.546 ->
         // 0.487 ms against 32 CTAs per SM; a second, partial wave costs more than it hides)
-        static thread_local int occ = 0;
-        if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grad_kernel, 256, 0) != cudaSuccess ||
-                         occ <= 0)) {
-            cudaGetLastError();
-            occ = 4;
-        }
+        static std::atomic<int> occ_table[kMaxDevices];
+        const int occ = occupancy_of(occ_table, grad_kernel, 256, 0, 4);
         const int grid_g = (int)std::min<int64_t>((total + 255) / 256,
                                                   (int64_t)sm_count() * (CD_GRAD_CTAS_PER_SM > 0 ? CD_GRAD_CTAS_PER_SM : occ));
         launch_pdl(grad_kernel, dim3(grid_g), dim3(256), 0, st, a);

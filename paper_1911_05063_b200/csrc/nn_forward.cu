@@ -530,30 +530,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs a) {
 // Host side.
 static int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
-static int device_sm_count() {
-    static thread_local int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+static int device_sm_count() { return current_sm_count(); }
 
 // Choose the target-split count S so that (query-tile units x S) CTAs fill the SMs in waves of
 // near-equal work: minimise ceil(U*S / slots) * (Mt/S + c0), c0 = per-unit overhead in target-
 // equivalents (query load + epilogue).
 int unfused_ctas_per_sm() {
-    static thread_local int occ = 0;
-    if (occ == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nn_fwd_kernel, kFwdThreads, 0) != cudaSuccess ||
-            occ <= 0) {
-            cudaGetLastError();
-            occ = 4;
-        }
-    }
-    return occ;
+    static std::atomic<int> table[kMaxDevices];
+    return occupancy_of(table, nn_fwd_kernel, kFwdThreads, 0, 4);
 }
 
 // Choose the target-split count S: every (query tile, split) is one CTA; split s covers target

@@ -225,19 +225,9 @@ __global__ void __launch_bounds__(kFwdThreads, CD_FUSED_MINB) nn_fused_kernel(Fu
 // ------------------------------------------------------------------------------------------------
 // ------------------------------------------------------------------------------------------------
 int fused_ctas_per_sm(int rows) {
-    static thread_local int occ[2] = {0, 0};
-    int& o = occ[rows == kR ? 0 : 1];
-    if (o == 0) {
-        const cudaError_t e = rows == kR
-                                  ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, nn_fused_kernel<false, kR>, kFwdThreads, 0)
-                                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, nn_fused_kernel<false, kRSmall>,
-                                                                                  kFwdThreads, 0);
-        if (e != cudaSuccess || o <= 0) {
-            cudaGetLastError();
-            o = 3;
-        }
-    }
-    return o;
+    static std::atomic<int> big[kMaxDevices], small[kMaxDevices];
+    return rows == kR ? occupancy_of(big, nn_fused_kernel<false, kR>, kFwdThreads, 0, 3)
+                      : occupancy_of(small, nn_fused_kernel<false, kRSmall>, kFwdThreads, 0, 3);
 }
 
 cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* yp, long long* colkey,

@@ -925,12 +925,7 @@ int pruned_launches(const PrunedPlan& p) {
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
                           cudaStream_t st) {
     char* w = static_cast<char*>(ws);
-    int sms = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = current_sm_count();
     float* bbox = reinterpret_cast<float*>(w + p.off_bbox);
     const bool segsort = pruned_segsort(p);
     if (!segsort) launch_bbox(x, p.npts[0], y, p.npts[1], p.B, bbox, st);

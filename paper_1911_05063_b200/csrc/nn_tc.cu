@@ -814,16 +814,7 @@ __global__ void __launch_bounds__(kMergeThreads) tc_chunks_kernel(TcChunkArgs a)
 // ------------------------------------------------------------------------------------------ host
 static int tc_cdiv(int64_t x, int64_t y) { return (int)((x + y - 1) / y); }
 
-static int tc_sms() {
-    static thread_local int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+static int tc_sms() { return current_sm_count(); }
 
 void plan_tc(TcPlan& p, int B, int N, int M, int forced_splits) {
     p.B = B;

@@ -288,7 +288,7 @@ static void plan_p2s(P2sPlan& p, int B, int N, int Nv, int Nf) {
     p.Nfpad = cdiv(Nf, kFaceTile) * kFaceTile;
     p.qtiles = p.Ppad / kP2sQ;
     p.ftiles = p.Nfpad / kFaceTile;
-    int sms = 148;
+    const int sms = current_sm_count();
     const int64_t units = (int64_t)B * p.qtiles, slots = (int64_t)sms * 3;
     // t(S) = U (T + S c0) / slots + (ceil(T/S) + c0) / 2, c0 = 0.1 face tile: the fused kernel's fitted
     // split model (nn_forward.cu); sweep (tools/sweep_p2s_splits.py, NEXT-3 workload): S = 32-40
@@ -399,7 +399,7 @@ cudaError_t launch_p2s_backward(const float* points, const float* closest, const
     char* w = static_cast<char*>(ws);
     float* up = reinterpret_cast<float*>(w);
     const int64_t total = (int64_t)B * N;
-    p2s_grad_points_kernel<<<std::min(cdiv(total, 256), 148 * 16), 256, 0, st>>>(points, closest, g, g_scalar, upstream,
+    p2s_grad_points_kernel<<<std::min(cdiv(total, 256), current_sm_count() * 16), 256, 0, st>>>(points, closest, g, g_scalar, upstream,
                                                                                  total, grad_points, up);
     if (grad_verts)
         return launch_sample_backward(faces, face, bary, B, Nv, Nf, N, up, grad_verts,
