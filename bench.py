@@ -654,7 +654,8 @@ def main():
         alg = 28 * pts   # read both clouds (12 B) + both index arrays (4 B) + write both gradients (12 B)
         hbm_peak = _measured_peak("hbm_gbs", 7700.0)
         nbl = cd.launch_count(_lib.CD_OP_BACKWARD, B_local, N, M)
-        bwd_kern = ("cd_backward (seg_sort: one CTA per (direction, batch) segment sorts on chip; grad: "
+        bwd_kern = ("cd_backward (seg_sort_grad: each (direction, batch) segment part sorted on chip, its targets' "
+                    "gradients written by the same CTA: "
                     if max(N, M) <= 24576 else "cd_backward (keys+hist, radix passes, offsets, grad: ")
         bwd_roof = {"bound": "hbm", "kernel": f"{bwd_kern}{nbl} launches)", "ms": bms,
                     "achieved": alg / (bms * 1e-3) / 1e9, "peak": hbm_peak[0], "unit": "GB/s",

@@ -1,25 +1,27 @@
 // nn_backward.cu — backward of the Chamfer per-point distances, argmin held fixed
 // (SURVEY.md §8.a.6-a.8).  Deterministic and free of floating-point atomics.
 //
-// Clouds of <= kSegMax points (c1-c3): seg_sort_kernel (one or 2^p CTAs per (direction, batch)
-// segment; on-chip stable LSD sort of the segment's edges, see below) writes the sorted sources and
-// the key offsets directly, then grad_kernel: 2 launches.  Larger clouds (c4, c5):
+// Clouds of <= kSegMax points (c1-c3): seg_sort_grad_kernel, ONE launch: one or 2^p CTAs per
+// (direction, batch) segment sort the segment's edges on chip (stable LSD, see below), fill the key
+// offsets in shared memory and write the gradients of the part's targets.  Larger clouds (c4, c5),
+// the 2B (direction, batch) segments sorted as independent segments with segment-local keys:
 //
-//   keys_hist_kernel one (key, value) pair per NN edge: xy edge i -> a_i gets key b*M + a_i,
-//                    yx edge j -> b_j gets key B*M + b*N + b_j; value = the source row.  Built in
+//   keys_hist_kernel one (key, value) pair per NN edge: xy edge i -> a_i gets key a_i (segment b),
+//                    yx edge j -> b_j gets key b_j (segment B + b); value = the source row.  Built in
 //                    ascending source order; also the first radix pass's per-tile histogram.
-//   radix passes     stable LSD radix sort by key, digits of <= 11 bits (2 passes up to 2^22
-//                    keys), reduce-then-scan:
+//   radix passes     stable LSD radix sort by key, digits of <= 11 bits (widths from a measured
+//                    per-width cost), reduce-then-scan:
 //                      radix_hist_kernel   per-tile digit histograms (shared-memory integer adds)
-//                      radix_rowscan_kernel exclusive scan of each digit's row of tile counts (the
-//                                          digit bases are scanned inside the scatter kernel)
+//                      radix_rowscan_kernel exclusive scan of each (segment, digit) row of tile counts
+//                                          (one warp per row; the digit bases are scanned inside
+//                                          the scatter kernel)
 //                      radix_scatter_kernel stable in-tile ranks (warp ballot multisplit + per-warp
 //                                          counts in element order) -> scatter.  Stability keeps ascending
 //                                          source rows inside every key segment.
-//   offsets_kernel   segment offsets from the sorted keys (disjoint gap fills, no atomics).
-//   grad_kernel      one thread per output point: own term 2 g (p - partner) then the segment's
-//                    scatter terms in ascending source order, accumulated in fp64 with explicit
-//                    .rn ops (no contraction), one fp32 store.
+//   offsets_kernel   global key offsets from the sorted keys (disjoint gap fills, no atomics).
+//   grad_kernel      one thread per output point (batch-major): own term 2 g (p - partner) then the
+//                    segment's scatter terms in ascending source order, accumulated in fp64 with
+//                    explicit .rn ops (no contraction), one fp32 store.
 #include "cd_device.cuh"
 #include "cd_internal.h"
 #include "seg_sort.cuh"
@@ -378,6 +380,29 @@ __global__ void __launch_bounds__(256) offsets_kernel(const uint32_t* __restrict
     }
 }
 
+struct GradArgs {
+    const float* x;
+    const float* y;
+    int B, N, M, q0, q1, r0, r1;
+    const int32_t* idx_xy;
+    const int32_t* idx_yx;
+    const float* g;
+    const float* h;
+    float g_scalar, h_scalar;
+    const float* upstream;   // optional device scalar u: the fills become RN(u * g_scalar), RN(u * h_scalar)
+    const uint32_t* vals;
+    const uint32_t* off;
+    float* grad_x;
+    float* grad_y;
+};
+
+// acc += (2 w) * (p - s), fp64, explicit roundings in the oracle's order (no FMA contraction).
+__device__ __forceinline__ void acc_term(double acc[3], const float* p, const float* s, double w) {
+    const double w2 = __dmul_rn(2.0, w);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c])));
+}
+
 // Segment-local sort (small clouds: max(N, M) <= kSegMax).  The edges of one (direction, batch
 // element) segment have keys in one range of T = M (xy) or N (yx) consecutive keys and land in one
 // contiguous range of the sorted order, so each segment sorts on its own: one CTA per segment, a
@@ -386,12 +411,11 @@ __global__ void __launch_bounds__(256) offsets_kernel(const uint32_t* __restrict
 // counts of a pass are integer shared-memory adds made while loading / while placing the previous
 // pass), then the sorted sources and the segment's key offsets (gap fill) go to global memory.
 // Replaces keys_hist + the global passes + offsets_kernel: 2 launches per backward, not 3 passes + 2.
-__global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __restrict__ idx_xy,
-                                                               const int32_t* __restrict__ idx_yx, int B, int N,
-                                                               int M, int nmax, int lparts,
-                                                               uint32_t* __restrict__ vals_out,
-                                                               uint32_t* __restrict__ off) {
+__global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga, int nmax, int lparts) {
     pdl_wait();
+    const int32_t* __restrict__ idx_xy = ga.idx_xy;
+    const int32_t* __restrict__ idx_yx = ga.idx_yx;
+    const int B = ga.B, N = ga.N, M = ga.M;
     extern __shared__ __align__(16) uint32_t smem_seg[];
     uint32_t* wcur = smem_seg;                   // [kSegWarps][D] this pass's per-warp digit counts
     uint32_t* wnext = wcur + kSegWarps * kSegD;  // next pass's, counted while placing
@@ -407,9 +431,6 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
     const int nseg = dir == 0 ? N : M;       // edges (sources) of the segment
     const int T = dir == 0 ? M : N;          // keys (targets) of the segment
     const int32_t* idx = dir == 0 ? idx_xy + (int64_t)b * N : idx_yx + (int64_t)b * M;
-    const uint32_t vbase = (uint32_t)((int64_t)b * nseg);                       // source rows b*n + i
-    const int64_t pbase = dir == 0 ? (int64_t)b * N : (int64_t)B * N + (int64_t)b * M;   // sorted positions
-    const int64_t kbase = dir == 0 ? (int64_t)b * M : (int64_t)B * M + (int64_t)b * N;   // keys
     int nb = 1;
     while ((1 << nb) < T) ++nb;
     // part h of the segment's 2^lparts CTAs owns the keys whose top lparts bits are h: [K0, K1)
@@ -452,7 +473,6 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
     }
     const int n = (int)n_u;                  // edges of this part
     CD_CHECK(n <= nmax && (int64_t)base_u + n <= nseg);
-    const int64_t obase = pbase + base_u;    // sorted positions of this part
     const int passes = kb_low > 0 ? (kb_low + kSegDigitBits - 1) / kSegDigitBits : 0;
     const int db = passes > 0 ? (kb_low + passes - 1) / passes : 1;
     const int D = 1 << db;
@@ -488,14 +508,54 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
     }
     seg_lsd_passes(kA, vA, kB, vB, wcur, wnext, dstart, n, passes, db, lspan, R);
     __syncthreads();
-    // sorted sources and key offsets over [K0, K1] (off[k] = first position with key >= k; gaps
-    // filled; off[K1] is written by both neighbouring parts with the same value)
+    // key offsets of this part in shared memory (the free key buffer): offs[k - K0] = first sorted
+    // position with key >= k for k in [K0, K1) (gap fill, disjoint writes); key K1 - 1's run ends at n
+    uint16_t* offs = kB;
     for (int p = threadIdx.x; p <= n; p += kSegThreads) {
-        if (p < n) vals_out[obase + p] = vbase + vA[p];
         const int lo = p == 0 ? K0 : (int)kA[p - 1] + 1;
-        const int hi = p == n ? K1 : (int)kA[p];
-        CD_CHECK(lo >= K0 && hi <= K1);
-        for (int k = lo; k <= hi; ++k) off[kbase + k] = (uint32_t)(obase + p);
+        const int hi = min(p == n ? K1 : (int)kA[p], K1 - 1);
+        CD_CHECK(lo >= K0 && hi < K1);
+        for (int k = lo; k <= hi; ++k) offs[k - K0] = (uint16_t)p;
+    }
+    __syncthreads();
+    // the gradients of this part's targets, as grad_kernel computes them: own term 2 w_t (p - partner)
+    // first, then the sources in ascending index (the stable sort's order), fp64 with explicit .rn ops
+    float gs = ga.g_scalar, hs = ga.h_scalar;
+    if (ga.upstream) {
+        const float u = *ga.upstream;
+        gs = __fmul_rn(u, gs);
+        hs = __fmul_rn(u, hs);
+    }
+    const int S = dir == 0 ? N : M;                              // sources (and partners) per batch
+    const float* tgt = dir == 0 ? ga.y + (int64_t)b * M * 3 : ga.x + (int64_t)b * N * 3;
+    const float* src = dir == 0 ? ga.x + (int64_t)b * N * 3 : ga.y + (int64_t)b * M * 3;
+    const int32_t* pidx = dir == 0 ? idx_yx + (int64_t)b * M : idx_xy + (int64_t)b * N;
+    const float* wt = dir == 0 ? (ga.h ? ga.h + (int64_t)b * M : nullptr) : (ga.g ? ga.g + (int64_t)b * N : nullptr);
+    const float* wsrc = dir == 0 ? (ga.g ? ga.g + (int64_t)b * N : nullptr) : (ga.h ? ga.h + (int64_t)b * M : nullptr);
+    const float wt_s = dir == 0 ? hs : gs, wsrc_s = dir == 0 ? gs : hs;
+    const int t0 = dir == 0 ? ga.r0 : ga.q0, t1 = dir == 0 ? ga.r1 : ga.q1;
+    float* out = dir == 0 ? ga.grad_y + (int64_t)b * (ga.r1 - ga.r0) * 3 : ga.grad_x + (int64_t)b * (ga.q1 - ga.q0) * 3;
+    for (int t = max(K0, t0) + threadIdx.x; t < min(K1, t1); t += kSegThreads) {
+        const float* pt = tgt + (int64_t)t * 3;
+        const int part = min(max(pidx[t], 0), S - 1);
+        const double wtt = wt ? (double)wt[t] : (double)wt_s;
+        double acc[3];
+        {
+            const float* ps = src + (int64_t)part * 3;
+            const double w2 = __dmul_rn(2.0, wtt);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn((double)pt[c], (double)ps[c]));
+        }
+        const int e0 = offs[t - K0], e1 = t + 1 < K1 ? (int)offs[t + 1 - K0] : n;
+        CD_CHECK(e0 <= e1 && e1 <= n);
+        for (int e = e0; e < e1; ++e) {
+            const int sidx = vA[e];
+            acc_term(acc, pt, src + (int64_t)sidx * 3, wsrc ? (double)wsrc[sidx] : (double)wsrc_s);
+        }
+        float* o = out + (int64_t)(t - t0) * 3;
+        o[0] = (float)acc[0];
+        o[1] = (float)acc[1];
+        o[2] = (float)acc[2];
     }
 }
 
@@ -508,29 +568,6 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_kernel(const int32_t* __
 #ifndef CD_GRAD_CTAS_PER_SM
 #define CD_GRAD_CTAS_PER_SM 0   // 0: the occupancy (one resident wave)
 #endif
-struct GradArgs {
-    const float* x;
-    const float* y;
-    int B, N, M, q0, q1, r0, r1;
-    const int32_t* idx_xy;
-    const int32_t* idx_yx;
-    const float* g;
-    const float* h;
-    float g_scalar, h_scalar;
-    const float* upstream;   // optional device scalar u: the fills become RN(u * g_scalar), RN(u * h_scalar)
-    const uint32_t* vals;
-    const uint32_t* off;
-    float* grad_x;
-    float* grad_y;
-};
-
-// acc += (2 w) * (p - s), fp64, explicit roundings in the oracle's order (no FMA contraction).
-__device__ __forceinline__ void acc_term(double acc[3], const float* p, const float* s, double w) {
-    const double w2 = __dmul_rn(2.0, w);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c])));
-}
-
 __global__ void __launch_bounds__(256, CD_GRAD_MINB) grad_kernel(GradArgs a) {
     pdl_wait();
     if (a.upstream) {
@@ -742,7 +779,7 @@ void plan_backward(BwdPlan& p, int B, int N, int M, int q0, int q1, int r0, int 
 }
 
 int backward_launches(const BwdPlan& p) {
-    return p.segsort ? 2 : 3 * p.npasses + 2;   // keys fused with the pass-0 histogram
+    return p.segsort ? 1 : 3 * p.npasses + 2;   // keys fused with the pass-0 histogram
 }
 
 cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, const int32_t* idx_xy,
@@ -754,30 +791,6 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     uint32_t* counts = reinterpret_cast<uint32_t*>(w + p.off_counts);
     uint32_t* totals = reinterpret_cast<uint32_t*>(w + p.off_totals);
     uint32_t* off = reinterpret_cast<uint32_t*>(w + p.off_offsets);
-    int cur = 0;
-    if (p.segsort) {
-        const int nmax = std::max(p.N, p.M);
-        const size_t smem = seg_sort_smem(nmax);
-        ensure_smem_attr((const void*)seg_sort_kernel, (int)seg_sort_smem(kSegMax));
-        // 2^lparts CTAs per segment (split by the keys' top bits) while the segments alone leave SMs idle
-        int lparts = 0;
-        while (lparts < CD_SEG_MAXPARTS && (int64_t)2 * p.B << (lparts + 1) <= sm_count()) ++lparts;
-        launch_pdl(seg_sort_kernel, dim3((unsigned)((int64_t)2 * p.B << lparts)), dim3(kSegThreads), smem, st,
-                   idx_xy, idx_yx, p.B, p.N, p.M, nmax, lparts, vals[0], off);
-    } else {
-        const RadixPlan r = radix_plan(p.segs, p.nbits, true);
-        const int D = 1 << r.digit_bits;
-        if (r.items == kSortItemsWide)
-            keys_hist_kernel<kSortItemsWide><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
-                idx_xy, idx_yx, p.B, p.N, p.M, D, r.g, keys[0], vals[0], counts);
-        else
-            keys_hist_kernel<kSortItems><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
-                idx_xy, idx_yx, p.B, p.N, p.M, D, r.g, keys[0], vals[0], counts);
-        cur = radix_sort_pairs(keys, vals, p.segs, p.nbits, counts, totals, st, /*first_hist_done=*/true,
-                               /*narrow=*/true);
-        const int grid_o = (int)std::min<int64_t>((p.L / kOffRun + 1 + 255) / 256, (int64_t)sm_count() * 16);
-        offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], r.g, p.M, p.N, p.kmax, off);
-    }
     GradArgs a;
     a.x = x;
     a.y = y;
@@ -795,10 +808,37 @@ cudaError_t launch_backward(const BwdPlan& p, const float* x, const float* y, co
     a.g_scalar = g_scalar;
     a.h_scalar = h_scalar;
     a.upstream = upstream;
-    a.vals = vals[cur];
-    a.off = off;
     a.grad_x = grad_x;
     a.grad_y = grad_y;
+    if (p.segsort) {
+        // one launch: each CTA sorts its (direction, batch) segment part on chip and writes the
+        // gradients of that part's targets
+        const int nmax = std::max(p.N, p.M);
+        const size_t smem = seg_sort_smem(nmax);
+        ensure_smem_attr((const void*)seg_sort_grad_kernel, (int)seg_sort_smem(kSegMax));
+        // 2^lparts CTAs per segment (split by the keys' top bits) while the segments alone leave SMs idle
+        int lparts = 0;
+        while (lparts < CD_SEG_MAXPARTS && (int64_t)2 * p.B << (lparts + 1) <= sm_count()) ++lparts;
+        a.vals = nullptr;
+        a.off = nullptr;
+        launch_pdl(seg_sort_grad_kernel, dim3((unsigned)((int64_t)2 * p.B << lparts)), dim3(kSegThreads), smem, st, a,
+                   nmax, lparts);
+        return cudaGetLastError();
+    }
+    const RadixPlan r = radix_plan(p.segs, p.nbits, true);
+    const int D = 1 << r.digit_bits;
+    if (r.items == kSortItemsWide)
+        keys_hist_kernel<kSortItemsWide><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
+            idx_xy, idx_yx, p.B, p.N, p.M, D, r.g, keys[0], vals[0], counts);
+    else
+        keys_hist_kernel<kSortItems><<<p.ntiles, kSortThreads, (size_t)D * 4, st>>>(
+            idx_xy, idx_yx, p.B, p.N, p.M, D, r.g, keys[0], vals[0], counts);
+    const int cur = radix_sort_pairs(keys, vals, p.segs, p.nbits, counts, totals, st, /*first_hist_done=*/true,
+                                     /*narrow=*/true);
+    const int grid_o = (int)std::min<int64_t>((p.L / kOffRun + 1 + 255) / 256, (int64_t)sm_count() * 16);
+    offsets_kernel<<<grid_o, 256, 0, st>>>(keys[cur], r.g, p.M, p.N, p.kmax, off);
+    a.vals = vals[cur];
+    a.off = off;
     const int64_t total = (int64_t)p.B * ((p.q1 - p.q0) + (p.r1 - p.r0));
     if (total > 0) {
         // exactly one wave of resident CTAs striding over the points (measured: c5 backward 0.546 ->

@@ -55,9 +55,10 @@ def test_workspace_sizes(lib):
 def test_launch_counts(lib):
     # fused forward: pack + fused + epilogue (row merge | column resolve) + partials
     assert lib.cd_launch_count(0, 32, 16384, 16384) == 4
-    # backward, clouds of <= 24576 points: segment sort on chip + grad
-    assert lib.cd_launch_count(2, 32, 16384, 16384) == 2
-    assert lib.cd_launch_count(3, 32, 16384, 16384) == 4 + 1 + 2
+    # backward, clouds of <= 24576 points: one launch sorts each segment part on chip and writes its
+    # targets' gradients
+    assert lib.cd_launch_count(2, 32, 16384, 16384) == 1
+    assert lib.cd_launch_count(3, 32, 16384, 16384) == 4 + 1 + 1
     assert lib.cd_launch_count(2, 8, 24577, 100) == 2 * 3 + 2   # 15-bit segment-local keys: 2 passes of 8 bits
     # backward, larger clouds: keys+hist, radix passes x 3 kernels - 1 hist, offsets, grad
     assert lib.cd_launch_count(2, 8, 100000, 100000) == 2 * 3 + 2   # 17-bit local keys: 2 passes of 9 bits

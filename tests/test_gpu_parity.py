@@ -284,7 +284,7 @@ def test_backward_slices_match_full(cd):
 
 @pytest.mark.parametrize("N,M", [(24576, 700), (24577, 700), (3, 24576), (5000, 24577)])
 def test_backward_segment_sort_boundary(cd, N, M):
-    """max(N, M) <= 24576 sorts each (direction, batch) segment on chip (seg_sort_kernel), larger
+    """max(N, M) <= 24576 sorts each (direction, batch) segment on chip (seg_sort_grad_kernel), larger
     clouds take the global radix passes: both against the oracle bit for bit, with skewed in-degree
     (many sources on few targets) and a single-target segment."""
     rng = np.random.default_rng(N + 7 * M)

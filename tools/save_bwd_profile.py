@@ -20,10 +20,10 @@ for r in csv.DictReader(io.StringIO(txt)):
         {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}.get(r["Metric Unit"], 1)
 # the backward = the last contiguous run of backward kernels (after the forward of run_backward.py)
 names = ("keys_hist_kernel", "radix_hist_kernel", "radix_rowscan_kernel", "radix_scatter_kernel", "offsets_kernel",
-         "seg_sort_kernel", "grad_kernel")
+         "seg_sort_grad_kernel", "grad_kernel")
 items = [(k, v) for k, v in per.items() if k[1].split("::")[-1] in names]
 # one backward call: from the last first-kernel (keys_hist: radix path; seg_sort: clouds <= 24576) to the end
-start = max(i for i, (k, _) in enumerate(items) if k[1].endswith(("keys_hist_kernel", "seg_sort_kernel")))
+start = max(i for i, (k, _) in enumerate(items) if k[1].endswith(("keys_hist_kernel", "seg_sort_grad_kernel")))
 items = items[start:]
 tot_t = sum(v.get("gpu__time_duration.sum", 0) for _, v in items) / 1e9
 tot_b = sum(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for _, v in items)
