@@ -37,6 +37,12 @@ def _worker(rank, world, port, mode, result_q):
             X, Y = synth.shape_pair(B, 300, 260, config_index=60, b0=rank * B)
             out = pd.batch_sharded_step(OracleEngine(), torch.from_numpy(X), torch.from_numpy(Y), B * world, rank * B,
                                         tau=tau, w1=0.5, w2=2.0)
+        elif mode == "batch_strong":   # bench.py's c4 under --gpus N: a fixed batch split over the ranks
+            Bg = 5
+            b0, b1 = pd.shard_range(Bg, rank, world)
+            X, Y = synth.shape_pair(b1 - b0, 300, 260, config_index=62, b0=b0)
+            out = pd.batch_sharded_step(OracleEngine(), torch.from_numpy(X), torch.from_numpy(Y), Bg, b0,
+                                        tau=tau, w1=0.5, w2=2.0)
         else:
             X, Y = synth.shape_pair(2, 301, 277, config_index=61)
             x, y = torch.from_numpy(X), torch.from_numpy(Y)
@@ -98,6 +104,27 @@ def test_batch_sharded(world):
         np.testing.assert_array_equal(out["d_yx"], ref["d_yx"][sl])
         np.testing.assert_array_equal(out["grad_x"], ref["grad_x"][sl])
         np.testing.assert_array_equal(out["grad_y"], ref["grad_y"][sl])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_sharded_strong(world):
+    """A fixed global batch (B = 5) split over the ranks (strong scaling, bench.py's c4 mode): every
+    rank's per-point outputs and gradients equal its slice of the 1-process result, and the loss / F
+    (after the partials all-reduce) are the global ones."""
+    from paper_1911_05063_b200 import synth
+    from paper_1911_05063_b200.distributed import shard_range
+    res = _run(world, "batch_strong")
+    X, Y = synth.shape_pair(5, 300, 260, config_index=62)
+    ref = _reference(X, Y, 0.01, 0.5, 2.0)
+    for r in range(world):
+        out = res[r]
+        b0, b1 = shard_range(5, r, world)
+        np.testing.assert_allclose(out["loss"], ref["loss"], rtol=1e-12)
+        np.testing.assert_allclose(out["fscore"], ref["fscore"], rtol=1e-12)
+        np.testing.assert_array_equal(out["idx_xy"], ref["idx_xy"][b0:b1])
+        np.testing.assert_array_equal(out["idx_yx"], ref["idx_yx"][b0:b1])
+        np.testing.assert_array_equal(out["grad_x"], ref["grad_x"][b0:b1])
+        np.testing.assert_array_equal(out["grad_y"], ref["grad_y"][b0:b1])
 
 
 @pytest.mark.parametrize("world,mode", [(2, "query_fused"), (3, "query_fused"), (2, "query_slices")])

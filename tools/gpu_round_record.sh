@@ -10,3 +10,6 @@ tools/gpu_ncu_kernel.sh ${TAG}_pruned nn_pruned 1 tools/run_forward.py c4 pruned
 tools/gpu_ncu_kernel.sh ${TAG}_p2s p2s_kernel 1 tools/run_p2s.py brute
 tools/gpu_ncu_kernel.sh ${TAG}_p2sp p2s_pruned_kernel 1 tools/run_p2s.py pruned
 tools/gpu_ncu_kernel.sh ${TAG}_tc nn_tc_kernel 0 tools/run_tc.py c3 1
+tools/gpu_ncu_kernel.sh ${TAG}_segg seg_sort_grad_kernel 1 tools/run_backward.py c3 2
+tools/gpu_ncu_kernel.sh ${TAG}_gradc5 grad_kernel 1 tools/run_backward.py c5 2
+tools/gpu_ncu_kernel.sh ${TAG}_scatc5 radix_scatter_kernel 1 tools/run_backward.py c5 2
