@@ -705,13 +705,15 @@ def main():
         xh = cd.pinned_copy(X)
         yh = cd.pinned_copy(Y)
         if world == 1:
-            stepper = cd.HostStepper(B_local, N, M, tau=tau, w1=w1, w2=w2, device=dev)
+            stepper = cd.HostStepper(B_local, N, M, tau=tau, w1=w1, w2=w2, device=dev, graph=not args.no_graph)
 
             def e2e_step():
                 stepper.step(xh, yh)
             api_desc = (f"cd_step_host_overlapped via api.HostStepper (pinned host clouds -> H2D in {stepper.nchunks} "
-                        "batch ranges on a copy stream, each range's forward starting as it lands -> finalize -> "
-                        "backward -> D2H of loss, F and both gradients; every step copies its inputs and results)")
+                        "batch ranges on a copy stream, each range's forward starting as it lands and its loss "
+                        "backward + gradient D2H following -> finalize -> D2H of loss and F; every step copies its "
+                        "inputs and results" + ("; the call is captured once in a CUDA graph and replayed)"
+                                                if not args.no_graph else ")"))
             h2d, d2h = int(X.nbytes + Y.nbytes), stepper.d2h_bytes()
         else:
             # the public API under torch.distributed: the clouds land from pinned host memory (rank 0 only

@@ -311,8 +311,10 @@ CD_API cd_status cd_p2s_forward_pruned(const float* points, const float* verts, 
  * compute; finalize and the loss / F-score copies follow on `stream`, which finally waits for the
  * gradient copies.  Results are identical to cd_step_host (per-batch outputs do not depend on the
  * chunking).  events: nchunks + 1 cudaEvent_t created by the caller (disable-timing events are
- * fine); events[nchunks] is recorded at the end of the step, and the next call's copies wait on it
- * before overwriting the staging buffers.  nchunks in [1, B].  Workspace: cd_workspace_size(CD_OP_STEP).
+ * fine); the copy stream first waits for everything already queued on `stream` (events[nchunks]
+ * recorded there: the previous step's staging buffers are free) and joins `stream` again before
+ * the step ends, so the call can be captured in a CUDA graph and replayed (static pointers and
+ * sizes).  nchunks in [1, B].  Workspace: cd_workspace_size(CD_OP_STEP).
  */
 CD_API cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int B, int N, int M,
                        float tau, float w1, float w2,

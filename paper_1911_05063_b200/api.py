@@ -302,10 +302,12 @@ class HostStepper:
     host tensors.  step() is asynchronous: call synchronize() (or read after the stream syncs)."""
 
     def __init__(self, B: int, N: int, M: int, tau: float | None = None, w1: float = 1.0, w2: float = 1.0,
-                 nchunks: int | None = None, device=None, want_grads: bool = True):
+                 nchunks: int | None = None, device=None, want_grads: bool = True, graph: bool = False):
         self.B, self.N, self.M, self.tau, self.w1, self.w2 = B, N, M, tau, w1, w2
-        # measured (tools/time_e2e.py c3, gradients copied back): 1 range 2.52 ms, 2: 2.36, 3: 2.29, 4: 2.26, 6: 2.35
-        self.nchunks = nchunks or min(4, B)
+        # measured (tools/time_e2e.py, gradients copied back, graph replay): c3 1 range 2.48 ms, 2: 2.30, 3: 2.25,
+        # 4: 2.20, 8: 2.34; c2 1: 0.153, 2: 0.149, 4: 0.191 (each range's forward then under-fills the GPU)
+        # -> up to 4 ranges of at least 2^31 distance evaluations each
+        self.nchunks = nchunks or max(1, min(4, B, (B * N * M) >> 31))
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         # a private workspace: its staging area is written by this stepper's copy stream
         n = int(_lib.load().cd_workspace_size(_lib.CD_OP_STEP, B, N, M))
@@ -322,6 +324,12 @@ class HostStepper:
         self.fscore = pinned_empty((B,))
         self.grad_x = pinned_empty((B, N, 3)) if want_grads else None
         self.grad_y = pinned_empty((B, M, 3)) if want_grads else None
+        # graph=True: the first step() with given host buffers is captured (the C call forks and joins
+        # its copy stream, so it is capturable) and later steps replay it — every replay still copies
+        # that step's inputs in and its results out; only the host-side launch work is saved
+        self.graph = graph
+        self._graph = None
+        self._graph_key = None
 
     def d2h_bytes(self) -> int:
         """Bytes copied device -> host per step (loss, F-score, gradients)."""
@@ -329,13 +337,27 @@ class HostStepper:
             (12 * self.B * (self.N + self.M) if self.grad_x is not None else 0)
 
     def step(self, x_host: torch.Tensor, y_host: torch.Tensor):
+        if self.graph:
+            key = (x_host.data_ptr(), y_host.data_ptr())
+            if self._graph is None or self._graph_key != key:
+                self._call(x_host, y_host)                     # warm-up (plans, attributes) outside capture
+                torch.cuda.current_stream().synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._call(x_host, y_host)
+                self._graph, self._graph_key = g, key
+            self._graph.replay()
+            return self.loss, self.fscore, self.grad_x, self.grad_y
+        self._call(x_host, y_host)
+        return self.loss, self.fscore, self.grad_x, self.grad_y
+
+    def _call(self, x_host, y_host):
         check(_lib.load().cd_step_host_overlapped(
             _host_ptr(x_host), _host_ptr(y_host), self.B, self.N, self.M,
             float(-1.0 if self.tau is None else self.tau), float(self.w1), float(self.w2),
             _host_ptr(self.loss), _host_ptr(self.fscore) if self.tau is not None else None,
             _host_ptr(self.grad_x), _host_ptr(self.grad_y), self.nchunks, _ptr(self.ws), self.ws.numel(), _stream(),
             ctypes.c_void_p(self.copy_stream.cuda_stream), self._evp))
-        return self.loss, self.fscore, self.grad_x, self.grad_y
 
 
 def _host_ptr(t):

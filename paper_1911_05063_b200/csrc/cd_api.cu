@@ -658,8 +658,11 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
         if (c == nchunks - 1 && last > 0) return B - last;
         return first + (int)((int64_t)(B - first - last) * (c - 1) / mid);
     };
-    // the staging buffers are free once the previous step on `stream` is done (never-recorded: no-op)
-    cudaError_t e = cudaStreamWaitEvent(cs, done, 0);
+    // fork: the copy stream starts after everything already queued on `stream` (so the staging
+    // buffers of the previous step are free); the same pattern makes the call capturable in a CUDA
+    // graph (the copy stream joins `stream` again below)
+    cudaError_t e = cudaEventRecord(done, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, done, 0);
     for (int c = 0; c < nchunks && e == cudaSuccess; ++c) {
         const int b0 = bound(c), b1 = bound(c + 1);
         e = cudaMemcpyAsync(x + (size_t)b0 * N * 3, x_host + (size_t)b0 * N * 3, (size_t)(b1 - b0) * N * 12,

@@ -505,8 +505,8 @@ def test_step_host_overlapped_equals_step_host(cd):
     X, Y = synth.shape_pair(8, 3000, 2500, config_index=29)
     xh, yh = cd.pinned_copy(X), cd.pinned_copy(Y)
     ref = cd.step_host(xh.numpy(), yh.numpy(), tau=0.01, want_grads=True)
-    for nchunks in (1, 2, 3, 8, None):          # None: the default (2 ranges, the first short)
-        st = cd.HostStepper(8, 3000, 2500, tau=0.01, nchunks=nchunks)
+    for nchunks, graph in ((1, False), (2, False), (3, False), (8, False), (None, False), (None, True), (3, True)):
+        st = cd.HostStepper(8, 3000, 2500, tau=0.01, nchunks=nchunks, graph=graph)
         for _ in range(2):                      # back-to-back steps reuse the staging buffers
             loss, fs, gx, gy = st.step(xh, yh)
         torch.cuda.synchronize()
@@ -521,6 +521,25 @@ def test_step_host_overlapped_equals_step_host(cd):
                                        h_scalar=np.float32(1.0 / (8 * 2500)))
     np.testing.assert_array_equal(ref["grad_x"].numpy(), gxr.astype(np.float32))
     np.testing.assert_array_equal(ref["grad_y"].numpy(), gyr.astype(np.float32))
+
+
+def test_host_stepper_graph_replay_sees_new_inputs(cd):
+    """A captured HostStepper replays the H2D copies: new data written into the same pinned buffers
+    gives that data's results (graph replay is not a cached output)."""
+    X1, Y1 = synth.shape_pair(4, 2000, 1500, config_index=33)
+    X2, Y2 = synth.shape_pair(4, 2000, 1500, config_index=34)
+    xh, yh = cd.pinned_copy(X1), cd.pinned_copy(Y1)
+    st = cd.HostStepper(4, 2000, 1500, tau=0.01, graph=True)
+    st.step(xh, yh)
+    torch.cuda.synchronize()
+    xh.numpy()[...] = X2
+    yh.numpy()[...] = Y2
+    loss, fs, gx, gy = st.step(xh, yh)
+    torch.cuda.synchronize()
+    ref = cd.step_host(cd.pinned_copy(X2).numpy(), cd.pinned_copy(Y2).numpy(), tau=0.01, want_grads=True)
+    assert float(loss[0]) == float(ref["loss"][0])
+    np.testing.assert_array_equal(gx.numpy(), ref["grad_x"].numpy())
+    np.testing.assert_array_equal(gy.numpy(), ref["grad_y"].numpy())
 
 
 def test_loss_backward_device_upstream(cd):
