@@ -304,23 +304,26 @@ CD_API cd_status cd_p2s_forward_pruned(const float* points, const float* verts, 
  * the clouds are copied in `nchunks` batch ranges on `copy_stream` (the first range half an equal
  * share, max(1, B / (2 nchunks)) elements, since only its copy is exposed; with nchunks >= 3 the
  * last range is as short, since only its backward and gradient copy are exposed; the rest split
- * equally).  On `stream`, range c's forward starts as soon as range c has landed
- * (cudaStreamWaitEvent) and range c's loss backward follows at once (the fills w/(B P) use the whole
- * batch's B and do not depend on the loss value; each batch element's gradients depend only on its
- * own clouds and indices), and range c's gradients go back on `copy_stream` while later ranges
- * compute; finalize and the loss / F-score copies follow on `stream`, which finally waits for the
- * gradient copies.  Results are identical to cd_step_host (per-batch outputs do not depend on the
+ * equally).  Range c computes on `stream` (c even) or `stream2` (c odd; stream2 == NULL: every range
+ * on `stream`), so a range's forward fills the SMs the previous range's last wave leaves idle; its
+ * forward starts as soon as range c has landed (cudaStreamWaitEvent) and its loss backward follows
+ * at once (the fills w/(B P) use the whole batch's B and do not depend on the loss value; each batch
+ * element's gradients depend only on its own clouds and indices), and range c's gradients go back
+ * on `copy_stream` while later ranges compute; `stream` then joins `stream2`, runs finalize and the
+ * loss / F-score copies, and finally waits for the gradient copies.  Results are identical to cd_step_host (per-batch outputs do not depend on the
  * chunking).  events: nchunks + 1 cudaEvent_t created by the caller (disable-timing events are
- * fine); the copy stream first waits for everything already queued on `stream` (events[nchunks]
- * recorded there: the previous step's staging buffers are free) and joins `stream` again before
- * the step ends, so the call can be captured in a CUDA graph and replayed (static pointers and
- * sizes).  nchunks in [1, B].  Workspace: cd_workspace_size(CD_OP_STEP).
+ * fine); the copy stream and stream2 first wait for everything already queued on `stream`
+ * (events[nchunks] recorded there: the previous step's staging buffers are free) and join `stream`
+ * again before the step ends, so the call can be captured in a CUDA graph and replayed (static
+ * pointers and sizes).  nchunks in [1, B].  Workspace: cd_workspace_size(CD_OP_STEP) (it holds a
+ * scratch region per compute stream).
  */
 CD_API cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int B, int N, int M,
                        float tau, float w1, float w2,
                        float* loss_host, float* fscore_host, float* grad_x_host, float* grad_y_host,
                        int nchunks, void* workspace, size_t workspace_bytes,
-                       cd_stream_t stream, cd_stream_t copy_stream, void* const* events);
+                       cd_stream_t stream, cd_stream_t copy_stream, cd_stream_t stream2,
+                       void* const* events);
 
 /* Workspace bytes needed by an operation for these sizes (full slices).  0 on invalid sizes. */
 CD_API size_t cd_workspace_size(int op, int B, int N, int M);

@@ -39,8 +39,8 @@ _SIGS = {
     "cd_backward": ([vp, vp, i32, i32, i32, vp, vp, vp, vp, f32, f32, i32, i32, i32, i32, vp, vp, vp, sz, vp], i32),
     "cd_loss_backward": ([vp, vp, i32, i32, i32, vp, vp, vp, f32, f32, i32, i32, i32, i32, vp, vp, vp, sz, vp], i32),
     "cd_step_host": ([vp, vp, i32, i32, i32, f32, f32, f32, vp, vp, vp, vp, vp, sz, vp], i32),
-    "cd_step_host_overlapped": ([vp, vp, i32, i32, i32, f32, f32, f32, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp],
-                                i32),
+    "cd_step_host_overlapped": ([vp, vp, i32, i32, i32, f32, f32, f32, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp,
+                                 vp], i32),
     "cd_workspace_size": ([i32, i32, i32, i32], sz),
     "cd_launch_count": ([i32, i32, i32, i32], i32),
     "cd_status_string": ([i32], ctypes.c_char_p),

@@ -302,7 +302,8 @@ class HostStepper:
     host tensors.  step() is asynchronous: call synchronize() (or read after the stream syncs)."""
 
     def __init__(self, B: int, N: int, M: int, tau: float | None = None, w1: float = 1.0, w2: float = 1.0,
-                 nchunks: int | None = None, device=None, want_grads: bool = True, graph: bool = False):
+                 nchunks: int | None = None, device=None, want_grads: bool = True, graph: bool = False,
+                 two_streams: bool = True):
         self.B, self.N, self.M, self.tau, self.w1, self.w2 = B, N, M, tau, w1, w2
         # measured (tools/time_e2e.py, gradients copied back, graph replay): c3 1 range 2.48 ms, 2: 2.30, 3: 2.25,
         # 4: 2.20, 8: 2.34; c2 1: 0.153, 2: 0.149, 4: 0.191 (each range's forward then under-fills the GPU)
@@ -315,6 +316,8 @@ class HostStepper:
             raise _lib.CdError(1, f"invalid sizes B={B} N={N} M={M}")
         self.ws = torch.empty(n, dtype=torch.uint8, device=self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
+        # odd batch ranges compute on a second stream (overlapping the previous range's tail wave)
+        self.stream2 = torch.cuda.Stream(device=self.device) if two_streams and self.nchunks > 1 else None
         self.events = [torch.cuda.Event() for _ in range(self.nchunks + 1)]
         for ev in self.events:       # materialise the cudaEvent handles
             ev.record()
@@ -357,7 +360,8 @@ class HostStepper:
             float(-1.0 if self.tau is None else self.tau), float(self.w1), float(self.w2),
             _host_ptr(self.loss), _host_ptr(self.fscore) if self.tau is not None else None,
             _host_ptr(self.grad_x), _host_ptr(self.grad_y), self.nchunks, _ptr(self.ws), self.ws.numel(), _stream(),
-            ctypes.c_void_p(self.copy_stream.cuda_stream), self._evp))
+            ctypes.c_void_p(self.copy_stream.cuda_stream),
+            ctypes.c_void_p(self.stream2.cuda_stream) if self.stream2 is not None else None, self._evp))
 
 
 def _host_ptr(t):

@@ -90,7 +90,7 @@ int fwd_launches(int B, int N, int M) {
 // cd_step_host workspace: staging of x, y, outputs of forward, partials/loss/fscore, grads, plus
 // the larger of the forward and backward workspaces.
 struct StepLayout {
-    size_t x, y, dxy, ixy, dyx, iyx, part, loss, fs, gx, gy, inner, inner_bytes, bytes;
+    size_t x, y, dxy, ixy, dyx, iyx, part, loss, fs, gx, gy, inner, inner2, inner_bytes, bytes;
 };
 StepLayout step_layout(int B, int N, int M) {
     StepLayout s;
@@ -115,6 +115,7 @@ StepLayout step_layout(int B, int N, int M) {
     cdk::plan_backward(bp, B, N, M, 0, N, 0, M);
     s.inner_bytes = std::max(forward_ws(B, N, M, 0, N, 0, M), bp.bytes);
     s.inner = take(s.inner_bytes);
+    s.inner2 = take(s.inner_bytes);   // cd_step_host_overlapped's second compute stream
     s.bytes = off;
     return s;
 }
@@ -614,7 +615,8 @@ cd_status cd_step_host(const float* x_host, const float* y_host, int B, int N, i
 cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int B, int N, int M, float tau, float w1,
                                   float w2, float* loss_host, float* fscore_host, float* grad_x_host,
                                   float* grad_y_host, int nchunks, void* workspace, size_t workspace_bytes,
-                                  cd_stream_t stream, cd_stream_t copy_stream, void* const* events) {
+                                  cd_stream_t stream, cd_stream_t copy_stream, cd_stream_t stream2,
+                                  void* const* events) {
     g_err.clear();
     cd_status s = check_sizes(B, N, M);
     if (s != CD_OK) return s;
@@ -631,6 +633,11 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
     if (s != CD_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaStream_t cs = static_cast<cudaStream_t>(copy_stream);
+    // ranges alternate between `stream` and `stream2` (when given): a range's fused forward then fills
+    // the SMs the previous range's last wave leaves idle (measured on c3's [4, 12, 12, 4] ranges:
+    // 2.124 ms on one stream, 2.047 ms alternating, 1.994 ms unchunked; tools/time_chunk_streams.py)
+    const bool two = stream2 != nullptr && nchunks > 1;
+    cudaStream_t sc2 = two ? static_cast<cudaStream_t>(stream2) : st;
     char* w = static_cast<char*>(workspace);
     float* x = reinterpret_cast<float*>(w + L.x);
     float* y = reinterpret_cast<float*>(w + L.y);
@@ -643,12 +650,10 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
     float* fs = reinterpret_cast<float*>(w + L.fs);
     float* gx = reinterpret_cast<float*>(w + L.gx);
     float* gy = reinterpret_cast<float*>(w + L.gy);
-    void* inner = w + L.inner;
     cudaEvent_t done = static_cast<cudaEvent_t>(events[nchunks]);
     // batch ranges: the first range is 1/CD_STEP_FIRST_DIV of an equal share (its copy is the only
-    // exposed one), the rest split equally
-    // with 3 or more ranges the last one is as short as the first (only its backward and gradient
-    // copy are exposed)
+    // exposed one); with 3 or more ranges the last one is as short as the first (only its backward
+    // and gradient copy are exposed); the rest split equally
     auto bound = [&](int c) -> int {
         if (c <= 0) return 0;
         if (c >= nchunks) return B;
@@ -658,11 +663,12 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
         if (c == nchunks - 1 && last > 0) return B - last;
         return first + (int)((int64_t)(B - first - last) * (c - 1) / mid);
     };
-    // fork: the copy stream starts after everything already queued on `stream` (so the staging
-    // buffers of the previous step are free); the same pattern makes the call capturable in a CUDA
-    // graph (the copy stream joins `stream` again below)
+    // fork: the copy stream (and the second compute stream) start after everything already queued on
+    // `stream` (so the staging buffers of the previous step are free); the same pattern makes the call
+    // capturable in a CUDA graph (both join `stream` again below)
     cudaError_t e = cudaEventRecord(done, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, done, 0);
+    if (e == cudaSuccess && two) e = cudaStreamWaitEvent(sc2, done, 0);
     for (int c = 0; c < nchunks && e == cudaSuccess; ++c) {
         const int b0 = bound(c), b1 = bound(c + 1);
         e = cudaMemcpyAsync(x + (size_t)b0 * N * 3, x_host + (size_t)b0 * N * 3, (size_t)(b1 - b0) * N * 12,
@@ -681,21 +687,23 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
     const float hs = loss_fill(w2, B, M);
     for (int c = 0; c < nchunks; ++c) {
         const int b0 = bound(c), b1 = bound(c + 1);
+        cudaStream_t sc = (c & 1) ? sc2 : st;
+        void* inner = w + ((c & 1) && two ? L.inner2 : L.inner);
         cudaEvent_t ev = static_cast<cudaEvent_t>(events[c]);
-        e = cudaStreamWaitEvent(st, ev, 0);
+        e = cudaStreamWaitEvent(sc, ev, 0);
         if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped wait");
         float* xr = x + (size_t)b0 * N * 3;
         float* yr = y + (size_t)b0 * M * 3;
         s = cd_forward(xr, yr, b1 - b0, N, M, 0, N, 0, M, dxy + (size_t)b0 * N, ixy + (size_t)b0 * N,
                        dyx + (size_t)b0 * M, iyx + (size_t)b0 * M, part + 4 * (size_t)b0, tau, inner, L.inner_bytes,
-                       stream);
+                       sc);
         if (s != CD_OK) return s;
         s = cd_backward(xr, yr, b1 - b0, N, M, ixy + (size_t)b0 * N, iyx + (size_t)b0 * M, nullptr, nullptr, gs, hs,
-                        0, N, 0, M, gx + (size_t)b0 * N * 3, gy + (size_t)b0 * M * 3, inner, L.inner_bytes, stream);
+                        0, N, 0, M, gx + (size_t)b0 * N * 3, gy + (size_t)b0 * M * 3, inner, L.inner_bytes, sc);
         if (s != CD_OK) return s;
         if (grad_x_host || grad_y_host) {
             // the wait above already captured ev's H2D record, so it can be re-recorded here
-            e = cudaEventRecord(ev, st);
+            e = cudaEventRecord(ev, sc);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev, 0);
             if (e == cudaSuccess && grad_x_host)
                 e = cudaMemcpyAsync(grad_x_host + (size_t)b0 * N * 3, gx + (size_t)b0 * N * 3,
@@ -706,13 +714,19 @@ cd_status cd_step_host_overlapped(const float* x_host, const float* y_host, int 
             if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped gradient D2H");
         }
     }
+    if (two) {
+        // join the second compute stream (all its waits above were enqueued before this re-record)
+        e = cudaEventRecord(static_cast<cudaEvent_t>(events[1]), sc2);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(events[1]), 0);
+        if (e != cudaSuccess) return cuda_status(e, "cd_step_host_overlapped join");
+    }
     s = cd_finalize(part, B, N, M, w1, w2, nullptr, loss, tau >= 0.f ? fs : nullptr, nullptr, nullptr, stream);
     if (s != CD_OK) return s;
     e = cudaMemcpyAsync(loss_host, loss, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess && fscore_host && tau >= 0.f)
         e = cudaMemcpyAsync(fscore_host, fs, (size_t)B * 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && (grad_x_host || grad_y_host)) {
-        // `stream` completes only after the gradient copies (the caller synchronises `stream`)
+    if (e == cudaSuccess) {
+        // `stream` completes only after the copy stream's work (the caller synchronises `stream`)
         e = cudaEventRecord(static_cast<cudaEvent_t>(events[0]), cs);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(events[0]), 0);
     }

@@ -505,8 +505,10 @@ def test_step_host_overlapped_equals_step_host(cd):
     X, Y = synth.shape_pair(8, 3000, 2500, config_index=29)
     xh, yh = cd.pinned_copy(X), cd.pinned_copy(Y)
     ref = cd.step_host(xh.numpy(), yh.numpy(), tau=0.01, want_grads=True)
-    for nchunks, graph in ((1, False), (2, False), (3, False), (8, False), (None, False), (None, True), (3, True)):
-        st = cd.HostStepper(8, 3000, 2500, tau=0.01, nchunks=nchunks, graph=graph)
+    for nchunks, graph, two in ((1, False, True), (2, False, True), (3, False, True), (8, False, True),
+                                (None, False, True), (None, True, True), (3, True, True), (4, False, False),
+                                (5, True, False)):
+        st = cd.HostStepper(8, 3000, 2500, tau=0.01, nchunks=nchunks, graph=graph, two_streams=two)
         for _ in range(2):                      # back-to-back steps reuse the staging buffers
             loss, fs, gx, gy = st.step(xh, yh)
         torch.cuda.synchronize()

@@ -15,7 +15,7 @@ txt = open(src).read()
 txt = txt[txt.index('"ID"'):]
 per = collections.OrderedDict()
 for r in csv.DictReader(io.StringIO(txt)):
-    k = (int(r["ID"]), r["Kernel Name"].split("(")[0])
+    k = (int(r["ID"]), r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", ""))
     per.setdefault(k, {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * \
         {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}.get(r["Metric Unit"], 1)
 # the backward = the last contiguous run of backward kernels (after the forward of run_backward.py)

@@ -11,9 +11,9 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 X, Y = synth.config_inputs(cfg)
 B, N, M = X.shape[0], X.shape[1], Y.shape[1]
 xh, yh = cd.pinned_copy(X), cd.pinned_copy(Y)
-for graph in (False, True):
+for graph, two in ((False, False), (True, False), (True, True)):
     for nc in [int(v) for v in sys.argv[2:]]:
-        st = cd.HostStepper(B, N, M, tau=synth.CONFIGS[cfg]["tau"], nchunks=min(nc, B), graph=graph)
+        st = cd.HostStepper(B, N, M, tau=synth.CONFIGS[cfg]["tau"], nchunks=min(nc, B), graph=graph, two_streams=two)
         for _ in range(20):
             st.step(xh, yh)
         torch.cuda.synchronize()
@@ -26,4 +26,5 @@ for graph in (False, True):
             b.record()
             torch.cuda.synchronize()
             best = min(best, a.elapsed_time(b) / 20)
-        print(cfg, "graph" if graph else "eager", "nchunks", nc, "e2e ms/step", best, flush=True)
+        print(cfg, "graph" if graph else "eager", "2 streams" if two else "1 stream", "nchunks", nc, "e2e ms/step", best,
+              flush=True)
