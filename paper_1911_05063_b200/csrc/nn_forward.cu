@@ -267,6 +267,7 @@ __device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
     }
     const int tdir = 1 - dir;
     const float4* T = a.pack[tdir] + (int64_t)b * a.ppad[tdir];
+    asm("" : "+l"(T));   // one opaque base pointer: each gather address is a single IMAD.WIDE.U32
     CD_CHECK(bb < 0 || (bb < a.npts[tdir] && bb % kBlockK == 0));
     // the warp's 32 rows staged in shared memory: (query, minimum) and block start, read back as
     // warp-wide broadcasts; targets past the cloud are the +inf padding (bb + 31 < ppad)
@@ -276,26 +277,25 @@ __device__ __forceinline__ void row_merge_block(const MergeArgs& a, int blk) {
     s_b[threadIdx.x] = bb;
     __syncwarp();
     const int wb = threadIdx.x & ~31;
-    const float4* Tl = T + lane;
-    for (int r0 = 0; r0 < 32; r0 += 4) {
-        int base[4];
-        float4 t[4];
+    unsigned myc = 32u;   // this lane's row: the lowest matching lane of its block (32: none)
+    constexpr int kRowsInFlight = 8;
+    for (int r0 = 0; r0 < 32; r0 += kRowsInFlight) {
+        int base[kRowsInFlight];
+        float4 t[kRowsInFlight];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kRowsInFlight; ++k) {
             base[k] = s_b[wb + r0 + k];
-            t[k] = Tl[max(base[k], 0)];
+            t[k] = __ldg(T + (unsigned)(max(base[k], 0) + lane));   // 32-bit index: one IMAD.WIDE per address
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kRowsInFlight; ++k) {
             const float4 q = s_q[wb + r0 + k];
             const float d = dist_rn(q.x, q.y, q.z, t[k].x, t[k].y, t[k].z);
             const unsigned c = __reduce_min_sync(0xffffffffu, d == q.w ? (unsigned)lane : 32u);
-            // the row's index goes back through its staging slot (a uniform value: one store)
-            if (lane == 0) s_b[wb + r0 + k] = (base[k] >= 0 && c < 32u) ? base[k] + (int)c : -1;
+            myc = lane == r0 + k ? c : myc;
         }
     }
-    __syncwarp();
-    const int idx = s_b[threadIdx.x];
+    const int idx = (bb >= 0 && myc < 32u) ? bb + (int)myc : -1;
     double v = 0.0;
     int h = 0;
     if (valid) {
@@ -353,6 +353,7 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
         }
     }
     const float4* X = a.xp + (int64_t)b * a.xpad;
+    asm("" : "+l"(X));   // one opaque base pointer (as in the row merge)
     static_assert(kR == 16, "the column resolve re-scans 16-row groups with half-warps");
     // the warp's 32 columns staged in shared memory: (target, minimum) and group start
     __shared__ float4 sc[kMergeThreads];
@@ -361,28 +362,27 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
     si[threadIdx.x] = i0;
     __syncwarp();
     const int wb = threadIdx.x & ~31;
-    for (int r0 = 0; r0 < 32; r0 += 4) {   // two steps of two columns (one per half-warp) in flight
-        int g[2];
-        float4 q[2];
+    unsigned myc = 16u;   // this lane's column: the lowest matching row of its group (16: none)
+    constexpr int kStepsInFlight = 4;   // steps of two columns (one per half-warp) in flight
+    for (int r0 = 0; r0 < 32; r0 += 2 * kStepsInFlight) {
+        int g[kStepsInFlight];
+        float4 q[kStepsInFlight];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kStepsInFlight; ++k) {
             g[k] = si[wb + r0 + 2 * k + half];
-            q[k] = X[min(max(g[k], 0) + hl, a.q1 - 1)];   // a partial last group re-reads row q1 - 1
+            q[k] = __ldg(X + (unsigned)min(max(g[k], 0) + hl, a.q1 - 1));   // past the slice end: row q1 - 1
         }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kStepsInFlight; ++k) {
             const float4 c = sc[wb + r0 + 2 * k + half];
             const float d = dist_rn(q[k].x, q[k].y, q[k].z, c.x, c.y, c.z);  // same operand order as the kernel
-            const unsigned v = (g[k] >= 0 && g[k] + hl < a.q1 && d == c.w) ? (unsigned)hl : 16u;
+            const unsigned v = (g[k] + hl < a.q1 && d == c.w) ? (unsigned)hl : 16u;
             const unsigned c0 = __reduce_min_sync(0xffffffffu, half == 0 ? v : 16u);
             const unsigned c1 = __reduce_min_sync(0xffffffffu, half == 1 ? v : 16u);
-            // results back through the staging slots (lane 0 / lane 16 own the two columns' slots)
-            const unsigned cm = half == 0 ? c0 : c1;
-            if (hl == 0) si[wb + r0 + 2 * k + half] = cm < 16u ? g[k] + (int)cm : -1;
+            myc = lane == r0 + 2 * k ? c0 : (lane == r0 + 2 * k + 1 ? c1 : myc);
         }
     }
-    __syncwarp();
-    int idx = si[threadIdx.x];
+    int idx = (i0 >= 0 && myc < 16u) ? i0 + (int)myc : -1;
     if (idx < 0) m = INFINITY;  // no finite candidate, or every distance was NaN
     double v = 0.0;
     int h = 0;
