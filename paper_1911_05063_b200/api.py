@@ -340,6 +340,10 @@ class HostStepper:
             (12 * self.B * (self.N + self.M) if self.grad_x is not None else 0)
 
     def step(self, x_host: torch.Tensor, y_host: torch.Tensor):
+        with torch.cuda.device(self.device):   # the stepper's workspace, streams and events live there
+            return self._step(x_host, y_host)
+
+    def _step(self, x_host, y_host):
         if self.graph:
             key = (x_host.data_ptr(), y_host.data_ptr())
             if self._graph is None or self._graph_key != key:
