@@ -277,10 +277,16 @@ def step_host(x_host: np.ndarray, y_host: np.ndarray, tau: float | None = None, 
               want_grads: bool = True, device=None, out=None):
     """cd_step_host: one whole step through HOST buffers (H2D of the clouds, forward, finalize,
     loss backward, D2H of loss / F-score / gradients).  Host arrays should be pinned (see
-    pinned_like).  Synchronises the current stream before returning (loss, fscore, grad_x, grad_y)."""
+    pinned_copy / pinned_empty).  Synchronises the device's current stream before returning
+    (loss, fscore, grad_x, grad_y)."""
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(device):
+        return _step_host(x_host, y_host, tau, w1, w2, want_grads, device, out)
+
+
+def _step_host(x_host, y_host, tau, w1, w2, want_grads, device, out):
     B, N, _ = x_host.shape
     M = y_host.shape[1]
-    device = device or torch.device("cuda", torch.cuda.current_device())
     ws = workspace(_lib.CD_OP_STEP, B, N, M, device)
     if out is None:
         out = dict(loss=pinned_empty((1,)), fscore=pinned_empty((B,)),
@@ -297,9 +303,11 @@ def step_host(x_host: np.ndarray, y_host: np.ndarray, tau: float | None = None, 
 
 
 class HostStepper:
-    """End-to-end steps from pinned host clouds with the H2D copies overlapped with the compute
-    (cd_step_host_overlapped).  Owns a copy stream and nchunks + 1 events; outputs land in pinned
-    host tensors.  step() is asynchronous: call synchronize() (or read after the stream syncs)."""
+    """End-to-end steps from pinned host clouds with the host<->device copies overlapped with the
+    compute (cd_step_host_overlapped).  Owns a private workspace, a copy stream, a second compute
+    stream (two_streams) and nchunks + 1 events on its device; outputs (loss, F-score, gradients)
+    land in pinned host tensors.  step() is asynchronous on the device's current stream: synchronise
+    it before reading the outputs.  graph=True captures the call once and replays it."""
 
     def __init__(self, B: int, N: int, M: int, tau: float | None = None, w1: float = 1.0, w2: float = 1.0,
                  nchunks: int | None = None, device=None, want_grads: bool = True, graph: bool = False,
@@ -309,7 +317,17 @@ class HostStepper:
         # 4: 2.20, 8: 2.34; c2 1: 0.153, 2: 0.149, 4: 0.191 (each range's forward then under-fills the GPU)
         # -> up to 4 ranges of at least 2^31 distance evaluations each
         self.nchunks = nchunks or max(1, min(4, B, (B * N * M) >> 31))
-        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(self.device):
+            self._init_device_state(B, N, M, want_grads, two_streams)
+        # graph=True: the first step() with given host buffers is captured (the C call forks and joins
+        # its copy stream, so it is capturable) and later steps replay it — every replay still copies
+        # that step's inputs in and its results out; only the host-side launch work is saved
+        self.graph = graph
+        self._graph = None
+        self._graph_key = None
+
+    def _init_device_state(self, B, N, M, want_grads, two_streams):
         # a private workspace: its staging area is written by this stepper's copy stream
         n = int(_lib.load().cd_workspace_size(_lib.CD_OP_STEP, B, N, M))
         if n == 0:
@@ -327,12 +345,6 @@ class HostStepper:
         self.fscore = pinned_empty((B,))
         self.grad_x = pinned_empty((B, N, 3)) if want_grads else None
         self.grad_y = pinned_empty((B, M, 3)) if want_grads else None
-        # graph=True: the first step() with given host buffers is captured (the C call forks and joins
-        # its copy stream, so it is capturable) and later steps replay it — every replay still copies
-        # that step's inputs in and its results out; only the host-side launch work is saved
-        self.graph = graph
-        self._graph = None
-        self._graph_key = None
 
     def d2h_bytes(self) -> int:
         """Bytes copied device -> host per step (loss, F-score, gradients)."""
