@@ -396,11 +396,17 @@ struct GradArgs {
     float* grad_y;
 };
 
-// acc += (2 w) * (p - s), fp64, explicit roundings in the oracle's order (no FMA contraction).
-__device__ __forceinline__ void acc_term(double acc[3], const float* p, const float* s, double w) {
+// acc += (2 w) * (p - s), fp64, explicit roundings in the oracle's order (no FMA contraction); p is
+// the output point, promoted to fp64 once (exactly) by the caller and kept in registers.
+__device__ __forceinline__ void acc_term(double acc[3], const double p[3], const float* s, double w) {
     const double w2 = __dmul_rn(2.0, w);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c])));
+    for (int c = 0; c < 3; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(w2, __dsub_rn(p[c], (double)s[c])));
+}
+__device__ __forceinline__ void load_point64(const float* p, double out[3]) {
+    out[0] = (double)p[0];
+    out[1] = (double)p[1];
+    out[2] = (double)p[2];
 }
 
 // Segment-local sort (small clouds: max(N, M) <= kSegMax).  The edges of one (direction, batch
@@ -536,7 +542,8 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga,
     const int t0 = dir == 0 ? ga.r0 : ga.q0, t1 = dir == 0 ? ga.r1 : ga.q1;
     float* out = dir == 0 ? ga.grad_y + (int64_t)b * (ga.r1 - ga.r0) * 3 : ga.grad_x + (int64_t)b * (ga.q1 - ga.q0) * 3;
     for (int t = max(K0, t0) + threadIdx.x; t < min(K1, t1); t += kSegThreads) {
-        const float* pt = tgt + (int64_t)t * 3;
+        double pt[3];
+        load_point64(tgt + (int64_t)t * 3, pt);
         const int part = min(max(pidx[t], 0), S - 1);
         const double wtt = wt ? (double)wt[t] : (double)wt_s;
         double acc[3];
@@ -544,7 +551,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga,
             const float* ps = src + (int64_t)part * 3;
             const double w2 = __dmul_rn(2.0, wtt);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn((double)pt[c], (double)ps[c]));
+            for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn(pt[c], (double)ps[c]));
         }
         const int e0 = offs[t - K0], e1 = t + 1 < K1 ? (int)offs[t + 1 - K0] : n;
         CD_CHECK(e0 <= e1 && e1 <= n);
@@ -589,7 +596,8 @@ __global__ void __launch_bounds__(256, CD_GRAD_MINB) grad_kernel(GradArgs a) {
         if (u < sq) {
             const int i = a.q0 + u;
             const int64_t xi = b * a.N + i;
-            const float* p = a.x + xi * 3;
+            double p[3];
+            load_point64(a.x + xi * 3, p);
             const int part = min(max(a.idx_xy[xi], 0), a.M - 1);
             const double gi = a.g ? (double)a.g[xi] : (double)a.g_scalar;
             // own term, then: every term has the form 2 w (p - s) with p = this point
@@ -598,7 +606,7 @@ __global__ void __launch_bounds__(256, CD_GRAD_MINB) grad_kernel(GradArgs a) {
                 const float* s = a.y + (b * a.M + part) * 3;
                 const double w2 = __dmul_rn(2.0, gi);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) own[c] = __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c]));
+                for (int c = 0; c < 3; ++c) own[c] = __dmul_rn(w2, __dsub_rn(p[c], (double)s[c]));
                 acc[0] = own[0];
                 acc[1] = own[1];
                 acc[2] = own[2];
@@ -619,14 +627,15 @@ __global__ void __launch_bounds__(256, CD_GRAD_MINB) grad_kernel(GradArgs a) {
         } else {
             const int j = a.r0 + (u - sq);
             const int64_t yj = b * a.M + j;
-            const float* p = a.y + yj * 3;
+            double p[3];
+            load_point64(a.y + yj * 3, p);
             const int part = min(max(a.idx_yx[yj], 0), a.N - 1);
             const double hj = a.h ? (double)a.h[yj] : (double)a.h_scalar;
             {
                 const float* s = a.x + (b * a.N + part) * 3;
                 const double w2 = __dmul_rn(2.0, hj);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn((double)p[c], (double)s[c]));
+                for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn(p[c], (double)s[c]));
             }
             const int64_t key = b * a.M + j;
             const uint32_t e0 = a.off[key], e1 = a.off[key + 1];
