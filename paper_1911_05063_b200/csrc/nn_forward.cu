@@ -43,32 +43,25 @@ struct PackArgs {
     int64_t nrowkey;
 };
 
+// grid (x: point blocks of one row, y: batch element, z: cloud) — no per-element division; the key
+// resets are spread over the whole grid
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
     pdl_wait();
-    const int64_t n0 = (int64_t)a.B * a.ppad[0];
-    const int64_t total = n0 + (int64_t)a.B * a.ppad[1];
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int c = e < n0 ? 0 : 1;
-        const int64_t f = c == 0 ? e : e - n0;
-        const int64_t b = f / a.ppad[c];
-        const int i = (int)(f - b * a.ppad[c]);
-        float4 v;
-        if (i < a.npts[c]) {
-            const float* s = a.src[c] + (b * a.npts[c] + i) * 3;
-            v = make_float4(__ldg(s), __ldg(s + 1), __ldg(s + 2), 0.f);
-        } else {
-            // padding targets: +inf coordinates give d = +inf, never selected by min / strict <
-            v = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
-        }
-        a.dst[c][f] = v;
+    const int c = blockIdx.z, b = blockIdx.y;
+    const int n = a.npts[c], pad = a.ppad[c];
+    const float* __restrict__ src = a.src[c] + (int64_t)b * n * 3;
+    float4* __restrict__ dst = a.dst[c] + (int64_t)b * pad;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < pad; i += gridDim.x * blockDim.x) {
+        // padding targets: +inf coordinates give d = +inf, never selected by min / strict <
+        float4 v = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+        if (i < n) v = make_float4(__ldg(src + 3 * i), __ldg(src + 3 * i + 1), __ldg(src + 3 * i + 2), 0.f);
+        dst[i] = v;
     }
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.ncolkey;
-         e += (int64_t)gridDim.x * blockDim.x)
-        a.colkey[e] = kColKeyEmpty;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.nrowkey;
-         e += (int64_t)gridDim.x * blockDim.x)
-        a.rowkey[e] = kColKeyEmpty;
+    const int64_t nthreads = (int64_t)gridDim.x * gridDim.y * gridDim.z * blockDim.x;
+    const int64_t tid = (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x +
+                        threadIdx.x;
+    for (int64_t e = tid; e < a.ncolkey; e += nthreads) a.colkey[e] = kColKeyEmpty;
+    for (int64_t e = tid; e < a.nrowkey; e += nthreads) a.rowkey[e] = kColKeyEmpty;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -727,9 +720,11 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
         a.ncolkey = init ? (int64_t)p.B * p.npts[1] : 0;
         a.rowkey = rowkey;
         a.nrowkey = p.mode == kFusedCols ? 0 : p.slice_total;
-        const int64_t total = (int64_t)p.B * (p.ppad[0] + p.ppad[1]);
-        const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)device_sm_count() * 16);
-        launch_pdl(pack_kernel, dim3(grid), dim3(256), 0, st, a);
+        // one row (cloud, batch element) per (y, z); enough x blocks for ~16 CTAs per SM overall
+        const int pmax = std::max(p.ppad[0], p.ppad[1]);
+        const int64_t want = (int64_t)device_sm_count() * 16 / std::max<int64_t>(1, 2 * (int64_t)p.B);
+        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((pmax + 255) / 256, want));
+        launch_pdl(pack_kernel, dim3(gx, p.B, 2), dim3(256), 0, st, a);
     }
     if (p.mode == kUnfused) {
         const int gx = p.qtiles[0] * p.splits[0] + p.qtiles[1] * p.splits[1];

@@ -341,11 +341,11 @@ cudaError_t launch_p2s(const float* points, const float* verts, const int* faces
     double* chunk = reinterpret_cast<double*>(w + p.off_chunk);
     {
         P2sPackArgs a{points, pts, N, p.Ppad, B};
-        p2s_pack_kernel<<<std::min(cdiv((int64_t)B * p.Ppad, 256), 148 * 16), 256, 0, st>>>(a);
+        p2s_pack_kernel<<<std::min(cdiv((int64_t)B * p.Ppad, 256), current_sm_count() * 16), 256, 0, st>>>(a);
     }
     {
         PrepArgs a{verts, faces, B, Nv, Nf, p.Nfpad, fd};
-        p2s_prep_kernel<<<std::min(cdiv((int64_t)B * p.Nfpad, 256), 148 * 16), 256, 0, st>>>(a);
+        p2s_prep_kernel<<<std::min(cdiv((int64_t)B * p.Nfpad, 256), current_sm_count() * 16), 256, 0, st>>>(a);
     }
     {
         P2sArgs a;

@@ -806,12 +806,7 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
     plan_ps(p, B, N, Nv, Nf);
     if (!p.supported) return cudaErrorInvalidValue;
     char* w = static_cast<char*>(ws);
-    int sms = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = current_sm_count();
     float* bbox = reinterpret_cast<float*>(w + p.off_bbox);
     launch_bbox(points, N, verts, Nv, B, bbox, st);
     uint32_t* keys[2] = {reinterpret_cast<uint32_t*>(w + p.off_keys[0]), reinterpret_cast<uint32_t*>(w + p.off_keys[1])};
