@@ -139,6 +139,16 @@ def test_large_configs_sampled(cd, name, nrows):
     np.testing.assert_array_equal(gy.cpu().numpy(), gyr.astype(np.float32))
 
 
+def test_c4_every_row_fp32_mirror(cd):
+    """c4 (B=8, N=M=100,000) on EVERY row of both directions against the fp32 mirror of DESIGN.md
+    §4.2's op order (oracle/, written from the formula): distance bits and indices identical, ties
+    included (the mirror takes the lowest index in the same fp32 arithmetic)."""
+    X, Y = synth.config_inputs("c4")
+    x, y, (d_xy, i_xy, d_yx, i_yx, part) = _run(cd, X, Y, tau=0.01)
+    gate_mirror(X, Y, d_xy, i_xy)
+    gate_mirror(Y, X, d_yx, i_yx)
+
+
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_large_configs_all_points_kdtree(cd, name):
     """Every point of c4 / c5 (not a sample): the GPU minimum equals the exact nearest-neighbour
