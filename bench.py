@@ -772,7 +772,7 @@ def main():
     roofline = {
         "bound": "alu", "kernel": "nn_fused_kernel", "unit": "Tops/s (FP32-pipe lane ops: FADD/FMUL/FFMA = 1)",
         "achieved": achieved_ops, "peak": peak_ops, "frac": achieved_ops / peak_ops,
-        "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz (max SM clock); DESIGN.md §7",
+        "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz (max SM clock); DESIGN.md §4.3",
         "algorithmic": (f"{FP32_OPS_PER_PAIR} FP32-pipe ops per distance evaluation x {evals_fwd_launch} evaluations "
                         "per launch (B*N*M: each distance serves both directions)"),
         "kernel_ms": fwd_kernel_ms, "kernel_share_of_step": fwd_kernel_ms / ms_per_step,
