@@ -363,7 +363,7 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
 #pragma unroll
         for (int k = 0; k < kStepsInFlight; ++k) {
             g[k] = si[wb + r0 + 2 * k + half];
-            q[k] = __ldg(X + (unsigned)min(max(g[k], 0) + hl, a.q1 - 1));   // past the slice end: row q1 - 1
+            q[k] = __ldg(X + (unsigned)min(max(g[k], 0) + hl, max(a.q1 - 1, 0)));   // past the slice end: row q1 - 1
         }
 #pragma unroll
         for (int k = 0; k < kStepsInFlight; ++k) {
