@@ -417,6 +417,30 @@ __device__ __forceinline__ void load_point64(const float* p, double out[3]) {
 // counts of a pass are integer shared-memory adds made while loading / while placing the previous
 // pass), then the sorted sources and the segment's key offsets (gap fill) go to global memory.
 // Replaces keys_hist + the global passes + offsets_kernel: 2 launches per backward, not 3 passes + 2.
+#ifndef CD_SEG_COUNTING
+#define CD_SEG_COUNTING 1   // counting sort for part key ranges that fit the counter words (see below)
+#endif
+constexpr int kRunMax = 32;   // longest key run the counting mode's insertion sort handles
+
+
+// Exclusive scan of one value per thread over the kSegThreads threads of the CTA (warp shuffles +
+// the warp totals in `wtot[kSegWarps]`); contains the barriers it needs.
+__device__ __forceinline__ uint32_t seg_block_exclusive_scan(uint32_t v, uint32_t* wtot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    __syncthreads();   // wtot may still be read by an earlier phase
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wtot[w];
+    return before + incl - v;
+}
+
 __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga, int nmax, int lparts) {
     pdl_wait();
     const int32_t* __restrict__ idx_xy = ga.idx_xy;
@@ -485,6 +509,11 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga,
     int lspan = 5;   // rounds per warp R = span / 32, a power of two: warp w owns [w*span, (w+1)*span)
     while (kSegWarps << lspan < n) ++lspan;
     const int R = 1 << (lspan - 5);
+    // counting mode (the part's key range fits the 2 x 32 x 128 counter words): a counting sort
+    // instead of the LSD passes — per-key counts, an exclusive scan, placement by integer shared-memory
+    // atomics (unordered inside a key) and each key's run then sorted by source index, which restores
+    // the stable order exactly; a part with a run longer than kRunMax falls back to the LSD passes
+    const bool counting = CD_SEG_COUNTING && K1 - K0 <= 2 * kSegWarps * kSegD;
     // phase B: ordered compaction of the part's edges + the first pass's per-warp digit counts
     // (integer shared-memory adds: order-free)
     {
@@ -506,24 +535,83 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga,
                     CD_CHECK(pos < (uint32_t)n && (pos >> lspan) < (uint32_t)kSegWarps);
                     kA[pos] = (uint16_t)k[u];
                     vA[pos] = (uint16_t)(e0 + u * 32 + lane);
-                    if (passes > 0) atomicAdd(&wcur[(pos >> lspan) * D + (k[u] & (D - 1))], 1u);
+                    if (counting)
+                        atomicAdd(&wcur[k[u] - K0], 1u);   // per-key counts (integer adds: order-free)
+                    else if (passes > 0)
+                        atomicAdd(&wcur[(pos >> lspan) * D + (k[u] & (D - 1))], 1u);
                 }
                 run += __popc(m);
             }
         }
     }
-    seg_lsd_passes(kA, vA, kB, vB, wcur, wnext, dstart, n, passes, db, lspan, R);
-    __syncthreads();
-    // key offsets of this part in shared memory (the free key buffer): offs[k - K0] = first sorted
-    // position with key >= k for k in [K0, K1) (gap fill, disjoint writes); key K1 - 1's run ends at n
-    uint16_t* offs = kB;
-    for (int p = threadIdx.x; p <= n; p += kSegThreads) {
-        const int lo = p == 0 ? K0 : (int)kA[p - 1] + 1;
-        const int hi = min(p == n ? K1 : (int)kA[p], K1 - 1);
-        CD_CHECK(lo >= K0 && hi < K1);
-        for (int k = lo; k <= hi; ++k) offs[k - K0] = (uint16_t)p;
+    bool counted = false;   // the counting sort produced the grouped sources (in vB, runs from wcur)
+    if (counting) {
+        __syncthreads();
+        const int KK = K1 - K0;
+        uint32_t* cnt = wcur;   // [KK]: counts, then exclusive offsets, then (after placement) run ends
+        const int per = (KK + kSegThreads - 1) / kSegThreads;
+        const int c0 = min(threadIdx.x * per, KK), c1 = min(c0 + per, KK);
+        uint32_t loc = 0;
+        bool longrun = false;
+        for (int i = c0; i < c1; ++i) {
+            loc += cnt[i];
+            longrun |= cnt[i] > (uint32_t)kRunMax;
+        }
+        const uint32_t excl = seg_block_exclusive_scan(loc, &wsum[0][0]);
+        if (!__syncthreads_or(longrun)) {
+            uint32_t run = excl;
+            for (int i = c0; i < c1; ++i) {
+                const uint32_t c = cnt[i];
+                cnt[i] = run;
+                run += c;
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < n; e += kSegThreads) {
+                const uint32_t pos = atomicAdd(&cnt[kA[e] - K0], 1u);   // cnt[k] ends as the end of k's run
+                CD_CHECK(pos < (uint32_t)n);
+                vB[pos] = vA[e];
+            }
+            __syncthreads();
+            for (int kk = threadIdx.x; kk < KK; kk += kSegThreads) {   // runs of <= kRunMax: insertion sort
+                const int r0 = kk == 0 ? 0 : (int)cnt[kk - 1], r1 = (int)cnt[kk];
+                for (int i = r0 + 1; i < r1; ++i) {
+                    const uint16_t v = vB[i];
+                    int j = i - 1;
+                    while (j >= r0 && vB[j] > v) {
+                        vB[j + 1] = vB[j];
+                        --j;
+                    }
+                    vB[j + 1] = v;
+                }
+            }
+            __syncthreads();
+            counted = true;
+        } else {
+            // fallback: the first LSD pass's per-warp digit counts from the compacted keys
+            for (int i = threadIdx.x; i < 2 * kSegWarps * kSegD; i += kSegThreads) wcur[i] = 0;
+            __syncthreads();
+            if (passes > 0)
+                for (int e = threadIdx.x; e < n; e += kSegThreads)
+                    atomicAdd(&wcur[(e >> lspan) * D + (kA[e] & (D - 1))], 1u);
+        }
     }
-    __syncthreads();
+    uint16_t* offs = kB;
+    if (!counted) {
+        seg_lsd_passes(kA, vA, kB, vB, wcur, wnext, dstart, n, passes, db, lspan, R);
+        __syncthreads();
+        // key offsets of this part in shared memory (the free key buffer): offs[k - K0] = first sorted
+        // position with key >= k for k in [K0, K1) (gap fill, disjoint writes); key K1 - 1's run ends at n
+        offs = kB;
+        for (int p = threadIdx.x; p <= n; p += kSegThreads) {
+            const int lo = p == 0 ? K0 : (int)kA[p - 1] + 1;
+            const int hi = min(p == n ? K1 : (int)kA[p], K1 - 1);
+            CD_CHECK(lo >= K0 && hi < K1);
+            for (int k = lo; k <= hi; ++k) offs[k - K0] = (uint16_t)p;
+        }
+        __syncthreads();
+    }
+    const uint16_t* srt = counted ? vB : vA;           // sources grouped by key, ascending inside a key
+    const uint32_t* cend = wcur;                       // counting: end of key k's run at cend[k - K0]
     // the gradients of this part's targets, as grad_kernel computes them: own term 2 w_t (p - partner)
     // first, then the sources in ascending index (the stable sort's order), fp64 with explicit .rn ops
     float gs = ga.g_scalar, hs = ga.h_scalar;
@@ -541,22 +629,29 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga,
     const float wt_s = dir == 0 ? hs : gs, wsrc_s = dir == 0 ? gs : hs;
     const int t0 = dir == 0 ? ga.r0 : ga.q0, t1 = dir == 0 ? ga.r1 : ga.q1;
     float* out = dir == 0 ? ga.grad_y + (int64_t)b * (ga.r1 - ga.r0) * 3 : ga.grad_x + (int64_t)b * (ga.q1 - ga.q0) * 3;
-    for (int t = max(K0, t0) + threadIdx.x; t < min(K1, t1); t += kSegThreads) {
+    const int tlo = max(K0, t0), thi = min(K1, t1);
+    for (int t = tlo + threadIdx.x; t < thi; t += kSegThreads) {
         double pt[3];
         load_point64(tgt + (int64_t)t * 3, pt);
-        const int part = min(max(pidx[t], 0), S - 1);
         const double wtt = wt ? (double)wt[t] : (double)wt_s;
         double acc[3];
         {
-            const float* ps = src + (int64_t)part * 3;
+            const float* ps = src + (int64_t)min(max(pidx[t], 0), S - 1) * 3;
             const double w2 = __dmul_rn(2.0, wtt);
 #pragma unroll
             for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn(pt[c], (double)ps[c]));
         }
-        const int e0 = offs[t - K0], e1 = t + 1 < K1 ? (int)offs[t + 1 - K0] : n;
+        int e0, e1;
+        if (counted) {
+            e0 = t == K0 ? 0 : (int)cend[t - K0 - 1];
+            e1 = (int)cend[t - K0];
+        } else {
+            e0 = offs[t - K0];
+            e1 = t + 1 < K1 ? (int)offs[t + 1 - K0] : n;
+        }
         CD_CHECK(e0 <= e1 && e1 <= n);
         for (int e = e0; e < e1; ++e) {
-            const int sidx = vA[e];
+            const int sidx = srt[e];
             acc_term(acc, pt, src + (int64_t)sidx * 3, wsrc ? (double)wsrc[sidx] : (double)wsrc_s);
         }
         float* o = out + (int64_t)(t - t0) * 3;
