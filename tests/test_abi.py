@@ -30,6 +30,19 @@ def test_exports_every_declared_symbol(lib):
         assert hasattr(lib, s)
 
 
+def test_binding_declares_every_entry_point():
+    """The ctypes binding (argument marshalling) carries a signature for every declared function, with
+    the header's argument count, so a changed C signature cannot be called with stale arguments."""
+    import re
+    with open(_lib.HEADER) as f:
+        text = re.sub(r"/\*.*?\*/", "", f.read(), flags=re.S)
+    for name in _lib.declared_symbols():
+        assert name in _lib._SIGS, name
+        m = re.search(r"\b" + name + r"\s*\(([^)]*)\)", text)
+        params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
+        assert len(_lib._SIGS[name][0]) == len(params), (name, len(_lib._SIGS[name][0]), len(params))
+
+
 def test_only_cd_symbols_exported():
     out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
     names = [line.split()[-1] for line in out.splitlines() if " T " in line]
