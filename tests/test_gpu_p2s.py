@@ -69,6 +69,15 @@ def _gate(P, V, F, out, rows=None, min_clear=0.3):
     bb = rows // N
     corners = V[bb[:, None], F[fg]]                       # (n, 3, 3)
     np.testing.assert_allclose(cg, (lg[:, :, None] * corners).sum(1), atol=1e-5 * R)
+    # and equal to the oracle's own closest point / barycentrics (region decomposition, fp64) on the
+    # same face: the kernels' plane-or-edges evaluation differs only by fp64 rounding, then the fp32
+    # store (2^-24 relative); barycentrics to fp32 rounding of values in [0, 1]
+    np.testing.assert_allclose(cg[clear], c1[clear], rtol=0, atol=2.0 ** -22 * R)
+    # (a zero-area face's barycentrics are not unique: compare them on proper faces only)
+    c64 = corners.astype(np.float64)
+    area2 = np.linalg.norm(np.cross(c64[:, 1] - c64[:, 0], c64[:, 2] - c64[:, 0]), axis=1)
+    proper = clear & (area2 > 1e-6 * R * R)
+    np.testing.assert_allclose(lg[proper], l1[proper], rtol=0, atol=2.0 ** -20)
     return d1, f1, clear
 
 
