@@ -67,9 +67,18 @@ cudaError_t launch_fused_rows(const FwdPlan& p, const float4* xp, const float4* 
 
 
 // Exact pruned forward (nn_pruned.cu, NEXT-2): Hilbert-sorted tiles + box lower-bound culling.
+// A sequence sorted as independent segments: nA segments of szA elements, then nB of szB.
+struct SegSpec {
+    int nA;
+    int64_t szA;
+    int nB;
+    int64_t szB;
+};
+
 struct PrunedPlan {
     int B, npts[2], ppad[2], qtiles[2], ttiles[2];
-    int bbits, kbits, nbits;
+    int kbits, nbits;          // nbits = 3*kbits: segment-local Hilbert keys
+    SegSpec segs;              // the 2B (cloud, batch) segments the radix passes sort on their own
     int64_t L, cand_off[2];
     int nchunks[2];
     int64_t chunk_off[2];
@@ -112,7 +121,7 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
                               float* d, int* face, float* closest, float* bary, float* per_batch, float* loss,
                               void* ws, cudaStream_t st);
 // Per-(cloud, batch) sample bounding boxes [2][B][6] (nn_pruned.cu).
-int hilbert_bits(int bbits, int nmax);
+int hilbert_bits(int nmax);
 void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, float* bbox, cudaStream_t st);
 
 // Stats of given distances (for cd_fscore): per-chunk sums + hits, then partials.
@@ -123,14 +132,6 @@ constexpr int kFscoreLaunches = 3;
 
 cudaError_t launch_finalize(const double* partials, int B, int N, int M, float w1, float w2, float* cd,
                             float* loss, float* fscore, float* precision, float* recall, cudaStream_t st);
-
-// A sequence sorted as independent segments: nA segments of szA elements, then nB of szB.
-struct SegSpec {
-    int nA;
-    int64_t szA;
-    int nB;
-    int64_t szB;
-};
 
 // Backward.
 struct BwdPlan {
@@ -155,6 +156,13 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits,
 int radix_digit_bits(int64_t L, int nbits);
 size_t radix_sort_counts_words(int64_t L, int nbits);
 int radix_sort_launches(int64_t L, int nbits);
+// Segmented form: every segment of `sp` sorted on its own by the low `nbits` bits of segment-local
+// keys; narrow = true picks the digit width by the measured pass-cost model (nn_backward.cu).
+int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], const SegSpec& sp, int nbits, uint32_t* counts,
+                     uint32_t* totals, cudaStream_t st, bool first_hist_done, bool narrow);
+size_t radix_sort_counts_words(const SegSpec& sp, int nbits, bool narrow);
+size_t radix_sort_totals_words(const SegSpec& sp, int nbits, bool narrow);
+int radix_sort_launches(const SegSpec& sp, int nbits, bool narrow);
 constexpr int kSortTotalsWords = 1 << 12;   // >= 2^kMaxDigitBits
 
 // thread-local measurement hook (cd_set_profile_events)

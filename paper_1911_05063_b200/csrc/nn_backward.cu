@@ -839,6 +839,7 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t L, int nbits,
 }
 
 int radix_sort_launches(int64_t L, int nbits) { return 3 * radix_plan(one_segment(L), nbits).npasses; }
+int radix_sort_launches(const SegSpec& sp, int nbits, bool narrow) { return 3 * radix_plan(sp, nbits, narrow).npasses; }
 
 int radix_digit_bits(int64_t L, int nbits) { return radix_plan(one_segment(L), nbits).digit_bits; }
 

@@ -4,8 +4,8 @@
 // every pair that could matter), far fewer pairs on large clouds:
 //   bbox_kernel        per (cloud, batch) bounding box of a fixed-stride sample (min/max: order-free;
 //                      only the Hilbert quantisation depends on it).
-//   hilbert_kernel      key = (cloud | batch | 3k-bit Hilbert index) per point, value = row.
-//   radix sort         (nn_backward.cu) -> every (cloud, batch) segment in Hilbert order.
+//   hilbert_kernel      key = 3k-bit Hilbert index per point, value = row.
+//   radix sort         (nn_backward.cu) every (cloud, batch) segment on its own -> Hilbert order.
 //   gather_kernel      sorted packed float4 clouds + permutation (sorted position -> original row).
 //   aabb_kernel        bounding box of every 512-point tile of the sorted clouds.
 //   candidates_kernel  per query tile (256 sorted rows): lower bound LB of the squared distance to
@@ -95,7 +95,7 @@ void launch_bbox(const float* src0, int n0, const float* src1, int n1, int B, fl
 struct HilbertArgs {
     const float* src[2];
     int npts[2];
-    int B, kbits, bbits;
+    int B, kbits;
     const float* bbox;
     uint32_t* keys;
     uint32_t* vals;
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) hilbert_kernel(HilbertArgs a) {
             q[k] = (uint32_t)(t * qmax + 0.5f);
         }
         const uint32_t code = hilbert3(q[0], q[1], q[2], a.kbits);
-        a.keys[e] = ((uint32_t)c << (a.bbits + 3 * a.kbits)) | ((uint32_t)b << (3 * a.kbits)) | code;
+        a.keys[e] = code;   // segment-local: the (cloud, batch) segment is the sort's SegSpec
         a.vals[e] = (uint32_t)e;
     }
 }
@@ -842,15 +842,15 @@ __global__ void __launch_bounds__(256) pruned_tie_kernel(PrResolveArgs a) {
 }
 
 // --------------------------------------------------------------------------------------------- host
-// Bits per axis of the Hilbert codes (key = set | batch | code).  A 2-pass radix sort (<= 22 key bits)
-// when it still leaves <= ~8 points per occupied surface cell (4^k >= n / 48); else up to 10 bits
-// (3 passes).  The order only affects how much is culled, never the results.
-int hilbert_bits(int bbits, int nmax) {
-    const int k2 = (21 - bbits) / 3;
+// Bits per axis of the Hilbert codes (segment-local keys of 3k bits): the smallest k that leaves
+// <= ~8 points per occupied surface cell (4^k >= n / 48), at least 6 (18-bit keys: 2 radix passes of
+// 9 bits), at most 10.  Measured on the pruned forward (r02_experiments.txt): c4 (100k points) k = 5 /
+// 6 / 7: 1.050 / 0.972 / 0.998 ms; c5 (1M points) k = 7 / 8 / 9 / 10: 6.34 / 6.17 / 6.42 / 6.50 ms.
+// The order only affects how much is culled, never the results.
+int hilbert_bits(int nmax) {
     int need = 1;
     while (((int64_t)1 << (2 * need)) * 48 < (int64_t)nmax) ++need;
-    if (k2 >= need) return std::max(1, k2);
-    return std::max(1, std::min(10, (32 - 1 - bbits) / 3));
+    return std::min(10, std::max(6, need));
 }
 
 static int cdiv(int64_t x, int64_t y) { return (int)((x + y - 1) / y); }
@@ -865,11 +865,9 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
         p.qtiles[c] = cdiv(p.npts[c], kPrQ);
         p.ttiles[c] = p.ppad[c] / kTile;
     }
-    int bb = 0;
-    while ((1 << bb) < B) ++bb;
-    p.bbits = bb;
-    p.kbits = hilbert_bits(bb, std::max(N, M));
-    p.nbits = 1 + bb + 3 * p.kbits;
+    p.kbits = hilbert_bits(std::max(N, M));
+    p.nbits = 3 * p.kbits;
+    p.segs = SegSpec{B, N, B, M};
     p.L = (int64_t)B * (N + M);
     p.cand_off[0] = 0;
     p.cand_off[1] = (int64_t)B * p.qtiles[0] * p.ttiles[1];
@@ -890,8 +888,8 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
         p.off_keys[i] = take((size_t)p.L * 4);
         p.off_vals[i] = take((size_t)p.L * 4);
     }
-    p.off_counts = take(radix_sort_counts_words(p.L, p.nbits) * 4);
-    p.off_totals = take((size_t)kSortTotalsWords * 4);
+    p.off_counts = take(radix_sort_counts_words(p.segs, p.nbits, true) * 4);
+    p.off_totals = take(radix_sort_totals_words(p.segs, p.nbits, true) * 4);
     for (int c = 0; c < 2; ++c) {
         p.off_sorted[c] = take((size_t)B * p.ppad[c] * 16);
         p.off_perm[c] = take((size_t)B * p.npts[c] * 4);
@@ -919,7 +917,7 @@ static bool pruned_segsort(const PrunedPlan& p) {
 
 int pruned_launches(const PrunedPlan& p) {
     // segment sort: sort+boxes, candidates, kernel, resolve, tie, partials
-    return pruned_segsort(p) ? 6 : 2 + radix_sort_launches(p.L, p.nbits) + 7;
+    return pruned_segsort(p) ? 6 : 2 + radix_sort_launches(p.segs, p.nbits, true) + 7;
 }
 
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
@@ -969,15 +967,14 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         a.npts[1] = p.npts[1];
         a.B = p.B;
         a.kbits = p.kbits;
-        a.bbits = p.bbits;
         a.bbox = bbox;
         a.keys = keys[0];
         a.vals = vals[0];
         a.fb_count = reinterpret_cast<unsigned*>(w + p.off_fb);
         hilbert_kernel<<<grid_l, 256, 0, st>>>(a);
     }
-    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
-                                     reinterpret_cast<uint32_t*>(w + p.off_totals), st);
+    const int cur = radix_sort_pairs(keys, vals, p.segs, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
+                                     reinterpret_cast<uint32_t*>(w + p.off_totals), st, false, true);
     {
         GatherArgs a;
         a.src[0] = x;

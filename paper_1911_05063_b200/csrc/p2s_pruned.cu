@@ -79,7 +79,7 @@ struct PsHilbertArgs {
     const float* points;
     const float* verts;
     const int* faces;
-    int B, N, Nv, Nf, kbits, bbits;
+    int B, N, Nv, Nf, kbits;
     const float* bbox;   // [2][B][6]
     uint32_t* keys;
     uint32_t* vals;
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) ps_hilbert_kernel(PsHilbertArgs a) {
             q[k] = (uint32_t)(t * qmax + 0.5f);
         }
         const uint32_t code = hilbert3(q[0], q[1], q[2], a.kbits);
-        a.keys[e] = ((uint32_t)c << (a.bbits + 3 * a.kbits)) | ((uint32_t)b << (3 * a.kbits)) | code;
+        a.keys[e] = code;   // segment-local: the (points | faces, batch) segment is the sort's SegSpec
         a.vals[e] = (uint32_t)e;
     }
 }
@@ -726,7 +726,8 @@ __global__ void __launch_bounds__(kMergeThreads) ps_resolve_kernel(PsResolveArgs
 static int ps_cdiv(int64_t x, int64_t y) { return (int)((x + y - 1) / y); }
 
 struct PsPlan {
-    int B, N, Nv, Nf, Fpad, qtiles, ftiles, nchunks, bbits, kbits, nbits;
+    int B, N, Nv, Nf, Fpad, qtiles, ftiles, nchunks, kbits, nbits;
+    SegSpec segs;
     int64_t L;
     size_t off_bbox, off_keys[2], off_vals[2], off_counts, off_totals, off_spts, off_perm_p, off_perm_f, off_fd,
         off_qbox, off_fbox, off_fbox32, off_cand, off_rowkey, off_tieflag, off_tieface, off_tiequeue, off_tiecount, off_chunk, bytes;
@@ -743,11 +744,9 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
     p.qtiles = ps_cdiv(N, kPsQ);
     p.ftiles = p.Fpad / kPsTile;
     p.nchunks = ps_cdiv(N, kMergeThreads);
-    int bb = 0;
-    while ((1 << bb) < B) ++bb;
-    p.bbits = bb;
-    p.kbits = hilbert_bits(bb, std::max(N, Nf));
-    p.nbits = 1 + bb + 3 * p.kbits;
+    p.kbits = hilbert_bits(std::max(N, Nf));
+    p.nbits = 3 * p.kbits;
+    p.segs = SegSpec{B, N, B, Nf};
     p.L = (int64_t)B * N + (int64_t)B * Nf;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -760,8 +759,8 @@ static void plan_ps(PsPlan& p, int B, int N, int Nv, int Nf) {
         p.off_keys[i] = take((size_t)p.L * 4);
         p.off_vals[i] = take((size_t)p.L * 4);
     }
-    p.off_counts = take(radix_sort_counts_words(p.L, p.nbits) * 4);
-    p.off_totals = take((size_t)kSortTotalsWords * 4);
+    p.off_counts = take(radix_sort_counts_words(p.segs, p.nbits, true) * 4);
+    p.off_totals = take(radix_sort_totals_words(p.segs, p.nbits, true) * 4);
     p.off_spts = take((size_t)B * N * 16);
     p.off_perm_p = take((size_t)B * N * 4);
     p.off_perm_f = take((size_t)B * Nf * 4);
@@ -796,7 +795,7 @@ size_t p2s_pruned_workspace(int B, int N, int Nv, int Nf) {
 int p2s_pruned_launches(int B, int N, int Nv, int Nf) {
     PsPlan p;
     plan_ps(p, B, N, Nv, Nf);
-    return 2 + radix_sort_launches(p.L, p.nbits) + 7 + (p.nchunk > 0 ? 1 : 0) + 1;   // + ties + finalize
+    return 2 + radix_sort_launches(p.segs, p.nbits, true) + 7 + (p.nchunk > 0 ? 1 : 0) + 1;   // + ties + finalize
 }
 
 cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int* faces, int B, int N, int Nv, int Nf,
@@ -813,11 +812,11 @@ cudaError_t launch_p2s_pruned(const float* points, const float* verts, const int
     uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(w + p.off_vals[0]), reinterpret_cast<uint32_t*>(w + p.off_vals[1])};
     const int grid_l = (int)std::min<int64_t>((p.L + 255) / 256, (int64_t)sms * 16);
     {
-        PsHilbertArgs a{points, verts, faces, B, N, Nv, Nf, p.kbits, p.bbits, bbox, keys[0], vals[0]};
+        PsHilbertArgs a{points, verts, faces, B, N, Nv, Nf, p.kbits, bbox, keys[0], vals[0]};
         ps_hilbert_kernel<<<grid_l, 256, 0, st>>>(a);
     }
-    const int cur = radix_sort_pairs(keys, vals, p.L, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
-                                     reinterpret_cast<uint32_t*>(w + p.off_totals), st);
+    const int cur = radix_sort_pairs(keys, vals, p.segs, p.nbits, reinterpret_cast<uint32_t*>(w + p.off_counts),
+                                     reinterpret_cast<uint32_t*>(w + p.off_totals), st, false, true);
     float4* spts = reinterpret_cast<float4*>(w + p.off_spts);
     int* perm_p = reinterpret_cast<int*>(w + p.off_perm_p);
     int* perm_f = reinterpret_cast<int*>(w + p.off_perm_f);
