@@ -499,7 +499,7 @@ def test_pruned_equals_brute_configs(cd, name):
 
 
 @pytest.mark.parametrize("B,N,M", [(1, 1, 1), (2, 3, 7), (1, 1, 5000), (2, 5000, 1), (3, 2049, 4097),
-                                   (2, 100000, 30000)])
+                                   (2, 100000, 30000), (3, 30001, 25999)])
 def test_pruned_ragged(cd, B, N, M):
     X, Y = synth.shape_pair(B, N, M, config_index=70 + N % 5)
     _check_pruned_vs_brute(cd, X, Y)
