@@ -8,7 +8,8 @@ from paper_1911_05063_b200 import api as cd, synth
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 splits = [int(s) for s in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32]
-X, Y = synth.config_inputs(cfg)
+# SWEEP_B=k: the config's first k batch elements (one rank's share of batch sharding)
+X, Y = synth.config_inputs(cfg, B=int(os.environ["SWEEP_B"]) if os.environ.get("SWEEP_B") else None)
 x, y = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
 tau = synth.CONFIGS[cfg]["tau"]
 reps = 20 if cfg in ("c1", "c2", "c3") else 3
