@@ -630,17 +630,14 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga,
     const int t0 = dir == 0 ? ga.r0 : ga.q0, t1 = dir == 0 ? ga.r1 : ga.q1;
     float* out = dir == 0 ? ga.grad_y + (int64_t)b * (ga.r1 - ga.r0) * 3 : ga.grad_x + (int64_t)b * (ga.q1 - ga.q0) * 3;
     const int tlo = max(K0, t0), thi = min(K1, t1);
+    // the part's partner rows staged in the 16-bit buffer the sort left free (sources < kSegMax <
+    // 2^16), so each target's loads — its point, its partner and its first source — are ONE round
+    // trip: the three addresses come from shared memory
+    uint16_t* spart = counted ? vA : vB;
+    for (int t = tlo + threadIdx.x; t < thi; t += kSegThreads)
+        spart[t - K0] = (uint16_t)min(max(__ldg(pidx + t), 0), S - 1);
+    __syncthreads();
     for (int t = tlo + threadIdx.x; t < thi; t += kSegThreads) {
-        double pt[3];
-        load_point64(tgt + (int64_t)t * 3, pt);
-        const double wtt = wt ? (double)wt[t] : (double)wt_s;
-        double acc[3];
-        {
-            const float* ps = src + (int64_t)min(max(pidx[t], 0), S - 1) * 3;
-            const double w2 = __dmul_rn(2.0, wtt);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) acc[c] = __dmul_rn(w2, __dsub_rn(pt[c], (double)ps[c]));
-        }
         int e0, e1;
         if (counted) {
             e0 = t == K0 ? 0 : (int)cend[t - K0 - 1];
@@ -650,7 +647,30 @@ __global__ void __launch_bounds__(kSegThreads) seg_sort_grad_kernel(GradArgs ga,
             e1 = t + 1 < K1 ? (int)offs[t + 1 - K0] : n;
         }
         CD_CHECK(e0 <= e1 && e1 <= n);
-        for (int e = e0; e < e1; ++e) {
+        const float* pp = tgt + (int64_t)t * 3;
+        const float* ps = src + (int64_t)spart[t - K0] * 3;
+        const int s0 = e0 < e1 ? (int)srt[e0] : 0;   // an empty run reads row 0 (valid) and ignores it
+        const float* pf = src + (int64_t)s0 * 3;
+        const float tx = pp[0], ty = pp[1], tz = pp[2];
+        const float px = ps[0], py = ps[1], pz = ps[2];
+        const float fx = pf[0], fy = pf[1], fz = pf[2];
+        const double wtt = wt ? (double)wt[t] : (double)wt_s;
+        const double wf = wsrc ? (double)wsrc[s0] : (double)wsrc_s;
+        const double pt[3] = {(double)tx, (double)ty, (double)tz};
+        double acc[3];
+        {
+            const double w2 = __dmul_rn(2.0, wtt);
+            acc[0] = __dmul_rn(w2, __dsub_rn(pt[0], (double)px));
+            acc[1] = __dmul_rn(w2, __dsub_rn(pt[1], (double)py));
+            acc[2] = __dmul_rn(w2, __dsub_rn(pt[2], (double)pz));
+        }
+        if (e0 < e1) {
+            const double w2 = __dmul_rn(2.0, wf);
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(w2, __dsub_rn(pt[0], (double)fx)));
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(w2, __dsub_rn(pt[1], (double)fy)));
+            acc[2] = __dadd_rn(acc[2], __dmul_rn(w2, __dsub_rn(pt[2], (double)fz)));
+        }
+        for (int e = e0 + 1; e < e1; ++e) {
             const int sidx = srt[e];
             acc_term(acc, pt, src + (int64_t)sidx * 3, wsrc ? (double)wsrc[sidx] : (double)wsrc_s);
         }
