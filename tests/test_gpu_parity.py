@@ -442,6 +442,26 @@ def test_fused_equals_unfused_bitwise(cd, B, N, M):
     np.testing.assert_array_equal(fused[4][:, 2:], unf[4][:, 2:])
 
 
+def test_pack_alignment_paths_agree(cd):
+    """pack_kernel reads four points per thread with 16-byte loads when a cloud is 16-B aligned with
+    n % 4 == 0, and one point per thread otherwise: the same clouds at a 4-B offset (scalar path) give
+    bit-identical results."""
+    X, Y = synth.shape_pair(3, 4096, 2048, config_index=46)
+    x = torch.from_numpy(X).cuda()
+    y = torch.from_numpy(Y).cuda()
+    bx = torch.empty(x.numel() + 1, dtype=torch.float32, device="cuda")
+    by = torch.empty(y.numel() + 1, dtype=torch.float32, device="cuda")
+    xm = bx[1:].view(x.shape)
+    ym = by[1:].view(y.shape)
+    xm.copy_(x)
+    ym.copy_(y)
+    assert xm.data_ptr() % 16 != 0 and ym.data_ptr() % 16 != 0
+    a = cd.forward(x, y, tau=0.01)
+    m = cd.forward(xm, ym, tau=0.01)
+    for p, q in zip(a, m):
+        assert torch.equal(p, q)
+
+
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_rows_cols_sharding_emulated(cd, world):
     """Query sharding on one GPU: every 'rank' runs cd_forward_rows on its X slice, the column keys
