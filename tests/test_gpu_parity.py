@@ -543,6 +543,25 @@ def test_pruned_adversarial(cd):
     _check_pruned_vs_brute(cd, (g[:, :700] + 2.0 ** -6).astype(np.float32), g)   # exact 8-way ties
 
 
+@pytest.mark.parametrize("B,N,M", [(1, 2000, 1800), (2, 30000, 26000)])
+def test_pruned_nonfinite(cd, B, N, M):
+    """Non-finite coordinates (R6): the pruned path (on-chip and global-radix Hilbert sorts) returns
+    what the brute force returns — NaN distances never win, an all-+inf row is (+inf, -1)."""
+    X, Y = synth.shape_pair(B, N, M, config_index=74)
+    X = X.copy()
+    Y = Y.copy()
+    X[0, 5] = np.nan
+    X[0, 7, 1] = np.inf
+    Y[0, 11] = np.nan
+    Y[0, 13, 2] = -np.inf
+    x, y = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    brute = [t.cpu().numpy() for t in cd.forward(x, y, tau=0.01)]
+    pr = [t.cpu().numpy() for t in cd.forward(x, y, tau=0.01, algorithm="pruned")]
+    for k in range(4):
+        np.testing.assert_array_equal(pr[k], brute[k])   # NaN == NaN for assert_array_equal
+    np.testing.assert_array_equal(pr[4][:, 2:], brute[4][:, 2:])
+
+
 def test_pruned_large_sampled(cd):
     X, Y = synth.config_inputs("c5")
     x, y = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
