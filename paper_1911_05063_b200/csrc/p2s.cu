@@ -180,17 +180,23 @@ __global__ void __launch_bounds__(kMergeThreads) p2s_merge_kernel(P2sMergeArgs a
             }
             if (face < 0) face = bb;
         }
-        // fp64 closest point on the chosen face
+        // fp64 closest point on the chosen face; no finite candidate (a non-finite point, R6):
+        // (+inf, face -1, closest 0, bary 0), the oracle's values
         const float* vv = a.verts + (int64_t)b * a.Nv * 3;
-        double A[3], Bv[3], C[3], p[3] = {pp.x, pp.y, pp.z}, c[3], lam[3];
-        const int ia = min(max(a.faces[3 * face], 0), a.Nv - 1), ib = min(max(a.faces[3 * face + 1], 0), a.Nv - 1),
-                  ic = min(max(a.faces[3 * face + 2], 0), a.Nv - 1);
-        for (int k = 0; k < 3; ++k) {
-            A[k] = vv[3 * ia + k];
-            Bv[k] = vv[3 * ib + k];
-            C[k] = vv[3 * ic + k];
+        double A[3], Bv[3], C[3], p[3] = {pp.x, pp.y, pp.z}, c[3] = {0.0, 0.0, 0.0}, lam[3] = {0.0, 0.0, 0.0};
+        double dd = INFINITY;
+        if (bb >= 0) {
+            const int ia = min(max(a.faces[3 * face], 0), a.Nv - 1), ib = min(max(a.faces[3 * face + 1], 0), a.Nv - 1),
+                      ic = min(max(a.faces[3 * face + 2], 0), a.Nv - 1);
+            for (int k = 0; k < 3; ++k) {
+                A[k] = vv[3 * ia + k];
+                Bv[k] = vv[3 * ib + k];
+                C[k] = vv[3 * ic + k];
+            }
+            dd = face_foot64(p, A, Bv, C, c, lam);
+        } else {
+            face = -1;
         }
-        const double dd = face_foot64(p, A, Bv, C, c, lam);
         a.d_out[row] = (float)dd;
         a.face_out[row] = face;
         if (a.closest)

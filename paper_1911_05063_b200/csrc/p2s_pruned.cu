@@ -691,16 +691,22 @@ __global__ void __launch_bounds__(kMergeThreads) ps_resolve_kernel(PsResolveArgs
             }
             face = low != 0x7fffffff ? low : a.perm_f[(int64_t)b * a.Nf + min(bb, a.Nf - 1)];
         }
+        // no finite candidate (a non-finite point, R6): (+inf, face -1, closest 0, bary 0) as the oracle
         const float* vv = a.verts + (int64_t)b * a.Nv * 3;
-        double A[3], Bv[3], C[3], q[3] = {pp.x, pp.y, pp.z}, c[3], lam[3];
-        const int ia = min(max(a.faces[3 * face], 0), a.Nv - 1), ib = min(max(a.faces[3 * face + 1], 0), a.Nv - 1),
-                  ic = min(max(a.faces[3 * face + 2], 0), a.Nv - 1);
-        for (int k = 0; k < 3; ++k) {
-            A[k] = vv[3 * ia + k];
-            Bv[k] = vv[3 * ib + k];
-            C[k] = vv[3 * ic + k];
+        double A[3], Bv[3], C[3], q[3] = {pp.x, pp.y, pp.z}, c[3] = {0.0, 0.0, 0.0}, lam[3] = {0.0, 0.0, 0.0};
+        double dd = INFINITY;
+        if (bb >= 0) {
+            const int ia = min(max(a.faces[3 * face], 0), a.Nv - 1), ib = min(max(a.faces[3 * face + 1], 0), a.Nv - 1),
+                      ic = min(max(a.faces[3 * face + 2], 0), a.Nv - 1);
+            for (int k = 0; k < 3; ++k) {
+                A[k] = vv[3 * ia + k];
+                Bv[k] = vv[3 * ib + k];
+                C[k] = vv[3 * ic + k];
+            }
+            dd = face_foot64(q, A, Bv, C, c, lam);
+        } else {
+            face = -1;
         }
-        const double dd = face_foot64(q, A, Bv, C, c, lam);
         const int64_t row = (int64_t)b * a.N + a.perm_p[srow];
         a.d_out[row] = (float)dd;
         a.face_out[row] = face;

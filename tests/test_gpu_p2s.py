@@ -276,3 +276,28 @@ def test_p2s_degenerate_faces(cd):
         out = cd.p2s_forward(_t(P), _t(V), _t(F), algorithm=algo)
         torch.cuda.synchronize()
         _gate(P, V, F, out)
+
+
+def test_p2s_pruned_nonfinite_points(cd):
+    """Non-finite query points (R6): no finite candidate -> (+inf, face -1, closest 0, bary 0) as the
+    oracle, from both kernels; every other point is unaffected (bit-identical to the brute force)."""
+    B, N = 2, 3000
+    V, F = synth.mesh_batch(B, subdiv=3, config_index=139)
+    P = synth.shape_pair(B, N, 8, config_index=140)[0].copy()
+    bad = [(0, 3), (0, 9), (1, 17)]
+    P[0, 3] = np.nan
+    P[0, 9, 1] = np.inf
+    P[1, 17, 2] = -np.inf
+    do, fo = oracle.p2s(P, V, F)[:2]
+    for algo in ("brute", "pruned"):
+        out = [o.cpu().numpy() for o in cd.p2s_forward(_t(P), _t(V), _t(F), algorithm=algo)[:4]]
+        for i in bad:
+            assert out[0][i] == np.inf and out[1][i] == -1 and do[i] == np.inf and fo[i] == -1
+            assert not out[2][i].any() and not out[3][i].any()
+        if algo == "brute":
+            brute = out
+        else:
+            for a, b in zip(out, brute):
+                np.testing.assert_array_equal(a, b)
+    finite = np.isfinite(P).all(-1)
+    assert np.isfinite(brute[0][finite]).all()
