@@ -83,8 +83,9 @@ struct PrunedPlan {
     int nchunks[2];
     int64_t chunk_off[2];
     bool supported;
+    bool hier;                 // two-level (super-tile) candidate search
     size_t off_bbox, off_keys[2], off_vals[2], off_counts, off_totals, off_sorted[2], off_perm[2], off_box[2], off_box32[2],
-        off_best_d[2], off_best_blk[2], off_cand, off_ccount, off_chunk_sum, off_chunk_hits, off_fb, bytes;
+        off_best_d[2], off_best_blk[2], off_sbox[2], off_cand, off_ccount, off_chunk_sum, off_chunk_hits, off_fb, bytes;
 };
 void plan_pruned(PrunedPlan& p, int B, int N, int M);
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,

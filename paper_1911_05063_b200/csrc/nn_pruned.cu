@@ -369,7 +369,39 @@ struct CandArgs {
     int64_t cand_off[2];      // offset of dir's lists in `cand` (u64 entries)
     unsigned long long* cand; // per (dir, b, query tile): up to ttiles(1-dir) keys (LB' bits << 32 | tile)
     int* ccount;              // per list: number of entries (LB <= UB), lists of dir 1 after dir 0's
+    const float4* sbox[2];    // [B][nst][2] super-tile boxes (kSuper tiles), or null: flat scan
 };
+
+// Super tiles: kSuper consecutive 512-point tiles of a Hilbert-sorted cloud (8192 points, spatially
+// compact).  superbox_kernel: their boxes (union of the non-empty tile boxes; empty: lo = +inf).
+constexpr int kSuper = 16;
+constexpr int kHierMinTiles = 64;   // target clouds of >= 64 tiles use the two-level candidate search
+#ifndef CD_PR_HIER
+#define CD_PR_HIER 1   // two-level candidate search for clouds of >= kHierMinTiles tiles
+#endif
+
+__global__ void __launch_bounds__(256) superbox_kernel(const float4* box0, const float4* box1, int nt0, int nt1,
+                                                       int B, float4* sbox0, float4* sbox1) {
+    const int ns0 = (nt0 + kSuper - 1) / kSuper, ns1 = (nt1 + kSuper - 1) / kSuper;
+    const int64_t S0 = (int64_t)B * ns0, S = S0 + (int64_t)B * ns1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = i < S0 ? 0 : 1;
+        const int64_t f = c == 0 ? i : i - S0;
+        const int ns = c == 0 ? ns0 : ns1, nt = c == 0 ? nt0 : nt1;
+        const int bb = (int)(f / ns), sidx = (int)(f - (int64_t)bb * ns);
+        const float4* bx = (c == 0 ? box0 : box1) + (int64_t)bb * nt * 2;
+        float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.f), hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+        for (int t = sidx * kSuper; t < min(nt, (sidx + 1) * kSuper); ++t) {
+            const float4 l = bx[2 * t], h = bx[2 * t + 1];
+            if (l.x > h.x) continue;   // empty tile
+            lo.x = fminf(lo.x, l.x); lo.y = fminf(lo.y, l.y); lo.z = fminf(lo.z, l.z);
+            hi.x = fmaxf(hi.x, h.x); hi.y = fmaxf(hi.y, h.y); hi.z = fmaxf(hi.z, h.z);
+        }
+        float4* o = (c == 0 ? sbox0 : sbox1) + f * 2;
+        o[0] = lo;
+        o[1] = hi;
+    }
+}
 
 __device__ __forceinline__ float gap(float qlo, float qhi, float tlo, float thi) {
     return fmaxf(fmaxf(tlo - qhi, qlo - thi), 0.f);
@@ -402,37 +434,79 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
     // LB <= UB, compacted, then sorted (keys are unique, so the order is deterministic).
     __shared__ float s_ub[8];
     __shared__ int s_cnt;
-    float ub = INFINITY;
-    for (int t = threadIdx.x; t < tnt; t += 256) {
-        const float4* bx = a.box[tc] + ((int64_t)b * tnt + t) * 2;
-        const float4 lo = bx[0], hi = bx[1];
-        if (lo.x <= hi.x) {
-            const float fx = fmaxf(fabsf(hi.x - qlo[0]), fabsf(qhi[0] - lo.x));
-            const float fy = fmaxf(fabsf(hi.y - qlo[1]), fabsf(qhi[1] - lo.y));
-            const float fz = fmaxf(fabsf(hi.z - qlo[2]), fabsf(qhi[2] - lo.z));
-            ub = fminf(ub, (fx * fx + fy * fy + fz * fz) * 1.00001f);
-        }
-    }
+    const float4* tbox = a.box[tc] + (int64_t)b * tnt * 2;
+    auto far2 = [&](float4 lo, float4 hi) {   // farthest box-to-box corner distance, x (1 + 1e-5)
+        const float fx = fmaxf(fabsf(hi.x - qlo[0]), fabsf(qhi[0] - lo.x));
+        const float fy = fmaxf(fabsf(hi.y - qlo[1]), fabsf(qhi[1] - lo.y));
+        const float fz = fmaxf(fabsf(hi.z - qlo[2]), fabsf(qhi[2] - lo.z));
+        return (fx * fx + fy * fy + fz * fz) * 1.00001f;
+    };
+    auto tile_lb = [&](float4 lo, float4 hi) {
+        if (lo.x > hi.x) return INFINITY;   // empty tile (all padding)
+        const float gx = gap(qlo[0], qhi[0], lo.x, hi.x);
+        const float gy = gap(qlo[1], qhi[1], lo.y, hi.y);
+        const float gz = gap(qlo[2], qhi[2], lo.z, hi.z);
+        return (gx * gx + gy * gy + gz * gz) * kLbScale;
+    };
+    auto block_min = [&](float v) {   // min over the CTA (all threads call it)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ub = fminf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
-    if ((threadIdx.x & 31) == 0) s_ub[threadIdx.x >> 5] = ub;
+        for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) s_ub[threadIdx.x >> 5] = v;
+        __syncthreads();
+        v = s_ub[0];
+        for (int w = 1; w < 8; ++w) v = fminf(v, s_ub[w]);
+        return v;
+    };
     if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    ub = s_ub[0];
-    for (int w = 1; w < 8; ++w) ub = fminf(ub, s_ub[w]);
-    for (int t = threadIdx.x; t < tnt; t += 256) {
-        const float4* bx = a.box[tc] + ((int64_t)b * tnt + t) * 2;
-        const float4 lo = bx[0], hi = bx[1];
-        float lb;
-        if (lo.x > hi.x) {
-            lb = INFINITY;   // empty tile (all padding)
-        } else {
-            const float gx = gap(qlo[0], qhi[0], lo.x, hi.x);
-            const float gy = gap(qlo[1], qhi[1], lo.y, hi.y);
-            const float gz = gap(qlo[2], qhi[2], lo.z, hi.z);
-            lb = (gx * gx + gy * gy + gz * gz) * kLbScale;
+    float ub = INFINITY;
+    if (a.sbox[tc] == nullptr) {
+        // flat: every tile's farthest corner, then every tile's LB
+        for (int t = threadIdx.x; t < tnt; t += 256) {
+            const float4 lo = tbox[2 * t], hi = tbox[2 * t + 1];
+            if (lo.x <= hi.x) ub = fminf(ub, far2(lo, hi));
         }
-        if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+        ub = block_min(ub);
+        for (int t = threadIdx.x; t < tnt; t += 256) {
+            const float lb = tile_lb(tbox[2 * t], tbox[2 * t + 1]);
+            if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+        }
+    } else {
+        // two levels (large clouds): LB of every super tile (kSuper tiles; a tile's LB >= its super
+        // tile's), UB from the tiles of the nearest super tile only (a minimum over fewer tiles: >= the
+        // flat UB, so the list below is a superset of the flat one whose extra entries all have LB > the
+        // flat UB — after the kernel's stopping point: the same tiles are visited in the same order),
+        // then the tiles of the super tiles with LB <= UB
+        const int tns = (tnt + kSuper - 1) / kSuper;
+        const float4* sb = a.sbox[tc] + (int64_t)b * tns * 2;
+        float* slb = reinterpret_cast<float*>(keys + tnt);   // [tns] super LBs (after the key area)
+        __shared__ int s_sup[kPrMaxTiles / kSuper];
+        __shared__ int s_nsup;
+        float mlb = INFINITY;
+        for (int t = threadIdx.x; t < tns; t += 256) {
+            const float lb = tile_lb(sb[2 * t], sb[2 * t + 1]);
+            slb[t] = lb;
+            mlb = fminf(mlb, lb);
+        }
+        mlb = block_min(mlb);   // (contains the barriers slb needs)
+        if (threadIdx.x == 0) s_nsup = 0;
+        // UB over the tiles of every super tile at the minimum LB (usually one: the query's own region)
+        for (int t = threadIdx.x; t < tnt; t += 256) {
+            if (slb[t / kSuper] != mlb) continue;
+            const float4 lo = tbox[2 * t], hi = tbox[2 * t + 1];
+            if (lo.x <= hi.x) ub = fminf(ub, far2(lo, hi));
+        }
+        ub = block_min(ub);
+        for (int t = threadIdx.x; t < tns; t += 256)
+            if (slb[t] <= ub) s_sup[atomicAdd(&s_nsup, 1)] = t;
+        __syncthreads();
+        const int nsup = s_nsup;
+        for (int i = threadIdx.x; i < nsup * kSuper; i += 256) {
+            const int t = s_sup[i / kSuper] * kSuper + (i % kSuper);
+            if (t >= tnt) continue;
+            const float lb = tile_lb(tbox[2 * t], tbox[2 * t + 1]);
+            if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+        }
     }
     __syncthreads();
     const int n = s_cnt;
@@ -715,6 +789,9 @@ struct PrResolveArgs {
     unsigned* fb_list;     // (dir << 31) | b * P + p
 };
 
+#ifndef CD_RESOLVE_BATCH
+#define CD_RESOLVE_BATCH 8   // targets loaded together per row
+#endif
 __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolveArgs a) {
     int u = blockIdx.x;
     int dir = 0;
@@ -729,37 +806,57 @@ __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolve
     const int p = chunk * kMergeThreads + threadIdx.x;
     double v = 0.0;
     int h = 0;
+    float best = INFINITY;
+    int bb = -1;
+    bool tie = false;
+    float4 qp = make_float4(0.f, 0.f, 0.f, 0.f);
     if (p < P) {
-        const float best = a.best_d[dir][(int64_t)b * P + p];
+        best = a.best_d[dir][(int64_t)b * P + p];
         const int bbt = a.best_blk[dir][(int64_t)b * P + p];
-        const bool tie = bbt != -1 && (bbt & (int)0x80000000) != 0;
-        const int bb = bbt == -1 ? -1 : (bbt & 0x7fffffff);
+        tie = bbt != -1 && (bbt & (int)0x80000000) != 0;
+        bb = bbt == -1 ? -1 : (bbt & 0x7fffffff);
         CD_CHECK(bb < a.ppad[tc]);
-        int idx = -1;
-        if (bb >= 0) {
-            // the lowest ORIGINAL index among the block's targets at the minimum distance
-            const float4 qp = a.sorted[qc][(int64_t)b * a.ppad[qc] + p];
-            const float4* T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
-            const int* PT = a.perm[tc] + (int64_t)b * a.npts[tc];
-            const int jend = min(bb + kBlockK, a.npts[tc]);
-            for (int c = bb; c < jend; c += 8) {
-                float d[8];
+        if (bb >= 0) qp = a.sorted[qc][(int64_t)b * a.ppad[qc] + p];
+    }
+    // the lowest ORIGINAL index among the winning block's targets at the minimum distance, warp-
+    // cooperatively: the warp's 32 rows staged in shared memory, then per row the 32 lanes load the
+    // block's 32 sorted targets (one coalesced 512-B read, 8 rows in flight), the matching lanes their
+    // original indices, and one REDUX.MIN; targets past the cloud are the +inf padding (bb + 31 < ppad)
+    __shared__ float4 s_q[kMergeThreads];
+    __shared__ int s_b[kMergeThreads];
+    s_q[threadIdx.x] = make_float4(qp.x, qp.y, qp.z, best);
+    s_b[threadIdx.x] = bb;
+    __syncwarp();
+    const int lane = threadIdx.x & 31, wb = threadIdx.x & ~31;
+    const float4* T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
+    const int* PT = a.perm[tc] + (int64_t)b * a.npts[tc];
+    const int nt = a.npts[tc];
+    unsigned myidx = 0xffffffffu;
+    constexpr int kRowsInFlight = 8;
+    for (int r0 = 0; r0 < 32; r0 += kRowsInFlight) {
+        int base[kRowsInFlight];
+        float4 t[kRowsInFlight];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const float4 t = T[min(c + r, jend - 1)];
-                    d[r] = dist_rn(qp.x, qp.y, qp.z, t.x, t.y, t.z);
-                }
+        for (int k = 0; k < kRowsInFlight; ++k) {
+            base[k] = s_b[wb + r0 + k];
+            t[k] = T[max(base[k], 0) + lane];
+        }
 #pragma unroll
-                for (int r = 0; r < 8; ++r)
-                    if (c + r < jend && d[r] == best) {
-                        const int o = PT[c + r];
-                        idx = (idx < 0 || o < idx) ? o : idx;
-                    }
-            }
-            if (tie) {
-                const unsigned slot = atomicAdd(a.fb_count, 1u);
-                a.fb_list[slot] = ((unsigned)dir << 31) | (unsigned)((int64_t)b * P + p);
-            }
+        for (int k = 0; k < kRowsInFlight; ++k) {
+            const float4 q = s_q[wb + r0 + k];
+            const float d = dist_rn(q.x, q.y, q.z, t[k].x, t[k].y, t[k].z);
+            const int j = base[k] + lane;
+            const bool m = base[k] >= 0 && j < nt && d == q.w;
+            const unsigned o = m ? (unsigned)PT[j] : 0xffffffffu;
+            const unsigned low = __reduce_min_sync(0xffffffffu, o);
+            myidx = lane == r0 + k ? low : myidx;
+        }
+    }
+    if (p < P) {
+        const int idx = (bb >= 0 && myidx != 0xffffffffu) ? (int)myidx : -1;
+        if (bb >= 0 && tie) {
+            const unsigned slot = atomicAdd(a.fb_count, 1u);
+            a.fb_list[slot] = ((unsigned)dir << 31) | (unsigned)((int64_t)b * P + p);
         }
         const int i = a.perm[qc][(int64_t)b * P + p];
         a.d_out[dir][(int64_t)b * P + i] = best;
@@ -897,7 +994,9 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
         p.off_box32[c] = take((size_t)B * p.ttiles[c] * kBlocksPerTile * 32);
         p.off_best_d[c] = take((size_t)B * p.npts[c] * 4);
         p.off_best_blk[c] = take((size_t)B * p.npts[c] * 4);
+        p.off_sbox[c] = take((size_t)B * ((p.ttiles[c] + kSuper - 1) / kSuper) * 32);
     }
+    p.hier = CD_PR_HIER && std::max(p.ttiles[0], p.ttiles[1]) >= kHierMinTiles;
     p.off_cand = take((size_t)ncand * 8);
     p.off_ccount = take((size_t)B * (p.qtiles[0] + p.qtiles[1]) * 4);
     p.off_chunk_sum = take((size_t)chunks * 8);
@@ -916,8 +1015,8 @@ static bool pruned_segsort(const PrunedPlan& p) {
 }
 
 int pruned_launches(const PrunedPlan& p) {
-    // segment sort: sort+boxes, candidates, kernel, resolve, tie, partials
-    return pruned_segsort(p) ? 6 : 2 + radix_sort_launches(p.segs, p.nbits, true) + 7;
+    // segment sort: sort+boxes, candidates, kernel, resolve, tie, partials (+ super boxes)
+    return (pruned_segsort(p) ? 6 : 2 + radix_sort_launches(p.segs, p.nbits, true) + 7) + (p.hier ? 1 : 0);
 }
 
 cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, const FwdOutputs& o, void* ws,
@@ -1004,6 +1103,12 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         aabb_kernel<<<cdiv(tiles * 32, 256), 256, 0, st>>>(a);
     }
     unsigned long long* cand = reinterpret_cast<unsigned long long*>(w + p.off_cand);
+    float4* sbox[2] = {reinterpret_cast<float4*>(w + p.off_sbox[0]), reinterpret_cast<float4*>(w + p.off_sbox[1])};
+    if (p.hier) {
+        const int64_t n = (int64_t)p.B * ((p.ttiles[0] + kSuper - 1) / kSuper + (p.ttiles[1] + kSuper - 1) / kSuper);
+        superbox_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 4)), 256, 0,
+                          st>>>(box[0], box[1], p.ttiles[0], p.ttiles[1], p.B, sbox[0], sbox[1]);
+    }
     {
         CandArgs a;
         a.B = p.B;
@@ -1013,13 +1118,15 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
             a.ppad[c] = p.ppad[c];
             a.qtiles[c] = p.qtiles[c];
             a.cand_off[c] = p.cand_off[c];
+            a.sbox[c] = p.hier ? sbox[c] : nullptr;
         }
         a.cand = cand;
         a.ccount = reinterpret_cast<int*>(w + p.off_ccount);
         int npow = 1;
         while (npow < std::max(p.ttiles[0], p.ttiles[1])) npow <<= 1;
-        const size_t smem = (size_t)npow * 8;
-        ensure_smem_attr((const void*)candidates_kernel, kPrMaxTiles * 8);
+        // keys (npow u64) + the super LBs (two-level search: ceil(T / kSuper) floats)
+        const size_t smem = (size_t)npow * 8 + (size_t)(std::max(p.ttiles[0], p.ttiles[1]) / kSuper + 1) * 4;
+        ensure_smem_attr((const void*)candidates_kernel, kPrMaxTiles * 8 + (kPrMaxTiles / kSuper + 1) * 4);
         candidates_kernel<<<p.B * (p.qtiles[0] + p.qtiles[1]), 256, smem, st>>>(a);
     }
     float* best_d[2];
