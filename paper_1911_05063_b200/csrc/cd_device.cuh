@@ -133,13 +133,16 @@ __device__ __forceinline__ uint32_t hilbert3(uint32_t x0, uint32_t x1, uint32_t 
     X[0] ^= t;
     X[1] ^= t;
     X[2] ^= t;
-    uint32_t code = 0;
-    for (int bit = k - 1; bit >= 0; --bit) {
-        code = (code << 1) | ((X[0] >> bit) & 1u);
-        code = (code << 1) | ((X[1] >> bit) & 1u);
-        code = (code << 1) | ((X[2] >> bit) & 1u);
-    }
-    return code;
+    // bit interleave (k <= 10): bit i of X[0] / X[1] / X[2] -> code bit 3i + 2 / 3i + 1 / 3i
+    auto spread3 = [](uint32_t x) {
+        x &= 0x3ffu;
+        x = (x | (x << 16)) & 0x030000FFu;
+        x = (x | (x << 8)) & 0x0300F00Fu;
+        x = (x | (x << 4)) & 0x030C30C3u;
+        x = (x | (x << 2)) & 0x09249249u;
+        return x;
+    };
+    return (spread3(X[0]) << 2) | (spread3(X[1]) << 1) | spread3(X[2]);
 }
 
 // ---------------------------------------------------------------- mbarrier + TMA bulk copy

@@ -104,20 +104,23 @@ struct HilbertArgs {
 
 __global__ void __launch_bounds__(256) hilbert_kernel(HilbertArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.fb_count) *a.fb_count = 0u;
-    const int64_t L0 = (int64_t)a.B * a.npts[0];
-    const int64_t L = L0 + (int64_t)a.B * a.npts[1];
+    // L = B (N + M) < 2^31 (cd_forward_pruned's size limit): 32-bit index arithmetic
+    const int L0 = a.B * a.npts[0];
+    const int L = L0 + a.B * a.npts[1];
     const float qmax = (float)((1 << a.kbits) - 1);
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L; e += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t e64 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e64 < L; e64 += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)e64;
         const int c = e < L0 ? 0 : 1;
-        const int64_t f = c == 0 ? e : e - L0;
-        const int b = (int)(f / a.npts[c]);
+        const int f = c == 0 ? e : e - L0;
+        const int b = f / a.npts[c];
         const float* bb = a.bbox + ((int64_t)c * a.B + b) * 6;
-        const float* p = a.src[c] + f * 3;
+        const float* p = a.src[c] + (int64_t)f * 3;
         uint32_t q[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
+            // any quantisation is valid (the order only steers the culling): fast division
             const float ext = bb[3 + k] - bb[k];
-            float t = ext > 0.f ? (__ldg(p + k) - bb[k]) / ext : 0.f;
+            float t = ext > 0.f ? __fdividef(__ldg(p + k) - bb[k], ext) : 0.f;
             t = fminf(fmaxf(t, 0.f), 1.f);          // NaN -> 0 via fmaxf
             q[k] = (uint32_t)(t * qmax + 0.5f);
         }
@@ -142,9 +145,9 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
     const int64_t L = L0 + (int64_t)a.B * a.npts[1];
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L; s += (int64_t)gridDim.x * blockDim.x) {
         const int c = s < L0 ? 0 : 1;
-        const int64_t f = c == 0 ? s : s - L0;          // (b, p) of the sorted position
-        const int b = (int)(f / a.npts[c]);
-        const int p = (int)(f - (int64_t)b * a.npts[c]);
+        const int f = (int)(c == 0 ? s : s - L0);       // (b, p) of the sorted position (< 2^31)
+        const int b = f / a.npts[c];
+        const int p = f - b * a.npts[c];
         const int64_t v = (int64_t)a.vals[s] - (c == 0 ? 0 : L0);  // original flat row of the same cloud
         const float* q = a.src[c] + v * 3;
         a.sorted[c][(int64_t)b * a.ppad[c] + p] = make_float4(__ldg(q), __ldg(q + 1), __ldg(q + 2), 0.f);
