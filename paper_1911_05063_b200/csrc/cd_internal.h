@@ -76,7 +76,7 @@ struct SegSpec {
 };
 
 struct PrunedPlan {
-    int B, npts[2], ppad[2], qtiles[2], ttiles[2];
+    int B, npts[2], ppad[2], qtiles[2], cqtiles[2], ttiles[2];
     int kbits, nbits;          // nbits = 3*kbits: segment-local Hilbert keys
     SegSpec segs;              // the 2B (cloud, batch) segments the radix passes sort on their own
     int64_t L, cand_off[2];

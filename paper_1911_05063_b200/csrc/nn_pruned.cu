@@ -28,9 +28,20 @@
 
 namespace cdk {
 
-constexpr int kPrR = 2;                         // query rows per thread (one packed f32x2 pair)
-constexpr int kPrThreads = 128;                 // threads per query-tile CTA
-constexpr int kPrQ = kPrThreads * kPrR;         // 256 sorted rows per query tile: tight boxes
+#ifndef CD_PR_R
+#define CD_PR_R 2
+#endif
+#ifndef CD_PR_THREADS
+#define CD_PR_THREADS 64
+#endif
+constexpr int kPrR = CD_PR_R;                   // query rows per thread (packed f32x2 pairs)
+constexpr int kPrThreads = CD_PR_THREADS;       // threads per query-tile CTA
+constexpr int kPrQ = kPrThreads * kPrR;         // sorted rows per query tile of the main kernel
+#ifndef CD_CAND_Q
+#define CD_CAND_Q kPrQ
+#endif
+constexpr int kCandQ = CD_CAND_Q;               // sorted rows per candidate list (query tiles may share one)
+static_assert(kCandQ % kPrQ == 0, "a candidate list covers whole query tiles");
 constexpr int kPrMaxTiles = 8192;               // target tiles per batch supported by the LB sort
 constexpr float kLbScale = 0.99999f;            // LB' = LB * (1 - 1e-5): strict lower bound margin
 
@@ -368,7 +379,7 @@ struct CandArgs {
     const float4* box32[2];   // 32-point block boxes: the query tile box is their union
     int ppad[2];
     int B;
-    int qtiles[2];            // query tiles (kPrQ rows) per batch element, per dir
+    int qtiles[2];            // candidate lists (kCandQ rows) per batch element, per dir
     int64_t cand_off[2];      // offset of dir's lists in `cand` (u64 entries)
     unsigned long long* cand; // per (dir, b, query tile): up to ttiles(1-dir) keys (LB' bits << 32 | tile)
     int* ccount;              // per list: number of entries (LB <= UB), lists of dir 1 after dir 0's
@@ -410,7 +421,11 @@ __device__ __forceinline__ float gap(float qlo, float qhi, float tlo, float thi)
     return fmaxf(fmaxf(tlo - qhi, qlo - thi), 0.f);
 }
 
-__global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
+#ifndef CD_CAND_THREADS
+#define CD_CAND_THREADS 128
+#endif
+constexpr int kCandThreads = CD_CAND_THREADS;
+__global__ void __launch_bounds__(kCandThreads) candidates_kernel(CandArgs a) {
     extern __shared__ unsigned long long keys[];
     int u = blockIdx.x;
     int dir = 0;
@@ -422,10 +437,10 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
     const int q = u - b * a.qtiles[dir];
     const int qc = dir, tc = 1 - dir;
     const int qnt = a.ppad[qc] / kTile, tnt = a.ppad[tc] / kTile;
-    // query tile box = union of its kPrQ / kBlockK 32-point block boxes
+    // query box = union of its kCandQ / kBlockK 32-point block boxes
     float qlo[3] = {INFINITY, INFINITY, INFINITY}, qhi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int s = 0; s < kPrQ / kBlockK; ++s) {
-        const float4* bx = a.box32[qc] + ((int64_t)b * qnt * kBlocksPerTile + q * (kPrQ / kBlockK) + s) * 2;
+    for (int s = 0; s < kCandQ / kBlockK; ++s) {
+        const float4* bx = a.box32[qc] + ((int64_t)b * qnt * kBlocksPerTile + q * (kCandQ / kBlockK) + s) * 2;
         const float4 lo = bx[0], hi = bx[1];
         qlo[0] = fminf(qlo[0], lo.x); qlo[1] = fminf(qlo[1], lo.y); qlo[2] = fminf(qlo[2], lo.z);
         qhi[0] = fmaxf(qhi[0], hi.x); qhi[1] = fmaxf(qhi[1], hi.y); qhi[2] = fmaxf(qhi[2], hi.z);
@@ -435,7 +450,7 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
     // upper bound of the fp32-evaluated distance too).  Tiles with LB > UB can never be visited
     // (the kernel stops at LB > max over rows of the current minimum <= UB): the list keeps only
     // LB <= UB, compacted, then sorted (keys are unique, so the order is deterministic).
-    __shared__ float s_ub[8];
+    __shared__ float s_ub[kCandThreads / 32];
     __shared__ int s_cnt;
     const float4* tbox = a.box[tc] + (int64_t)b * tnt * 2;
     auto far2 = [&](float4 lo, float4 hi) {   // farthest box-to-box corner distance, x (1 + 1e-5)
@@ -458,19 +473,19 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
         if ((threadIdx.x & 31) == 0) s_ub[threadIdx.x >> 5] = v;
         __syncthreads();
         v = s_ub[0];
-        for (int w = 1; w < 8; ++w) v = fminf(v, s_ub[w]);
+        for (int w = 1; w < kCandThreads / 32; ++w) v = fminf(v, s_ub[w]);
         return v;
     };
     if (threadIdx.x == 0) s_cnt = 0;
     float ub = INFINITY;
     if (a.sbox[tc] == nullptr) {
         // flat: every tile's farthest corner, then every tile's LB
-        for (int t = threadIdx.x; t < tnt; t += 256) {
+        for (int t = threadIdx.x; t < tnt; t += kCandThreads) {
             const float4 lo = tbox[2 * t], hi = tbox[2 * t + 1];
             if (lo.x <= hi.x) ub = fminf(ub, far2(lo, hi));
         }
         ub = block_min(ub);
-        for (int t = threadIdx.x; t < tnt; t += 256) {
+        for (int t = threadIdx.x; t < tnt; t += kCandThreads) {
             const float lb = tile_lb(tbox[2 * t], tbox[2 * t + 1]);
             if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
         }
@@ -486,7 +501,7 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
         __shared__ int s_sup[kPrMaxTiles / kSuper];
         __shared__ int s_nsup;
         float mlb = INFINITY;
-        for (int t = threadIdx.x; t < tns; t += 256) {
+        for (int t = threadIdx.x; t < tns; t += kCandThreads) {
             const float lb = tile_lb(sb[2 * t], sb[2 * t + 1]);
             slb[t] = lb;
             mlb = fminf(mlb, lb);
@@ -494,17 +509,17 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
         mlb = block_min(mlb);   // (contains the barriers slb needs)
         if (threadIdx.x == 0) s_nsup = 0;
         // UB over the tiles of every super tile at the minimum LB (usually one: the query's own region)
-        for (int t = threadIdx.x; t < tnt; t += 256) {
+        for (int t = threadIdx.x; t < tnt; t += kCandThreads) {
             if (slb[t / kSuper] != mlb) continue;
             const float4 lo = tbox[2 * t], hi = tbox[2 * t + 1];
             if (lo.x <= hi.x) ub = fminf(ub, far2(lo, hi));
         }
         ub = block_min(ub);
-        for (int t = threadIdx.x; t < tns; t += 256)
+        for (int t = threadIdx.x; t < tns; t += kCandThreads)
             if (slb[t] <= ub) s_sup[atomicAdd(&s_nsup, 1)] = t;
         __syncthreads();
         const int nsup = s_nsup;
-        for (int i = threadIdx.x; i < nsup * kSuper; i += 256) {
+        for (int i = threadIdx.x; i < nsup * kSuper; i += kCandThreads) {
             const int t = s_sup[i / kSuper] * kSuper + (i % kSuper);
             if (t >= tnt) continue;
             const float lb = tile_lb(tbox[2 * t], tbox[2 * t + 1]);
@@ -513,14 +528,46 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
     }
     __syncthreads();
     const int n = s_cnt;
+    const int64_t list = (int64_t)(dir == 0 ? 0 : a.B * a.qtiles[0]) + (int64_t)b * a.qtiles[dir] + q;
+    unsigned long long* out = a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + q) * tnt;
+    if (n <= 64) {
+        // short list (the common case): one warp sorts it in registers, two keys per lane (bitonic
+        // network over 64 slots by shuffles and an in-lane exchange; no block barriers)
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            unsigned long long v0 = lane < n ? keys[lane] : ~0ull;        // slot lane
+            unsigned long long v1 = lane + 32 < n ? keys[lane + 32] : ~0ull;   // slot lane + 32
+            for (int k = 2; k <= 64; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    if (j == 32) {   // partner slot is in the same lane
+                        const bool up = (lane & k) == 0;   // k == 64: ascending
+                        const unsigned long long lo = min(v0, v1), hi = max(v0, v1);
+                        v0 = up ? lo : hi;
+                        v1 = up ? hi : lo;
+                    } else {
+                        const unsigned long long o0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                        const unsigned long long o1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                        const bool lower = (lane & j) == 0;
+                        const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
+                        v0 = (lower == up0) ? min(v0, o0) : max(v0, o0);
+                        v1 = (lower == up1) ? min(v1, o1) : max(v1, o1);
+                    }
+                }
+            }
+            if (lane < n) out[lane] = v0;
+            if (lane + 32 < n) out[lane + 32] = v1;
+            if (lane == 0) a.ccount[list] = n;
+        }
+        return;
+    }
     int npow = 1;
     while (npow < n) npow <<= 1;
-    for (int t = n + threadIdx.x; t < npow; t += 256) keys[t] = ~0ull;
+    for (int t = n + threadIdx.x; t < npow; t += kCandThreads) keys[t] = ~0ull;
     __syncthreads();
     // bitonic sort ascending (npow <= kPrMaxTiles)
     for (int k = 2; k <= npow; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < npow; i += 256) {
+            for (int i = threadIdx.x; i < npow; i += kCandThreads) {
                 const int l = i ^ j;
                 if (l > i) {
                     const unsigned long long x = keys[i], y = keys[l];
@@ -534,9 +581,7 @@ __global__ void __launch_bounds__(256) candidates_kernel(CandArgs a) {
             __syncthreads();
         }
     }
-    const int64_t list = (int64_t)(dir == 0 ? 0 : a.B * a.qtiles[0]) + (int64_t)b * a.qtiles[dir] + q;
-    unsigned long long* out = a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + q) * tnt;
-    for (int t = threadIdx.x; t < n; t += 256) out[t] = keys[t];
+    for (int t = threadIdx.x; t < n; t += kCandThreads) out[t] = keys[t];
     if (threadIdx.x == 0) a.ccount[list] = n;
 }
 
@@ -546,7 +591,8 @@ struct PrunedArgs {
     const float4* bbox32[2];
     const float4* tbox[2];    // 512-point tile boxes
     int npts[2], ppad[2];
-    int qtiles[2];
+    int qtiles[2];        // query tiles (kPrQ rows)
+    int cqtiles[2];       // candidate lists (kCandQ rows): query tile u reads list u / (kCandQ / kPrQ)
     int64_t cand_off[2];
     const unsigned long long* cand;
     const int* ccount;    // entries per list (candidates_kernel)
@@ -587,9 +633,12 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
     const float4* __restrict__ Q = a.sorted[qc] + (int64_t)b * a.ppad[qc];
     const float4* __restrict__ T = a.sorted[tc] + (int64_t)b * a.ppad[tc];
     const float4* __restrict__ TB = a.bbox32[tc] + (int64_t)b * tnt * kBlocksPerTile * 2;
+    // the list of the kCandQ-row group holding this tile: sorted by the group box's LB, a lower bound
+    // of this tile's (the group box contains it) — every skipped tile still has LB > every row's minimum
+    const int cu = u / (kCandQ / kPrQ);
     const unsigned long long* __restrict__ cand =
-        a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + u) * tnt;
-    const int ncand = a.ccount[(int64_t)(dir == 0 ? 0 : (int64_t)gridDim.y * a.qtiles[0]) + (int64_t)b * a.qtiles[dir] + u];
+        a.cand + a.cand_off[dir] + ((int64_t)b * a.cqtiles[dir] + cu) * tnt;
+    const int ncand = a.ccount[(int64_t)(dir == 0 ? 0 : (int64_t)gridDim.y * a.cqtiles[0]) + (int64_t)b * a.cqtiles[dir] + cu];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     if (threadIdx.x == 0) {
@@ -630,6 +679,19 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
             if (qbase + 2 * r + 1 < P) { llo[q] = fminf(llo[q], v1); lhi[q] = fmaxf(lhi[q], v1); }
         }
     }
+    // the warp's union box (all its lanes' rows): a block whose LB against it exceeds the warp's largest
+    // row minimum is needed by no lane (each lane box lies inside it)
+    float wlo[3], whi[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        wlo[q] = llo[q];
+        whi[q] = lhi[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wlo[q] = fminf(wlo[q], __shfl_xor_sync(0xffffffffu, wlo[q], o));
+            whi[q] = fmaxf(whi[q], __shfl_xor_sync(0xffffffffu, whi[q], o));
+        }
+    }
     auto lane_max = [&]() {
         float lmax = -1.0f;   // no valid row: never needs anything
 #pragma unroll
@@ -664,6 +726,9 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
             }
             const int t = (int)(e & 0xffffffffull);
             ++pos;
+#ifdef CD_PR_STATS
+            if (threadIdx.x == 0) atomicAdd(&g_pr_stats[3], 1ull);
+#endif
             const bool need = box_lb(llo, lhi, TT[2 * t], TT[2 * t + 1]) <= lmax;
             if (__syncthreads_or(need)) {
                 found = t;
@@ -700,7 +765,18 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         const float4* tb = sm[s];
         const float4* bb = smb[s];
         const int jt = t * kTile;
-        for (int kb = 0; kb < kTile; kb += kBlockK) {
+        // the tile's blocks some lane may still need, one lane per block against the warp's union box
+        // and largest row minimum (a superset: the exact per-lane test below decides)
+        unsigned bmask;
+        {
+            const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(lane_max(), 0.f))));
+            bool wneed = false;
+            if (lane < kBlocksPerTile) wneed = box_lb(wlo, whi, bb[2 * lane], bb[2 * lane + 1]) <= wmax;
+            bmask = __ballot_sync(0xffffffffu, wneed);
+        }
+        while (bmask) {
+            const int kb = (__ffs(bmask) - 1) * kBlockK;
+            bmask &= bmask - 1;
             // skip unless some lane may improve or tie: LB(lane box, block) <= the lane's largest minimum
             {
                 float lmax = -1.0f;   // no valid row: never needs a block
@@ -963,6 +1039,7 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
         const int unit = std::max(kPrQ, kTile);
         p.ppad[c] = cdiv(p.npts[c], unit) * unit;
         p.qtiles[c] = cdiv(p.npts[c], kPrQ);
+        p.cqtiles[c] = cdiv(p.npts[c], kCandQ);
         p.ttiles[c] = p.ppad[c] / kTile;
     }
     p.kbits = hilbert_bits(std::max(N, M));
@@ -970,8 +1047,8 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
     p.segs = SegSpec{B, N, B, M};
     p.L = (int64_t)B * (N + M);
     p.cand_off[0] = 0;
-    p.cand_off[1] = (int64_t)B * p.qtiles[0] * p.ttiles[1];
-    const int64_t ncand = p.cand_off[1] + (int64_t)B * p.qtiles[1] * p.ttiles[0];
+    p.cand_off[1] = (int64_t)B * p.cqtiles[0] * p.ttiles[1];
+    const int64_t ncand = p.cand_off[1] + (int64_t)B * p.cqtiles[1] * p.ttiles[0];
     p.nchunks[0] = cdiv(N, kMergeThreads);
     p.nchunks[1] = cdiv(M, kMergeThreads);
     p.chunk_off[0] = 0;
@@ -1001,7 +1078,7 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
     }
     p.hier = CD_PR_HIER && std::max(p.ttiles[0], p.ttiles[1]) >= kHierMinTiles;
     p.off_cand = take((size_t)ncand * 8);
-    p.off_ccount = take((size_t)B * (p.qtiles[0] + p.qtiles[1]) * 4);
+    p.off_ccount = take((size_t)B * (p.cqtiles[0] + p.cqtiles[1]) * 4);
     p.off_chunk_sum = take((size_t)chunks * 8);
     p.off_chunk_hits = take((size_t)chunks * 4);
     p.off_fb = take(256 + (size_t)p.L * 4);
@@ -1119,7 +1196,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
             a.box[c] = box[c];
             a.box32[c] = box32[c];
             a.ppad[c] = p.ppad[c];
-            a.qtiles[c] = p.qtiles[c];
+            a.qtiles[c] = p.cqtiles[c];
             a.cand_off[c] = p.cand_off[c];
             a.sbox[c] = p.hier ? sbox[c] : nullptr;
         }
@@ -1130,7 +1207,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         // keys (npow u64) + the super LBs (two-level search: ceil(T / kSuper) floats)
         const size_t smem = (size_t)npow * 8 + (size_t)(std::max(p.ttiles[0], p.ttiles[1]) / kSuper + 1) * 4;
         ensure_smem_attr((const void*)candidates_kernel, kPrMaxTiles * 8 + (kPrMaxTiles / kSuper + 1) * 4);
-        candidates_kernel<<<p.B * (p.qtiles[0] + p.qtiles[1]), 256, smem, st>>>(a);
+        candidates_kernel<<<p.B * (p.cqtiles[0] + p.cqtiles[1]), kCandThreads, smem, st>>>(a);
     }
     float* best_d[2];
     int* best_blk[2];
@@ -1147,6 +1224,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
             a.npts[c] = p.npts[c];
             a.ppad[c] = p.ppad[c];
             a.qtiles[c] = p.qtiles[c];
+            a.cqtiles[c] = p.cqtiles[c];
             a.cand_off[c] = p.cand_off[c];
             a.best_d[c] = best_d[c];
             a.best_blk[c] = best_blk[c];
@@ -1188,7 +1266,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         printf("pruned tie rows: %u of %lld\n", h, (long long)p.L);
         unsigned long long st3[4];
         cudaMemcpyFromSymbol(st3, g_pr_stats, sizeof(st3));
-        printf("tiles fetched %llu, tiles with >= 1 evaluated block %llu, warp-blocks evaluated %llu\n", st3[0], st3[2], st3[1]);
+        printf("candidates considered %llu, tiles fetched %llu, tiles with >= 1 evaluated block %llu, warp-blocks evaluated %llu\n", st3[3], st3[0], st3[2], st3[1]);
         unsigned long long z[4] = {0, 0, 0, 0};
         cudaMemcpyToSymbol(g_pr_stats, z, sizeof(z));
 #endif
