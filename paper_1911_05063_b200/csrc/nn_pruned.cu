@@ -610,10 +610,17 @@ __device__ __forceinline__ float box_lb(const float wlo[3], const float whi[3], 
 #ifdef CD_PR_STATS
 __device__ unsigned long long g_pr_stats[4];
 #endif
-__global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) {
-    __shared__ __align__(128) float4 sm[kStages][kTile];
-    __shared__ __align__(128) float4 smb[kStages][kBlocksPerTile * 2];   // the tile's 32-point block boxes
-    __shared__ __align__(8) u64 full_bar[kStages];
+#ifndef CD_PR_STAGES
+#define CD_PR_STAGES 2
+#endif
+constexpr int kPrStages = CD_PR_STAGES;   // TMA ring depth of the pruned kernel
+#ifndef CD_PR_MINB
+#define CD_PR_MINB 4
+#endif
+__global__ void __launch_bounds__(kPrThreads, CD_PR_MINB) nn_pruned_kernel(PrunedArgs a) {
+    __shared__ __align__(128) float4 sm[kPrStages][kTile];
+    __shared__ __align__(128) float4 smb[kPrStages][kBlocksPerTile * 2];   // the tile's 32-point block boxes
+    __shared__ __align__(8) u64 full_bar[kPrStages];
     __shared__ unsigned s_wmax[kPrThreads / 32];
 #ifdef CD_PR_STATS
     __shared__ int s_used;
@@ -642,7 +649,7 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+        for (int s = 0; s < kPrStages; ++s) mbar_init(&full_bar[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -746,10 +753,10 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
             tma_load_1d(smb[s], TB + (int64_t)t * kBlocksPerTile * 2, kBlocksPerTile * 32, &full_bar[s]);
         }
     };
-    int tiles[kStages];
+    int tiles[kPrStages];
     int tail = 0;
 #pragma unroll
-    for (int k = 0; k < kStages; ++k) {
+    for (int k = 0; k < kPrStages; ++k) {
         const int t = advance();
         tiles[k] = t;
         if (t < 0) break;
@@ -757,11 +764,11 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         ++tail;
     }
     for (int head = 0; head < tail; ++head) {
-        const int s = head % kStages;
+        const int s = head % kPrStages;
         int t = tiles[0];
 #pragma unroll
-        for (int q = 1; q < kStages; ++q) t = s == q ? tiles[q] : t;
-        mbar_wait(&full_bar[s], (head / kStages) & 1);
+        for (int q = 1; q < kPrStages; ++q) t = s == q ? tiles[q] : t;
+        mbar_wait(&full_bar[s], (head / kPrStages) & 1);
         const float4* tb = sm[s];
         const float4* bb = smb[s];
         const int jt = t * kTile;
@@ -832,7 +839,7 @@ __global__ void __launch_bounds__(kPrThreads, 4) nn_pruned_kernel(PrunedArgs a) 
         const int tn = advance();
         if (tn >= 0) {
 #pragma unroll
-            for (int q = 0; q < kStages; ++q) tiles[q] = s == q ? tn : tiles[q];
+            for (int q = 0; q < kPrStages; ++q) tiles[q] = s == q ? tn : tiles[q];
             issue(tn, s);
             ++tail;
         }
