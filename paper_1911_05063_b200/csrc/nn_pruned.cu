@@ -8,10 +8,11 @@
 //   radix sort         (nn_backward.cu) every (cloud, batch) segment on its own -> Hilbert order.
 //   gather_kernel      sorted packed float4 clouds + permutation (sorted position -> original row).
 //   aabb_kernel        bounding box of every 512-point tile of the sorted clouds.
-//   candidates_kernel  per query tile (256 sorted rows): lower bound LB of the squared distance to
+//   candidates_kernel  per query tile (128 sorted rows): lower bound LB of the squared distance to
 //                      every target tile (box-box gap, scaled by (1 - 1e-5) so it is a strict lower
-//                      bound of the fp32-evaluated distances), bitonic-sorted ascending.
-//   nn_pruned_kernel   per query tile: target tiles in LB order through the 3-stage TMA ring, the
+//                      bound of the fp32-evaluated distances; large clouds: via 16-tile super tiles),
+//                      sorted ascending.
+//   nn_pruned_kernel   per query tile: target tiles in LB order through the 2-stage TMA ring, the
 //                      same packed-FP32 value-only min + block argmin tracking as nn_fwd_kernel; stops
 //                      at the first tile with LB > max over the CTA's rows of the current minimum:
 //                      every skipped pair has d > that row's minimum, so the minimum is exact.
@@ -28,6 +29,8 @@
 
 namespace cdk {
 
+// Geometry (the -D overrides exist for tools/build_variant.py sweeps; the defaults are the measured
+// best of profiles/r02_experiments.txt): 2 rows x 64 threads = 128-row query tiles, own candidate lists.
 #ifndef CD_PR_R
 #define CD_PR_R 2
 #endif
@@ -875,9 +878,6 @@ struct PrResolveArgs {
     unsigned* fb_list;     // (dir << 31) | b * P + p
 };
 
-#ifndef CD_RESOLVE_BATCH
-#define CD_RESOLVE_BATCH 8   // targets loaded together per row
-#endif
 __global__ void __launch_bounds__(kMergeThreads) pruned_resolve_kernel(PrResolveArgs a) {
     int u = blockIdx.x;
     int dir = 0;
