@@ -46,7 +46,16 @@ constexpr int kPrQ = kPrThreads * kPrR;         // sorted rows per query tile of
 constexpr int kCandQ = CD_CAND_Q;               // sorted rows per candidate list (query tiles may share one)
 static_assert(kCandQ % kPrQ == 0, "a candidate list covers whole query tiles");
 constexpr int kPrMaxTiles = 8192;               // target tiles per batch supported by the LB sort
+static_assert(kPrMaxTiles <= (1 << 13), "candidate keys hold a 13-bit tile index");
 constexpr float kLbScale = 0.99999f;            // LB' = LB * (1 - 1e-5): strict lower bound margin
+// Candidate keys: the top 19 bits of LB' (>= 0: sign, exponent, 10 mantissa bits — truncation rounds
+// DOWN, so the key's LB is still a lower bound) above the 13-bit tile index (< kPrMaxTiles); ascending
+// keys = ascending LB, ties by tile.  32 bits halve the sort's shared memory (more CTAs per SM).
+__device__ __forceinline__ uint32_t cand_key(float lb, int t) {
+    return (__float_as_uint(lb) & 0xFFFFE000u) | (uint32_t)t;
+}
+__device__ __forceinline__ float cand_lb(uint32_t k) { return __uint_as_float(k & 0xFFFFE000u); }
+__device__ __forceinline__ int cand_tile(uint32_t k) { return (int)(k & 0x1FFFu); }
 
 // --------------------------------------------------------------------------------------------- bbox
 struct BoxArgs {
@@ -384,7 +393,7 @@ struct CandArgs {
     int B;
     int qtiles[2];            // candidate lists (kCandQ rows) per batch element, per dir
     int64_t cand_off[2];      // offset of dir's lists in `cand` (u64 entries)
-    unsigned long long* cand; // per (dir, b, query tile): up to ttiles(1-dir) keys (LB' bits << 32 | tile)
+    uint32_t* cand;           // per (dir, b, query tile): up to ttiles(1-dir) keys (cand_key: LB' | tile)
     int* ccount;              // per list: number of entries (LB <= UB), lists of dir 1 after dir 0's
     const float4* sbox[2];    // [B][nst][2] super-tile boxes (kSuper tiles), or null: flat scan
 };
@@ -429,7 +438,7 @@ __device__ __forceinline__ float gap(float qlo, float qhi, float tlo, float thi)
 #endif
 constexpr int kCandThreads = CD_CAND_THREADS;
 __global__ void __launch_bounds__(kCandThreads) candidates_kernel(CandArgs a) {
-    extern __shared__ unsigned long long keys[];
+    extern __shared__ uint32_t keys[];
     int u = blockIdx.x;
     int dir = 0;
     if (u >= a.B * a.qtiles[0]) {
@@ -490,7 +499,7 @@ __global__ void __launch_bounds__(kCandThreads) candidates_kernel(CandArgs a) {
         ub = block_min(ub);
         for (int t = threadIdx.x; t < tnt; t += kCandThreads) {
             const float lb = tile_lb(tbox[2 * t], tbox[2 * t + 1]);
-            if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+            if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = cand_key(lb, t);
         }
     } else {
         // two levels (large clouds): LB of every super tile (kSuper tiles; a tile's LB >= its super
@@ -526,30 +535,30 @@ __global__ void __launch_bounds__(kCandThreads) candidates_kernel(CandArgs a) {
             const int t = s_sup[i / kSuper] * kSuper + (i % kSuper);
             if (t >= tnt) continue;
             const float lb = tile_lb(tbox[2 * t], tbox[2 * t + 1]);
-            if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = ((unsigned long long)__float_as_uint(lb) << 32) | (unsigned)t;
+            if (lb <= ub) keys[atomicAdd(&s_cnt, 1)] = cand_key(lb, t);
         }
     }
     __syncthreads();
     const int n = s_cnt;
     const int64_t list = (int64_t)(dir == 0 ? 0 : a.B * a.qtiles[0]) + (int64_t)b * a.qtiles[dir] + q;
-    unsigned long long* out = a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + q) * tnt;
+    uint32_t* out = a.cand + a.cand_off[dir] + ((int64_t)b * a.qtiles[dir] + q) * tnt;
     if (n <= 64) {
         // short list (the common case): one warp sorts it in registers, two keys per lane (bitonic
         // network over 64 slots by shuffles and an in-lane exchange; no block barriers)
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
-            unsigned long long v0 = lane < n ? keys[lane] : ~0ull;        // slot lane
-            unsigned long long v1 = lane + 32 < n ? keys[lane + 32] : ~0ull;   // slot lane + 32
+            uint32_t v0 = lane < n ? keys[lane] : ~0u;        // slot lane
+            uint32_t v1 = lane + 32 < n ? keys[lane + 32] : ~0u;   // slot lane + 32
             for (int k = 2; k <= 64; k <<= 1) {
                 for (int j = k >> 1; j > 0; j >>= 1) {
                     if (j == 32) {   // partner slot is in the same lane
                         const bool up = (lane & k) == 0;   // k == 64: ascending
-                        const unsigned long long lo = min(v0, v1), hi = max(v0, v1);
+                        const uint32_t lo = min(v0, v1), hi = max(v0, v1);
                         v0 = up ? lo : hi;
                         v1 = up ? hi : lo;
                     } else {
-                        const unsigned long long o0 = __shfl_xor_sync(0xffffffffu, v0, j);
-                        const unsigned long long o1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, v1, j);
                         const bool lower = (lane & j) == 0;
                         const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
                         v0 = (lower == up0) ? min(v0, o0) : max(v0, o0);
@@ -565,7 +574,7 @@ __global__ void __launch_bounds__(kCandThreads) candidates_kernel(CandArgs a) {
     }
     int npow = 1;
     while (npow < n) npow <<= 1;
-    for (int t = n + threadIdx.x; t < npow; t += kCandThreads) keys[t] = ~0ull;
+    for (int t = n + threadIdx.x; t < npow; t += kCandThreads) keys[t] = ~0u;
     __syncthreads();
     // bitonic sort ascending (npow <= kPrMaxTiles)
     for (int k = 2; k <= npow; k <<= 1) {
@@ -573,7 +582,7 @@ __global__ void __launch_bounds__(kCandThreads) candidates_kernel(CandArgs a) {
             for (int i = threadIdx.x; i < npow; i += kCandThreads) {
                 const int l = i ^ j;
                 if (l > i) {
-                    const unsigned long long x = keys[i], y = keys[l];
+                    const uint32_t x = keys[i], y = keys[l];
                     const bool up = (i & k) == 0;
                     if ((x > y) == up) {
                         keys[i] = y;
@@ -597,7 +606,7 @@ struct PrunedArgs {
     int qtiles[2];        // query tiles (kPrQ rows)
     int cqtiles[2];       // candidate lists (kCandQ rows): query tile u reads list u / (kCandQ / kPrQ)
     int64_t cand_off[2];
-    const unsigned long long* cand;
+    const uint32_t* cand;
     const int* ccount;    // entries per list (candidates_kernel)
     float* best_d[2];     // [B][npts] sorted order
     int* best_blk[2];     // sorted target position of the winning block
@@ -646,7 +655,7 @@ __global__ void __launch_bounds__(kPrThreads, CD_PR_MINB) nn_pruned_kernel(Prune
     // the list of the kCandQ-row group holding this tile: sorted by the group box's LB, a lower bound
     // of this tile's (the group box contains it) — every skipped tile still has LB > every row's minimum
     const int cu = u / (kCandQ / kPrQ);
-    const unsigned long long* __restrict__ cand =
+    const uint32_t* __restrict__ cand =
         a.cand + a.cand_off[dir] + ((int64_t)b * a.cqtiles[dir] + cu) * tnt;
     const int ncand = a.ccount[(int64_t)(dir == 0 ? 0 : (int64_t)gridDim.y * a.cqtiles[0]) + (int64_t)b * a.cqtiles[dir] + cu];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -729,12 +738,12 @@ __global__ void __launch_bounds__(kPrThreads, CD_PR_MINB) nn_pruned_kernel(Prune
         const float lmax = lane_max();
         int found = -1;
         while (pos < ncand) {
-            const unsigned long long e = cand[pos];
-            if (__uint_as_float((unsigned)(e >> 32)) > maxbest) {
+            const uint32_t e = cand[pos];
+            if (cand_lb(e) > maxbest) {
                 pos = ncand;
                 break;
             }
-            const int t = (int)(e & 0xffffffffull);
+            const int t = cand_tile(e);
             ++pos;
 #ifdef CD_PR_STATS
             if (threadIdx.x == 0) atomicAdd(&g_pr_stats[3], 1ull);
@@ -1084,7 +1093,7 @@ void plan_pruned(PrunedPlan& p, int B, int N, int M) {
         p.off_sbox[c] = take((size_t)B * ((p.ttiles[c] + kSuper - 1) / kSuper) * 32);
     }
     p.hier = CD_PR_HIER && std::max(p.ttiles[0], p.ttiles[1]) >= kHierMinTiles;
-    p.off_cand = take((size_t)ncand * 8);
+    p.off_cand = take((size_t)ncand * 4);
     p.off_ccount = take((size_t)B * (p.cqtiles[0] + p.cqtiles[1]) * 4);
     p.off_chunk_sum = take((size_t)chunks * 8);
     p.off_chunk_hits = take((size_t)chunks * 4);
@@ -1189,7 +1198,7 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         const int64_t tiles = (int64_t)p.B * (p.ttiles[0] + p.ttiles[1]);
         aabb_kernel<<<cdiv(tiles * 32, 256), 256, 0, st>>>(a);
     }
-    unsigned long long* cand = reinterpret_cast<unsigned long long*>(w + p.off_cand);
+    uint32_t* cand = reinterpret_cast<uint32_t*>(w + p.off_cand);
     float4* sbox[2] = {reinterpret_cast<float4*>(w + p.off_sbox[0]), reinterpret_cast<float4*>(w + p.off_sbox[1])};
     if (p.hier) {
         const int64_t n = (int64_t)p.B * ((p.ttiles[0] + kSuper - 1) / kSuper + (p.ttiles[1] + kSuper - 1) / kSuper);
@@ -1212,8 +1221,8 @@ cudaError_t launch_pruned(const PrunedPlan& p, const float* x, const float* y, c
         int npow = 1;
         while (npow < std::max(p.ttiles[0], p.ttiles[1])) npow <<= 1;
         // keys (npow u64) + the super LBs (two-level search: ceil(T / kSuper) floats)
-        const size_t smem = (size_t)npow * 8 + (size_t)(std::max(p.ttiles[0], p.ttiles[1]) / kSuper + 1) * 4;
-        ensure_smem_attr((const void*)candidates_kernel, kPrMaxTiles * 8 + (kPrMaxTiles / kSuper + 1) * 4);
+        const size_t smem = (size_t)npow * 4 + (size_t)(std::max(p.ttiles[0], p.ttiles[1]) / kSuper + 1) * 4;
+        ensure_smem_attr((const void*)candidates_kernel, kPrMaxTiles * 4 + (kPrMaxTiles / kSuper + 1) * 4);
         candidates_kernel<<<p.B * (p.cqtiles[0] + p.cqtiles[1]), kCandThreads, smem, st>>>(a);
     }
     float* best_d[2];
