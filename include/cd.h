@@ -41,7 +41,8 @@
 extern "C" {
 #endif
 
-#define CD_ABI_VERSION 4
+#define CD_ABI_VERSION 5
+#define CD_MAX_PEERS 16   /* cd_forward_cols_peers: most key arrays reduced on read */
 
 #if defined(__GNUC__)
 #define CD_API __attribute__((visibility("default")))
@@ -119,6 +120,24 @@ CD_API cd_status cd_forward_cols(const float* x, const float* y, int B, int N, i
                           const int64_t* colkeys, int r0, int r1, float* d_yx, int32_t* idx_yx,
                           double* partials, float tau,
                           void* workspace, size_t workspace_bytes, cd_stream_t stream);
+
+/*
+ * cd_forward_cols_peers — cd_forward_cols with the all-reduce MIN of the column keys fused into the
+ * resolve (query sharding without a separate collective): the key of column j is the
+ * element-wise MIN over the npeers arrays colkeys[0..npeers) (each B x M int64 as cd_forward_rows
+ * writes them), read directly — typically this rank's array and its peers' arrays mapped over
+ * NVLink (CUDA peer access / symmetric memory).  Only the keys of the resolved slice [r0, r1) are
+ * read (a reduce-scatter's traffic, not an all-reduce's).
+ *   colkeys: HOST array of npeers DEVICE pointers, each 8-byte aligned and readable from the
+ *     current device; the caller guarantees every array is complete (all ranks' cd_forward_rows
+ *     finished, e.g. a cross-device barrier) before the launch and stays unmodified until it ends.
+ *   1 <= npeers <= CD_MAX_PEERS, else CD_ERR_INVALID_VALUE; other arguments, outputs and results
+ *   exactly as cd_forward_cols given the MIN-reduced keys (bit-identical).
+ */
+CD_API cd_status cd_forward_cols_peers(const float* x, const float* y, int B, int N, int M,
+                                const int64_t* const* colkeys, int npeers, int r0, int r1,
+                                float* d_yx, int32_t* idx_yx, double* partials, float tau,
+                                void* workspace, size_t workspace_bytes, cd_stream_t stream);
 
 /*
  * cd_forward_pruned — the same outputs as cd_forward on the full problem (q0=0,q1=N,r0=0,r1=M)

@@ -18,7 +18,7 @@ if os.environ.get("CD_LIB_VARIANT"):
 HEADER = os.path.join(os.path.dirname(HERE), "include", "cd.h")
 
 CD_OK = 0
-ABI_VERSION = 4
+ABI_VERSION = 5
 CD_OP_FORWARD, CD_OP_FSCORE, CD_OP_BACKWARD, CD_OP_STEP, CD_OP_FORWARD_PRUNED = 0, 1, 2, 3, 4
 CD_OP_SAMPLE, CD_OP_SAMPLE_BACKWARD, CD_OP_P2S, CD_OP_P2S_BACKWARD, CD_OP_P2S_PRUNED = 5, 6, 7, 8, 9
 STATUS_NAMES = {0: "CD_OK", 1: "CD_ERR_INVALID_VALUE", 2: "CD_ERR_MISALIGNED", 3: "CD_ERR_TOO_LARGE",
@@ -62,6 +62,7 @@ _SIGS = {
     "cd_p2s_forward_pruned": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "cd_forward_rows": ([vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, f32, vp, sz, vp], i32),
     "cd_forward_cols": ([vp, vp, i32, i32, i32, vp, i32, i32, vp, vp, vp, f32, vp, sz, vp], i32),
+    "cd_forward_cols_peers": ([vp, vp, i32, i32, i32, vp, i32, i32, i32, vp, vp, vp, f32, vp, sz, vp], i32),
 }
 
 

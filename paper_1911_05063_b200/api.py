@@ -146,9 +146,10 @@ COLKEY_EMPTY = (1 << 63) - 1
 
 
 @_device_guard
-def forward_rows(x: torch.Tensor, y: torch.Tensor, q_slice, tau: float | None = None, partials=None):
+def forward_rows(x: torch.Tensor, y: torch.Tensor, q_slice, tau: float | None = None, partials=None, keys=None):
     """cd_forward_rows: X rows q_slice fully + column keys for every Y point (query sharding).
 
+    keys: optional [B,M] int64 output tensor (e.g. a symmetric-memory buffer peers read).
     Returns (d_xy, idx_xy, colkeys[B,M] int64, partials[B,4] fp64 with columns 0 and 2 set)."""
     x = _check_cloud(x, "x")
     y = _check_cloud(y, "y")
@@ -158,7 +159,10 @@ def forward_rows(x: torch.Tensor, y: torch.Tensor, q_slice, tau: float | None = 
     dev = x.device
     d_xy = torch.empty((B, q1 - q0), dtype=torch.float32, device=dev)
     i_xy = torch.empty((B, q1 - q0), dtype=torch.int32, device=dev)
-    keys = torch.empty((B, M), dtype=torch.int64, device=dev)
+    if keys is None:
+        keys = torch.empty((B, M), dtype=torch.int64, device=dev)
+    elif keys.dtype != torch.int64 or tuple(keys.shape) != (B, M) or not keys.is_contiguous() or keys.device != dev:
+        raise TypeError(f"keys must be a contiguous int64 ({B}, {M}) tensor on {dev}")
     if partials is None:
         partials = torch.zeros((B, 4), dtype=torch.float64, device=dev)
     ws = workspace(_lib.CD_OP_FORWARD, B, N, M, dev)
@@ -187,6 +191,39 @@ def forward_cols(x: torch.Tensor, y: torch.Tensor, colkeys: torch.Tensor, r_slic
     check(_lib.load().cd_forward_cols(_ptr(x), _ptr(y), B, N, M, _ptr(colkeys.contiguous()), r0, r1, _ptr(d_yx),
                                       _ptr(i_yx), _ptr(partials), float(-1.0 if tau is None else tau), _ptr(ws),
                                       ws.numel(), _stream()))
+    return d_yx, i_yx, partials
+
+
+@_device_guard
+def forward_cols_peers(x: torch.Tensor, y: torch.Tensor, colkeys, r_slice, tau: float | None = None,
+                       partials=None):
+    """cd_forward_cols_peers: resolve Y rows r_slice from the element-wise MIN of several [B,M] int64 key
+    arrays read directly by the resolve kernel (the all-reduce fused into it).  colkeys: a list of
+    tensors on x's device or of raw device pointers (ints, e.g. symmetric-memory peer buffers the
+    caller has synchronised).  Returns (d_yx, idx_yx, partials) as forward_cols."""
+    x = _check_cloud(x, "x")
+    y = _check_cloud(y, "y")
+    B, N, _ = x.shape
+    M = y.shape[1]
+    r0, r1 = r_slice
+    dev = x.device
+    ptrs = []
+    for k in colkeys:
+        if isinstance(k, torch.Tensor):
+            if k.dtype != torch.int64 or tuple(k.shape) != (B, M) or not k.is_contiguous() or k.device != dev:
+                raise TypeError(f"each key array must be a contiguous int64 ({B}, {M}) tensor on {dev}")
+            ptrs.append(k.data_ptr())
+        else:
+            ptrs.append(int(k))
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
+    d_yx = torch.empty((B, r1 - r0), dtype=torch.float32, device=dev)
+    i_yx = torch.empty((B, r1 - r0), dtype=torch.int32, device=dev)
+    if partials is None:
+        partials = torch.zeros((B, 4), dtype=torch.float64, device=dev)
+    ws = workspace(_lib.CD_OP_FORWARD, B, N, M, dev)
+    check(_lib.load().cd_forward_cols_peers(_ptr(x), _ptr(y), B, N, M, arr, len(ptrs), r0, r1, _ptr(d_yx),
+                                            _ptr(i_yx), _ptr(partials), float(-1.0 if tau is None else tau),
+                                            _ptr(ws), ws.numel(), _stream()))
     return d_yx, i_yx, partials
 
 

@@ -287,6 +287,44 @@ cd_status cd_forward_cols(const float* x, const float* y, int B, int N, int M, c
                        "cd_forward_cols");
 }
 
+cd_status cd_forward_cols_peers(const float* x, const float* y, int B, int N, int M, const int64_t* const* colkeys,
+                                int npeers, int r0, int r1, float* d_yx, int32_t* idx_yx, double* partials,
+                                float tau, void* workspace, size_t workspace_bytes, cd_stream_t stream) {
+    g_err.clear();
+    cd_status s = check_sizes(B, N, M);
+    if (s != CD_OK) return s;
+    if (!x || !y || !workspace || !colkeys) return fail(CD_ERR_INVALID_VALUE, "null x, y, colkeys or workspace");
+    if (npeers < 1 || npeers > CD_MAX_PEERS)
+        return fail(CD_ERR_INVALID_VALUE, "npeers must be in [1, %d] (got %d)", CD_MAX_PEERS, npeers);
+    for (int q = 0; q < npeers; ++q) {
+        if (!colkeys[q]) return fail(CD_ERR_INVALID_VALUE, "colkeys[%d] is null", q);
+        if (!aligned(colkeys[q], 8)) return fail(CD_ERR_MISALIGNED, "colkeys[%d] must be 8-byte aligned", q);
+    }
+    if (r0 < 0 || r1 < r0 || r1 > M) return fail(CD_ERR_INVALID_VALUE, "bad column slice [%d,%d) of M=%d", r0, r1, M);
+    if (r1 > r0 && (!d_yx || !idx_yx)) return fail(CD_ERR_INVALID_VALUE, "null d_yx / idx_yx");
+    if (tau != tau) return fail(CD_ERR_INVALID_VALUE, "tau is NaN");
+    if (!aligned(x, 4) || !aligned(y, 4)) return fail(CD_ERR_MISALIGNED, "cloud pointers must be 4-byte aligned");
+    if (!aligned(workspace, 256)) return fail(CD_ERR_MISALIGNED, "workspace must be 256-byte aligned");
+    cdk::FwdPlan p;
+    cdk::plan_forward(p, cdk::kFusedCols, B, N, M, 0, 0, r0, r1, g_forced_splits);
+    if (workspace_bytes < p.bytes)
+        return fail(CD_ERR_TOO_LARGE, "workspace too small: %zu < %zu bytes", workspace_bytes, p.bytes);
+    s = check_device();
+    if (s != CD_OK) return s;
+    cdk::FwdOutputs o;
+    o.d[0] = nullptr;
+    o.d[1] = d_yx;
+    o.idx[0] = nullptr;
+    o.idx[1] = idx_yx;
+    o.partials = partials;
+    o.tau = tau;
+    o.colkey = const_cast<long long*>(reinterpret_cast<const long long*>(colkeys[0]));
+    o.npeers = npeers;
+    for (int q = 0; q < npeers; ++q) o.colkey_peers[q] = reinterpret_cast<const long long*>(colkeys[q]);
+    return cuda_status(cdk::launch_forward(p, x, y, o, workspace, static_cast<cudaStream_t>(stream)),
+                       "cd_forward_cols_peers");
+}
+
 cd_status cd_forward_pruned(const float* x, const float* y, int B, int N, int M, float* d_xy, int32_t* idx_xy,
                             float* d_yx, int32_t* idx_yx, double* partials, float tau, void* workspace,
                             size_t workspace_bytes, cd_stream_t stream) {

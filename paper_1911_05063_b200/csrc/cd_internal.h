@@ -15,6 +15,8 @@ enum FwdMode { kUnfused = 0, kFusedFull = 1, kFusedRows = 2, kFusedCols = 3, kTe
 constexpr long long kColKeyEmpty = 0x7fffffffffffffffLL;
 
 // Forward problem description (one direction = "dir": 0 = X queries vs Y targets, 1 = Y vs X).
+constexpr int kMaxPeers = 16;   // cd_forward_cols_peers: key arrays reduced on read (CD_MAX_PEERS)
+
 struct FwdPlan {
     int mode;
     int B;
@@ -42,6 +44,10 @@ struct FwdOutputs {
     double* partials;   // B x 4 or nullptr
     float tau;          // < 0: no hits
     long long* colkey;  // fused rows/cols modes: caller's B x M column keys (out / in)
+    // cols mode, peer reads (cd_forward_cols_peers): the column keys are the element-wise MIN of
+    // npeers B x M arrays (this rank's and its peers', read over NVLink), reduced as they are read
+    const long long* colkey_peers[kMaxPeers];
+    int npeers = 0;
 };
 
 // Tensor-core forward (nn_tc.cu, R27): full problems only.

@@ -340,6 +340,8 @@ struct ResolveArgs {
     int r0, r1;            // Y rows to resolve
     int B, nchunks;
     const long long* colkey;
+    const long long* colkey_peers[kMaxPeers];   // npeers > 0: key = MIN over these arrays (peer reads)
+    int npeers;
     float* d_out;          // [B][r1-r0]
     int32_t* idx_out;
     double* chunk_sum;     // dir-1 chunk partials
@@ -361,7 +363,16 @@ __device__ __forceinline__ void col_resolve_block(const ResolveArgs& a, int blk)
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sj < slen) {
         const int j = a.r0 + sj;
-        const unsigned long long key = (unsigned long long)a.colkey[(int64_t)b * a.M + j];
+        long long kk;
+        if (a.npeers > 0) {
+            // the fused all-reduce: this column's keys from every rank's array (peer loads over
+            // NVLink), MIN on read — only the resolved slice's keys cross the fabric
+            kk = __ldcv(a.colkey_peers[0] + (int64_t)b * a.M + j);
+            for (int q = 1; q < a.npeers; ++q) kk = min(kk, __ldcv(a.colkey_peers[q] + (int64_t)b * a.M + j));
+        } else {
+            kk = a.colkey[(int64_t)b * a.M + j];
+        }
+        const unsigned long long key = (unsigned long long)kk;
         // a +inf minimum is no finite candidate (R6): (+inf, -1) like the row direction
         if ((long long)key != kColKeyEmpty && __uint_as_float((unsigned)(key >> 32)) < INFINITY) {
             m = __uint_as_float((unsigned)(key >> 32));
@@ -822,6 +833,8 @@ cudaError_t launch_forward(const FwdPlan& p, const float* x, const float* y, con
         ra.B = p.B;
         ra.nchunks = p.nchunks[1];
         ra.colkey = colkey;
+        ra.npeers = o.npeers;
+        for (int q = 0; q < kMaxPeers; ++q) ra.colkey_peers[q] = q < o.npeers ? o.colkey_peers[q] : nullptr;
         ra.d_out = o.d[1];
         ra.idx_out = o.idx[1];
         ra.chunk_sum = chunk_sum + p.chunk_off[1];

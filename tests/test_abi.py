@@ -50,7 +50,7 @@ def test_only_cd_symbols_exported():
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.cd_abi_version() == 4
+    assert lib.cd_abi_version() == 5
     assert lib.cd_status_string(0) == b"CD_OK"
     assert lib.cd_status_string(1) == b"CD_ERR_INVALID_VALUE"
     assert lib.cd_status_string(5) == b"CD_ERR_CUDA"

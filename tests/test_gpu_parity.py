@@ -493,6 +493,41 @@ def test_rows_cols_sharding_emulated(cd, world):
     np.testing.assert_array_equal(part.cpu().numpy()[:, 2:], full[4][:, 2:])
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_cols_peers_fused_reduce(cd, world):
+    """cd_forward_cols_peers (the column-key all-reduce fused into the resolve: MIN over the ranks'
+    key arrays as they are read) on one GPU with each emulated rank's keys in its own array: every
+    rank's Y slice equals cd_forward_cols on the MIN-reduced keys and the full forward, bit for bit;
+    the partials' columns 1 and 3 as well."""
+    from paper_1911_05063_b200.distributed import shard_range
+    X, Y = synth.shape_pair(2, 5000, 4100, config_index=51)
+    x, y, full = _run(cd, X, Y, tau=0.01)
+    B, N, M = 2, 5000, 4100
+    keys = []
+    for r in range(world):
+        kr = torch.empty((B, M), dtype=torch.int64, device="cuda")
+        cd.forward_rows(x, y, shard_range(N, r, world), tau=0.01, keys=kr)
+        keys.append(kr)
+    red = keys[0].clone()
+    for k in keys[1:]:
+        red = torch.minimum(red, k)
+    dcat, icat = [], []
+    for r in range(world):
+        sl = shard_range(M, r, world)
+        d1, i1, p1 = cd.forward_cols_peers(x, y, keys, sl, tau=0.01)
+        d2, i2, p2 = cd.forward_cols(x, y, red, sl, tau=0.01)
+        assert torch.equal(d1, d2) and torch.equal(i1, i2) and torch.equal(p1, p2)
+        dcat.append(d1)
+        icat.append(i1)
+    np.testing.assert_array_equal(torch.cat(dcat, 1).cpu().numpy(), full[2])
+    np.testing.assert_array_equal(torch.cat(icat, 1).cpu().numpy(), full[3])
+    # raw device pointers are accepted too (peer buffers), and bad counts are rejected
+    d3, i3, _ = cd.forward_cols_peers(x, y, [k.data_ptr() for k in keys], (0, M), tau=0.01)
+    np.testing.assert_array_equal(d3.cpu().numpy(), full[2])
+    with pytest.raises(Exception):
+        cd.forward_cols_peers(x, y, [], (0, M))
+
+
 # ------------------------------------------------------------------------------ exact pruned path (NEXT-2)
 def _check_pruned_vs_brute(cd, X, Y, tau=0.01):
     """cd_forward_pruned must give the brute-force results bit for bit: distances, and indices
