@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline oracle sample")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--colkey-exchange", choices=("nccl", "peer"), default="nccl",
+                    help="query sharding's column-key exchange: NCCL all-reduce MIN, or peer reads of "
+                         "symmetric-memory key arrays reduced inside the resolve kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--quiet", action="store_true")
@@ -264,7 +267,8 @@ def _traffic(kernel, cfg):
         return None
 
 
-COLL_NAMES = ("broadcast_clouds", "all_reduce_min_colkeys", "all_reduce_partials", "all_gather_idx")
+COLL_NAMES = ("broadcast_clouds", "all_reduce_min_colkeys", "peer_barrier_keys_ready", "peer_barrier_keys_read",
+              "all_reduce_partials", "all_gather_idx")
 
 
 def _mean_ms(torch, fn, flush, K, warmup=1):
@@ -514,11 +518,23 @@ def main():
     # the fused kernel evaluates each distance once for both directions: B*N*M evaluations per launch
     evals_fwd_launch = (B * N * M) // world if query_sharded else B_local * N * M
     prof = pdist.CollectiveTimer() if world > 1 else None
+    # column-key exchange of query sharding: the NCCL all-reduce MIN (default), or --colkey-exchange
+    # peer: symmetric-memory key arrays MIN-reduced inside the resolve kernel (cd_forward_cols_peers);
+    # every rank must agree, so an unavailable peer path falls back to NCCL on all ranks
+    peer = None
+    if query_sharded and args.colkey_exchange == "peer":
+        peer = pdist.PeerColKeys.create(B, M, dev)
+        ok = torch.tensor([1 if peer is not None else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            peer = None
+    colkey_exchange = ("peer reads of symmetric-memory key arrays, MIN fused into the resolve"
+                       if peer is not None else f"{dist.get_backend()} all_reduce MIN") if query_sharded else None
 
     def step():
         if query_sharded:
             pdist.broadcast_clouds(x, y, src=0, prof=prof)
-            return pdist.query_sharded_step(cd, x, y, tau=tau, w1=w1, w2=w2, prof=prof)
+            return pdist.query_sharded_step(cd, x, y, tau=tau, w1=w1, w2=w2, prof=prof, peer=peer)
         return pdist.batch_sharded_step(cd, x, y, B_global, b0, tau=tau, w1=w1, w2=w2, prof=prof)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -591,7 +607,7 @@ def main():
         ct = torch.tensor([sum(coll.values())] + [coll.get(n, 0.0) for n in COLL_NAMES], dtype=torch.float64,
                           device=dev)
         dist.all_reduce(ct, op=dist.ReduceOp.MAX)
-        multi = {"ranks": dist.get_world_size(), "backend": dist.get_backend(),
+        multi = {"ranks": dist.get_world_size(), "backend": dist.get_backend(), "colkey_exchange": colkey_exchange,
                  "collective_ms_per_step_max_rank": ct[0].item() / K,
                  "collective_share_of_step": ct[0].item() / K / ms_per_step,
                  "collectives_ms_per_step": {n: ct[i + 1].item() / K for i, n in enumerate(COLL_NAMES)

@@ -135,8 +135,47 @@ def allreduce_colkeys(keys: torch.Tensor, group=None, prof=None) -> torch.Tensor
     return keys
 
 
+class PeerColKeys:
+    """The column-key exchange of query sharding without a separate collective: every rank's
+    [B, M] int64 key array lives in torch symmetric memory (CUDA peer-mapped over NVLink); each rank's
+    cd_forward_rows writes its own array, a cross-device barrier publishes them, and each rank's
+    cd_forward_cols_peers reads the keys of ITS Y slice from every array and takes the MIN as it reads
+    (the all-reduce fused into the resolve kernel: a reduce-scatter's NVLink traffic, no NCCL call).
+    A second barrier before the arrays are rewritten.  create() returns None where symmetric memory is
+    unavailable (gloo, one rank, no peer access): callers keep the NCCL all-reduce path."""
+
+    def __init__(self, buf, handle, ptrs):
+        self.buf = buf
+        self.handle = handle
+        self.ptrs = ptrs
+
+    @staticmethod
+    def create(B: int, M: int, device, group=None):
+        try:
+            if not dist.is_initialized() or dist.get_world_size(group) < 2 or dist.get_backend(group) != "nccl":
+                return None
+            import torch.distributed._symmetric_memory as symm
+            grp = group if group is not None else dist.group.WORLD
+            if hasattr(symm, "enable_symm_mem_for_group"):
+                symm.enable_symm_mem_for_group(grp.group_name)
+            buf = symm.empty((B, M), dtype=torch.int64, device=device)
+            handle = symm.rendezvous(buf, grp)
+            ptrs = [int(p) for p in handle.buffer_ptrs]
+            if len(ptrs) != dist.get_world_size(group) or any(p == 0 for p in ptrs):
+                return None
+            return PeerColKeys(buf, handle, ptrs)
+        except Exception:   # no symmetric memory / peer access on this node: the all-reduce path
+            return None
+
+    def sources(self):
+        return self.ptrs
+
+    def barrier(self):
+        self.handle.barrier(channel=0)
+
+
 def query_sharded_step(engine, x, y, tau=None, w1: float = 1.0, w2: float = 1.0, group=None,
-                       backward: bool = True, prof=None):
+                       backward: bool = True, prof=None, peer=None):
     """One step with query rows split across ranks; x, y are full replicas on every rank.
 
     Rank r evaluates X rows q_r against all of Y ONCE (fused kernel): its d_xy rows are final and
@@ -146,7 +185,14 @@ def query_sharded_step(engine, x, y, tau=None, w1: float = 1.0, w2: float = 1.0,
     B, N, M = x.shape[0], x.shape[1], y.shape[1]
     q = shard_range(N, rank, world)
     r = shard_range(M, rank, world)
-    if hasattr(engine, "forward_rows"):
+    if peer is not None and hasattr(engine, "forward_cols_peers"):
+        # keys into this rank's peer-visible array; barrier; the resolve MIN-reduces every rank's
+        # keys of its Y slice as it reads them; barrier before the arrays are written again
+        d_xy, i_xy, _, part = engine.forward_rows(x, y, q, tau=tau, keys=peer.buf)
+        _coll(prof, "peer_barrier_keys_ready", peer.barrier)
+        d_yx, i_yx, part = engine.forward_cols_peers(x, y, peer.sources(), r, tau=tau, partials=part)
+        _coll(prof, "peer_barrier_keys_read", peer.barrier)
+    elif hasattr(engine, "forward_rows"):
         d_xy, i_xy, keys, part = engine.forward_rows(x, y, q, tau=tau)
         keys = allreduce_colkeys(keys, group, prof)
         d_yx, i_yx, part = engine.forward_cols(x, y, keys, r, tau=tau, partials=part)

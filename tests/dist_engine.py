@@ -5,6 +5,7 @@ include/cd.h (cd_forward slices, cd_forward_rows / cd_forward_cols keys, cd_fina
 cd_backward slices) with torch CPU tensors."""
 import numpy as np
 import torch
+import torch.distributed as dist
 
 import oracle
 
@@ -59,7 +60,8 @@ class OracleEngine:
 class FusedOracleEngine(OracleEngine):
     """Adds the cd_forward_rows / cd_forward_cols contract (column keys)."""
 
-    def forward_rows(self, x, y, q_slice, tau=None, partials=None):
+    def forward_rows(self, x, y, q_slice, tau=None, partials=None, keys=None):
+        out_keys = keys
         X, Y = _np(x), _np(y)
         B, N, M = X.shape[0], X.shape[1], Y.shape[1]
         q0, q1 = q_slice
@@ -73,8 +75,12 @@ class FusedOracleEngine(OracleEngine):
         part = np.zeros((B, 4)) if partials is None else _np(partials).copy()
         part[:, 0] = dxy.astype(np.float32).astype(np.float64).sum(1)
         part[:, 2] = (dxy <= oracle.tau_sq(tau)).sum(1) if tau is not None else 0
+        kt = torch.from_numpy(keys)
+        if out_keys is not None:
+            out_keys.copy_(kt)
+            kt = out_keys
         return (torch.from_numpy(dxy.astype(np.float32)), torch.from_numpy((ixy + 0).astype(np.int32)),
-                torch.from_numpy(keys), torch.from_numpy(part))
+                kt, torch.from_numpy(part))
 
     def forward_cols(self, x, y, keys, r_slice, tau=None, partials=None):
         X, Y = _np(x), _np(y)
@@ -94,3 +100,27 @@ class FusedOracleEngine(OracleEngine):
         part[:, 3] = (d <= oracle.tau_sq(tau)).sum(1) if tau is not None else 0
         return torch.from_numpy(d.copy()), torch.from_numpy(idx), torch.from_numpy(part)
 
+    def forward_cols_peers(self, x, y, keys_list, r_slice, tau=None, partials=None):
+        """The cd_forward_cols_peers contract: the element-wise MIN of the given key arrays, then
+        forward_cols."""
+        red = keys_list[0].clone()
+        for k in keys_list[1:]:
+            red = torch.minimum(red, k)
+        return self.forward_cols(x, y, red, r_slice, tau=tau, partials=partials)
+
+
+class GlooPeerKeys:
+    """Test stand-in for distributed.PeerColKeys on gloo/CPU: the peer reads are emulated by an
+    all-gather of every rank's key array after the barrier (the orchestration — keys into the
+    rank's own array, barrier, MIN-reducing resolve, barrier — is what is tested)."""
+
+    def __init__(self, B, M):
+        self.buf = torch.empty((B, M), dtype=torch.int64)
+
+    def barrier(self):
+        dist.barrier()
+
+    def sources(self):
+        out = [torch.empty_like(self.buf) for _ in range(dist.get_world_size())]
+        dist.all_gather(out, self.buf)
+        return out

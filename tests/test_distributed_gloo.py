@@ -50,8 +50,13 @@ def _worker(rank, world, port, mode, result_q):
                 x.zero_()
                 y.zero_()
             pd.broadcast_clouds(x, y, src=0)
-            eng = FusedOracleEngine() if mode == "query_fused" else OracleEngine()
-            out = pd.query_sharded_step(eng, x, y, tau=tau, w1=0.5, w2=2.0)
+            eng = FusedOracleEngine() if mode in ("query_fused", "query_peer") else OracleEngine()
+            peer = None
+            if mode == "query_peer":   # the fused-reduce orchestration (peer reads emulated on gloo)
+                from tests.dist_engine import GlooPeerKeys
+                assert pd.PeerColKeys.create(2, 277, "cpu") is None   # no symmetric memory on gloo
+                peer = GlooPeerKeys(2, 277)
+            out = pd.query_sharded_step(eng, x, y, tau=tau, w1=0.5, w2=2.0, peer=peer)
         res = {k: (v.numpy() if isinstance(v, torch.Tensor) else v) for k, v in out.items()}
         result_q.put((rank, res))
     finally:
@@ -127,7 +132,8 @@ def test_batch_sharded_strong(world):
         np.testing.assert_array_equal(out["grad_y"], ref["grad_y"][b0:b1])
 
 
-@pytest.mark.parametrize("world,mode", [(2, "query_fused"), (3, "query_fused"), (2, "query_slices")])
+@pytest.mark.parametrize("world,mode", [(2, "query_fused"), (3, "query_fused"), (2, "query_slices"),
+                                        (2, "query_peer"), (3, "query_peer")])
 def test_query_sharded(world, mode):
     from paper_1911_05063_b200 import synth
     from paper_1911_05063_b200.distributed import shard_range
