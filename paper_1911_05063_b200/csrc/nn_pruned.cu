@@ -808,13 +808,13 @@ __global__ void __launch_bounds__(kPrThreads, CD_PR_MINB) nn_pruned_kernel(Prune
                 if (lane == 0) { atomicAdd(&g_pr_stats[1], 1ull); s_used = 1; }
 #endif
             }
-            float cur[kPrR];   // this block's minimum per row
+            float cur[kPrR], cur2[kPrR];   // this block's minimum per row: two independent fold chains
 #pragma unroll
-            for (int r = 0; r < kPrR; ++r) cur[r] = INFINITY;
-#pragma unroll 4
-            for (int jj = 0; jj < kBlockK; jj += 2) {
-                const float4 t0 = tb[kb + jj];
-                const float4 t1 = tb[kb + jj + 1];
+            for (int r = 0; r < kPrR; ++r) {
+                cur[r] = INFINITY;
+                cur2[r] = INFINITY;
+            }
+            auto fold_pair = [&](const float4 t0, const float4 t1, float* acc) {
                 const u64 t0x = pk2(t0.x, t0.x), t0y = pk2(t0.y, t0.y), t0z = pk2(t0.z, t0.z);
                 const u64 t1x = pk2(t1.x, t1.x), t1y = pk2(t1.y, t1.y), t1z = pk2(t1.z, t1.z);
 #pragma unroll
@@ -832,10 +832,17 @@ __global__ void __launch_bounds__(kPrThreads, CD_PR_MINB) nn_pruned_kernel(Prune
                     float a0, a1, c0, c1;
                     upk2(s0, a0, a1);
                     upk2(s1, c0, c1);
-                    cur[2 * r] = fmin3(cur[2 * r], a0, c0);
-                    cur[2 * r + 1] = fmin3(cur[2 * r + 1], a1, c1);
+                    acc[2 * r] = fmin3(acc[2 * r], a0, c0);
+                    acc[2 * r + 1] = fmin3(acc[2 * r + 1], a1, c1);
                 }
+            };
+#pragma unroll 2
+            for (int jj = 0; jj < kBlockK; jj += 4) {
+                fold_pair(tb[kb + jj], tb[kb + jj + 1], cur);
+                fold_pair(tb[kb + jj + 2], tb[kb + jj + 3], cur2);
             }
+#pragma unroll
+            for (int r = 0; r < kPrR; ++r) cur[r] = fminf(cur[r], cur2[r]);   // min: order-free, exact
             // a strictly smaller block minimum takes over; an EQUAL finite one is an exact tie across
             // blocks (Hilbert order is not index order): flagged, the resolve then scans the row
 #pragma unroll
