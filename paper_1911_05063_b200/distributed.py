@@ -158,7 +158,7 @@ class PeerColKeys:
             grp = group if group is not None else dist.group.WORLD
             if hasattr(symm, "enable_symm_mem_for_group"):
                 symm.enable_symm_mem_for_group(grp.group_name)
-            buf = symm.empty((B, M), dtype=torch.int64, device=device)
+            buf = symm.empty(B, M, dtype=torch.int64, device=device)
             handle = symm.rendezvous(buf, grp)
             ptrs = [int(p) for p in handle.buffer_ptrs]
             if len(ptrs) != dist.get_world_size(group) or any(p == 0 for p in ptrs):
